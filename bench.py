@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark of the pseudo-Verlet SPH density pass on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+One step = one pass of the whole hot path over the config's particle set:
+sph_build_cells -> sph_sort_cells -> sph_density_all (+ the x-slab ghost
+exchange when N > 1).  Inputs are resident in HBM when the timed region
+starts (`value`); the `e2e` figure repeats the step through the public API
+with pinned HOST buffers, the H2D copy of the inputs and the D2H copy of all
+outputs inside the timed region.  Rank 0 prints one JSON line.
+
+Metric: in-range pair interactions per second (sum_i nngb_i per step / step
+time), whole job.  `--impl reference` times the fp64 CPU oracle (the only
+reference this tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "in-range pair interactions/sec (whole job)"
+UNIT = "interactions/s"
+FLOP_CAND, FLOP_HIT = 8, 48                  # algorithmic flops
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.45, SMs x FP32 lanes x FMA x max clock
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 5 + k and r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def _profile_traffic():
+    """dram bytes per density launch from the committed ncu capture (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "density_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle's cell list on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_baseline(p, seconds: float):
+    import oracle
+    n_probe = 2000
+    rng = np.random.default_rng(123)
+    probe = np.sort(rng.choice(p.n, n_probe, replace=False))
+    t0 = time.perf_counter()
+    r = oracle.celllist(p.xyzh, p.vm, p.nc, targets=probe)
+    t_probe = time.perf_counter() - t0
+    n_s = int(min(p.n, max(n_probe, n_probe * seconds / max(t_probe, 1e-3))))
+    tgt = np.sort(rng.choice(p.n, n_s, replace=False))
+    t0 = time.perf_counter()
+    r = oracle.celllist(p.xyzh, p.vm, p.nc, targets=tgt)
+    dt = time.perf_counter() - t0
+    inter = float(r["nngb"].sum())
+    return {"value": inter / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"oracle_celllist (fp64, OpenMP) on {n_s} random targets of {p.name} (N={p.n}), "
+                      f"incl. binning all N; {inter:.0f} interactions in {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle, timed on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    p = synth.make(args.config)
+    per_step = max(5.0, 60.0 / max(1, args.steps + args.warmup))
+    rng = np.random.default_rng(7)
+    n_probe = 2000
+    t0 = time.perf_counter()
+    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(rng.choice(p.n, n_probe, replace=False)))
+    t_probe = time.perf_counter() - t0
+    n_s = int(min(p.n, max(n_probe, n_probe * per_step / max(t_probe, 1e-3))))
+    times, inters = [], []
+    for s in range(args.warmup + args.steps):
+        tgt = np.sort(rng.choice(p.n, n_s, replace=False))
+        t0 = time.perf_counter()
+        r = oracle.celllist(p.xyzh, p.vm, p.nc, targets=tgt)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+            inters.append(float(r["nngb"].sum()))
+    value = sum(inters) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.config} (BASELINE.json configs, DESIGN.md §3)",
+                                            "n_particles": p.n, "cells": f"{p.nc}^3",
+                                            "sample_targets_per_step": n_s},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"oracle_celllist on {n_s} random target particles of {p.name} per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import paper_1804_06231_b200 as pv
+    import synth
+    from paper_1804_06231_b200 import slabs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pv.load()
+
+    t_gen = time.perf_counter()
+    if world == 1:
+        p = synth.make(args.config)
+        part = slabs.Slab.single(p)
+    else:
+        part = slabs.Slab.from_config(args.config, rank, world)
+    t_gen = time.perf_counter() - t_gen
+
+    runner = slabs.SlabRunner(part, dist=dist)
+    runner.upload()
+    stream = torch.cuda.current_stream()
+
+    # one counted pass (outside the timed region): interactions, candidates per kind
+    st = pv.Stats()
+    runner.step(stats=st)
+    runner.check()
+    counts = st.read()
+    nngb_sum = int(runner.out.nngb[:runner.n_own].sum(dtype=torch.int64).item())
+    cand_sum, hit_sum = sum(counts["cand"]), sum(counts["hits"])
+    assert hit_sum == nngb_sum, (hit_sum, nngb_sum)
+    if dist:
+        t = torch.tensor([nngb_sum, cand_sum], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        tot_inter, tot_cand = int(t[0]), int(t[1])
+    else:
+        tot_inter, tot_cand = nngb_sum, cand_sum
+
+    for _ in range(args.warmup):
+        runner.step()
+    torch.cuda.synchronize()
+
+    nst = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(nst)]
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(nst):
+            runner.step(events=ev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    stage = {"exchange": [], "build": [], "sort": [], "density": []}
+    for k in range(nst):
+        e = ev[k]
+        stage["exchange"].append(e[0].elapsed_time(e[1]))
+        stage["build"].append(e[1].elapsed_time(e[2]))
+        stage["sort"].append(e[2].elapsed_time(e[3]))
+        stage["density"].append(e[3].elapsed_time(e[4]))
+    ms_step = ms_total / nst
+    if dist:
+        t = torch.tensor([ms_step, statistics.mean(stage["density"])], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step_max, dens_max = float(t[0]), float(t[1])
+    else:
+        ms_step_max, dens_max = ms_step, statistics.mean(stage["density"])
+    value = tot_inter / (ms_step_max * 1e-3)
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h = runner.e2e_time(steps=max(2, min(nst, 3)), warmup=1)
+        if dist:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": tot_inter / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    dens_ms_local = statistics.mean(stage["density"])
+    flops = FLOP_CAND * cand_sum + FLOP_HIT * hit_sum          # this rank's density launch
+    achieved = flops / (dens_ms_local * 1e-3) / 1e12
+    traffic = _profile_traffic()
+    roof = {"bound": "alu", "kernel": "k_density_all", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §6.2)",
+            "traffic": (traffic or {}).get(args.config) if traffic else None,
+            "flops_per_launch": flops, "launch_ms": dens_ms_local}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(part.pset, args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": nst,
+                "warmup": args.warmup, "ms_per_step": ms_step_max, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{args.config} (BASELINE.json configs, DESIGN.md §3)",
+                           "n_particles": part.n_global, "cells": f"{part.nc}^3",
+                           "parallelism": f"x-slab{world}" if world > 1 else "single",
+                           "l2": "inputs (>= 4 GB at c5) larger than L2; no flush",
+                           "step": "ghost exchange + build_cells + sort_cells + density_all"},
+                "interactions_per_step": tot_inter, "candidates_per_step": tot_cand,
+                "hit_fraction": tot_inter / max(1, tot_cand),
+                "stage_ms": {k: statistics.mean(v) for k, v in stage.items()},
+                "density_ms_max_over_ranks": dens_max,
+                "gpu_launches": runner.launches_per_step * nst,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "gen_seconds": t_gen}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * sph.h -- C ABI of libpvsph.so: the pseudo-Verlet SPH density loop of
+ * Willis, Schaller, Gonnet, Bower & Draper, "An Efficient SIMD Implementation
+ * of Pseudo-Verlet Lists for Neighbour Interactions in Particle-Based Codes"
+ * (arXiv:1804.06231), on NVIDIA B200 (sm_100a).
+ *
+ * Citations "P:n" are lines of the paper text (reference PAPER.md).
+ *
+ * Problem statement:
+ *   N particles with positions x_i, per-particle smoothing length h_i,
+ *   velocity v_i and mass m_i in a periodic box.  The cut-off radius of
+ *   particle i is H_i = gamma * h_i (the paper's "h_i"); j is a neighbour of
+ *   i iff j != i and |x_i - x_j|^2 < H_i^2 (minimum image; gather on h_i).
+ *   The box is decomposed into cells of edge C_l >= max H, particles
+ *   of a cell are stored together, and for each of the 13 symmetry-reduced
+ *   cell-pair directions every cell keeps its particles sorted by
+ *   their projection on the unit axis ("dist" and "index").  For each
+ *   pair of neighbouring cells only the particles of the neighbour whose
+ *   projected separation is below H_i are tested (Code 2).
+ *   For every particle the library computes, with the M4 cubic spline
+ *   W(r,h) = (16/pi) H^-3 w(r/H) (support H = gamma h):
+ *     rho       = m_i W(0,h_i) + sum_j m_j W(r_ij,h_i)
+ *     wcount    =     W(0,h_i) + sum_j     W(r_ij,h_i)
+ *     rho_dh    = d rho / d h_i,   wcount_dh = d wcount / d h_i
+ *     div_v     = -(1/rho) sum_j m_j (v_ij . x_ij) W'(r_ij)/r_ij
+ *     curl_v    =  (1/rho) sum_j m_j (v_ij x x_ij) W'(r_ij)/r_ij
+ *     nngb      = number of neighbours (self excluded)
+ *
+ * Conventions for every call:
+ *   - All array pointers are DEVICE pointers unless stated otherwise; the
+ *     caller allocates and owns all memory (inputs, sph_cells arrays,
+ *     outputs, workspace).  The library allocates nothing and keeps no
+ *     global mutable state; calls on different streams with disjoint
+ *     outputs and workspaces may run concurrently.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
+ *     Calls are asynchronous: argument errors are returned at once,
+ *     data-dependent errors set the device status word in the workspace,
+ *     read by sph_status() (one stream synchronisation).
+ *   - Return codes: SPH_OK, SPH_EINVAL (null pointer, bad size or grid,
+ *     workspace too small), SPH_EH_RANGE (h <= 0, m <= 0 or gamma*h > C_l),
+ *     SPH_ECAPACITY (a cell holds more than SPH_MAX_CELL particles, or the
+ *     particle arrays are too small), SPH_EDOMAIN (non-finite value, or a
+ *     position outside [0, box) / outside the rank's slab), SPH_ECUDA (a
+ *     CUDA launch failed; sph_strerror(SPH_ECUDA) gives the CUDA message).
+ */
+#ifndef PVSPH_SPH_H
+#define PVSPH_SPH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPH_ABI_VERSION 1
+
+#define SPH_OK 0
+#define SPH_EINVAL 1
+#define SPH_EH_RANGE 2
+#define SPH_ECAPACITY 3
+#define SPH_EDOMAIN 4
+#define SPH_ECUDA 5
+
+/* Largest number of particles one cell may hold. */
+#define SPH_MAX_CELL 65535
+
+/* Number of sort directions and the window margin: a candidate is
+ * swept when its projected separation is below H_i + SPH_DELTA_FRAC * C_l
+ * (reading R5: covers fp32 rounding of the keys). */
+#define SPH_NDIR 13
+#define SPH_DELTA_FRAC (1.0 / 65536.0)
+
+/* Cell grid of one rank.  Cells are numbered x-major on the LOCAL grid:
+ *   cell = (ixl * nc[1] + iy) * nc[2] + iz,  ixl = ix - x_lo + ghost_x,
+ * whose x extent is nx_local = (x_hi - x_lo) + 2 * ghost_x planes.  With
+ * ghost_x = 0 the rank must own every plane (x_lo = 0, x_hi = nc[0]) and x
+ * is periodic like y and z; with ghost_x = 1 planes x_lo-1 and x_hi (mod
+ * nc[0]) are read-only ghost planes (x-slab decomposition). */
+typedef struct sph_grid {
+    int32_t nc[3];      /* global cells per dimension, each >= 3            */
+    int32_t x_lo, x_hi; /* owned x planes [x_lo, x_hi)                      */
+    int32_t ghost_x;    /* 0 or 1                                           */
+    int32_t reserved;   /* must be 0                                        */
+    double box[3];      /* periodic box lengths (> 0)                       */
+    float gamma;        /* support / smoothing length (1.825742)            */
+    float reserved2;    /* must be 0                                        */
+} sph_grid;
+
+/* One entry of a per-direction sorted list ("dist"/"index" of P:92):
+ * key = cell-local projection on the unit axis of the direction (fp32 of
+ * an fp64 dot product of x - cell corner), j = slot of the particle in the
+ * cell-sorted arrays.  Entries of one cell are ascending in key, ties by
+ * the particle's input index. */
+typedef struct sph_pv_entry {
+    float key;
+    int32_t j;
+} sph_pv_entry;
+
+/* Cell-sorted particle storage (caller-allocated device arrays).
+ *   cell_start[ncell + 1]   first slot of each local cell (written by build)
+ *   xyzh[4 * capacity]      x, y, z, h  in cell order (float4 per particle)
+ *   vm[4 * capacity]        vx, vy, vz, m in cell order
+ *   perm[capacity]          slot -> input index
+ *   cell_hmax[ncell]        max h in each cell
+ *   pv[SPH_NDIR * capacity] sorted lists: direction d, slot range of cell c
+ *                           at pv[d * capacity + cell_start[c] ...]
+ * n is written by sph_build_cells (stored particles).  16-byte alignment
+ * is required for xyzh and vm, 8 bytes for pv. */
+typedef struct sph_cells {
+    int64_t capacity;
+    int64_t n;
+    int32_t *cell_start;
+    float *xyzh;
+    float *vm;
+    int32_t *perm;
+    float *cell_hmax;
+    sph_pv_entry *pv;
+} sph_cells;
+
+/* Outputs, each an array of n_out elements indexed by INPUT index (only
+ * owned particles are written); curl_v is [3][n_out] (x, y, z planes). */
+typedef struct sph_out {
+    int64_t n_out;
+    float *rho, *rho_dh, *wcount, *wcount_dh, *div_v, *curl_v;
+    int32_t *nngb;
+} sph_out;
+
+/* Optional device-side counters (pass NULL to skip; counting costs time).
+ * Index k: 0 self cell, 1 face, 2 edge, 3 corner neighbour cells.
+ * cand = candidate distance evaluations, hits = in-range pairs. */
+typedef struct sph_stats {
+    unsigned long long cand[4];
+    unsigned long long hits[4];
+} sph_stats;
+
+/* Number of local cells of `grid` (< 0 on a bad grid). */
+int64_t sph_ncell(const sph_grid *grid);
+
+/* Bytes of workspace the calls need for up to n_total stored particles. */
+size_t sph_workspace_bytes(const sph_grid *grid, int64_t n_total);
+
+/* Bin particles into cells and write the cell-sorted SoA
+ * arrays, perm, cell_start, cell_hmax and cells->n = n_own + n_ghost.
+ * Inputs xyzh_in/vm_in hold n_own owned particles followed by n_ghost
+ * ghost particles (float4 each, device).  Owned particles must lie in the
+ * rank's owned planes, ghosts in its ghost planes (n_ghost > 0 needs
+ * ghost_x = 1).  Resets the status word, then reports SPH_EDOMAIN /
+ * SPH_EH_RANGE / SPH_ECAPACITY through it.  Cell bins use fp64:
+ * ix = floor(x * nc / box), clamped to [0, nc-1]. */
+int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in,
+                    const float *vm_in, sph_cells *cells, void *ws, size_t ws_bytes, void *stream);
+
+/* Sort every cell of [cell_begin, cell_end) along the 13 directions (P:92,
+ * P:102): fills cells->pv for those cells.  cell_end = -1 means all. */
+int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/* Self-cell interactions of each listed cell (device int32 list): every
+ * ordered pair i != j in the cell plus the self term of i.  ACCUMULATES
+ * with atomics into acc (caller zeroes it first): rho, wcount, rho_dh,
+ * wcount_dh and nngb receive their final contributions, div_v and curl_v
+ * receive rho-weighted sums (rho*div, rho*curl); see sph_density_finalize. */
+int sph_density_self(const sph_grid *grid, const sph_cells *cells, const int32_t *cell_list, int64_t ncells_list,
+                     sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream);
+
+/* One-sided pseudo-Verlet pair sweeps: for each
+ * device pair (ci, cj) of `pairs` ([npairs][2] int32), particles of ci
+ * gather from cj, which must be one of the 26 neighbours of ci.  One CTA
+ * per cell pair; accumulates like sph_density_self.  The paper's symmetric
+ * pair is the two calls (ci, cj) and (cj, ci). */
+int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t *pairs, int64_t npairs,
+                     sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream);
+
+/* div_v /= rho and curl_v /= rho for the first n elements (after the self
+ * and pair calls). */
+int sph_density_finalize(sph_out *acc, int64_t n, void *stream);
+
+/* The fused hot path: every owned particle gathers from its own cell and
+ * the 26 neighbour cells with pseudo-Verlet windows, one writer per
+ * particle, no atomics, deterministic; writes FINAL values in input order. */
+int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, sph_stats *stats, void *ws,
+                    size_t ws_bytes, void *stream);
+
+/* Synchronises `stream`, returns the status word's error code (SPH_OK if
+ * none), or SPH_ECUDA if the stream reports a CUDA error. */
+int sph_status(void *ws, void *stream);
+
+/* Clears the status word (asynchronous). */
+int sph_status_reset(void *ws, void *stream);
+
+/* Static description of an error code (the last CUDA error text for
+ * SPH_ECUDA). */
+const char *sph_strerror(int code);
+
+/* SPH_ABI_VERSION of the loaded library. */
+int sph_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PVSPH_SPH_H */

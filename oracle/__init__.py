@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "liboracle.so")
 SRC_PATH = os.path.join(_HERE, "oracle.c")
 
 FIELDS = ("rho", "wcount", "rho_dh", "wcount_dh", "div_v", "curl_x", "curl_y", "curl_z",
-          "nngb", "band", "a_rho_dh", "a_wcount_dh", "a_div", "a_curl")
+          "nngb", "band", "a_rho_dh", "a_wcount_dh", "a_div", "a_curl", "c_div", "c_curl")
 KINDS = ("self", "face", "edge", "corner")
 DELTA_FRAC = 2.0 ** -16      # window margin delta = 2^-16 C_l (reading R5)
 

@@ -24,6 +24,9 @@
  *     W(r,h) = (16/pi) H^-3 w(r/H),  w(x) = 3x^3 - 3x^2 + 1/2  (x < 1/2)
  *                                          = (1-x)^3           (1/2 <= x < 1)
  *                                          = 0                 (x >= 1).
+ *   Scales for the signed outputs (readings R13, R14): A = sum of |terms|,
+ *   C = sum of |terms| * (|x w''(x)/w'(x)| + 1), the first-order change of
+ *   the div/curl sums under a unit relative perturbation of every x = r/H.
  *   The neighbour list of each i is sorted by j and summed in that order in
  *   fp64 (reading R6), so the brute-force (O1) and cell-list (O2) variants
  *   give bitwise identical results.
@@ -55,10 +58,10 @@
 #include <omp.h>
 #endif
 
-#define ORC_NOUT 14
+#define ORC_NOUT 16
 enum {
     O_RHO = 0, O_WCOUNT, O_RHO_DH, O_WCOUNT_DH, O_DIV, O_CURLX, O_CURLY, O_CURLZ,
-    O_NNGB, O_BAND, O_A_RHODH, O_A_WDH, O_A_DIV, O_A_CURL
+    O_NNGB, O_BAND, O_A_RHODH, O_A_WDH, O_A_DIV, O_A_CURL, O_C_DIV, O_C_CURL
 };
 
 static const double ORC_PI = 3.14159265358979323846264338327950288;
@@ -79,6 +82,21 @@ static double dw_m4(double x)
     if (x < 0.5) return 9.0 * x * x - 6.0 * x;
     if (x < 1.0) { double u = 1.0 - x; return -3.0 * u * u; }
     return 0.0;
+}
+
+static double d2w_m4(double x)
+{
+    if (x < 0.5) return 18.0 * x - 6.0;
+    if (x < 1.0) return 6.0 * (1.0 - x);
+    return 0.0;
+}
+
+/* Condition factor of a gradient term m (v.x_ij) W'(r)/r ~ w'(x) (v . unit vector)
+ * under a relative perturbation of x = r/H (reading R14): |x w''/w'| + 1. */
+static double kappa_m4(double x)
+{
+    double dw = dw_m4(x);
+    return dw != 0.0 ? fabs(x * d2w_m4(x) / dw) + 1.0 : 1.0;
 }
 
 /* W(r,h), dW/dr and dW/dh for support H = gamma*h.
@@ -117,7 +135,7 @@ static void accumulate(int64_t i, const float *xyzh, const float *vm, double L, 
     oracle_kernel(0.0, hi, gamma, &W0, &dW0, &dWh0);
     double rho = mi * W0, wc = W0, rho_dh = mi * dWh0, wc_dh = dWh0;
     double a_rdh = fabs(mi * dWh0), a_wdh = fabs(dWh0);
-    double D = 0.0, Rx = 0.0, Ry = 0.0, Rz = 0.0, a_div = 0.0, a_curl = 0.0;
+    double D = 0.0, Rx = 0.0, Ry = 0.0, Rz = 0.0, a_div = 0.0, a_curl = 0.0, c_div = 0.0, c_curl = 0.0;
     for (int64_t q = 0; q < k; ++q) {
         int64_t j = nb[q];
         double dx = min_image(xi - (double)xyzh[4 * j + 0], L);
@@ -146,6 +164,9 @@ static void accumulate(int64_t i, const float *xyzh, const float *vm, double L, 
             Rz += f * (vx * dy - vy * dx);
             a_div += fabs(f * vdx);
             a_curl += fabs(f) * sqrt(vx * vx + vy * vy + vz * vz) * r;
+            double kap = kappa_m4(r / (gamma * hi));
+            c_div += fabs(f * vdx) * kap;
+            c_curl += fabs(f) * sqrt(vx * vx + vy * vy + vz * vz) * r * kap;
         }
     }
     out[O_RHO] = rho;
@@ -162,6 +183,8 @@ static void accumulate(int64_t i, const float *xyzh, const float *vm, double L, 
     out[O_A_WDH] = a_wdh;
     out[O_A_DIV] = a_div / rho;
     out[O_A_CURL] = a_curl / rho;
+    out[O_C_DIV] = c_div / rho;
+    out[O_C_CURL] = c_curl / rho;
 }
 
 /* Test candidate j for target i: push to nb if in range, count band. */

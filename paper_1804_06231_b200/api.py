@@ -1,0 +1,267 @@
+"""Thin Python binding of libpvsph.so with the C ABI's names.
+
+Argument marshalling only: torch supplies device memory and the stream;
+every step of the density path runs in the library's CUDA kernels.  There
+is no CPU fallback: without the built library or a GPU the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import SphCells, SphGrid, SphOut, SphStats
+
+GAMMA = 1.825742
+
+
+class SphError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        lib = _lib.load()
+        msg = lib.sph_strerror(code).decode()
+        super().__init__(f"{where}: {_lib.ERROR_NAMES.get(code, code)} ({msg})")
+        self.code = code
+
+
+def _check(code: int, where: str) -> None:
+    if code != _lib.SPH_OK:
+        raise SphError(code, where)
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0) -> SphGrid:
+    if isinstance(nc, int):
+        nc = (nc, nc, nc)
+    if isinstance(box, (int, float)):
+        box = (float(box),) * 3
+    g = SphGrid()
+    for k in range(3):
+        g.nc[k] = int(nc[k])
+        g.box[k] = float(box[k])
+    g.x_lo = int(x_lo)
+    g.x_hi = int(nc[0] if x_hi is None else x_hi)
+    g.ghost_x = int(ghost_x)
+    g.gamma = float(gamma)
+    return g
+
+
+def ncell(grid: SphGrid) -> int:
+    n = _lib.load().sph_ncell(ctypes.byref(grid))
+    if n < 0:
+        raise SphError(_lib.SPH_EINVAL, "sph_ncell")
+    return int(n)
+
+
+def workspace_bytes(grid: SphGrid, n_total: int) -> int:
+    b = _lib.load().sph_workspace_bytes(ctypes.byref(grid), int(n_total))
+    if b == 0:
+        raise SphError(_lib.SPH_EINVAL, "sph_workspace_bytes")
+    return int(b)
+
+
+@dataclass
+class Cells:
+    """Device storage of sph_cells (owned by torch)."""
+    capacity: int
+    cell_start: torch.Tensor
+    xyzh: torch.Tensor
+    vm: torch.Tensor
+    perm: torch.Tensor
+    cell_hmax: torch.Tensor
+    pv: torch.Tensor            # (13 * capacity, 2) int32 view of sph_pv_entry {float key; int j}
+    n: int = 0
+
+    @staticmethod
+    def alloc(grid: SphGrid, capacity: int, device="cuda") -> "Cells":
+        nce = ncell(grid)
+        cap = max(int(capacity), 1)
+        return Cells(cap, torch.empty(nce + 1, dtype=torch.int32, device=device),
+                     torch.empty((cap, 4), dtype=torch.float32, device=device),
+                     torch.empty((cap, 4), dtype=torch.float32, device=device),
+                     torch.empty(cap, dtype=torch.int32, device=device),
+                     torch.empty(nce, dtype=torch.float32, device=device),
+                     torch.empty((_lib.SPH_NDIR * cap, 2), dtype=torch.int32, device=device))
+
+    def struct(self) -> SphCells:
+        s = SphCells()
+        s.capacity = self.capacity
+        s.n = self.n
+        s.cell_start, s.xyzh, s.vm = self.cell_start.data_ptr(), self.xyzh.data_ptr(), self.vm.data_ptr()
+        s.perm, s.cell_hmax, s.pv = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.pv.data_ptr()
+        return s
+
+    def pv_keys(self) -> torch.Tensor:
+        return self.pv[:, 0].view(torch.float32).view(_lib.SPH_NDIR, self.capacity)
+
+    def pv_slots(self) -> torch.Tensor:
+        return self.pv[:, 1].view(_lib.SPH_NDIR, self.capacity)
+
+
+FIELDS = ("rho", "wcount", "rho_dh", "wcount_dh", "div_v", "curl_x", "curl_y", "curl_z", "nngb")
+
+
+@dataclass
+class Out:
+    n_out: int
+    rho: torch.Tensor
+    rho_dh: torch.Tensor
+    wcount: torch.Tensor
+    wcount_dh: torch.Tensor
+    div_v: torch.Tensor
+    curl_v: torch.Tensor        # (3, n_out)
+    nngb: torch.Tensor
+
+    @staticmethod
+    def alloc(n_out: int, device="cuda", zero=False) -> "Out":
+        n = max(int(n_out), 1)
+        f = (torch.zeros if zero else torch.empty)
+        return Out(int(n_out), *(f(n, dtype=torch.float32, device=device) for _ in range(5)),
+                   f((3, n), dtype=torch.float32, device=device), f(n, dtype=torch.int32, device=device))
+
+    def zero_(self) -> "Out":
+        for t in (self.rho, self.rho_dh, self.wcount, self.wcount_dh, self.div_v, self.curl_v, self.nngb):
+            t.zero_()
+        return self
+
+    def struct(self) -> SphOut:
+        s = SphOut()
+        s.n_out = self.n_out
+        s.rho, s.rho_dh, s.wcount = self.rho.data_ptr(), self.rho_dh.data_ptr(), self.wcount.data_ptr()
+        s.wcount_dh, s.div_v, s.curl_v = self.wcount_dh.data_ptr(), self.div_v.data_ptr(), self.curl_v.data_ptr()
+        s.nngb = self.nngb.data_ptr()
+        return s
+
+    def to_numpy(self) -> dict:
+        n = self.n_out
+        d = {"rho": self.rho[:n], "wcount": self.wcount[:n], "rho_dh": self.rho_dh[:n],
+             "wcount_dh": self.wcount_dh[:n], "div_v": self.div_v[:n], "curl_x": self.curl_v[0, :n],
+             "curl_y": self.curl_v[1, :n], "curl_z": self.curl_v[2, :n], "nngb": self.nngb[:n]}
+        return {k: v.cpu().numpy() for k, v in d.items()}
+
+
+class Stats:
+    def __init__(self, device="cuda"):
+        self.buf = torch.zeros(8, dtype=torch.int64, device=device)
+
+    def ptr(self):
+        return _ptr(self.buf)
+
+    def read(self) -> dict:
+        v = self.buf.cpu().tolist()
+        return {"cand": v[:4], "hits": v[4:]}
+
+
+def alloc_workspace(grid: SphGrid, capacity: int, device="cuda") -> torch.Tensor:
+    return torch.zeros(workspace_bytes(grid, capacity), dtype=torch.uint8, device=device)
+
+
+# ---- the C ABI calls ---------------------------------------------------------
+def sph_build_cells(grid: SphGrid, xyzh_in: torch.Tensor, vm_in: torch.Tensor, cells: Cells, ws: torch.Tensor,
+                    n_own: int | None = None, n_ghost: int = 0, stream=None) -> None:
+    n_total = xyzh_in.shape[0] if n_own is None else int(n_own) + int(n_ghost)
+    n_own = n_total - int(n_ghost) if n_own is None else int(n_own)
+    assert xyzh_in.is_contiguous() and vm_in.is_contiguous()
+    s = cells.struct()
+    _check(_lib.load().sph_build_cells(ctypes.byref(grid), n_own, int(n_ghost), _ptr(xyzh_in), _ptr(vm_in),
+                                       ctypes.byref(s), _ptr(ws), ws.numel(), _stream(stream)), "sph_build_cells")
+    cells.n = int(s.n)
+
+
+def sph_sort_cells(grid: SphGrid, cells: Cells, ws: torch.Tensor, cell_begin: int = 0, cell_end: int = -1,
+                   stream=None) -> None:
+    s = cells.struct()
+    _check(_lib.load().sph_sort_cells(ctypes.byref(grid), ctypes.byref(s), int(cell_begin), int(cell_end),
+                                      _ptr(ws), ws.numel(), _stream(stream)), "sph_sort_cells")
+
+
+def sph_density_self(grid: SphGrid, cells: Cells, cell_list: torch.Tensor, acc: Out, ws: torch.Tensor,
+                     stats: Stats | None = None, stream=None) -> None:
+    s, o = cells.struct(), acc.struct()
+    _check(_lib.load().sph_density_self(ctypes.byref(grid), ctypes.byref(s), _ptr(cell_list), cell_list.numel(),
+                                        ctypes.byref(o), stats.ptr() if stats else None, _ptr(ws), ws.numel(),
+                                        _stream(stream)), "sph_density_self")
+
+
+def sph_density_pair(grid: SphGrid, cells: Cells, pairs: torch.Tensor, acc: Out, ws: torch.Tensor,
+                     stats: Stats | None = None, stream=None) -> None:
+    assert pairs.dtype == torch.int32 and pairs.is_contiguous() and (pairs.numel() == 0 or pairs.shape[-1] == 2)
+    s, o = cells.struct(), acc.struct()
+    _check(_lib.load().sph_density_pair(ctypes.byref(grid), ctypes.byref(s), _ptr(pairs), pairs.numel() // 2,
+                                        ctypes.byref(o), stats.ptr() if stats else None, _ptr(ws), ws.numel(),
+                                        _stream(stream)), "sph_density_pair")
+
+
+def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
+    o = acc.struct()
+    _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),
+           "sph_density_finalize")
+
+
+def sph_density_all(grid: SphGrid, cells: Cells, out: Out, ws: torch.Tensor, stats: Stats | None = None,
+                    stream=None) -> None:
+    s, o = cells.struct(), out.struct()
+    _check(_lib.load().sph_density_all(ctypes.byref(grid), ctypes.byref(s), ctypes.byref(o),
+                                       stats.ptr() if stats else None, _ptr(ws), ws.numel(), _stream(stream)),
+           "sph_density_all")
+
+
+def sph_status(ws: torch.Tensor, stream=None) -> int:
+    return int(_lib.load().sph_status(_ptr(ws), _stream(stream)))
+
+
+def sph_status_reset(ws: torch.Tensor, stream=None) -> None:
+    _check(_lib.load().sph_status_reset(_ptr(ws), _stream(stream)), "sph_status_reset")
+
+
+def check_status(ws: torch.Tensor, stream=None) -> None:
+    _check(sph_status(ws, stream), "sph_status")
+
+
+# ---- convenience: one full density pass ---------------------------------------
+class DensityPass:
+    """Owns the device buffers of one configuration and runs
+    build_cells -> sort_cells -> density_all (the hot path)."""
+
+    def __init__(self, nc, n_own: int, box=1.0, gamma=GAMMA, capacity: int | None = None, device="cuda",
+                 x_lo=0, x_hi=None, ghost_x=0):
+        self.grid = make_grid(nc, box, gamma, x_lo, x_hi, ghost_x)
+        self.n_own = int(n_own)
+        cap = int(capacity if capacity is not None else n_own)
+        self.cells = Cells.alloc(self.grid, cap, device)
+        self.ws = alloc_workspace(self.grid, self.cells.capacity, device)
+        self.out = Out.alloc(self.n_own, device)
+        self.device = device
+
+    def run(self, xyzh: torch.Tensor, vm: torch.Tensor, n_ghost: int = 0, stats: Stats | None = None,
+            stream=None) -> Out:
+        sph_build_cells(self.grid, xyzh, vm, self.cells, self.ws, n_own=self.n_own, n_ghost=n_ghost, stream=stream)
+        sph_sort_cells(self.grid, self.cells, self.ws, stream=stream)
+        sph_density_all(self.grid, self.cells, self.out, self.ws, stats=stats, stream=stream)
+        return self.out
+
+    def check(self, stream=None) -> None:
+        check_status(self.ws, stream)
+
+
+def density(xyzh, vm, nc, box=1.0, gamma=GAMMA, stats: bool = False):
+    """One-shot helper: host or device float32 (N,4) arrays -> dict of numpy outputs."""
+    xyzh = torch.as_tensor(xyzh, dtype=torch.float32).cuda().contiguous()
+    vm = torch.as_tensor(vm, dtype=torch.float32).cuda().contiguous()
+    dp = DensityPass(nc, xyzh.shape[0], box, gamma)
+    st = Stats() if stats else None
+    out = dp.run(xyzh, vm, stats=st)
+    dp.check()
+    res = out.to_numpy()
+    if stats:
+        res["stats"] = st.read()
+    return res

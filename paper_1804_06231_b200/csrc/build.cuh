@@ -1,0 +1,252 @@
+// build.cuh -- sph_build_cells: cell binning as a counting sort.
+//
+//   k_bin          : validate, fp64 bin, atomic slot rank within the cell, cell_hmax
+//   k_scan_*       : exclusive scan of the per-cell counts -> cell_start
+//   k_scatter_perm : perm_tmp[cell_start[cell] + rank] = input index
+//   k_stable_*     : sort each cell's input indices ascending (the atomic ranks
+//                    arrive in any order) -> perm: in-cell order = input order
+//   k_gather       : xyzh, vm in cell order
+//
+// Stable in-cell order makes everything downstream deterministic and, with
+// slab ghosts received in the sender's cell order, identical across GPU
+// counts.  HBM traffic ~ 32 (read) + 12 (cell/rank/
+// count) + 12 (scatter) + 8 (stable) + 4+32+32 (gather) ~ 130 B/particle.
+#pragma once
+
+#include "common.cuh"
+
+namespace pvsph {
+
+__global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float4 *__restrict__ xyzh_in,
+                      const float4 *__restrict__ vm_in, int *__restrict__ cell_of, int *__restrict__ rank,
+                      int *__restrict__ count, float *__restrict__ cell_hmax, unsigned *status)
+{
+    double clmin = fmin(g.cl[0], fmin(g.cl[1], g.cl[2]));
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
+         p += (long long)gridDim.x * blockDim.x) {
+        float4 a = xyzh_in[p];
+        float4 b = vm_in[p];
+        int cell = -1;
+        bool finite = isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && isfinite(a.w) && isfinite(b.x) &&
+                      isfinite(b.y) && isfinite(b.z) && isfinite(b.w);
+        if (!finite) {
+            set_status(status, ST_EDOMAIN);
+        } else if (!(a.w > 0.0f) || !(b.w > 0.0f) || (double)g.gamma * (double)a.w > clmin) {
+            set_status(status, ST_EH_RANGE);
+        } else {
+            double x[3] = {a.x, a.y, a.z};
+            int ic[3];
+            bool inside = true;
+            for (int k = 0; k < 3; ++k) {
+                if (!(x[k] >= 0.0 && x[k] < g.box[k])) inside = false;
+                int c = (int)floor(x[k] * (double)g.nc[k] / g.box[k]);
+                ic[k] = c < 0 ? 0 : (c > g.nc[k] - 1 ? g.nc[k] - 1 : c);
+            }
+            int ixl = -1;
+            if (inside) {
+                if (p < n_own) {
+                    if (ic[0] >= g.x_lo && ic[0] < g.x_hi) ixl = ic[0] - g.x_lo + g.ghost_x;
+                } else if (g.ghost_x) {
+                    if (ic[0] == wrap_i(g.x_lo - 1, g.nc[0])) ixl = 0;
+                    else if (ic[0] == wrap_i(g.x_hi, g.nc[0])) ixl = g.nxl - 1;
+                }
+            }
+            if (ixl < 0) {
+                set_status(status, ST_EDOMAIN);
+            } else {
+                cell = (ixl * g.ny + ic[1]) * g.nz + ic[2];
+                rank[p] = atomicAdd(&count[cell], 1);
+                atomicMax(reinterpret_cast<int *>(&cell_hmax[cell]), __float_as_int(a.w));  // h > 0
+            }
+        }
+        cell_of[p] = cell;
+    }
+}
+
+// ---- three-phase exclusive scan of count[ncell] into start[ncell + 1] ------
+constexpr int SCAN_T = 1024;          // threads per block
+constexpr int SCAN_V = 4;             // values per thread
+constexpr int SCAN_TILE = SCAN_T * SCAN_V;
+
+__device__ __forceinline__ int block_exclusive_scan(int v, int *sh, int &total)
+{
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        sh[lane] = s;
+    }
+    __syncthreads();
+    int off = w ? sh[w - 1] : 0;
+    total = sh[(blockDim.x >> 5) - 1];
+    __syncthreads();
+    return off + x - v;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int *__restrict__ count, long long n,
+                                                        int *__restrict__ start, int *__restrict__ tile_sum,
+                                                        unsigned *status)
+{
+    __shared__ int sh[32];
+    long long base = (long long)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
+    int v[SCAN_V];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k) {
+        v[k] = base + k < n ? count[base + k] : 0;
+        if (v[k] > SPH_MAX_CELL) set_status(status, ST_ECAPACITY);
+        s += v[k];
+    }
+    int total;
+    int off = block_exclusive_scan(s, sh, total);
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k) {
+        if (base + k < n) start[base + k] = off;
+        off += v[k];
+    }
+    if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
+}
+
+// Single block: exclusive scan of the tile sums in place; writes start[n] = total.
+__global__ void __launch_bounds__(SCAN_T) k_scan_sums(int *__restrict__ tile_sum, long long ntiles,
+                                                       int *__restrict__ start, long long n)
+{
+    __shared__ int sh[32];
+    int carry = 0;
+    for (long long b = 0; b < ntiles; b += SCAN_T) {
+        long long i = b + threadIdx.x;
+        int v = i < ntiles ? tile_sum[i] : 0;
+        int total;
+        int e = block_exclusive_scan(v, sh, total);
+        if (i < ntiles) tile_sum[i] = carry + e;
+        carry += total;
+    }
+    if (threadIdx.x == 0) start[n] = carry;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_add(int *__restrict__ start, long long n,
+                                                      const int *__restrict__ tile_sum)
+{
+    int add = tile_sum[blockIdx.x];
+    long long base = (long long)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
+#pragma unroll
+    for (int k = 0; k < SCAN_V; ++k)
+        if (base + k < n) start[base + k] += add;
+}
+
+__global__ void k_scatter_perm(long long n_total, const int *__restrict__ cell_of, const int *__restrict__ rank,
+                               const int *__restrict__ start, int *__restrict__ perm_tmp)
+{
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
+         p += (long long)gridDim.x * blockDim.x) {
+        int c = cell_of[p];
+        if (c >= 0) perm_tmp[start[c] + rank[p]] = (int)p;
+    }
+}
+
+constexpr int STABLE_SMALL = 128;
+constexpr int STABLE_WARPS = 8;
+constexpr int STABLE_BIG_CHUNK = 256;
+constexpr int STABLE_BIG_TILE = 4096;
+
+// One warp per cell of <= STABLE_SMALL particles: rank each input index among the
+// cell's (all distinct) and place it.  Larger cells are queued as (cell, chunk).
+__global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
+                                                                    const int *__restrict__ perm_tmp,
+                                                                    int *__restrict__ perm, int2 *big_items,
+                                                                    int *big_count)
+{
+    __shared__ int sh[STABLE_WARPS][STABLE_SMALL];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int PER = STABLE_SMALL / 32;
+    for (long long cell = (long long)blockIdx.x * STABLE_WARPS + w; cell < ncell;
+         cell += (long long)gridDim.x * STABLE_WARPS) {
+        int s0 = start[cell];
+        int n = start[cell + 1] - s0;
+        if (n <= 1) {
+            if (n == 1 && lane == 0) perm[s0] = perm_tmp[s0];
+            continue;
+        }
+        if (n > STABLE_SMALL) {
+            if (lane == 0) {
+                int nch = (n + STABLE_BIG_CHUNK - 1) / STABLE_BIG_CHUNK;
+                int pos = atomicAdd(big_count, nch);
+                for (int k = 0; k < nch; ++k) big_items[pos + k] = make_int2((int)cell, k);
+            }
+            continue;
+        }
+        int v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            int e = lane + 32 * k;
+            v[k] = e < n ? perm_tmp[s0 + e] : 0;
+            if (e < n) sh[w][e] = v[k];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            int e = lane + 32 * k;
+            if (e < n) {
+                int r = 0;
+                for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
+                perm[s0 + r] = v[k];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__restrict__ start,
+                                                                  const int *__restrict__ perm_tmp,
+                                                                  int *__restrict__ perm, const int2 *big_items,
+                                                                  const int *big_count)
+{
+    __shared__ int tile[STABLE_BIG_TILE];
+    const int nitems = *big_count;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int2 item = big_items[it];
+        int s0 = start[item.x];
+        int n = start[item.x + 1] - s0;
+        int e = item.y * STABLE_BIG_CHUNK + threadIdx.x;
+        bool mine = e < n;
+        int v = mine ? perm_tmp[s0 + e] : 0;
+        int r = 0;
+        for (int t0 = 0; t0 < n; t0 += STABLE_BIG_TILE) {
+            int tn = min(STABLE_BIG_TILE, n - t0);
+            __syncthreads();
+            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = perm_tmp[s0 + t0 + m];
+            __syncthreads();
+            if (mine)
+                for (int m = 0; m < tn; ++m) r += tile[m] < v;
+        }
+        if (mine) perm[s0 + r] = v;
+        __syncthreads();
+    }
+}
+
+__global__ void k_gather(long long n_total, const int *__restrict__ start_end, const int *__restrict__ perm,
+                         const float4 *__restrict__ xyzh_in, const float4 *__restrict__ vm_in,
+                         float4 *__restrict__ xyzh_s, float4 *__restrict__ vm_s)
+{
+    const long long n_valid = *start_end;   // cell_start[ncell]: particles actually binned
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_valid && k < n_total;
+         k += (long long)gridDim.x * blockDim.x) {
+        int p = perm[k];
+        xyzh_s[k] = xyzh_in[p];
+        vm_s[k] = vm_in[p];
+    }
+}
+
+}  // namespace pvsph

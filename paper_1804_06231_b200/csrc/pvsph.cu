@@ -1,0 +1,357 @@
+// pvsph.cu -- C ABI of libpvsph.so (include/sph.h): argument checking,
+// workspace layout and kernel launches.  One translation unit (the kernels
+// live in the .cuh files) compiled for sm_100a only.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "build.cuh"
+#include "common.cuh"
+#include "density.cuh"
+#include "sort.cuh"
+
+using namespace pvsph;
+
+namespace {
+
+thread_local char g_cuda_msg[256] = "CUDA error";
+
+int cuda_fail(cudaError_t e)
+{
+    std::snprintf(g_cuda_msg, sizeof(g_cuda_msg), "CUDA error %d: %s", (int)e, cudaGetErrorString(e));
+    return SPH_ECUDA;
+}
+
+int check_launch()
+{
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SPH_OK : cuda_fail(e);
+}
+
+int make_grid(const sph_grid *gr, DevGrid &g)
+{
+    if (!gr) return SPH_EINVAL;
+    for (int k = 0; k < 3; ++k)
+        if (gr->nc[k] < 3 || !(gr->box[k] > 0.0) || !std::isfinite(gr->box[k])) return SPH_EINVAL;
+    if (gr->ghost_x != 0 && gr->ghost_x != 1) return SPH_EINVAL;
+    if (gr->x_lo < 0 || gr->x_hi > gr->nc[0] || gr->x_lo >= gr->x_hi) return SPH_EINVAL;
+    if (!gr->ghost_x && (gr->x_lo != 0 || gr->x_hi != gr->nc[0])) return SPH_EINVAL;
+    if (gr->ghost_x && gr->nc[0] - (gr->x_hi - gr->x_lo) == 1) return SPH_EINVAL;  // ghost planes coincide
+    if (!(gr->gamma > 0.0f) || !std::isfinite(gr->gamma)) return SPH_EINVAL;
+    std::memset(&g, 0, sizeof(g));
+    for (int k = 0; k < 3; ++k) {
+        g.nc[k] = gr->nc[k];
+        g.box[k] = gr->box[k];
+        g.boxf[k] = (float)gr->box[k];
+        g.cl[k] = gr->box[k] / gr->nc[k];
+    }
+    g.x_lo = gr->x_lo;
+    g.x_hi = gr->x_hi;
+    g.ghost_x = gr->ghost_x;
+    g.nxl = (gr->x_hi - gr->x_lo) + 2 * gr->ghost_x;
+    g.ny = gr->nc[1];
+    g.nz = gr->nc[2];
+    g.ncell = (long long)g.nxl * g.ny * g.nz;
+    g.n_owned_cells = (long long)(gr->x_hi - gr->x_lo) * g.ny * g.nz;
+    if (g.ncell >= (1LL << 31) - 1) return SPH_EINVAL;
+    g.gamma = gr->gamma;
+    double clmin = std::fmin(g.cl[0], std::fmin(g.cl[1], g.cl[2]));
+    g.delta = (float)(SPH_DELTA_FRAC * clmin);
+    for (int d = 0; d < SPH_NDIR; ++d) {
+        int nz = 0;
+        double q = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            int c = dir_component(d, a);
+            nz += c != 0;
+            q += (c != 0 ? 1.0 : 0.0) * g.cl[a];
+        }
+        g.q[d] = (float)(q / std::sqrt((double)nz));
+    }
+    return SPH_OK;
+}
+
+bool cells_ok(const sph_cells *c)
+{
+    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->pv && c->capacity >= 0 &&
+           c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
+           ((uintptr_t)c->pv % 8 == 0);
+}
+
+DevCells dev_cells(const sph_cells *c)
+{
+    DevCells d;
+    d.cap = c->capacity;
+    d.cell_start = c->cell_start;
+    d.xyzh = reinterpret_cast<const float4 *>(c->xyzh);
+    d.vm = reinterpret_cast<const float4 *>(c->vm);
+    d.perm = c->perm;
+    d.cell_hmax = c->cell_hmax;
+    d.pv = c->pv;
+    return d;
+}
+
+bool out_ok(const sph_out *o)
+{
+    return o && o->n_out >= 0 && o->rho && o->rho_dh && o->wcount && o->wcount_dh && o->div_v && o->curl_v &&
+           o->nngb;
+}
+
+DevOut dev_out(const sph_out *o)
+{
+    DevOut d;
+    d.n_out = o->n_out;
+    d.rho = o->rho;
+    d.rho_dh = o->rho_dh;
+    d.wcount = o->wcount;
+    d.wcount_dh = o->wcount_dh;
+    d.div_v = o->div_v;
+    d.curl_v = o->curl_v;
+    d.nngb = o->nngb;
+    return d;
+}
+
+// ---- workspace layout --------------------------------------------------------
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Ws {
+    size_t status, cell_of, rank, perm_tmp, count, tile_sum, big_count, big_items, total;
+};
+
+Ws ws_layout(long long ncell, long long n)
+{
+    Ws w;
+    size_t o = 0;
+    w.status = o;
+    o = align_up(o + 4, 256);
+    w.cell_of = o;
+    o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
+    w.rank = o;
+    o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
+    w.perm_tmp = o;
+    o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
+    w.count = o;
+    o = align_up(o + 4 * (size_t)(ncell + 1), 256);
+    long long ntiles = (ncell + SCAN_TILE - 1) / SCAN_TILE;
+    w.tile_sum = o;
+    o = align_up(o + 4 * (size_t)(ntiles + 1), 256);
+    w.big_count = o;
+    o = align_up(o + 4, 256);
+    w.big_items = o;
+    o = align_up(o + 8 * (size_t)(n / 64 + 64), 256);
+    w.total = o;
+    return w;
+}
+
+template <typename T>
+T *at(void *ws, size_t off)
+{
+    return reinterpret_cast<T *>(static_cast<char *>(ws) + off);
+}
+
+int grid_blocks(long long work, int per_block, int cap)
+{
+    long long b = (work + per_block - 1) / per_block;
+    if (b < 1) b = 1;
+    if (b > cap) b = cap;
+    return (int)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sph_abi_version(void) { return SPH_ABI_VERSION; }
+
+int64_t sph_ncell(const sph_grid *grid)
+{
+    DevGrid g;
+    if (make_grid(grid, g) != SPH_OK) return -1;
+    return g.ncell;
+}
+
+size_t sph_workspace_bytes(const sph_grid *grid, int64_t n_total)
+{
+    DevGrid g;
+    if (make_grid(grid, g) != SPH_OK || n_total < 0) return 0;
+    return ws_layout(g.ncell, n_total).total;
+}
+
+int sph_status_reset(void *ws, void *stream)
+{
+    if (!ws) return SPH_EINVAL;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 4, (cudaStream_t)stream);
+    return e == cudaSuccess ? SPH_OK : cuda_fail(e);
+}
+
+int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in, const float *vm_in,
+                    sph_cells *cells, void *ws, size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (n_own < 0 || n_ghost < 0 || !cells_ok(cells) || !ws) return SPH_EINVAL;
+    if (n_ghost > 0 && !g.ghost_x) return SPH_EINVAL;
+    long long n = n_own + n_ghost;
+    if (n > 0 && (!xyzh_in || !vm_in)) return SPH_EINVAL;
+    if (((uintptr_t)xyzh_in % 16) || ((uintptr_t)vm_in % 16)) return SPH_EINVAL;
+    if (n > cells->capacity) return SPH_ECAPACITY;
+    Ws w = ws_layout(g.ncell, cells->capacity);
+    if (ws_bytes < w.total) return SPH_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(at<unsigned>(ws, w.status), 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemsetAsync(at<int>(ws, w.count), 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemsetAsync(cells->cell_hmax, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
+    unsigned *status = at<unsigned>(ws, w.status);
+    int *cell_of = at<int>(ws, w.cell_of), *rank = at<int>(ws, w.rank), *count = at<int>(ws, w.count);
+    int *tile_sum = at<int>(ws, w.tile_sum);
+    const float4 *xin = reinterpret_cast<const float4 *>(xyzh_in);
+    const float4 *vin = reinterpret_cast<const float4 *>(vm_in);
+    if (n > 0) {
+        k_bin<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n_own, n, xin, vin, cell_of, rank, count,
+                                                            cells->cell_hmax, status);
+    }
+    long long ntiles = (g.ncell + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(count, g.ncell, cells->cell_start, tile_sum, status);
+    k_scan_sums<<<1, SCAN_T, 0, s>>>(tile_sum, ntiles, cells->cell_start, g.ncell);
+    k_scan_add<<<(int)ntiles, SCAN_T, 0, s>>>(cells->cell_start, g.ncell, tile_sum);
+    int *perm_tmp = at<int>(ws, w.perm_tmp);
+    int *big_count = at<int>(ws, w.big_count);
+    int2 *big_items = at<int2>(ws, w.big_items);
+    if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+    if (n > 0) {
+        k_scatter_perm<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cell_of, rank, cells->cell_start, perm_tmp);
+        k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
+            g.ncell, cells->cell_start, perm_tmp, cells->perm, big_items, big_count);
+        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, cells->perm, big_items,
+                                                          big_count);
+        k_gather<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cells->cell_start + g.ncell, cells->perm, xin, vin,
+                                                               reinterpret_cast<float4 *>(cells->xyzh),
+                                                               reinterpret_cast<float4 *>(cells->vm));
+    }
+    cells->n = n;
+    return check_launch();
+}
+
+int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end, void *ws,
+                   size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !ws) return SPH_EINVAL;
+    if (cell_end < 0) cell_end = g.ncell;
+    if (cell_begin < 0 || cell_begin > cell_end || cell_end > g.ncell) return SPH_EINVAL;
+    Ws w = ws_layout(g.ncell, cells->capacity);
+    if (ws_bytes < w.total) return SPH_EINVAL;
+    if (cell_end == cell_begin) return SPH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    int *big_count = at<int>(ws, w.big_count);
+    int2 *big_items = at<int2>(ws, w.big_items);
+    if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+    DevCells c = dev_cells(cells);
+    k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
+        g, c, cells->pv, cell_begin, cell_end, big_items, big_count);
+    k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->pv, big_items, big_count);
+    return check_launch();
+}
+
+int sph_density_self(const sph_grid *grid, const sph_cells *cells, const int32_t *cell_list, int64_t ncells_list,
+                     sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !out_ok(acc) || !ws || ncells_list < 0 || (ncells_list > 0 && !cell_list)) return SPH_EINVAL;
+    if (ws_bytes < 4) return SPH_EINVAL;
+    if (ncells_list == 0) return SPH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *status = at<unsigned>(ws, 0);
+    int blocks = grid_blocks(ncells_list, API_WARPS, 1 << 30);
+    if (stats)
+        k_density_self<true><<<blocks, API_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(acc), cell_list,
+                                                               ncells_list, stats, status);
+    else
+        k_density_self<false><<<blocks, API_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(acc), cell_list,
+                                                                ncells_list, nullptr, status);
+    return check_launch();
+}
+
+int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t *pairs, int64_t npairs, sph_out *acc,
+                     sph_stats *stats, void *ws, size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !out_ok(acc) || !ws || npairs < 0 || (npairs > 0 && !pairs)) return SPH_EINVAL;
+    if (((uintptr_t)pairs % 8) || ws_bytes < 4) return SPH_EINVAL;
+    if (npairs == 0) return SPH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *status = at<unsigned>(ws, 0);
+    int blocks = grid_blocks(npairs, 1, 1 << 30);
+    const int2 *pr = reinterpret_cast<const int2 *>(pairs);
+    if (stats)
+        k_density_pair<true><<<blocks, API_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(acc), pr, npairs, stats,
+                                                               status);
+    else
+        k_density_pair<false><<<blocks, API_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(acc), pr, npairs,
+                                                                nullptr, status);
+    return check_launch();
+}
+
+int sph_density_finalize(sph_out *acc, int64_t n, void *stream)
+{
+    if (!out_ok(acc) || n < 0 || n > acc->n_out) return SPH_EINVAL;
+    if (n == 0) return SPH_OK;
+    k_finalize<<<grid_blocks(n, 256, 148 * 32), 256, 0, (cudaStream_t)stream>>>(dev_out(acc), n);
+    return check_launch();
+}
+
+int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, sph_stats *stats, void *ws,
+                    size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !out_ok(out) || !ws || ws_bytes < 4) return SPH_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    int blocks = grid_blocks(g.n_owned_cells, V1_WARPS, 1 << 30);
+    if (stats)
+        k_density_all_v1<true><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
+    else
+        k_density_all_v1<false><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
+    return check_launch();
+}
+
+int sph_status(void *ws, void *stream)
+{
+    if (!ws) return SPH_EINVAL;
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+    unsigned st = 0;
+    e = cudaMemcpy(&st, ws, 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (st & ST_EINVAL) return SPH_EINVAL;
+    if (st & ST_EDOMAIN) return SPH_EDOMAIN;
+    if (st & ST_EH_RANGE) return SPH_EH_RANGE;
+    if (st & ST_ECAPACITY) return SPH_ECAPACITY;
+    return SPH_OK;
+}
+
+const char *sph_strerror(int code)
+{
+    switch (code) {
+    case SPH_OK: return "ok";
+    case SPH_EINVAL: return "invalid argument (null pointer, bad size or grid, workspace too small, bad cell list)";
+    case SPH_EH_RANGE: return "smoothing length or mass out of range (h <= 0, m <= 0 or gamma*h > cell edge)";
+    case SPH_ECAPACITY: return "capacity exceeded (cell occupancy > SPH_MAX_CELL or particle arrays too small)";
+    case SPH_EDOMAIN: return "position not finite or outside the box / the rank's slab";
+    case SPH_ECUDA: return g_cuda_msg;
+    default: return "unknown error";
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,153 @@
+// sort.cuh -- sph_sort_cells: per-cell sorted projections along the 13
+// directions ("projecting the particle positions ... sorted with respect
+// to their position along this axis"; "13 distinct directions").
+//
+// Key of particle k in cell c along d: fp32( (x_k - corner_c) . d/|d| ),
+// the difference and dot product in fp64.  Order: ascending
+// key, ties by input index perm[k] -- deterministic whatever the slot order.
+//
+// Small cells (n <= SORT_SMALL): one warp per cell, composite 64-bit keys
+// (orderable key << 32 | input index) staged in shared memory, rank by
+// counting.  Larger cells are queued as (cell, chunk) items and ranked by
+// k_sort_big, one CTA per chunk of SORT_BIG_CHUNK elements, streaming the
+// cell's composites through shared-memory tiles.
+#pragma once
+
+#include "common.cuh"
+
+namespace pvsph {
+
+constexpr int SORT_SMALL = 128;
+constexpr int SORT_WARPS = 8;
+constexpr int SORT_BIG_CHUNK = 256;
+constexpr int SORT_BIG_TILE = 2048;
+
+__device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, double corner[3])
+{
+    long long plane = (long long)g.ny * g.nz;
+    int ixl = (int)(cell / plane);
+    int iy = (int)((cell / g.nz) % g.ny);
+    int iz = (int)(cell % g.nz);
+    int ixg = wrap_i(ixl - g.ghost_x + g.x_lo, g.nc[0]);
+    corner[0] = (double)ixg * g.cl[0];
+    corner[1] = (double)iy * g.cl[1];
+    corner[2] = (double)iz * g.cl[2];
+}
+
+__global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCells c, sph_pv_entry *pv,
+                                                                 long long cbeg, long long cend, int2 *big_items,
+                                                                 int *big_count)
+{
+    __shared__ unsigned long long sh[SORT_WARPS][SORT_SMALL];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int PER = SORT_SMALL / 32;
+    for (long long cell = cbeg + (long long)blockIdx.x * SORT_WARPS + w; cell < cend;
+         cell += (long long)gridDim.x * SORT_WARPS) {
+        int s0 = c.cell_start[cell];
+        int n = c.cell_start[cell + 1] - s0;
+        if (n == 0) continue;
+        if (n > SORT_SMALL) {
+            if (lane == 0) {
+                int nch = (n + SORT_BIG_CHUNK - 1) / SORT_BIG_CHUNK;
+                int pos = atomicAdd(big_count, nch);
+                for (int k = 0; k < nch; ++k) big_items[pos + k] = make_int2((int)cell, k);
+            }
+            continue;
+        }
+        double corner[3];
+        cell_corner(g, cell, corner);
+        double u[PER][3];
+        unsigned tie[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            int e = lane + 32 * k;
+            if (e < n) {
+                float4 p = c.xyzh[s0 + e];
+                u[k][0] = (double)p.x - corner[0];
+                u[k][1] = (double)p.y - corner[1];
+                u[k][2] = (double)p.z - corner[2];
+                tie[k] = (unsigned)c.perm[s0 + e];
+            }
+        }
+        for (int d = 0; d < SPH_NDIR; ++d) {
+            float key[PER];
+            unsigned long long comp[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                int e = lane + 32 * k;
+                if (e < n) {
+                    key[k] = pv_key(u[k][0], u[k][1], u[k][2], d);
+                    comp[k] = ((unsigned long long)float_order(key[k]) << 32) | tie[k];
+                    sh[w][e] = comp[k];
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                int e = lane + 32 * k;
+                if (e < n) {
+                    int r = 0;
+                    for (int m = 0; m < n; ++m) r += sh[w][m] < comp[k];
+                    sph_pv_entry ent;
+                    ent.key = key[k];
+                    ent.j = s0 + e;
+                    pv[(long long)d * c.cap + s0 + r] = ent;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// One CTA per (cell, chunk) item; grid-strides over the queued items.
+__global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells c, sph_pv_entry *pv,
+                                                              const int2 *big_items, const int *big_count)
+{
+    __shared__ unsigned long long tile[SORT_BIG_TILE];
+    const int nitems = *big_count;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int2 item = big_items[it];
+        long long cell = item.x;
+        int s0 = c.cell_start[cell];
+        int n = c.cell_start[cell + 1] - s0;
+        double corner[3];
+        cell_corner(g, cell, corner);
+        int e = item.y * SORT_BIG_CHUNK + threadIdx.x;
+        bool mine = e < n;
+        double u0 = 0, u1 = 0, u2 = 0;
+        unsigned tie = 0;
+        if (mine) {
+            float4 p = c.xyzh[s0 + e];
+            u0 = (double)p.x - corner[0];
+            u1 = (double)p.y - corner[1];
+            u2 = (double)p.z - corner[2];
+            tie = (unsigned)c.perm[s0 + e];
+        }
+        for (int d = 0; d < SPH_NDIR; ++d) {
+            float key = mine ? pv_key(u0, u1, u2, d) : 0.0f;
+            unsigned long long comp = ((unsigned long long)float_order(key) << 32) | tie;
+            int r = 0;
+            for (int t0 = 0; t0 < n; t0 += SORT_BIG_TILE) {
+                int tn = min(SORT_BIG_TILE, n - t0);
+                __syncthreads();
+                for (int m = threadIdx.x; m < tn; m += blockDim.x) {
+                    float4 p = c.xyzh[s0 + t0 + m];
+                    float km = pv_key((double)p.x - corner[0], (double)p.y - corner[1], (double)p.z - corner[2], d);
+                    tile[m] = ((unsigned long long)float_order(km) << 32) | (unsigned)c.perm[s0 + t0 + m];
+                }
+                __syncthreads();
+                if (mine)
+                    for (int m = 0; m < tn; ++m) r += tile[m] < comp;
+            }
+            if (mine) {
+                sph_pv_entry ent;
+                ent.key = key;
+                ent.j = s0 + e;
+                pv[(long long)d * c.cap + s0 + r] = ent;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace pvsph

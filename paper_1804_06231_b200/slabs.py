@@ -1,0 +1,278 @@
+"""x-slab domain decomposition over GPUs with a one-cell ghost layer.
+
+Rank r owns the cell planes [x_lo, x_hi) = [r nc/p, (r+1) nc/p) and the
+particles inside them, in global input order.  Every step:
+
+  1. bin the owned particles (sph_build_cells without ghosts); cells are
+     x-major, so the boundary planes x_lo and x_hi-1 are contiguous slices of
+     the cell-sorted arrays;
+  2. NCCL send/recv (torch.distributed P2P) of those planes to the left and
+     right neighbours (periodic ring) -- counts first, then the particles --
+     straight into the input buffer behind the owned particles;
+  3. sph_build_cells over owned + ghost particles (ghost planes x_lo-1, x_hi),
+     sph_sort_cells, sph_density_all.
+
+The gather design needs no reverse exchange (ghosts are only j-sources).  With
+stable in-cell order (input order) and ghosts received in the sender's cell
+order, every particle sees the same neighbours in the same order as on one
+GPU, so the outputs are bitwise identical for any p (tests/test_gpu_slabs.py).
+
+PyTorch is plumbing here: device buffers, the stream, and the process group.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import api as pv
+
+BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_perm, k_stable_small/big, k_gather
+SORT_LAUNCHES = 2       # k_sort_small, k_sort_big
+DENSITY_LAUNCHES = 1    # k_density_all
+
+
+def slab_bounds(nc: int, world: int, rank: int) -> tuple[int, int]:
+    return rank * nc // world, (rank + 1) * nc // world
+
+
+def planes_of(xyzh: np.ndarray, nc: int, box: float = 1.0) -> np.ndarray:
+    """Cell x-plane of every particle: floor(x nc / box) in fp64, clamped (same rule as sph_build_cells)."""
+    return np.clip(np.floor(xyzh[:, 0].astype(np.float64) * nc / box), 0, nc - 1).astype(np.int64)
+
+
+@dataclass
+class Slab:
+    nc: int
+    box: float
+    gamma: float
+    rank: int
+    world: int
+    x_lo: int
+    x_hi: int
+    xyzh: np.ndarray          # owned particles, global order
+    vm: np.ndarray
+    gid: np.ndarray           # their global indices
+    n_global: int
+    pset: object = None       # the full ParticleSet (single-GPU only)
+
+    @staticmethod
+    def single(p) -> "Slab":
+        return Slab(p.nc, p.box, p.gamma, 0, 1, 0, p.nc, p.xyzh, p.vm, np.arange(p.n), p.n, p)
+
+    @staticmethod
+    def from_set(p, rank: int, world: int) -> "Slab":
+        if world == 1:
+            return Slab.single(p)
+        if p.nc // world < 2:
+            raise ValueError("each slab needs >= 2 cell planes")
+        lo, hi = slab_bounds(p.nc, world, rank)
+        pl = planes_of(p.xyzh, p.nc, p.box)
+        gid = np.nonzero((pl >= lo) & (pl < hi))[0]
+        return Slab(p.nc, p.box, p.gamma, rank, world, lo, hi, np.ascontiguousarray(p.xyzh[gid]),
+                    np.ascontiguousarray(p.vm[gid]), gid, p.n)
+
+    @staticmethod
+    def from_config(cfg: str, rank: int, world: int) -> "Slab":
+        import synth
+        return Slab.from_set(synth.make(cfg), rank, world)
+
+    @property
+    def n_own(self) -> int:
+        return int(self.xyzh.shape[0])
+
+
+def exchange_planes(dist, rank: int, world: int, send_lo, send_hi, recv) -> tuple[int, int]:
+    """Periodic-ring ghost exchange (NCCL P2P via torch.distributed, or gloo on CPU in tests).
+
+    send_lo = (xyzh, vm) of this rank's plane x_lo  -> goes to the left neighbour
+    send_hi = (xyzh, vm) of this rank's plane x_hi-1 -> goes to the right neighbour
+    recv    = (xyzh_buf, vm_buf): the left neighbour's plane x_hi-1 (our ghost plane
+              x_lo-1) is written at [0, n_glo), the right neighbour's plane x_lo (our
+              ghost plane x_hi) at [n_glo, n_glo + n_ghi).  Returns (n_glo, n_ghi).
+    Counts travel first so the receives have exact sizes.  With p = 2 both
+    neighbours are the same rank; NCCL matches same-peer messages in issue order,
+    so every rank issues sends [to right, to left] and receives [from left, from right]."""
+    left, right = (rank - 1) % world, (rank + 1) % world
+    dev = send_lo[0].device
+    cnt_send = torch.tensor([send_hi[0].shape[0], send_lo[0].shape[0]], dtype=torch.int64, device=dev)
+    cnt_recv = torch.zeros(2, dtype=torch.int64, device=dev)
+    ops = [dist.P2POp(dist.isend, cnt_send[0:1], right), dist.P2POp(dist.isend, cnt_send[1:2], left),
+           dist.P2POp(dist.irecv, cnt_recv[0:1], left), dist.P2POp(dist.irecv, cnt_recv[1:2], right)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    n_glo, n_ghi = (int(v) for v in cnt_recv.tolist())
+    xb, vb = recv
+    if n_glo + n_ghi > xb.shape[0]:
+        raise RuntimeError(f"ghost capacity {xb.shape[0]} < {n_glo + n_ghi}")
+    ops = []
+    if send_hi[0].shape[0]:
+        ops += [dist.P2POp(dist.isend, send_hi[0], right), dist.P2POp(dist.isend, send_hi[1], right)]
+    if send_lo[0].shape[0]:
+        ops += [dist.P2POp(dist.isend, send_lo[0], left), dist.P2POp(dist.isend, send_lo[1], left)]
+    if n_glo:
+        ops += [dist.P2POp(dist.irecv, xb[0:n_glo], left), dist.P2POp(dist.irecv, vb[0:n_glo], left)]
+    if n_ghi:
+        ops += [dist.P2POp(dist.irecv, xb[n_glo:n_glo + n_ghi], right),
+                dist.P2POp(dist.irecv, vb[n_glo:n_glo + n_ghi], right)]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return n_glo, n_ghi
+
+
+class SlabRunner:
+    """Device buffers and one density step of one rank."""
+
+    def __init__(self, slab: Slab, dist=None, device="cuda", ghost_capacity: int | None = None):
+        self.slab = slab
+        self.dist = dist
+        self.world = slab.world
+        self.rank = slab.rank
+        self.n_own = slab.n_own
+        self.nc = slab.nc
+        self.n_global = slab.n_global
+        self.pset = slab.pset
+        ghost = self.world > 1
+        self.grid = pv.make_grid(slab.nc, slab.box, slab.gamma, slab.x_lo, slab.x_hi, int(ghost))
+        if ghost:
+            per_plane = self.n_own / max(1, slab.x_hi - slab.x_lo)
+            gcap = ghost_capacity if ghost_capacity is not None else int(2 * 1.5 * per_plane + 4096)
+        else:
+            gcap = 0
+        self.cap = self.n_own + gcap
+        self.xin = torch.zeros((max(self.cap, 1), 4), dtype=torch.float32, device=device)
+        self.vin = torch.zeros((max(self.cap, 1), 4), dtype=torch.float32, device=device)
+        self.cells = pv.Cells.alloc(self.grid, self.cap, device)
+        self.ws = pv.alloc_workspace(self.grid, self.cells.capacity, device)
+        self.out = pv.Out.alloc(self.n_own, device)
+        self.n_ghost = 0
+        self.plane = self.grid.nc[1] * self.grid.nc[2]   # cells per x plane
+        self.nxl = (slab.x_hi - slab.x_lo) + (2 if ghost else 0)
+        self.launches_per_step = BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES + (BUILD_LAUNCHES if ghost else 0)
+        self.device = device
+
+    # -- data ---------------------------------------------------------------
+    def upload(self) -> None:
+        if self.n_own:
+            self.xin[:self.n_own].copy_(torch.from_numpy(self.slab.xyzh))
+            self.vin[:self.n_own].copy_(torch.from_numpy(self.slab.vm))
+
+    # -- ghost exchange -----------------------------------------------------
+    def boundary_slices(self):
+        """Bin the owned particles and return the slot ranges of planes x_lo and x_hi-1."""
+        pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own, n_ghost=0)
+        P = self.plane
+        idx = torch.tensor([P, 2 * P, (self.nxl - 2) * P, (self.nxl - 1) * P], device=self.device)
+        lo_a, lo_b, hi_a, hi_b = self.cells.cell_start[idx].tolist()
+        return (lo_a, lo_b), (hi_a, hi_b)
+
+    def exchange(self) -> None:
+        (lo_a, lo_b), (hi_a, hi_b) = self.boundary_slices()
+        xs, vs = self.cells.xyzh, self.cells.vm
+        free = (self.xin[self.n_own:], self.vin[self.n_own:])
+        n_glo, n_ghi = exchange_planes(self.dist, self.rank, self.world, (xs[lo_a:lo_b], vs[lo_a:lo_b]),
+                                       (xs[hi_a:hi_b], vs[hi_a:hi_b]), free)
+        self.n_ghost = n_glo + n_ghi
+
+    # -- one step -----------------------------------------------------------
+    def step(self, stats=None, events=None) -> None:
+        s = torch.cuda.current_stream()
+        rec = (lambda k: events[k].record(s)) if events else (lambda k: None)
+        rec(0)
+        if self.world > 1:
+            self.exchange()
+        rec(1)
+        pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own,
+                           n_ghost=self.n_ghost)
+        rec(2)
+        pv.sph_sort_cells(self.grid, self.cells, self.ws)
+        rec(3)
+        pv.sph_density_all(self.grid, self.cells, self.out, self.ws, stats=stats)
+        rec(4)
+
+    def check(self) -> None:
+        pv.check_status(self.ws)
+
+    # -- end to end through host buffers -----------------------------------
+    def e2e_time(self, steps: int = 3, warmup: int = 1):
+        """ms per step with the H2D copy of the owned inputs (pinned) and the D2H copy of all
+        outputs inside the timed region; returns (ms, h2d_bytes, d2h_bytes)."""
+        n = self.n_own
+        hx = torch.from_numpy(self.slab.xyzh).pin_memory()
+        hv = torch.from_numpy(self.slab.vm).pin_memory()
+        o = self.out
+        outs = [o.rho, o.rho_dh, o.wcount, o.wcount_dh, o.div_v, o.curl_v, o.nngb]
+        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+
+        def one():
+            self.xin[:n].copy_(hx, non_blocking=True)
+            self.vin[:n].copy_(hv, non_blocking=True)
+            self.step()
+            for h, t in zip(host, outs):
+                h.copy_(t, non_blocking=True)
+
+        for _ in range(warmup):
+            one()
+        torch.cuda.synchronize()
+        if self.dist:
+            self.dist.barrier()
+        s = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(steps):
+            one()
+        e1.record(s)
+        torch.cuda.synchronize()
+        h2d = 2 * n * 16
+        d2h = sum(t.numel() * t.element_size() for t in outs)
+        return e0.elapsed_time(e1) / steps, h2d, d2h
+
+
+class FakeRanks:
+    """p slab ranks emulated in ONE process on one GPU, the ghost exchange done with
+    device copies instead of NCCL (a test harness for the slab logic; nothing waits
+    on another rank, every launch is ordered on one stream)."""
+
+    def __init__(self, p, world: int, device="cuda"):
+        self.world = world
+        self.runners = [SlabRunner(Slab.from_set(p, r, world), dist=None, device=device) for r in range(world)]
+        for r in self.runners:
+            r.upload()
+        self.n_global = p.n
+
+    def step(self) -> None:
+        sl = [r.boundary_slices() for r in self.runners]
+        planes = []
+        for r, ((lo_a, lo_b), (hi_a, hi_b)) in zip(self.runners, sl):
+            planes.append(((r.cells.xyzh[lo_a:lo_b].clone(), r.cells.vm[lo_a:lo_b].clone()),
+                           (r.cells.xyzh[hi_a:hi_b].clone(), r.cells.vm[hi_a:hi_b].clone())))
+        W = self.world
+        for k, r in enumerate(self.runners):
+            gx_lo, gv_lo = planes[(k - 1) % W][1]      # left neighbour's plane x_hi-1
+            gx_hi, gv_hi = planes[(k + 1) % W][0]      # right neighbour's plane x_lo
+            a, b = r.n_own, r.n_own + gx_lo.shape[0]
+            c = b + gx_hi.shape[0]
+            r.xin[a:b].copy_(gx_lo)
+            r.vin[a:b].copy_(gv_lo)
+            r.xin[b:c].copy_(gx_hi)
+            r.vin[b:c].copy_(gv_hi)
+            r.n_ghost = c - r.n_own
+        for r in self.runners:
+            pv.sph_build_cells(r.grid, r.xin, r.vin, r.cells, r.ws, n_own=r.n_own, n_ghost=r.n_ghost)
+            pv.sph_sort_cells(r.grid, r.cells, r.ws)
+            pv.sph_density_all(r.grid, r.cells, r.out, r.ws)
+        for r in self.runners:
+            r.check()
+
+    def gather(self) -> dict:
+        res = {}
+        for r in self.runners:
+            o = r.out.to_numpy()
+            for k, v in o.items():
+                if k not in res:
+                    res[k] = np.zeros(self.n_global, v.dtype)
+                res[k][r.slab.gid] = v
+        return res

@@ -1,0 +1,353 @@
+"""GPU parity: the CUDA path through the C ABI against the fp64 oracle.
+
+All tests need a B200 (marker gpu).  Inputs are the seeded synth sets; every
+expected value comes from oracle/ (or the cited golden files)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._compare import compare
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def pv():
+    import paper_1804_06231_b200 as pv
+    assert torch.cuda.is_available()
+    pv.load()
+    return pv
+
+
+def run(pv, xyzh, vm, nc, stats=False, box=1.0):
+    return pv.density(xyzh, vm, nc, box=box, stats=stats)
+
+
+# ---------------------------------------------------------------------------
+# build_cells / sort_cells
+# ---------------------------------------------------------------------------
+def _built(pv, p):
+    xyzh = torch.from_numpy(p.xyzh).cuda()
+    vm = torch.from_numpy(p.vm).cuda()
+    dp = pv.DensityPass(p.nc, p.n)
+    pv.sph_build_cells(dp.grid, xyzh, vm, dp.cells, dp.ws)
+    pv.sph_sort_cells(dp.grid, dp.cells, dp.ws)
+    dp.check()
+    return dp
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_build_cells_matches_oracle_binning(pv, cfg):
+    p = synth.make(cfg)
+    dp = _built(pv, p)
+    cell, order, start = oracle.bin_cells(p.xyzh, p.nc)
+    cs = dp.cells.cell_start.cpu().numpy().astype(np.int64)
+    assert np.array_equal(cs, start)
+    perm = dp.cells.perm[:p.n].cpu().numpy()
+    assert np.array_equal(perm, order)           # stable: input order inside each cell
+    xs = dp.cells.xyzh[:p.n].cpu().numpy()
+    assert np.array_equal(xs, p.xyzh[perm])
+    assert np.array_equal(dp.cells.vm[:p.n].cpu().numpy(), p.vm[perm])
+    hmax = dp.cells.cell_hmax.cpu().numpy()
+    exp = np.zeros(p.nc ** 3, np.float32)
+    np.maximum.at(exp, cell, p.xyzh[:, 3])
+    assert np.array_equal(hmax, exp)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_sort_cells_orders_keys(pv, cfg):
+    p = synth.make(cfg)
+    dp = _built(pv, p)
+    cs = dp.cells.cell_start.cpu().numpy().astype(np.int64)
+    perm = dp.cells.perm[:p.n].cpu().numpy()
+    keys = dp.cells.pv_keys()[:, :p.n].cpu().numpy()
+    slots = dp.cells.pv_slots()[:, :p.n].cpu().numpy()
+    ref = oracle.cell_keys(p.xyzh, p.nc)            # [13, N] fp64, input order
+    Cl = 1.0 / p.nc
+    for d in range(13):
+        for c in range(p.nc ** 3):
+            a, b = cs[c], cs[c + 1]
+            sl = slots[d, a:b]
+            assert np.array_equal(np.sort(sl), np.arange(a, b))          # a permutation of the cell
+            k = keys[d, a:b]
+            tie = perm[sl]
+            order = np.lexsort((tie, k))
+            assert np.array_equal(order, np.arange(b - a))               # ascending key, ties by input index
+            assert np.all(np.abs(k.astype(np.float64) - ref[d, perm[sl]]) <= 1e-6 * Cl)
+
+
+# ---------------------------------------------------------------------------
+# density_all vs the oracle
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_density_all_vs_bruteforce(pv, cfg):
+    p = synth.make(cfg)
+    got = run(pv, p.xyzh, p.vm, p.nc, stats=True)
+    if cfg == "c1":
+        ref = oracle.bruteforce(p.xyzh, p.vm)
+        idx = None
+    else:
+        idx = np.random.default_rng(0).choice(p.n, 4000, replace=False)
+        ref = oracle.bruteforce(p.xyzh, p.vm, targets=idx)
+    compare(got, ref, idx, cfg)
+    if idx is None:
+        assert sum(got["stats"]["hits"]) == int(ref["nngb"].sum()) - 0  # hits == interactions
+    assert sum(got["stats"]["hits"]) == int(got["nngb"].astype(np.int64).sum())
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_density_all_vs_celllist_full(pv, cfg):
+    p = synth.make(cfg)
+    got = run(pv, p.xyzh, p.vm, p.nc)
+    compare(got, oracle.celllist(p.xyzh, p.vm, p.nc), None, cfg)
+
+
+def test_density_all_c3_vs_celllist(pv):
+    p = synth.make("c3")
+    got = run(pv, p.xyzh, p.vm, p.nc)
+    rng = np.random.default_rng(1)
+    idx = np.sort(rng.choice(p.n, 200_000, replace=False))
+    compare(got, oracle.celllist(p.xyzh, p.vm, p.nc, targets=idx), idx, "c3")
+
+
+def test_candidate_counters_match_pv_counts(pv):
+    """COUNT counters: hits per kind equal the oracle's in-range counts exactly (outside the band);
+    candidates per kind equal Code 2 counts of oracle_pv_counts to 1e-5 (window-edge rounding)."""
+    p = synth.make("c1")
+    got = run(pv, p.xyzh, p.vm, p.nc, stats=True)
+    c, unsafe = oracle.pv_counts(p.xyzh, p.nc)
+    assert unsafe == 0
+    ref = oracle.bruteforce(p.xyzh, p.vm)
+    band = int(ref["band"].sum())
+    tot = c.sum(0)
+    for k in range(4):
+        assert abs(got["stats"]["hits"][k] - tot[k, 2]) <= band
+        assert abs(got["stats"]["cand"][k] - tot[k, 1]) <= max(2, 1e-5 * tot[k, 1])
+
+
+def test_worked_example(pv):
+    g = json.load(open(os.path.join(GOLDEN, "worked_example_4p.json")))
+    xyzh = np.array(g["xyzh"], np.float32)
+    vm = np.array(g["vm"], np.float32)
+    ref = oracle.bruteforce(xyzh, vm)
+    for nc in (3, 8, 16):
+        for shift in (0.0, g["translation_x"]):
+            x = xyzh.copy()
+            x[:, 0] = np.mod(x[:, 0].astype(np.float64) + shift, 1.0)
+            got = run(pv, x, vm, nc)
+            compare(got, ref, None, f"worked nc={nc} shift={shift}")
+            for f in ("rho", "wcount"):
+                e = np.array(g["expected"][f])
+                assert np.all(np.abs(got[f] - e) <= 1e-5 * e)
+            assert list(got["nngb"]) == g["expected"]["nngb"]
+
+
+def test_self_plus_pairs_equals_all(pv):
+    """sph_density_self over every cell + sph_density_pair over all 26 ordered pairs
+    (+ finalize) reproduces sph_density_all within tolerance (P:167 symmetric = 2 one-sided)."""
+    p = synth.make("c1")
+    xyzh = torch.from_numpy(p.xyzh).cuda()
+    vm = torch.from_numpy(p.vm).cuda()
+    dp = pv.DensityPass(p.nc, p.n)
+    dp.run(xyzh, vm)
+    ref_all = dp.out.to_numpy()
+    nc = p.nc
+    cells = np.arange(nc ** 3, dtype=np.int32)
+    ix, iy, iz = cells // (nc * nc), (cells // nc) % nc, cells % nc
+    pairs = []
+    for ox in (-1, 0, 1):
+        for oy in (-1, 0, 1):
+            for oz in (-1, 0, 1):
+                if ox == oy == oz == 0:
+                    continue
+                cj = (((ix + ox) % nc) * nc + (iy + oy) % nc) * nc + (iz + oz) % nc
+                pairs.append(np.stack([cells, cj], 1))
+    pairs = torch.from_numpy(np.concatenate(pairs).astype(np.int32)).cuda().contiguous()
+    acc = pv.Out.alloc(p.n, zero=True)
+    st = pv.Stats()
+    pv.sph_density_self(dp.grid, dp.cells, torch.from_numpy(cells).cuda(), acc, dp.ws, stats=st)
+    pv.sph_density_pair(dp.grid, dp.cells, pairs, acc, dp.ws, stats=st)
+    pv.sph_density_finalize(acc)
+    dp.check()
+    got = acc.to_numpy()
+    ref = oracle.bruteforce(p.xyzh, p.vm)
+    compare(got, ref, None, "self+pair")
+    assert np.array_equal(got["nngb"], ref_all["nngb"])
+    assert sum(st.read()["hits"]) == int(got["nngb"].astype(np.int64).sum())
+
+
+def test_pair_rejects_non_neighbours(pv):
+    p = synth.make("c1")
+    dp = _built(pv, p)
+    acc = pv.Out.alloc(p.n, zero=True)
+    bad = torch.tensor([[0, 2 * 25 + 2 * 5 + 2]], dtype=torch.int32).cuda()   # offset (2,2,2)
+    pv.sph_density_pair(dp.grid, dp.cells, bad, acc, dp.ws)
+    assert pv.sph_status(dp.ws) == 1
+
+
+# ---------------------------------------------------------------------------
+# determinism, invariances
+# ---------------------------------------------------------------------------
+def test_bitwise_deterministic(pv):
+    p = synth.make("c2")
+    a = run(pv, p.xyzh, p.vm, p.nc)
+    b = run(pv, p.xyzh, p.vm, p.nc)
+    for f in a:
+        assert np.array_equal(a[f], b[f]), f
+
+
+def test_translation_invariance(pv):
+    p = synth.make("c1")
+    q = p.xyzh.copy()
+    q[:, :3] = np.mod(q[:, :3].astype(np.float64) + 0.5, 1.0)
+    ref = oracle.bruteforce(p.xyzh, p.vm)
+    compare(run(pv, q, p.vm, p.nc), ref, None, "translated")
+
+
+def test_permutation_invariance(pv):
+    p = synth.make("c1")
+    perm = np.random.default_rng(9).permutation(p.n)
+    a = run(pv, p.xyzh, p.vm, p.nc)
+    b = run(pv, p.xyzh[perm], p.vm[perm], p.nc)
+    ref = oracle.bruteforce(p.xyzh, p.vm)
+    compare({k: v[perm] for k, v in a.items()}, {k: v[perm] for k, v in ref.items()}, None, "perm-a")
+    compare(b, {k: v[perm] for k, v in ref.items()}, None, "perm-b")
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+def test_single_and_two_particles(pv):
+    xyzh = np.array([[0.3, 0.6, 0.9, 0.1]], np.float32)
+    vm = np.array([[0.4, -1.0, 2.0, 0.25]], np.float32)
+    compare(run(pv, xyzh, vm, 3), oracle.bruteforce(xyzh, vm), None, "N=1")
+    xyzh = np.array([[0.5, 0.5, 0.5, 0.1], [0.55, 0.52, 0.49, 0.08]], np.float32)
+    vm = np.array([[0.4, -1.0, 2.0, 0.25], [0.1, 0.2, 0.3, 0.5]], np.float32)
+    compare(run(pv, xyzh, vm, 3), oracle.bruteforce(xyzh, vm), None, "N=2")
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_tiny_random_sets(pv, seed):
+    """Empty cells, faces, x = 0 and 1 - 2^-24, coincident particles, nc = 3..5, wrapped pairs."""
+    nc = 3 + seed % 3
+    p = synth.tiny_random_set(seed, 50 + 41 * seed, nc, h_frac=1.0, h_jitter=0.6)
+    x = p.xyzh.copy()
+    x[0, 0] = np.float32(1.0 / nc)
+    x[1, 1] = 0.0
+    x[2, 2] = np.float32(1 - 2 ** -24)
+    x[3, :3] = x[4, :3]
+    x[5, :3] = [0.0, 0.0, 0.0]
+    x[6, :3] = np.float32(1 - 2 ** -24)
+    compare(run(pv, x, p.vm, nc), oracle.bruteforce(x, p.vm), None, f"tiny{seed}")
+
+
+@pytest.mark.parametrize("occ", [1, 31, 32, 33, 63, 65, 97, 129, 257, 300])
+def test_cell_occupancy_tile_boundaries(pv, occ):
+    """A dense cell with occupancy around warp/tile/sort-path boundaries (33, 65, 129, 257)."""
+    rng = np.random.default_rng(occ)
+    nc = 4
+    Cl = 1.0 / nc
+    n_bg = 200
+    pos = rng.integers(0, 2 ** 24, size=(n_bg, 3)) / 2 ** 24
+    dense = (1 + rng.random((occ, 3))) * Cl        # all in cell (1,1,1)
+    xyzh = np.zeros((n_bg + occ, 4), np.float32)
+    xyzh[:n_bg, :3] = pos
+    xyzh[n_bg:, :3] = np.floor(dense * 2 ** 24) / 2 ** 24
+    xyzh[:, 3] = (0.9 * Cl / synth.GAMMA) * (1 - 0.5 * rng.random(n_bg + occ))
+    vm = np.zeros_like(xyzh)
+    vm[:, :3] = rng.standard_normal((n_bg + occ, 3))
+    vm[:, 3] = 1.0 / (n_bg + occ)
+    compare(run(pv, xyzh, vm, nc), oracle.bruteforce(xyzh, vm), None, f"occ{occ}")
+
+
+def test_on_axis_near_cutoff_pairs(pv):
+    """Adversarial pairs at r = H (1 - 10^-k) along face/edge/corner axes, across the periodic boundary."""
+    nc = 5
+    Cl = 1.0 / nc
+    h = np.float32(0.95 * Cl / synth.GAMMA)
+    H = synth.GAMMA * float(h)
+    rows = []
+    for k in range(3, 8):
+        r = H * (1 - 10.0 ** -k)
+        for axis in ([1, 0, 0], [1, 1, 0], [1, 1, 1], [1, -1, 0], [0, 1, -1]):
+            a = np.array(axis, np.float64) / np.linalg.norm(axis)
+            p0 = np.array([0.999, 0.5, 0.0005 + 0.01 * k])
+            p1 = np.mod(p0 + r * a, 1.0)
+            rows.append(p0)
+            rows.append(p1)
+    x = np.floor(np.array(rows) * 2 ** 24) / 2 ** 24
+    xyzh = np.zeros((len(rows), 4), np.float32)
+    xyzh[:, :3] = x
+    xyzh[:, 3] = h
+    vm = np.ones_like(xyzh)
+    vm[:, 3] = 0.01
+    ref = oracle.bruteforce(xyzh, vm)
+    compare(run(pv, xyzh, vm, nc), ref, None, "on-axis")
+
+
+def test_lattice_pin_on_gpu(pv):
+    """Uniform lattice: nngb = 56 everywhere and rho/(mn) within 1e-5 of the golden value."""
+    g = json.load(open(os.path.join(GOLDEN, "lattice_eta1.2348.json")))
+    side = g["side"]
+    n = side ** 3
+    i = np.arange(n)
+    xyzh = np.zeros((n, 4), np.float32)
+    xyzh[:, 0], xyzh[:, 1], xyzh[:, 2] = (i // (side * side) + 0.5) / side, ((i // side) % side + 0.5) / side, \
+        (i % side + 0.5) / side
+    xyzh[:, 3] = g["eta"] / side
+    vm = np.zeros((n, 4), np.float32)
+    vm[:, 3] = 1.0 / n
+    got = run(pv, xyzh, vm, int(1 / (synth.GAMMA * g["eta"] / side)))
+    assert np.all(got["nngb"] == 56)
+    assert np.all(np.abs(got["rho"] / g["rho_over_mn"] - 1) < 1e-5)
+
+
+@pytest.mark.parametrize("bad", ["h0", "mneg", "nan", "outside", "hbig"])
+def test_input_errors(pv, bad):
+    p = synth.tiny_random_set(3, 100, 4)
+    x, v = p.xyzh.copy(), p.vm.copy()
+    if bad == "h0":
+        x[7, 3] = 0.0
+    elif bad == "mneg":
+        v[7, 3] = -1.0
+    elif bad == "nan":
+        x[7, 1] = np.nan
+    elif bad == "outside":
+        x[7, 0] = 1.0
+    elif bad == "hbig":
+        x[7, 3] = np.float32(1.01 * 0.25 / synth.GAMMA)
+    dp = pv.DensityPass(4, p.n)
+    dp.run(torch.from_numpy(x).cuda(), torch.from_numpy(v).cuda())
+    exp = {"h0": 2, "mneg": 2, "nan": 4, "outside": 4, "hbig": 2}[bad]
+    assert pv.sph_status(dp.ws) == exp
+
+
+@pytest.mark.parametrize("occ,code", [(65535, 0), (65536, 3)])
+def test_max_cell_occupancy(pv, occ, code):
+    """SPH_MAX_CELL = 65535 particles in one cell is accepted; 65536 returns SPH_ECAPACITY."""
+    rng = np.random.default_rng(5)
+    nc = 3
+    xyzh = np.zeros((occ, 4), np.float32)
+    xyzh[:, :3] = np.floor((1 + rng.random((occ, 3))) / nc * 2 ** 24) / 2 ** 24
+    xyzh[:, 3] = np.float32(1e-4)
+    vm = np.zeros_like(xyzh)
+    vm[:, 3] = 1.0 / occ
+    dp = pv.DensityPass(nc, occ)
+    xd, vd = torch.from_numpy(xyzh).cuda(), torch.from_numpy(vm).cuda()
+    pv.sph_build_cells(dp.grid, xd, vd, dp.cells, dp.ws)
+    st = pv.sph_status(dp.ws)
+    assert st == code
+    if code == 0:
+        pv.sph_sort_cells(dp.grid, dp.cells, dp.ws)
+        pv.sph_density_all(dp.grid, dp.cells, dp.out, dp.ws)
+        dp.check()
+        got = dp.out.to_numpy()
+        idx = np.arange(0, occ, 997)
+        compare(got, oracle.bruteforce(xyzh, vm, targets=idx), idx, "maxocc")

@@ -1,0 +1,49 @@
+"""x-slab decomposition on one GPU (fake ranks: the exchange done with device copies):
+outputs bitwise identical to the single-GPU pass for p = 2, 3, 4."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._compare import compare
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pv():
+    import paper_1804_06231_b200 as pv
+    pv.load()
+    return pv
+
+
+@pytest.mark.parametrize("cfg,world", [("c1", 2), ("c2", 2), ("c2", 3), ("c2", 4), ("c3", 2), ("c3", 4)])
+def test_fake_ranks_bitwise_equal_single(pv, cfg, world):
+    from paper_1804_06231_b200.slabs import FakeRanks
+    p = synth.make(cfg)
+    single = pv.density(p.xyzh, p.vm, p.nc)
+    fr = FakeRanks(p, world)
+    fr.step()
+    got = fr.gather()
+    for f in single:
+        assert np.array_equal(single[f], got[f]), (cfg, world, f)
+    if cfg == "c1":
+        compare(got, oracle.bruteforce(p.xyzh, p.vm), None, f"{cfg} p={world}")
+
+
+def test_slab_boundary_particles_vs_oracle(pv):
+    """Particles within one cell of a slab boundary (p = 4, c3) against the oracle."""
+    from paper_1804_06231_b200.slabs import FakeRanks, planes_of, slab_bounds
+    p = synth.make("c3")
+    fr = FakeRanks(p, 4)
+    fr.step()
+    got = fr.gather()
+    pl = planes_of(p.xyzh, p.nc)
+    edges = set()
+    for r in range(4):
+        lo, hi = slab_bounds(p.nc, 4, r)
+        edges |= {lo, hi - 1}
+    idx = np.nonzero(np.isin(pl, sorted(edges)))[0]
+    idx = idx[:: max(1, idx.size // 50000)]
+    compare(got, oracle.celllist(p.xyzh, p.vm, p.nc, targets=idx), idx, "slab boundaries")

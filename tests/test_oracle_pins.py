@@ -151,6 +151,32 @@ def test_two_particle_div_curl_closed_form():
         assert abs(a[f][0] - curl[k]) < 1e-13 * np.abs(curl).max()
 
 
+@pytest.mark.parametrize("x", [0.2, 0.45, 0.6, 0.9, 0.995])
+def test_condition_scale_matches_radial_finite_difference(x):
+    """c_div - a_div = |d(rho div)/d ln r| for one pair (reading R14): the div term of a pair
+    scales as w'(r/H) along a fixed direction, so its log-derivative is x w''/w'."""
+    h = 0.0625
+    H = GAMMA * h
+    u = np.array([2.0, -1.0, 2.0]) / 3.0
+    p0 = np.array([0.5, 0.5, 0.5])
+    v = np.array([[0.25, -0.5, 1.0, 0.5], [-1.0, 0.75, 0.125, 0.25]], np.float32)
+
+    def D(scale):
+        xyzh = np.array([[*p0, h], [*(p0 + u * x * H * scale), h]], np.float32)
+        a = oracle.bruteforce(xyzh, v)
+        d = xyzh[1, :3].astype(np.float64) - xyzh[0, :3].astype(np.float64)
+        return a["div_v"][0] * a["rho"][0], a, np.linalg.norm(d)
+
+    eps = 1e-4
+    d0, a0, r0 = D(1.0)
+    d1, _, r1 = D(1.0 + eps)
+    d2, _, r2 = D(1.0 - eps)
+    dlog = np.log(r1 / r2)
+    sens = abs(d1 - d2) / dlog                       # |d(rho div)/d ln r|
+    expect = (a0["c_div"][0] - a0["a_div"][0]) * a0["rho"][0]
+    assert abs(sens - expect) <= 2e-3 * expect + 1e-12
+
+
 def test_asymmetric_cutoffs():
     """H_j < r < H_i: i counts j, j does not count i (gather with h_i)."""
     xyzh = np.array([[0.5, 0.5, 0.5, 0.05], [0.58, 0.5, 0.5, 0.02]], np.float32)

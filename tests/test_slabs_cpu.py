@@ -1,0 +1,81 @@
+"""Host-side x-slab logic on CPU: partition and the ghost exchange over gloo (world sizes 2-4)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import synth
+
+
+def test_slab_partition_covers_every_particle_once():
+    from paper_1804_06231_b200.slabs import Slab, planes_of, slab_bounds
+    p = synth.make("c2")
+    for world in (2, 3, 4, 6):
+        seen = np.zeros(p.n, np.int64)
+        for r in range(world):
+            s = Slab.from_set(p, r, world)
+            lo, hi = slab_bounds(p.nc, world, r)
+            assert (s.x_lo, s.x_hi) == (lo, hi)
+            pl = planes_of(s.xyzh, p.nc)
+            assert np.all((pl >= lo) & (pl < hi))
+            assert np.all(np.diff(s.gid) > 0)             # global order preserved
+            seen[s.gid] += 1
+        assert np.all(seen == 1)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, sizes, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1804_06231_b200.slabs import exchange_planes
+
+    def plane(r, which):
+        n = sizes[r][which]
+        x = torch.zeros((n, 4), dtype=torch.float32)
+        x[:, 0] = r
+        x[:, 1] = which
+        x[:, 2] = torch.arange(n, dtype=torch.float32)
+        return x, x + 1000.0
+
+    lo, hi = plane(rank, 0), plane(rank, 1)
+    xb = torch.full((64, 4), -1.0)
+    vb = torch.full((64, 4), -1.0)
+    n_glo, n_ghi = exchange_planes(dist, rank, world, lo, hi, (xb, vb))
+    left, right = (rank - 1) % world, (rank + 1) % world
+    exp_lo, exp_hi = plane(left, 1), plane(right, 0)
+    ok = (n_glo == exp_lo[0].shape[0] and n_ghi == exp_hi[0].shape[0] and
+          torch.equal(xb[:n_glo], exp_lo[0]) and torch.equal(vb[:n_glo], exp_lo[1]) and
+          torch.equal(xb[n_glo:n_glo + n_ghi], exp_hi[0]) and torch.equal(vb[n_glo:n_glo + n_ghi], exp_hi[1]) and
+          bool((xb[n_glo + n_ghi:] == -1).all()))
+    q.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,sizes", [
+    (2, [(3, 5), (4, 2)]),
+    (2, [(0, 5), (4, 0)]),          # empty planes on both sides
+    (3, [(1, 2), (3, 4), (5, 6)]),
+    (4, [(2, 0), (0, 3), (7, 1), (1, 1)]),
+])
+def test_ghost_exchange_gloo(world, sizes):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sizes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
