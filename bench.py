@@ -109,23 +109,41 @@ def _profile_traffic():
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle's cell list on a bounded sample
 # ---------------------------------------------------------------------------
+def _oracle_rate(p, seconds: float, rng):
+    """Time oracle_celllist on two random target samples of p; the difference removes the
+    one-off binning of all N particles, which a full run amortises over N targets.
+    Returns (interactions/s for a full run, n_targets, description)."""
+    import oracle
+    n1 = 1000
+    t1 = rng.choice(p.n, n1, replace=False)
+    t0 = time.perf_counter()
+    r1 = oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(t1))
+    d1 = time.perf_counter() - t0
+    # second sample sized for ~`seconds` of target work (probe slope from a 2x sample)
+    t2 = rng.choice(p.n, 2 * n1, replace=False)
+    t0 = time.perf_counter()
+    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(t2))
+    d2 = time.perf_counter() - t0
+    slope = max((d2 - d1) / n1, 1e-9)
+    n_s = int(min(p.n, max(4 * n1, seconds / slope)))
+    ts = rng.choice(p.n, n_s, replace=False)
+    t0 = time.perf_counter()
+    rs = oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(ts))
+    ds = time.perf_counter() - t0
+    per_target = (ds - d1) / (n_s - n1)
+    t_bin = max(0.0, d1 - n1 * per_target)
+    inter_per_target = float(rs["nngb"].sum()) / n_s
+    rate = inter_per_target * p.n / (t_bin + per_target * p.n)
+    desc = (f"oracle_celllist (fp64, OpenMP) timed on {n1} and {n_s} random targets of {p.name} (N={p.n}); "
+            f"per-target {per_target * 1e6:.2f} us, binning {t_bin:.2f} s, extrapolated to all N")
+    del r1
+    return rate, n_s, desc
+
+
 def cpu_baseline(p, seconds: float):
     import oracle
-    n_probe = 2000
-    rng = np.random.default_rng(123)
-    probe = np.sort(rng.choice(p.n, n_probe, replace=False))
-    t0 = time.perf_counter()
-    r = oracle.celllist(p.xyzh, p.vm, p.nc, targets=probe)
-    t_probe = time.perf_counter() - t0
-    n_s = int(min(p.n, max(n_probe, n_probe * seconds / max(t_probe, 1e-3))))
-    tgt = np.sort(rng.choice(p.n, n_s, replace=False))
-    t0 = time.perf_counter()
-    r = oracle.celllist(p.xyzh, p.vm, p.nc, targets=tgt)
-    dt = time.perf_counter() - t0
-    inter = float(r["nngb"].sum())
-    return {"value": inter / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"oracle_celllist (fp64, OpenMP) on {n_s} random targets of {p.name} (N={p.n}), "
-                      f"incl. binning all N; {inter:.0f} interactions in {dt:.1f} s"}
+    rate, n_s, desc = _oracle_rate(p, seconds, np.random.default_rng(123))
+    return {"value": rate, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle", "sample": desc}
 
 
 # ---------------------------------------------------------------------------

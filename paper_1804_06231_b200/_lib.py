@@ -14,7 +14,8 @@ SPH_NDIR = 13
 SPH_DELTA_FRAC = 1.0 / 65536.0
 ERROR_NAMES = {0: "SPH_OK", 1: "SPH_EINVAL", 2: "SPH_EH_RANGE", 3: "SPH_ECAPACITY", 4: "SPH_EDOMAIN", 5: "SPH_ECUDA"}
 
-# Every function declared in include/sph.h (checked by tests/test_abi.py).
+# Every function declared in include/sph.h (checked by tests/test_abi.py); sph_calibrate is
+# declared in include/sph_calib.h.
 EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cells", "sph_sort_cells",
            "sph_density_self", "sph_density_pair", "sph_density_finalize", "sph_density_all", "sph_status",
            "sph_status_reset", "sph_strerror")
@@ -68,6 +69,8 @@ def load(path: str = LIB):
     L.sph_density_all.argtypes = [G, C, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_status.argtypes = [c_vp, c_vp]
     L.sph_status_reset.argtypes = [c_vp, c_vp]
+    L.sph_calibrate.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp]
+    L.sph_calibrate.restype = ctypes.c_int
     L.sph_strerror.argtypes = [ctypes.c_int]
     L.sph_strerror.restype = ctypes.c_char_p
     for f in ("sph_build_cells", "sph_sort_cells", "sph_density_self", "sph_density_pair", "sph_density_finalize",

@@ -5,7 +5,9 @@
 #include <cstdio>
 #include <cstring>
 
+#include "../../include/sph_calib.h"
 #include "build.cuh"
+#include "calib.cuh"
 #include "common.cuh"
 #include "density.cuh"
 #include "sort.cuh"
@@ -339,6 +341,16 @@ int sph_status(void *ws, void *stream)
     if (st & ST_EH_RANGE) return SPH_EH_RANGE;
     if (st & ST_ECAPACITY) return SPH_ECAPACITY;
     return SPH_OK;
+}
+
+int sph_calibrate(int mode, int blocks, int threads, int iters, float *out, void *stream)
+{
+    if (mode < 0 || mode > 2 || blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out) return SPH_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (mode == 0) k_calib_ffma<<<blocks, threads, 0, s>>>(out, iters);
+    else if (mode == 1) k_calib_ffma2<<<blocks, threads, 0, s>>>(out, iters);
+    else k_calib_interact<<<blocks, threads, 0, s>>>(out, iters);
+    return check_launch();
 }
 
 const char *sph_strerror(int code)
