@@ -103,6 +103,7 @@ typedef struct sph_pv_entry {
  *   vm[4 * capacity]        vx, vy, vz, m in cell order
  *   perm[capacity]          slot -> input index
  *   cell_hmax[ncell]        max h in each cell
+ *   slot_cell[capacity]     local cell of each slot (written by build)
  *   pv[SPH_NDIR * capacity] sorted lists: direction d, slot range of cell c
  *                           at pv[d * capacity + cell_start[c] ...]
  * n is written by sph_build_cells (stored particles).  16-byte alignment
@@ -116,6 +117,7 @@ typedef struct sph_cells {
     int32_t *perm;
     float *cell_hmax;
     sph_pv_entry *pv;
+    int32_t *slot_cell;
 } sph_cells;
 
 /* Outputs, each an array of n_out elements indexed by INPUT index (only

@@ -79,6 +79,7 @@ class Cells:
     perm: torch.Tensor
     cell_hmax: torch.Tensor
     pv: torch.Tensor            # (13 * capacity, 2) int32 view of sph_pv_entry {float key; int j}
+    slot_cell: torch.Tensor     # (capacity,) int32
     n: int = 0
 
     @staticmethod
@@ -90,7 +91,8 @@ class Cells:
                      torch.empty((cap, 4), dtype=torch.float32, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device),
                      torch.empty(nce, dtype=torch.float32, device=device),
-                     torch.empty((_lib.SPH_NDIR * cap, 2), dtype=torch.int32, device=device))
+                     torch.empty((_lib.SPH_NDIR * cap, 2), dtype=torch.int32, device=device),
+                     torch.empty(cap, dtype=torch.int32, device=device))
 
     def struct(self) -> SphCells:
         s = SphCells()
@@ -98,6 +100,7 @@ class Cells:
         s.n = self.n
         s.cell_start, s.xyzh, s.vm = self.cell_start.data_ptr(), self.xyzh.data_ptr(), self.vm.data_ptr()
         s.perm, s.cell_hmax, s.pv = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.pv.data_ptr()
+        s.slot_cell = self.slot_cell.data_ptr()
         return s
 
     def pv_keys(self) -> torch.Tensor:

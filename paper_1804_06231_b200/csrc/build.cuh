@@ -237,8 +237,9 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
 }
 
 __global__ void k_gather(long long n_total, const int *__restrict__ start_end, const int *__restrict__ perm,
-                         const float4 *__restrict__ xyzh_in, const float4 *__restrict__ vm_in,
-                         float4 *__restrict__ xyzh_s, float4 *__restrict__ vm_s)
+                         const int *__restrict__ cell_of, const float4 *__restrict__ xyzh_in,
+                         const float4 *__restrict__ vm_in, float4 *__restrict__ xyzh_s, float4 *__restrict__ vm_s,
+                         int *__restrict__ slot_cell)
 {
     const long long n_valid = *start_end;   // cell_start[ncell]: particles actually binned
     for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_valid && k < n_total;
@@ -246,6 +247,7 @@ __global__ void k_gather(long long n_total, const int *__restrict__ start_end, c
         int p = perm[k];
         xyzh_s[k] = xyzh_in[p];
         vm_s[k] = vm_in[p];
+        slot_cell[k] = cell_of[p];
     }
 }
 

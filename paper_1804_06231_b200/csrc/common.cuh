@@ -41,6 +41,7 @@ struct DevCells {
     const int *perm;
     const float *cell_hmax;
     const sph_pv_entry *pv;
+    const int *slot_cell;
 };
 
 struct DevOut {

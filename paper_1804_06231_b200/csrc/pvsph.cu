@@ -2,6 +2,7 @@
 // workspace layout and kernel launches.  One translation unit (the kernels
 // live in the .cuh files) compiled for sm_100a only.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -10,6 +11,7 @@
 #include "calib.cuh"
 #include "common.cuh"
 #include "density.cuh"
+#include "density_v2.cuh"
 #include "sort.cuh"
 
 using namespace pvsph;
@@ -74,7 +76,8 @@ int make_grid(const sph_grid *gr, DevGrid &g)
 
 bool cells_ok(const sph_cells *c)
 {
-    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->pv && c->capacity >= 0 &&
+    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->pv && c->slot_cell &&
+           c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
            ((uintptr_t)c->pv % 8 == 0);
 }
@@ -89,6 +92,7 @@ DevCells dev_cells(const sph_cells *c)
     d.perm = c->perm;
     d.cell_hmax = c->cell_hmax;
     d.pv = c->pv;
+    d.slot_cell = c->slot_cell;
     return d;
 }
 
@@ -227,9 +231,9 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
             g.ncell, cells->cell_start, perm_tmp, cells->perm, big_items, big_count);
         k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, cells->perm, big_items,
                                                           big_count);
-        k_gather<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cells->cell_start + g.ncell, cells->perm, xin, vin,
-                                                               reinterpret_cast<float4 *>(cells->xyzh),
-                                                               reinterpret_cast<float4 *>(cells->vm));
+        k_gather<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cells->cell_start + g.ncell, cells->perm, cell_of,
+                                                               xin, vin, reinterpret_cast<float4 *>(cells->xyzh),
+                                                               reinterpret_cast<float4 *>(cells->vm), cells->slot_cell);
     }
     cells->n = n;
     return check_launch();
@@ -318,11 +322,21 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     if (rc) return rc;
     if (!cells_ok(cells) || !out_ok(out) || !ws || ws_bytes < 4) return SPH_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
-    int blocks = grid_blocks(g.n_owned_cells, V1_WARPS, 1 << 30);
+    const char *eng = std::getenv("PVSPH_ENGINE");   // "v1": reference engine (validation only)
+    if (eng && eng[0] == 'v' && eng[1] == '1') {
+        int blocks = grid_blocks(g.n_owned_cells, V1_WARPS, 1 << 30);
+        if (stats)
+            k_density_all_v1<true><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
+        else
+            k_density_all_v1<false><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
+        return check_launch();
+    }
+    long long warps = (cells->n + 31) / 32 + 1;
+    int blocks = grid_blocks(warps, V2_WARPS, 1 << 30);
     if (stats)
-        k_density_all_v1<true><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
+        k_density_all_v2<true><<<blocks, V2_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
     else
-        k_density_all_v1<false><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
+        k_density_all_v2<false><<<blocks, V2_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
     return check_launch();
 }
 

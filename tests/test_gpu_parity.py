@@ -52,6 +52,7 @@ def test_build_cells_matches_oracle_binning(pv, cfg):
     assert np.array_equal(cs, start)
     perm = dp.cells.perm[:p.n].cpu().numpy()
     assert np.array_equal(perm, order)           # stable: input order inside each cell
+    assert np.array_equal(dp.cells.slot_cell[:p.n].cpu().numpy(), cell[order])
     xs = dp.cells.xyzh[:p.n].cpu().numpy()
     assert np.array_equal(xs, p.xyzh[perm])
     assert np.array_equal(dp.cells.vm[:p.n].cpu().numpy(), p.vm[perm])
@@ -107,6 +108,21 @@ def test_density_all_vs_celllist_full(pv, cfg):
     p = synth.make(cfg)
     got = run(pv, p.xyzh, p.vm, p.nc)
     compare(got, oracle.celllist(p.xyzh, p.vm, p.nc), None, cfg)
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_reference_engine_v1(pv, cfg, monkeypatch):
+    """The reference engine (PVSPH_ENGINE=v1) passes parity too, and agrees with the default engine."""
+    p = synth.make(cfg)
+    b = run(pv, p.xyzh, p.vm, p.nc)
+    monkeypatch.setenv("PVSPH_ENGINE", "v1")
+    a = run(pv, p.xyzh, p.vm, p.nc)
+    monkeypatch.delenv("PVSPH_ENGINE")
+    idx = np.arange(0, p.n, 7)
+    ref = oracle.celllist(p.xyzh, p.vm, p.nc, targets=idx)
+    compare(a, ref, idx, f"v1 {cfg}")
+    compare(b, ref, idx, f"v2 {cfg}")
+    assert np.array_equal(a["nngb"], b["nngb"])
 
 
 def test_density_all_c3_vs_celllist(pv):
