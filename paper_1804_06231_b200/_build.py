@@ -31,7 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *NVCC_FLAGS, "-o", LIB, SRC]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+            errs = [l for l in (r.stdout + r.stderr).splitlines() if "error" in l.lower()]
+            raise RuntimeError("nvcc failed:\n" + "\n".join(errs[:40]))
         with open(os.path.join(PKG, "csrc", "ptxas_info.txt"), "w") as f:
             f.write(r.stderr)
         if verbose:

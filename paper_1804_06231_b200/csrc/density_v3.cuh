@@ -1,0 +1,277 @@
+// density_v3.cuh -- the production sph_density_all engine.
+//
+// Same method and per-particle arithmetic as the reference engine (density.cuh),
+// mapped onto the SIMT machine as follows:
+//
+//  * A warp owns 32 consecutive slots of the cell-sorted arrays (lane = particle
+//    i), so lanes are filled across cell boundaries.
+//  * The 27 cells are visited as the self cell plus 13 direction pairs: for the
+//    sort direction d the lane's window in the +d neighbour (a prefix of its list
+//    sorted along d) is followed by its window in the -d neighbour (a suffix of
+//    the same-direction list).  The two lengths are anti-correlated (a particle
+//    near the +d face sees much of +d and little of -d), so the per-lane total of
+//    a pair varies far less than either window.
+//  * Windows are exact: each lane binary-searches its bound on the sorted keys
+//    (the bound of P:151-165 computed exactly instead of by the single pass of
+//    the paper).  The warp then runs a loop of uniform trip count max(total); a
+//    lane tests candidate t of its own concatenated window while t < total.
+//    Lanes of one home cell read the same list region, so the loads stay
+//    L1-friendly (no shared-memory staging: L1 keeps its full size).
+//  * The candidate test computes r^2 only.  An in-range pair is pushed
+//    into the lane's hit queue in shared memory; hit k is stored in half (k & 1)
+//    of a packed pair slot, so a pop yields f32x2 operands directly and every
+//    particle sums its hits in sweep order whatever the warp does (deterministic,
+//    identical on any number of GPUs).  The left-packing of in-range candidates
+//    of P:185 ("if (ANY(mask))") becomes this compaction.
+//  * When most lanes hold a full pair (or a queue is nearly full) the warp pops
+//    one pair per lane and evaluates both interactions with FFMA2/FADD2/FMUL2,
+//    accumulating in registers; one writer per particle at the end.
+#pragma once
+
+#include "common.cuh"
+#include "density.cuh"
+#include "packed.cuh"
+
+namespace pvsph {
+
+constexpr int V3_WARPS = 4;
+constexpr int V3_QP = 4;                  // pair slots per lane (8 queued hits)
+constexpr int V3_NC = 7;                  // queued components: dx dy dz m (vj-vi)x y z
+
+// Packed accumulators; D and curl use v_j - v_i (= -v_ij) so the cross products
+// need no negation: Dn = -sum fac (v_ij . x_ij); R = P - N.
+struct Acc2 {
+    f2 rho, wc, srt, st, Dn, Px, Nx, Py, Ny, Pz, Nz;
+};
+
+__device__ __forceinline__ void acc2_zero(Acc2 &A)
+{
+    A.rho = A.wc = A.srt = A.st = A.Dn = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = 0ull;
+}
+
+// Two interactions from one pair slot.  mk = (1, 1) or (1, 0) when the odd half is
+// empty (its stale components are finite: the queue is zeroed at start).
+// M4 in branch-free form: w(x) = u^3 - v^3/2, w'(x) = 3 (v^2 - u^2),
+// u = 1 - x, v = max(0, 1 - 2x)   (equal to the two-branch form of R1).
+__device__ __forceinline__ void interact_pair(f2 Hinv2, f2 dx, f2 dy, f2 dz, f2 m, f2 nvx, f2 nvy, f2 nvz, f2 mk,
+                                              Acc2 &A)
+{
+    f2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    float r2a, r2b;
+    upk(r2, r2a, r2b);
+    // r^2 = 0 (coincident particles): rinv stays finite, x = 0 and w'(0) = 0 make every gradient term 0
+    f2 rinv = pk(rsqrtf(fmaxf(r2a, 1e-30f)), rsqrtf(fmaxf(r2b, 1e-30f)));
+    f2 x = mul2(mul2(r2, rinv), Hinv2);
+    f2 u = sub2(bc2(1.0f), x);
+    f2 v = fma2(bc2(-2.0f), x, bc2(1.0f));
+    float va, vb, xa, xb, ua, ub;
+    upk(v, va, vb);
+    upk(x, xa, xb);
+    upk(u, ua, ub);
+    v = pk(fmaxf(va, 0.0f), fmaxf(vb, 0.0f));
+    const f2 mn = pk(fminf(xa, ua), fminf(xb, ub));   // u - v without cancellation: min(x, u)
+    f2 uu = mul2(u, u), vv = mul2(v, v);
+    f2 w = mul2(fma2(uu, u, mul2(bc2(-0.5f), mul2(vv, v))), mk);
+    // w' = 3 (v^2 - u^2) = -3 (u - v)(u + v); the difference of squares would lose all
+    // precision for x -> 0 (w' ~ -6x while v^2, u^2 ~ 1)
+    f2 dw = mul2(mul2(bc2(-3.0f), mk), mul2(mn, add2(u, v)));
+    m = mul2(m, mk);
+    A.rho = fma2(m, w, A.rho);
+    A.wc = add2(A.wc, w);
+    f2 t = fma2(x, dw, mul2(bc2(3.0f), w));
+    A.srt = fma2(m, t, A.srt);
+    A.st = add2(A.st, t);
+    f2 nvdx = fma2(nvx, dx, fma2(nvy, dy, mul2(nvz, dz)));
+    f2 fac = mul2(mul2(m, dw), rinv);
+    A.Dn = fma2(fac, nvdx, A.Dn);
+    f2 fx = mul2(fac, nvx), fy = mul2(fac, nvy), fz = mul2(fac, nvz);
+    A.Px = fma2(fz, dy, A.Px);
+    A.Nx = fma2(fy, dz, A.Nx);
+    A.Py = fma2(fx, dz, A.Py);
+    A.Ny = fma2(fz, dx, A.Ny);
+    A.Pz = fma2(fy, dx, A.Pz);
+    A.Nz = fma2(fx, dy, A.Nz);
+}
+
+__device__ __forceinline__ int image_code(const int sh[3])
+{
+    int c = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) c |= (sh[a] > 0 ? 1 : (sh[a] < 0 ? 2 : 0)) << (2 * a);
+    return c;
+}
+
+__device__ __forceinline__ int kind_of_dir(int d)
+{
+    // faces (0,0,1) (0,1,0) (1,0,0); corners (1,-1,-1) (1,-1,1) (1,1,-1) (1,1,1); the rest edges
+    return (d == 0 || d == 2 || d == 8) ? 1 : ((d == 4 || d == 6 || d == 10 || d == 12) ? 3 : 2);
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(V3_WARPS * 32, 4) k_density_all_v3(DevGrid g, DevCells c, DevOut o, sph_stats *st)
+{
+    __shared__ float2 qp[V3_WARPS][V3_QP][V3_NC][32];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const long long plane = (long long)g.ny * g.nz;
+    const int slot_lo = c.cell_start[g.ghost_x ? plane : 0];
+    const int slot_hi = c.cell_start[g.ghost_x ? (g.nxl - 1) * plane : g.ncell];
+    const long long base = (long long)slot_lo + ((long long)blockIdx.x * V3_WARPS + wl) * 32;
+    if (base >= slot_hi) return;                       // whole warp idle (warp-uniform)
+    const int i = (int)base + lane;
+    const bool active = i < slot_hi;
+
+#pragma unroll
+    for (int s = 0; s < V3_QP; ++s)
+#pragma unroll
+        for (int cc = 0; cc < V3_NC; ++cc) qp[wl][s][cc][lane] = make_float2(0.0f, 0.0f);
+
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    HomeCell hc;
+    IPart p;
+    int home = 0;
+    if (active) {
+        home = c.slot_cell[i];
+        hc = home_cell(g, home);
+        p = load_i(g, c, i, hc.corner);
+    } else {
+        p.x = p.y = p.z = p.vx = p.vy = p.vz = p.m = p.h = 0.0f;
+        p.H2 = -1.0f;
+        p.Hinv = p.Hd = 0.0f;
+        p.u0 = p.u1 = p.u2 = 0.0;
+        p.slot = -1;
+        hc.ixl = hc.iy = hc.iz = hc.ixg = 0;
+    }
+    const float ux = (float)p.u0, uy = (float)p.u1, uz = (float)p.u2;   // cell-local coordinates
+    const f2 Hinv2 = bc2(p.Hinv);
+
+    Acc2 A;
+    acc2_zero(A);
+    int nngb = 0;
+    unsigned head = 0, tail = 0;                       // hit counters; head stays even
+    float2 (*Q)[V3_NC][32] = qp[wl];
+
+    // pop one pair slot per lane that holds a full pair (or, when final, any hit)
+    auto drain = [&](bool final) {
+        const unsigned n = tail - head;
+        if (n >= 2 || (final && n == 1)) {
+            const int s = (head >> 1) & (V3_QP - 1);
+            const f2 mk = pk(1.0f, n >= 2 ? 1.0f : 0.0f);
+            interact_pair(Hinv2, as_f2(Q[s][0][lane]), as_f2(Q[s][1][lane]), as_f2(Q[s][2][lane]),
+                          as_f2(Q[s][3][lane]), as_f2(Q[s][4][lane]), as_f2(Q[s][5][lane]), as_f2(Q[s][6][lane]),
+                          mk, A);
+            head += n >= 2 ? 2u : 1u;
+        }
+    };
+
+    for (int a = 0; a < 14; ++a) {
+        // lane's two windows for this pass: a = 0 the self cell; a = 1 + d the +d, -d neighbours
+        const int d = a == 0 ? 0 : a - 1;
+        const sph_pv_entry *L = c.pv + (long long)d * c.cap;
+        const int kind = a == 0 ? 0 : kind_of_dir(d);
+        int qb0 = 0, len0 = 0, qb1 = 0, len1 = 0, code0 = 0, code1 = 0;
+        if (active) {
+            if (a == 0) {
+                qb0 = c.cell_start[home];
+                len0 = c.cell_start[home + 1] - qb0;
+            } else {
+                const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                const float inv = kind == 1 ? 1.0f : (kind == 2 ? 0.70710678f : 0.57735027f);
+                const float key_i = fmaf(ux, (float)a0 * inv, fmaf(uy, (float)a1 * inv, uz * ((float)a2 * inv)));
+                const float B = p.Hd - g.q[d];
+                int cj, sh[3];
+                if (neighbour(g, hc, a0, a1, a2, cj, sh)) {        // +d: prefix {key < key_i + B}
+                    const float lim = key_i + B;
+                    int lo = c.cell_start[cj], hi = c.cell_start[cj + 1];
+                    qb0 = lo;
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (L[mid].key < lim) lo = mid + 1; else hi = mid;
+                    }
+                    len0 = lo - qb0;
+                    code0 = image_code(sh);
+                }
+                if (neighbour(g, hc, -a0, -a1, -a2, cj, sh)) {     // -d: suffix {key > key_i - B}
+                    const float lim = key_i - B;
+                    int lo = c.cell_start[cj], hi = c.cell_start[cj + 1];
+                    const int end = hi;
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (L[mid].key > lim) hi = mid; else lo = mid + 1;
+                    }
+                    qb1 = lo;
+                    len1 = end - lo;
+                    code1 = image_code(sh);
+                }
+            }
+        }
+        const int total = len0 + len1;
+        const int trip = __reduce_max_sync(0xffffffffu, total);
+        for (int t = 0; t < trip; ++t) {
+            if (t < total) {
+                const bool first = t < len0;
+                const int q = first ? qb0 + t : qb1 + (t - len0);
+                const int code = first ? code0 : code1;
+                const int j = L[q].j;
+                const float4 pj = c.xyzh[j];
+                float xi = p.x, yi = p.y, zi = p.z, xj = pj.x, yj = pj.y, zj = pj.z;
+                if (code) {                                    // periodic image: exact differences (R4)
+                    if (code & 1) xi -= g.boxf[0];
+                    if (code & 2) xj -= g.boxf[0];
+                    if (code & 4) yi -= g.boxf[1];
+                    if (code & 8) yj -= g.boxf[1];
+                    if (code & 16) zi -= g.boxf[2];
+                    if (code & 32) zj -= g.boxf[2];
+                }
+                const float ddx = xi - xj, ddy = yi - yj, ddz = zi - zj;
+                const float r2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
+                if (COUNT && (a != 0 || j != i)) ++cand[kind];
+                if (r2 < p.H2 && (a != 0 || j != i)) {
+                    const float4 vj = c.vm[j];
+                    float *slot = &Q[(tail >> 1) & (V3_QP - 1)][0][lane].x + (tail & 1);
+                    slot[0 * 64] = ddx;
+                    slot[1 * 64] = ddy;
+                    slot[2 * 64] = ddz;
+                    slot[3 * 64] = vj.w;
+                    slot[4 * 64] = vj.x - p.vx;
+                    slot[5 * 64] = vj.y - p.vy;
+                    slot[6 * 64] = vj.z - p.vz;
+                    ++tail;
+                    ++nngb;
+                    if (COUNT) ++hits[kind];
+                }
+            }
+            const unsigned n = tail - head;
+            if (__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= 2 * V3_QP - 1))
+                drain(false);
+        }
+    }
+    while (__any_sync(0xffffffffu, tail != head)) drain(true);
+
+    if (active) {
+        // finalise (self term w(0) = 1/2, t(0) = 3/2), as finalise() in density.cuh
+        float Hinv = p.Hinv;
+        float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;
+        float rho = K3 * fmaf(0.5f, p.m, sum2(A.rho));
+        float wc = K3 * (0.5f + sum2(A.wc));
+        float dh = -K3 * g.gamma * Hinv;
+        float rho_dh = dh * fmaf(1.5f, p.m, sum2(A.srt));
+        float wc_dh = dh * (1.5f + sum2(A.st));
+        float gf = K3 * Hinv;
+        float rinv = 1.0f / rho;
+        int out = c.perm[i];
+        if (out < o.n_out) {
+            o.rho[out] = rho;
+            o.wcount[out] = wc;
+            o.rho_dh[out] = rho_dh;
+            o.wcount_dh[out] = wc_dh;
+            o.div_v[out] = gf * sum2(A.Dn) * rinv;
+            o.curl_v[out] = gf * (sum2(A.Px) - sum2(A.Nx)) * rinv;
+            o.curl_v[o.n_out + out] = gf * (sum2(A.Py) - sum2(A.Ny)) * rinv;
+            o.curl_v[2 * o.n_out + out] = gf * (sum2(A.Pz) - sum2(A.Nz)) * rinv;
+            o.nngb[out] = nngb;
+        }
+    }
+    flush_stats<COUNT>(st, cand, hits);
+}
+
+}  // namespace pvsph

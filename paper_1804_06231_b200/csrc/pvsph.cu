@@ -11,7 +11,7 @@
 #include "calib.cuh"
 #include "common.cuh"
 #include "density.cuh"
-#include "density_v2.cuh"
+#include "density_v3.cuh"
 #include "sort.cuh"
 
 using namespace pvsph;
@@ -332,11 +332,11 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
         return check_launch();
     }
     long long warps = (cells->n + 31) / 32 + 1;
-    int blocks = grid_blocks(warps, V2_WARPS, 1 << 30);
+    int blocks = grid_blocks(warps, V3_WARPS, 1 << 30);
     if (stats)
-        k_density_all_v2<true><<<blocks, V2_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
+        k_density_all_v3<true><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
     else
-        k_density_all_v2<false><<<blocks, V2_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
+        k_density_all_v3<false><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
     return check_launch();
 }
 

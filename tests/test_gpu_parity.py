@@ -308,6 +308,29 @@ def test_on_axis_near_cutoff_pairs(pv):
     compare(run(pv, xyzh, vm, nc), ref, None, "on-axis")
 
 
+def test_close_pairs(pv):
+    """Pairs far inside the support (r from 2^-24 up to 0.1 H): the gradient terms stay accurate
+    (guards the x -> 0 limit of w'(x) ~ -6x, where naive branch-free forms cancel)."""
+    rng = np.random.default_rng(17)
+    nc = 4
+    h = np.float32(0.9 * 0.25 / synth.GAMMA)
+    H = synth.GAMMA * float(h)
+    rows = []
+    for k, r in enumerate([2 ** -24, 1e-6, 1e-5, 1e-4, 1e-3, 1e-2, 0.1 * H]):
+        base = np.array([0.1 + 0.11 * k, 0.4 + 0.05 * k, 0.6])
+        d = rng.standard_normal(3)
+        d /= np.linalg.norm(d)
+        rows += [base, base + max(r, 2 ** -24) * d]
+    x = np.floor(np.mod(np.array(rows), 1.0) * 2 ** 24) / 2 ** 24
+    xyzh = np.zeros((len(rows), 4), np.float32)
+    xyzh[:, :3] = x
+    xyzh[:, 3] = h
+    vm = np.zeros_like(xyzh)
+    vm[:, :3] = rng.standard_normal((len(rows), 3))
+    vm[:, 3] = 0.01
+    compare(run(pv, xyzh, vm, nc), oracle.bruteforce(xyzh, vm), None, "close pairs")
+
+
 def test_lattice_pin_on_gpu(pv):
     """Uniform lattice: nngb = 56 everywhere and rho/(mn) within 1e-5 of the golden value."""
     g = json.load(open(os.path.join(GOLDEN, "lattice_eta1.2348.json")))
