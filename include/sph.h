@@ -87,13 +87,16 @@ typedef struct sph_grid {
     float reserved2;    /* must be 0                                        */
 } sph_grid;
 
-/* One entry of a per-direction sorted list ("dist"/"index" of P:92):
- * key = cell-local projection on the unit axis of the direction (fp32 of
- * an fp64 dot product of x - cell corner), j = slot of the particle in the
- * cell-sorted arrays.  Entries of one cell are ascending in key, ties by
- * the particle's input index. */
+/* One entry of a per-direction sorted list ("dist"/"index" of P:92): the
+ * particle's position (x, y, z, fp32 copy) and j = its slot in the
+ * cell-sorted arrays.  Entries of one cell are ascending in the projection
+ * of the position on the unit axis of the direction, key = fp32(fp64
+ * (x - cell corner) . d/|d|), ties by the particle's input index.  The
+ * density sweeps compare projected separations (x_j - x_i) . axis computed
+ * from these positions; carrying the position makes one
+ * 16-byte load per candidate. */
 typedef struct sph_pv_entry {
-    float key;
+    float x, y, z;
     int32_t j;
 } sph_pv_entry;
 
@@ -107,7 +110,7 @@ typedef struct sph_pv_entry {
  *   pv[SPH_NDIR * capacity] sorted lists: direction d, slot range of cell c
  *                           at pv[d * capacity + cell_start[c] ...]
  * n is written by sph_build_cells (stored particles).  16-byte alignment
- * is required for xyzh and vm, 8 bytes for pv. */
+ * is required for xyzh, vm and pv. */
 typedef struct sph_cells {
     int64_t capacity;
     int64_t n;

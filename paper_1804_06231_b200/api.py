@@ -78,7 +78,7 @@ class Cells:
     vm: torch.Tensor
     perm: torch.Tensor
     cell_hmax: torch.Tensor
-    pv: torch.Tensor            # (13 * capacity, 2) int32 view of sph_pv_entry {float key; int j}
+    pv: torch.Tensor            # (13 * capacity, 4) float32 view of sph_pv_entry {float x, y, z; int j}
     slot_cell: torch.Tensor     # (capacity,) int32
     n: int = 0
 
@@ -91,7 +91,7 @@ class Cells:
                      torch.empty((cap, 4), dtype=torch.float32, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device),
                      torch.empty(nce, dtype=torch.float32, device=device),
-                     torch.empty((_lib.SPH_NDIR * cap, 2), dtype=torch.int32, device=device),
+                     torch.empty((_lib.SPH_NDIR * cap, 4), dtype=torch.float32, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device))
 
     def struct(self) -> SphCells:
@@ -103,11 +103,12 @@ class Cells:
         s.slot_cell = self.slot_cell.data_ptr()
         return s
 
-    def pv_keys(self) -> torch.Tensor:
-        return self.pv[:, 0].view(torch.float32).view(_lib.SPH_NDIR, self.capacity)
+    def pv_pos(self) -> torch.Tensor:
+        """(13, capacity, 3) positions stored in the sorted lists."""
+        return self.pv[:, :3].reshape(_lib.SPH_NDIR, self.capacity, 3)
 
     def pv_slots(self) -> torch.Tensor:
-        return self.pv[:, 1].view(_lib.SPH_NDIR, self.capacity)
+        return self.pv[:, 3].contiguous().view(torch.int32).view(_lib.SPH_NDIR, self.capacity)
 
 
 FIELDS = ("rho", "wcount", "rho_dh", "wcount_dh", "div_v", "curl_x", "curl_y", "curl_z", "nngb")

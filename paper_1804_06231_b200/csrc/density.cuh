@@ -98,12 +98,12 @@ template <bool COUNT>
 __device__ __forceinline__ void sweep_self(const DevCells &c, const IPart &p, int s0, int s1, Acc &a,
                                            unsigned &cand, unsigned &hits)
 {
-    const sph_pv_entry *L = c.pv;
+    const float4 *L = reinterpret_cast<const float4 *>(c.pv);
     for (int q = s0; q < s1; ++q) {
-        int j = L[q].j;
+        const float4 e = L[q];
+        const int j = __float_as_int(e.w);
         if (j == p.slot) continue;
-        float4 pj = c.xyzh[j];
-        float dx = p.x - pj.x, dy = p.y - pj.y, dz = p.z - pj.z;
+        float dx = p.x - e.x, dy = p.y - e.y, dz = p.z - e.z;
         float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         if (COUNT) ++cand;
         if (r2 < p.H2) {
@@ -113,16 +113,33 @@ __device__ __forceinline__ void sweep_self(const DevCells &c, const IPart &p, in
     }
 }
 
+// Unit vector of sort direction d (fp32).
+__device__ __forceinline__ void dir_unit(int d, float &ax, float &ay, float &az)
+{
+    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+    const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
+    const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
+    ax = (float)a0 * inv;
+    ay = (float)a1 * inv;
+    az = (float)a2 * inv;
+}
+
 // Neighbour cell at offset (ox,oy,oz) with periodic-image flags sh[k] in
-// {-1,0,+1} (neighbour lies beyond the low / high face of the box).
+// {-1,0,+1} (neighbour lies beyond the low / high face of the box).  The list
+// of cj sorted along d = canon(o) is swept from the end nearest to the home
+// cell; the sweep stops at the first j whose projected separation
+// sep = (x_j - x_i) . o/|o| reaches H_i + delta (Code 2; the per-particle
+// bound of P:156).  sep is computed from the exact coordinate differences, so no
+// cell corner enters.
 template <bool COUNT>
 __device__ __forceinline__ void sweep_pair(const DevGrid &g, const DevCells &c, const IPart &p, int cj, int ox, int oy,
                                            int oz, const int sh[3], Acc &a, unsigned &cand, unsigned &hits)
 {
     int s;
     int d = canon_dir(ox, oy, oz, s);
-    float key_i = pv_key(p.u0, p.u1, p.u2, d);
-    float B = p.Hd - g.q[d];                 // window: s (key_j - key_i) < B
+    float ax, ay, az;
+    dir_unit(d, ax, ay, az);
+    const float sx = -s * ax, sy = -s * ay, sz = -s * az;   // sep = (dx, dy, dz) . (sx, sy, sz), dx = x_i - x_j
     // exact-difference coordinates
     float xi = sh[0] > 0 ? p.x - g.boxf[0] : p.x;
     float yi = sh[1] > 0 ? p.y - g.boxf[1] : p.y;
@@ -130,35 +147,19 @@ __device__ __forceinline__ void sweep_pair(const DevGrid &g, const DevCells &c, 
     float sjx = sh[0] < 0 ? g.boxf[0] : 0.0f;
     float sjy = sh[1] < 0 ? g.boxf[1] : 0.0f;
     float sjz = sh[2] < 0 ? g.boxf[2] : 0.0f;
-    const sph_pv_entry *L = c.pv + (long long)d * c.cap;
+    const float4 *L = reinterpret_cast<const float4 *>(c.pv) + (long long)d * c.cap;
     int s0 = c.cell_start[cj], s1 = c.cell_start[cj + 1];
-    if (s > 0) {
-        float lim = key_i + B;
-        for (int q = s0; q < s1; ++q) {
-            sph_pv_entry e = L[q];
-            if (!(e.key < lim)) break;       // sorted early exit (Code 2)
-            float4 pj = c.xyzh[e.j];
-            float dx = xi - (pj.x - sjx), dy = yi - (pj.y - sjy), dz = zi - (pj.z - sjz);
-            float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            if (COUNT) ++cand;
-            if (r2 < p.H2) {
-                interact(p, dx, dy, dz, r2, c.vm[e.j], a);
-                if (COUNT) ++hits;
-            }
-        }
-    } else {
-        float lim = key_i - B;
-        for (int q = s1 - 1; q >= s0; --q) {
-            sph_pv_entry e = L[q];
-            if (!(e.key > lim)) break;
-            float4 pj = c.xyzh[e.j];
-            float dx = xi - (pj.x - sjx), dy = yi - (pj.y - sjy), dz = zi - (pj.z - sjz);
-            float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            if (COUNT) ++cand;
-            if (r2 < p.H2) {
-                interact(p, dx, dy, dz, r2, c.vm[e.j], a);
-                if (COUNT) ++hits;
-            }
+    int q = s > 0 ? s0 : s1 - 1;
+    const int qend = s > 0 ? s1 : s0 - 1;
+    for (; q != qend; q += s) {
+        const float4 e = L[q];
+        float dx = xi - (e.x - sjx), dy = yi - (e.y - sjy), dz = zi - (e.z - sjz);
+        if (!(fmaf(dx, sx, fmaf(dy, sy, dz * sz)) < p.Hd)) break;   // sorted early exit
+        float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        if (COUNT) ++cand;
+        if (r2 < p.H2) {
+            interact(p, dx, dy, dz, r2, c.vm[__float_as_int(e.w)], a);
+            if (COUNT) ++hits;
         }
     }
 }

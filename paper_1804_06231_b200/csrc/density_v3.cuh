@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(V3_WARPS * 32, 4) k_density_all_v3(DevGrid g, 
         p.slot = -1;
         hc.ixl = hc.iy = hc.iz = hc.ixg = 0;
     }
-    const float ux = (float)p.u0, uy = (float)p.u1, uz = (float)p.u2;   // cell-local coordinates
+    const int isafe = active ? i : slot_lo;                            // a valid slot for dummy loads
     const f2 Hinv2 = bc2(p.Hinv);
 
     Acc2 A;
@@ -163,10 +163,26 @@ __global__ void __launch_bounds__(V3_WARPS * 32, 4) k_density_all_v3(DevGrid g, 
         }
     };
 
+    // queue hit number `tail` in half (tail & 1) of its pair slot
+    auto push = [&](float ddx, float ddy, float ddz, int j, int kd) {
+        const float4 vj = c.vm[j];
+        float *slot = &Q[(tail >> 1) & (V3_QP - 1)][0][lane].x + (tail & 1);
+        slot[0 * 64] = ddx;
+        slot[1 * 64] = ddy;
+        slot[2 * 64] = ddz;
+        slot[3 * 64] = vj.w;
+        slot[4 * 64] = vj.x - p.vx;
+        slot[5 * 64] = vj.y - p.vy;
+        slot[6 * 64] = vj.z - p.vz;
+        ++tail;
+        ++nngb;
+        if (COUNT) ++hits[kd];
+    };
+
     for (int a = 0; a < 14; ++a) {
         // lane's two windows for this pass: a = 0 the self cell; a = 1 + d the +d, -d neighbours
         const int d = a == 0 ? 0 : a - 1;
-        const sph_pv_entry *L = c.pv + (long long)d * c.cap;
+        const float4 *L = reinterpret_cast<const float4 *>(c.pv) + (long long)d * c.cap;
         const int kind = a == 0 ? 0 : kind_of_dir(d);
         int qb0 = 0, len0 = 0, qb1 = 0, len1 = 0, code0 = 0, code1 = 0;
         if (active) {
@@ -175,73 +191,91 @@ __global__ void __launch_bounds__(V3_WARPS * 32, 4) k_density_all_v3(DevGrid g, 
                 len0 = c.cell_start[home + 1] - qb0;
             } else {
                 const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
-                const float inv = kind == 1 ? 1.0f : (kind == 2 ? 0.70710678f : 0.57735027f);
-                const float key_i = fmaf(ux, (float)a0 * inv, fmaf(uy, (float)a1 * inv, uz * ((float)a2 * inv)));
-                const float B = p.Hd - g.q[d];
-                int cj, sh[3];
-                if (neighbour(g, hc, a0, a1, a2, cj, sh)) {        // +d: prefix {key < key_i + B}
-                    const float lim = key_i + B;
-                    int lo = c.cell_start[cj], hi = c.cell_start[cj + 1];
-                    qb0 = lo;
-                    while (lo < hi) {
-                        int mid = (lo + hi) >> 1;
-                        if (L[mid].key < lim) lo = mid + 1; else hi = mid;
-                    }
-                    len0 = lo - qb0;
-                    code0 = image_code(sh);
-                }
-                if (neighbour(g, hc, -a0, -a1, -a2, cj, sh)) {     // -d: suffix {key > key_i - B}
-                    const float lim = key_i - B;
-                    int lo = c.cell_start[cj], hi = c.cell_start[cj + 1];
-                    const int end = hi;
-                    while (lo < hi) {
-                        int mid = (lo + hi) >> 1;
-                        if (L[mid].key > lim) hi = mid; else lo = mid + 1;
-                    }
-                    qb1 = lo;
-                    len1 = end - lo;
-                    code1 = image_code(sh);
-                }
-            }
-        }
-        const int total = len0 + len1;
-        const int trip = __reduce_max_sync(0xffffffffu, total);
-        for (int t = 0; t < trip; ++t) {
-            if (t < total) {
-                const bool first = t < len0;
-                const int q = first ? qb0 + t : qb1 + (t - len0);
-                const int code = first ? code0 : code1;
-                const int j = L[q].j;
-                const float4 pj = c.xyzh[j];
-                float xi = p.x, yi = p.y, zi = p.z, xj = pj.x, yj = pj.y, zj = pj.z;
-                if (code) {                                    // periodic image: exact differences (R4)
+                float ax, ay, az;
+                dir_unit(d, ax, ay, az);
+                // separation along the pair axis of x_j - x_i from exact differences;
+                // sorted lists make it monotone in q, so the window is found by bisection
+                auto sep_of = [&](int q, int code) {
+                    const float4 e = L[q];
+                    float xi = p.x, yi = p.y, zi = p.z, xj = e.x, yj = e.y, zj = e.z;
                     if (code & 1) xi -= g.boxf[0];
                     if (code & 2) xj -= g.boxf[0];
                     if (code & 4) yi -= g.boxf[1];
                     if (code & 8) yj -= g.boxf[1];
                     if (code & 16) zi -= g.boxf[2];
                     if (code & 32) zj -= g.boxf[2];
+                    return fmaf(xj - xi, ax, fmaf(yj - yi, ay, (zj - zi) * az));
+                };
+                int cj, sh[3];
+                if (neighbour(g, hc, a0, a1, a2, cj, sh)) {        // +d: prefix {sep < H + delta}
+                    code0 = image_code(sh);
+                    int lo = c.cell_start[cj], hi = c.cell_start[cj + 1];
+                    qb0 = lo;
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (sep_of(mid, code0) < p.Hd) lo = mid + 1; else hi = mid;
+                    }
+                    len0 = lo - qb0;
                 }
-                const float ddx = xi - xj, ddy = yi - yj, ddz = zi - zj;
-                const float r2 = fmaf(ddx, ddx, fmaf(ddy, ddy, ddz * ddz));
-                if (COUNT && (a != 0 || j != i)) ++cand[kind];
-                if (r2 < p.H2 && (a != 0 || j != i)) {
-                    const float4 vj = c.vm[j];
-                    float *slot = &Q[(tail >> 1) & (V3_QP - 1)][0][lane].x + (tail & 1);
-                    slot[0 * 64] = ddx;
-                    slot[1 * 64] = ddy;
-                    slot[2 * 64] = ddz;
-                    slot[3 * 64] = vj.w;
-                    slot[4 * 64] = vj.x - p.vx;
-                    slot[5 * 64] = vj.y - p.vy;
-                    slot[6 * 64] = vj.z - p.vz;
-                    ++tail;
-                    ++nngb;
-                    if (COUNT) ++hits[kind];
+                if (neighbour(g, hc, -a0, -a1, -a2, cj, sh)) {     // -d: suffix {-sep < H + delta}
+                    code1 = image_code(sh);
+                    int lo = c.cell_start[cj], hi = c.cell_start[cj + 1];
+                    const int end = hi;
+                    while (lo < hi) {
+                        int mid = (lo + hi) >> 1;
+                        if (-sep_of(mid, code1) < p.Hd) hi = mid; else lo = mid + 1;
+                    }
+                    qb1 = lo;
+                    len1 = end - lo;
                 }
             }
+        }
+        const int total = len0 + len1;
+        const int trip = __reduce_max_sync(0xffffffffu, total);
+        // warp-uniform: periodic-image arithmetic only in warps that need it
+        const bool any_image = __any_sync(0xffffffffu, (code0 | code1) != 0);
+        const bool selfpass = a == 0;
+        // Two candidates per iteration: both loads issued first, the pair tested in f32x2.
+        // slot of candidate t of the lane's concatenated window (i itself past the end: no load)
+        // list entry of candidate t of the lane's concatenated window (own slot past the end)
+        auto eat = [&](int t) { return t < total ? L[t < len0 ? qb0 + t : qb1 + (t - len0)] : c.xyzh[isafe]; };
+        for (int t = 0; t < trip; t += 2) {
+            const bool ok0 = t < total, ok1 = t + 1 < total;
+            const float4 pa = eat(t), pb = eat(t + 1);
+            const int j0 = ok0 ? __float_as_int(pa.w) : i, j1 = ok1 ? __float_as_int(pb.w) : i;
+            float xa = p.x, ya = p.y, za = p.z, xb = p.x, yb = p.y, zb = p.z;
+            float xja = pa.x, yja = pa.y, zja = pa.z, xjb = pb.x, yjb = pb.y, zjb = pb.z;
+            if (any_image) {                               // periodic image: exact differences (R4)
+                const int ca = t < len0 ? code0 : code1, cb = t + 1 < len0 ? code0 : code1;
+                if (ca & 1) xa -= g.boxf[0];
+                if (ca & 2) xja -= g.boxf[0];
+                if (ca & 4) ya -= g.boxf[1];
+                if (ca & 8) yja -= g.boxf[1];
+                if (ca & 16) za -= g.boxf[2];
+                if (ca & 32) zja -= g.boxf[2];
+                if (cb & 1) xb -= g.boxf[0];
+                if (cb & 2) xjb -= g.boxf[0];
+                if (cb & 4) yb -= g.boxf[1];
+                if (cb & 8) yjb -= g.boxf[1];
+                if (cb & 16) zb -= g.boxf[2];
+                if (cb & 32) zjb -= g.boxf[2];
+            }
+            const f2 dx = sub2(pk(xa, xb), pk(xja, xjb));
+            const f2 dy = sub2(pk(ya, yb), pk(yja, yjb));
+            const f2 dz = sub2(pk(za, zb), pk(zja, zjb));
+            float r2a, r2b;
+            upk(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))), r2a, r2b);
+            const bool ca_ok = ok0 && (!selfpass || j0 != i), cb_ok = ok1 && (!selfpass || j1 != i);
+            if (COUNT) cand[kind] += (unsigned)ca_ok + (unsigned)cb_ok;
+            float dxa, dxb, dya, dyb, dza, dzb;
+            upk(dx, dxa, dxb);
+            upk(dy, dya, dyb);
+            upk(dz, dza, dzb);
+            if (ca_ok && r2a < p.H2) push(dxa, dya, dza, j0, kind);
+            if (cb_ok && r2b < p.H2) push(dxb, dyb, dzb, j1, kind);
+            // two pushes per iteration: drain before a queue could overflow
             const unsigned n = tail - head;
-            if (__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= 2 * V3_QP - 1))
+            if (__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= 2 * V3_QP - 2))
                 drain(false);
         }
     }

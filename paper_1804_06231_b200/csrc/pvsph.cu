@@ -79,7 +79,7 @@ bool cells_ok(const sph_cells *c)
     return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->pv && c->slot_cell &&
            c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
-           ((uintptr_t)c->pv % 8 == 0);
+           ((uintptr_t)c->pv % 16 == 0);
 }
 
 DevCells dev_cells(const sph_cells *c)

@@ -5,6 +5,7 @@
 // Key of particle k in cell c along d: fp32( (x_k - corner_c) . d/|d| ),
 // the difference and dot product in fp64.  Order: ascending
 // key, ties by input index perm[k] -- deterministic whatever the slot order.
+// Each entry stores the particle's position and slot (sph_pv_entry).
 //
 // Small cells (n <= SORT_SMALL): one warp per cell, composite 64-bit keys
 // (orderable key << 32 | input index) staged in shared memory, rank by
@@ -57,12 +58,14 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCe
         double corner[3];
         cell_corner(g, cell, corner);
         double u[PER][3];
+        float4 pos[PER];
         unsigned tie[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             int e = lane + 32 * k;
             if (e < n) {
                 float4 p = c.xyzh[s0 + e];
+                pos[k] = p;
                 u[k][0] = (double)p.x - corner[0];
                 u[k][1] = (double)p.y - corner[1];
                 u[k][2] = (double)p.z - corner[2];
@@ -89,7 +92,9 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCe
                     int r = 0;
                     for (int m = 0; m < n; ++m) r += sh[w][m] < comp[k];
                     sph_pv_entry ent;
-                    ent.key = key[k];
+                    ent.x = pos[k].x;
+                    ent.y = pos[k].y;
+                    ent.z = pos[k].z;
                     ent.j = s0 + e;
                     pv[(long long)d * c.cap + s0 + r] = ent;
                 }
@@ -116,8 +121,9 @@ __global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells
         bool mine = e < n;
         double u0 = 0, u1 = 0, u2 = 0;
         unsigned tie = 0;
+        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
         if (mine) {
-            float4 p = c.xyzh[s0 + e];
+            p = c.xyzh[s0 + e];
             u0 = (double)p.x - corner[0];
             u1 = (double)p.y - corner[1];
             u2 = (double)p.z - corner[2];
@@ -141,7 +147,9 @@ __global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells
             }
             if (mine) {
                 sph_pv_entry ent;
-                ent.key = key;
+                ent.x = p.x;
+                ent.y = p.y;
+                ent.z = p.z;
                 ent.j = s0 + e;
                 pv[(long long)d * c.cap + s0 + r] = ent;
             }
