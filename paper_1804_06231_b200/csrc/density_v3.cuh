@@ -32,6 +32,8 @@
 #include "density.cuh"
 #include "packed.cuh"
 
+#include <type_traits>
+
 namespace pvsph {
 
 constexpr int V3_WARPS = 4;
@@ -60,7 +62,7 @@ __device__ __forceinline__ void interact_pair(f2 Hinv2, f2 dx, f2 dy, f2 dz, f2 
     float r2a, r2b;
     upk(r2, r2a, r2b);
     // r^2 = 0 (coincident particles): rinv stays finite, x = 0 and w'(0) = 0 make every gradient term 0
-    f2 rinv = pk(rsqrtf(fmaxf(r2a, 1e-30f)), rsqrtf(fmaxf(r2b, 1e-30f)));
+    f2 rinv = pk(rsqrt_fast(fmaxf(r2a, 1e-30f)), rsqrt_fast(fmaxf(r2b, 1e-30f)));
     f2 x = mul2(mul2(r2, rinv), Hinv2);
     f2 u = sub2(bc2(1.0f), x);
     f2 v = fma2(bc2(-2.0f), x, bc2(1.0f));
@@ -76,21 +78,21 @@ __device__ __forceinline__ void interact_pair(f2 Hinv2, f2 dx, f2 dy, f2 dz, f2 
     // precision for x -> 0 (w' ~ -6x while v^2, u^2 ~ 1)
     f2 dw = mul2(mul2(bc2(-3.0f), mk), mul2(mn, add2(u, v)));
     m = mul2(m, mk);
-    A.rho = fma2(m, w, A.rho);
-    A.wc = add2(A.wc, w);
+    acc_fma2(A.rho, m, w);
+    acc_add2(A.wc, w);
     f2 t = fma2(x, dw, mul2(bc2(3.0f), w));
-    A.srt = fma2(m, t, A.srt);
-    A.st = add2(A.st, t);
+    acc_fma2(A.srt, m, t);
+    acc_add2(A.st, t);
     f2 nvdx = fma2(nvx, dx, fma2(nvy, dy, mul2(nvz, dz)));
     f2 fac = mul2(mul2(m, dw), rinv);
-    A.Dn = fma2(fac, nvdx, A.Dn);
+    acc_fma2(A.Dn, fac, nvdx);
     f2 fx = mul2(fac, nvx), fy = mul2(fac, nvy), fz = mul2(fac, nvz);
-    A.Px = fma2(fz, dy, A.Px);
-    A.Nx = fma2(fy, dz, A.Nx);
-    A.Py = fma2(fx, dz, A.Py);
-    A.Ny = fma2(fz, dx, A.Ny);
-    A.Pz = fma2(fy, dx, A.Pz);
-    A.Nz = fma2(fx, dy, A.Nz);
+    acc_fma2(A.Px, fz, dy);
+    acc_fma2(A.Nx, fy, dz);
+    acc_fma2(A.Py, fx, dz);
+    acc_fma2(A.Ny, fz, dx);
+    acc_fma2(A.Pz, fy, dx);
+    acc_fma2(A.Nz, fx, dy);
 }
 
 __device__ __forceinline__ int image_code(const int sh[3])
@@ -108,7 +110,7 @@ __device__ __forceinline__ int kind_of_dir(int d)
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(V3_WARPS * 32, 4) k_density_all_v3(DevGrid g, DevCells c, DevOut o, sph_stats *st)
+__global__ void __launch_bounds__(V3_WARPS * 32, 6) k_density_all_v3(DevGrid g, DevCells c, DevOut o, sph_stats *st)
 {
     __shared__ float2 qp[V3_WARPS][V3_QP][V3_NC][32];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -237,47 +239,51 @@ __global__ void __launch_bounds__(V3_WARPS * 32, 4) k_density_all_v3(DevGrid g, 
         const bool selfpass = a == 0;
         // Two candidates per iteration: both loads issued first, the pair tested in f32x2.
         // slot of candidate t of the lane's concatenated window (i itself past the end: no load)
-        // list entry of candidate t of the lane's concatenated window (own slot past the end)
-        auto eat = [&](int t) { return t < total ? L[t < len0 ? qb0 + t : qb1 + (t - len0)] : c.xyzh[isafe]; };
-        for (int t = 0; t < trip; t += 2) {
-            const bool ok0 = t < total, ok1 = t + 1 < total;
-            const float4 pa = eat(t), pb = eat(t + 1);
-            const int j0 = ok0 ? __float_as_int(pa.w) : i, j1 = ok1 ? __float_as_int(pb.w) : i;
-            float xa = p.x, ya = p.y, za = p.z, xb = p.x, yb = p.y, zb = p.z;
-            float xja = pa.x, yja = pa.y, zja = pa.z, xjb = pb.x, yjb = pb.y, zjb = pb.z;
-            if (any_image) {                               // periodic image: exact differences (R4)
-                const int ca = t < len0 ? code0 : code1, cb = t + 1 < len0 ? code0 : code1;
-                if (ca & 1) xa -= g.boxf[0];
-                if (ca & 2) xja -= g.boxf[0];
-                if (ca & 4) ya -= g.boxf[1];
-                if (ca & 8) yja -= g.boxf[1];
-                if (ca & 16) za -= g.boxf[2];
-                if (ca & 32) zja -= g.boxf[2];
-                if (cb & 1) xb -= g.boxf[0];
-                if (cb & 2) xjb -= g.boxf[0];
-                if (cb & 4) yb -= g.boxf[1];
-                if (cb & 8) yjb -= g.boxf[1];
-                if (cb & 16) zb -= g.boxf[2];
-                if (cb & 32) zjb -= g.boxf[2];
+        // Candidates t, t+1 of the lane's concatenated window; two independent loads in
+        // flight per iteration.  IMAGE (warp-uniform) selects the periodic-image variant.
+        const float4 *const Lp = L;
+        const float4 *const Ldummy = c.xyzh + isafe;      // valid address past the end
+        auto sweep = [&](auto image_tag) {
+            constexpr bool IMAGE = decltype(image_tag)::value;
+            for (int t = 0; t < trip; t += 2) {
+                const bool ok0 = t < total, ok1 = t + 1 < total;
+                const bool f0 = t < len0, f1 = t + 1 < len0;
+                const float4 ea = *(ok0 ? Lp + (f0 ? qb0 + t : qb1 + (t - len0)) : Ldummy);
+                const float4 eb = *(ok1 ? Lp + (f1 ? qb0 + t + 1 : qb1 + (t + 1 - len0)) : Ldummy);
+                float xia = p.x, yia = p.y, zia = p.z, xja = ea.x, yja = ea.y, zja = ea.z;
+                float xib = p.x, yib = p.y, zib = p.z, xjb = eb.x, yjb = eb.y, zjb = eb.z;
+                if constexpr (IMAGE) {                     // periodic image: exact differences (R4)
+                    const int ca = f0 ? code0 : code1, cb = f1 ? code0 : code1;
+                    if (ca & 1) xia -= g.boxf[0];
+                    if (ca & 2) xja -= g.boxf[0];
+                    if (ca & 4) yia -= g.boxf[1];
+                    if (ca & 8) yja -= g.boxf[1];
+                    if (ca & 16) zia -= g.boxf[2];
+                    if (ca & 32) zja -= g.boxf[2];
+                    if (cb & 1) xib -= g.boxf[0];
+                    if (cb & 2) xjb -= g.boxf[0];
+                    if (cb & 4) yib -= g.boxf[1];
+                    if (cb & 8) yjb -= g.boxf[1];
+                    if (cb & 16) zib -= g.boxf[2];
+                    if (cb & 32) zjb -= g.boxf[2];
+                }
+                const float dxa = xia - xja, dya = yia - yja, dza = zia - zja;
+                const float dxb = xib - xjb, dyb = yib - yjb, dzb = zib - zjb;
+                const float r2a = fmaf(dxa, dxa, fmaf(dya, dya, dza * dza));
+                const float r2b = fmaf(dxb, dxb, fmaf(dyb, dyb, dzb * dzb));
+                const int j0 = __float_as_int(ea.w), j1 = __float_as_int(eb.w);
+                const bool ca_ok = ok0 && (!selfpass || j0 != i), cb_ok = ok1 && (!selfpass || j1 != i);
+                if (COUNT) cand[kind] += (unsigned)ca_ok + (unsigned)cb_ok;
+                if (ca_ok && r2a < p.H2) push(dxa, dya, dza, j0, kind);
+                if (cb_ok && r2b < p.H2) push(dxb, dyb, dzb, j1, kind);
+                // two pushes per iteration: drain before a queue could overflow
+                const unsigned n = tail - head;
+                if (__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 ||
+                    __any_sync(0xffffffffu, n >= 2 * V3_QP - 2))
+                    drain(false);
             }
-            const f2 dx = sub2(pk(xa, xb), pk(xja, xjb));
-            const f2 dy = sub2(pk(ya, yb), pk(yja, yjb));
-            const f2 dz = sub2(pk(za, zb), pk(zja, zjb));
-            float r2a, r2b;
-            upk(fma2(dx, dx, fma2(dy, dy, mul2(dz, dz))), r2a, r2b);
-            const bool ca_ok = ok0 && (!selfpass || j0 != i), cb_ok = ok1 && (!selfpass || j1 != i);
-            if (COUNT) cand[kind] += (unsigned)ca_ok + (unsigned)cb_ok;
-            float dxa, dxb, dya, dyb, dza, dzb;
-            upk(dx, dxa, dxb);
-            upk(dy, dya, dyb);
-            upk(dz, dza, dzb);
-            if (ca_ok && r2a < p.H2) push(dxa, dya, dza, j0, kind);
-            if (cb_ok && r2b < p.H2) push(dxb, dyb, dzb, j1, kind);
-            // two pushes per iteration: drain before a queue could overflow
-            const unsigned n = tail - head;
-            if (__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= 2 * V3_QP - 2))
-                drain(false);
-        }
+        };
+        if (any_image) sweep(std::true_type{}); else sweep(std::false_type{});
     }
     while (__any_sync(0xffffffffu, tail != head)) drain(true);
 

@@ -43,6 +43,22 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c)
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
+// acc += a * b and acc += a, updating the accumulator register pair in place
+__device__ __forceinline__ void acc_fma2(f2 &acc, f2 a, f2 b)
+{
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ void acc_add2(f2 &acc, f2 a)
+{
+    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(a));
+}
+// 1/sqrt(x) for normal x > 0 (MUFU.RSQ, no denormal fix-up; callers clamp x >= 1e-30)
+__device__ __forceinline__ float rsqrt_fast(float x)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float sum2(f2 v)
 {
     float a, b;
