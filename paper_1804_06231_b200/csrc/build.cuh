@@ -95,9 +95,9 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *sh, int &total)
     return off + x - v;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int *__restrict__ count, long long n,
-                                                        int *__restrict__ start, int *__restrict__ tile_sum,
-                                                        unsigned *status)
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int *count, long long n, int *start,
+                                                        int *__restrict__ tile_sum, unsigned *status,
+                                                        int vmax = SPH_MAX_CELL)
 {
     __shared__ int sh[32];
     long long base = (long long)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_V;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int *__restrict__ c
 #pragma unroll
     for (int k = 0; k < SCAN_V; ++k) {
         v[k] = base + k < n ? count[base + k] : 0;
-        if (v[k] > SPH_MAX_CELL) set_status(status, ST_ECAPACITY);
+        if (v[k] > vmax) set_status(status, ST_ECAPACITY);
         s += v[k];
     }
     int total;

@@ -109,17 +109,64 @@ __device__ __forceinline__ int kind_of_dir(int d)
     return (d == 0 || d == 2 || d == 8) ? 1 : ((d == 4 || d == 6 || d == 10 || d == 12) ? 3 : 2);
 }
 
+// ---- traversal order: owned rows (ix, iy) in ROW_TILE x ROW_TILE tiles -----------
+constexpr int ROW_TILE = 4;
+
+__host__ __device__ __forceinline__ int row_tiles_y(const DevGrid &g) { return (g.ny + ROW_TILE - 1) / ROW_TILE; }
+
+__host__ __device__ __forceinline__ long long row_nkeys(const DevGrid &g)
+{
+    const int nxo = g.x_hi - g.x_lo;
+    return (long long)((nxo + ROW_TILE - 1) / ROW_TILE) * row_tiles_y(g) * ROW_TILE * ROW_TILE;
+}
+
+// key -> owned row (ix relative to x_lo, iy); may fall outside the grid (ragged tiles)
+__device__ __forceinline__ void row_of_key(const DevGrid &g, int key, int &ix, int &iy)
+{
+    const int tile = key / (ROW_TILE * ROW_TILE), wi = key % (ROW_TILE * ROW_TILE);
+    const int nty = row_tiles_y(g);
+    ix = (tile / nty) * ROW_TILE + wi / ROW_TILE;
+    iy = (tile % nty) * ROW_TILE + wi % ROW_TILE;
+}
+
+// chunks[key] = number of 32-slot chunks of the row (0 outside the grid)
+__global__ void k_row_chunks(DevGrid g, const int *__restrict__ cell_start, int *__restrict__ chunks, int nkeys)
+{
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nkeys; k += gridDim.x * blockDim.x) {
+        int ix, iy;
+        row_of_key(g, k, ix, iy);
+        int nch = 0;
+        if (ix < g.x_hi - g.x_lo && iy < g.ny) {
+            const long long first = ((long long)(ix + g.ghost_x) * g.ny + iy) * g.nz;
+            nch = (cell_start[first + g.nz] - cell_start[first] + 31) >> 5;
+        }
+        chunks[k] = nch;
+    }
+}
+
 template <bool COUNT>
-__global__ void __launch_bounds__(V3_WARPS * 32, 6) k_density_all_v3(DevGrid g, DevCells c, DevOut o, sph_stats *st)
+__global__ void __launch_bounds__(V3_WARPS * 32, 6) k_density_all_v3(DevGrid g, DevCells c, DevOut o, sph_stats *st,
+                                                                       const int *row_prefix, int nkeys)
 {
     __shared__ float2 qp[V3_WARPS][V3_QP][V3_NC][32];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const long long plane = (long long)g.ny * g.nz;
-    const int slot_lo = c.cell_start[g.ghost_x ? plane : 0];
-    const int slot_hi = c.cell_start[g.ghost_x ? (g.nxl - 1) * plane : g.ncell];
-    const long long base = (long long)slot_lo + ((long long)blockIdx.x * V3_WARPS + wl) * 32;
-    if (base >= slot_hi) return;                       // whole warp idle (warp-uniform)
-    const int i = (int)base + lane;
+    // work unit of this warp: chunk w of the owned rows (ix, iy) taken in ROW_TILE x ROW_TILE
+    // tiles (k_row_chunks), so that concurrently running warps share their neighbour
+    // lists in L2; 32 consecutive slots of one row, lane = particle
+    const int w = (int)((long long)blockIdx.x * V3_WARPS + wl);
+    if (w >= row_prefix[nkeys]) return;                // whole warp idle (warp-uniform)
+    int klo = 0, khi = nkeys;                          // row_prefix[klo] <= w < row_prefix[khi]
+    while (khi - klo > 1) {
+        const int mid = (klo + khi) >> 1;
+        if (row_prefix[mid] <= w) klo = mid; else khi = mid;
+    }
+    int rix, riy;
+    row_of_key(g, klo, rix, riy);
+    const long long first_cell = ((long long)(rix + g.ghost_x) * g.ny + riy) * g.nz;
+    const int slot_lo = c.cell_start[first_cell];
+    const int slot_hi = c.cell_start[first_cell + g.nz];
+    const int i = slot_lo + 32 * (w - row_prefix[klo]) + lane;
     const bool active = i < slot_hi;
 
 #pragma unroll

@@ -120,11 +120,12 @@ DevOut dev_out(const sph_out *o)
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
-    size_t status, cell_of, rank, perm_tmp, count, tile_sum, big_count, big_items, total;
+    size_t status, cell_of, rank, perm_tmp, count, tile_sum, big_count, big_items, rows, rows_sum, total;
 };
 
-Ws ws_layout(long long ncell, long long n)
+Ws ws_layout(const DevGrid &g, long long n)
 {
+    const long long ncell = g.ncell;
     Ws w;
     size_t o = 0;
     w.status = o;
@@ -144,6 +145,11 @@ Ws ws_layout(long long ncell, long long n)
     o = align_up(o + 4, 256);
     w.big_items = o;
     o = align_up(o + 8 * (size_t)(n / 64 + 64), 256);
+    const long long nkeys = row_nkeys(g);
+    w.rows = o;
+    o = align_up(o + 4 * (size_t)(nkeys + 1), 256);
+    w.rows_sum = o;
+    o = align_up(o + 4 * (size_t)((nkeys + SCAN_TILE - 1) / SCAN_TILE + 1), 256);
     w.total = o;
     return w;
 }
@@ -179,7 +185,7 @@ size_t sph_workspace_bytes(const sph_grid *grid, int64_t n_total)
 {
     DevGrid g;
     if (make_grid(grid, g) != SPH_OK || n_total < 0) return 0;
-    return ws_layout(g.ncell, n_total).total;
+    return ws_layout(g, n_total).total;
 }
 
 int sph_status_reset(void *ws, void *stream)
@@ -201,7 +207,7 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     if (n > 0 && (!xyzh_in || !vm_in)) return SPH_EINVAL;
     if (((uintptr_t)xyzh_in % 16) || ((uintptr_t)vm_in % 16)) return SPH_EINVAL;
     if (n > cells->capacity) return SPH_ECAPACITY;
-    Ws w = ws_layout(g.ncell, cells->capacity);
+    Ws w = ws_layout(g, cells->capacity);
     if (ws_bytes < w.total) return SPH_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e;
@@ -248,7 +254,7 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     if (!cells_ok(cells) || !ws) return SPH_EINVAL;
     if (cell_end < 0) cell_end = g.ncell;
     if (cell_begin < 0 || cell_begin > cell_end || cell_end > g.ncell) return SPH_EINVAL;
-    Ws w = ws_layout(g.ncell, cells->capacity);
+    Ws w = ws_layout(g, cells->capacity);
     if (ws_bytes < w.total) return SPH_EINVAL;
     if (cell_end == cell_begin) return SPH_OK;
     cudaStream_t s = (cudaStream_t)stream;
@@ -331,12 +337,24 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
             k_density_all_v1<false><<<blocks, V1_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
         return check_launch();
     }
-    long long warps = (cells->n + 31) / 32 + 1;
+    Ws w = ws_layout(g, cells->capacity);
+    if (ws_bytes < w.total) return SPH_EINVAL;
+    const int nkeys = (int)row_nkeys(g);
+    int *rows = at<int>(ws, w.rows), *rows_sum = at<int>(ws, w.rows_sum);
+    k_row_chunks<<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, cells->cell_start, rows, nkeys);
+    const long long ntiles = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
+    unsigned *status = at<unsigned>(ws, w.status);
+    k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
+    k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles, rows, nkeys);
+    k_scan_add<<<(int)ntiles, SCAN_T, 0, s>>>(rows, nkeys, rows_sum);
+    const long long rows_total = (long long)(g.x_hi - g.x_lo) * g.ny;
+    const long long warps = (cells->n + 31) / 32 + rows_total + 1;   // >= sum over rows of ceil(slots/32)
     int blocks = grid_blocks(warps, V3_WARPS, 1 << 30);
     if (stats)
-        k_density_all_v3<true><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats);
+        k_density_all_v3<true><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats, rows, nkeys);
     else
-        k_density_all_v3<false><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr);
+        k_density_all_v3<false><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr, rows,
+                                                                 nkeys);
     return check_launch();
 }
 

@@ -31,7 +31,7 @@ from . import api as pv
 
 BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_perm, k_stable_small/big, k_gather
 SORT_LAUNCHES = 2       # k_sort_small, k_sort_big
-DENSITY_LAUNCHES = 1    # k_density_all
+DENSITY_LAUNCHES = 5    # k_row_chunks, 3 scan kernels, k_density_all
 
 
 def slab_bounds(nc: int, world: int, rank: int) -> tuple[int, int]:
