@@ -53,7 +53,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 1
+#define SPH_ABI_VERSION 2
 
 #define SPH_OK 0
 #define SPH_EINVAL 1
@@ -87,18 +87,17 @@ typedef struct sph_grid {
     float reserved2;    /* must be 0                                        */
 } sph_grid;
 
-/* One entry of a per-direction sorted list ("dist"/"index" of P:92): the
- * particle's position (x, y, z, fp32 copy) and j = its slot in the
- * cell-sorted arrays.  Entries of one cell are ascending in the projection
- * of the position on the unit axis of the direction, key = fp32(fp64
- * (x - cell corner) . d/|d|), ties by the particle's input index.  The
- * density sweeps compare projected separations (x_j - x_i) . axis computed
- * from these positions; carrying the position makes one
- * 16-byte load per candidate. */
-typedef struct sph_pv_entry {
-    float x, y, z;
-    int32_t j;
-} sph_pv_entry;
+/* Per-direction sorted lists ("index" of P:92).  For cell c and direction
+ * d, order[d * capacity + cell_start[c] + k] is the IN-CELL index (0 ..
+ * n_c - 1, uint16: SPH_MAX_CELL bounds the occupancy) of the particle of
+ * rank k when the cell's particles are ascending in the projection of their
+ * position on the unit axis of d, key = (x - cell corner) . d/|d| computed in
+ * fp64; keys closer than 2^-25 * 2 sqrt(3) C_l (far below the window margin
+ * delta) may be ordered by input index instead.  The projected distances
+ * ("dist" of P:92) are not stored: the density sweeps recompute projected
+ * separations (x_j - x_i) . d from exact coordinate differences
+ * (DESIGN.md §4.2), so a list costs 2 bytes per particle and direction. */
+#define SPH_ORDER_BYTES 2
 
 /* Cell-sorted particle storage (caller-allocated device arrays).
  *   cell_start[ncell + 1]   first slot of each local cell (written by build)
@@ -107,10 +106,11 @@ typedef struct sph_pv_entry {
  *   perm[capacity]          slot -> input index
  *   cell_hmax[ncell]        max h in each cell
  *   slot_cell[capacity]     local cell of each slot (written by build)
- *   pv[SPH_NDIR * capacity] sorted lists: direction d, slot range of cell c
- *                           at pv[d * capacity + cell_start[c] ...]
+ *   order[SPH_NDIR * capacity] sorted lists (uint16 in-cell indices):
+ *                           direction d, cell c at
+ *                           order[d * capacity + cell_start[c] ...]
  * n is written by sph_build_cells (stored particles).  16-byte alignment
- * is required for xyzh, vm and pv. */
+ * is required for xyzh and vm. */
 typedef struct sph_cells {
     int64_t capacity;
     int64_t n;
@@ -119,7 +119,7 @@ typedef struct sph_cells {
     float *vm;
     int32_t *perm;
     float *cell_hmax;
-    sph_pv_entry *pv;
+    uint16_t *order;
     int32_t *slot_cell;
 } sph_cells;
 
@@ -157,7 +157,7 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
                     const float *vm_in, sph_cells *cells, void *ws, size_t ws_bytes, void *stream);
 
 /* Sort every cell of [cell_begin, cell_end) along the 13 directions (P:92,
- * P:102): fills cells->pv for those cells.  cell_end = -1 means all. */
+ * P:102): fills cells->order for those cells.  cell_end = -1 means all. */
 int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end,
                    void *ws, size_t ws_bytes, void *stream);
 

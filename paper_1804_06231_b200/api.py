@@ -78,7 +78,7 @@ class Cells:
     vm: torch.Tensor
     perm: torch.Tensor
     cell_hmax: torch.Tensor
-    pv: torch.Tensor            # (13 * capacity, 4) float32 view of sph_pv_entry {float x, y, z; int j}
+    order: torch.Tensor         # (13, capacity) int16 storage of the uint16 sorted lists (include/sph.h)
     slot_cell: torch.Tensor     # (capacity,) int32
     n: int = 0
 
@@ -91,7 +91,7 @@ class Cells:
                      torch.empty((cap, 4), dtype=torch.float32, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device),
                      torch.empty(nce, dtype=torch.float32, device=device),
-                     torch.empty((_lib.SPH_NDIR * cap, 4), dtype=torch.float32, device=device),
+                     torch.empty((_lib.SPH_NDIR, cap), dtype=torch.int16, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device))
 
     def struct(self) -> SphCells:
@@ -99,16 +99,13 @@ class Cells:
         s.capacity = self.capacity
         s.n = self.n
         s.cell_start, s.xyzh, s.vm = self.cell_start.data_ptr(), self.xyzh.data_ptr(), self.vm.data_ptr()
-        s.perm, s.cell_hmax, s.pv = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.pv.data_ptr()
+        s.perm, s.cell_hmax, s.order = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.order.data_ptr()
         s.slot_cell = self.slot_cell.data_ptr()
         return s
 
-    def pv_pos(self) -> torch.Tensor:
-        """(13, capacity, 3) positions stored in the sorted lists."""
-        return self.pv[:, :3].reshape(_lib.SPH_NDIR, self.capacity, 3)
-
-    def pv_slots(self) -> torch.Tensor:
-        return self.pv[:, 3].contiguous().view(torch.int32).view(_lib.SPH_NDIR, self.capacity)
+    def order_np(self):
+        """(13, capacity) int64 numpy copy of the sorted lists (in-cell indices)."""
+        return self.order.cpu().numpy().view("uint16").astype("int64")
 
 
 FIELDS = ("rho", "wcount", "rho_dh", "wcount_dh", "div_v", "curl_x", "curl_y", "curl_z", "nngb")

@@ -40,7 +40,7 @@ struct DevCells {
     const float4 *vm;
     const int *perm;
     const float *cell_hmax;
-    const sph_pv_entry *pv;
+    const uint16_t *ord;    // sorted lists (include/sph.h), [SPH_NDIR][cap]
     const int *slot_cell;
 };
 

@@ -98,11 +98,10 @@ template <bool COUNT>
 __device__ __forceinline__ void sweep_self(const DevCells &c, const IPart &p, int s0, int s1, Acc &a,
                                            unsigned &cand, unsigned &hits)
 {
-    const float4 *L = reinterpret_cast<const float4 *>(c.pv);
     for (int q = s0; q < s1; ++q) {
-        const float4 e = L[q];
-        const int j = __float_as_int(e.w);
+        const int j = s0 + c.ord[q];
         if (j == p.slot) continue;
+        const float4 e = c.xyzh[j];
         float dx = p.x - e.x, dy = p.y - e.y, dz = p.z - e.z;
         float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         if (COUNT) ++cand;
@@ -147,18 +146,19 @@ __device__ __forceinline__ void sweep_pair(const DevGrid &g, const DevCells &c, 
     float sjx = sh[0] < 0 ? g.boxf[0] : 0.0f;
     float sjy = sh[1] < 0 ? g.boxf[1] : 0.0f;
     float sjz = sh[2] < 0 ? g.boxf[2] : 0.0f;
-    const float4 *L = reinterpret_cast<const float4 *>(c.pv) + (long long)d * c.cap;
+    const uint16_t *L = c.ord + (long long)d * c.cap;
     int s0 = c.cell_start[cj], s1 = c.cell_start[cj + 1];
     int q = s > 0 ? s0 : s1 - 1;
     const int qend = s > 0 ? s1 : s0 - 1;
     for (; q != qend; q += s) {
-        const float4 e = L[q];
+        const int j = s0 + L[q];
+        const float4 e = c.xyzh[j];
         float dx = xi - (e.x - sjx), dy = yi - (e.y - sjy), dz = zi - (e.z - sjz);
         if (!(fmaf(dx, sx, fmaf(dy, sy, dz * sz)) < p.Hd)) break;   // sorted early exit
         float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         if (COUNT) ++cand;
         if (r2 < p.H2) {
-            interact(p, dx, dy, dz, r2, c.vm[__float_as_int(e.w)], a);
+            interact(p, dx, dy, dz, r2, c.vm[j], a);
             if (COUNT) ++hits;
         }
     }

@@ -1,0 +1,737 @@
+// density_v4.cuh -- the production sph_density_all engine.
+//
+// Method (unchanged from the reference engine in density.cuh): every owned
+// particle i gathers from its own cell and the 26 neighbour cells; in a
+// neighbour cell only the window of its list sorted along the pair axis whose
+// projected separation is below H_i + delta is tested (Code 2; the
+// per-particle bound of P:151-165), in-range pairs are interacted
+// and the sums are written once per particle.
+//
+// Mapping onto the B200 SM:
+//
+//  * Tiles.  A tile is a z-range of cells in a PAIR of adjacent rows (x, y),
+//    (x, y+1) holding at most V4_TP = 256 particles (k_v4_tiles cuts the rows
+//    greedily; the cut depends only on the row pair's own counts, so tiles are
+//    identical on any number of GPUs).  Row pairs are enumerated in 4 x 4
+//    blocks so that CTAs running at the same time share neighbourhoods in L2.
+//  * Staging (the particle cache of P:136).  A CTA copies the tile's
+//    neighbourhood -- 4 x 3 rows times (z-range + 2) cells -- into shared
+//    memory: positions as SoA X, Y, Z (periodic images beyond a low face
+//    pre-shifted by -L, exact by Sterbenz: DESIGN.md §4.3) and (v, m) as
+//    float4.  Particles beyond a high face are left in place and the home
+//    coordinate is shifted instead (also exact).  ~1.8k particles at c5.
+//  * Lanes.  One lane per home particle (register accumulators, one writer).
+//    The self cell and the 13 direction pairs are swept in a fixed order; for
+//    direction d the lane's window in the +d neighbour (a prefix of its list)
+//    and in the -d neighbour (a suffix of the same-direction list) are found
+//    exactly by bisection on the staged positions and swept back to back (their
+//    lengths are anti-correlated, which evens the lanes out).
+//  * Hits (the left-packing of P:185) go to a per-lane queue of staged indices
+//    in shared memory ([slot][lane], conflict-free); when most lanes hold two
+//    the warp pops one pair per lane and evaluates both interactions with
+//    FFMA2/FADD2/FMUL2.  Every particle sums its hits in sweep order, so the
+//    result does not depend on the tile or the warp (deterministic, identical
+//    on any number of GPUs).
+//  * Tiles that do not fit (a slice of more than V4_TP particles, or a
+//    neighbourhood above the staging capacity: clustered data) are processed by
+//    the same CTA with the reference per-particle sweep reading global memory
+//    (identical arithmetic per pair).
+#pragma once
+
+#include "common.cuh"
+#include "density.cuh"
+#include "packed.cuh"
+
+#include <type_traits>
+
+namespace pvsph {
+
+constexpr int V4_WARPS = 8;
+constexpr int V4_TP = V4_WARPS * 32;     // home particles per tile (upper bound)
+constexpr int V4_Q = 16;                 // queued hits per lane (power of two)
+constexpr int V4_ROWS = 12;              // staged rows: ox in -1..1, oy in -1..2 (relative to the tile's first row)
+constexpr int V4_MAXZ = 32;              // staged cells per row
+constexpr int V4_MAXCELLS = V4_ROWS * V4_MAXZ;
+constexpr int V4_MAXH = 2 * (V4_MAXZ - 2);   // home cells per tile
+constexpr int V4_MS = 2176;              // staged particles
+constexpr int V4_ML = 8192;              // staged list entries (27 segments per home cell)
+constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size_t)V4_ML * 2 +
+                           (size_t)(V4_MAXH + 4) * 4 + (size_t)V4_WARPS * V4_Q * 32 * 4;
+
+
+// ---- tile list ------------------------------------------------------------------
+struct RowPairs {
+    int nxo, nyp, nby;
+    long long nkeys;
+};
+
+__host__ __device__ __forceinline__ RowPairs row_pairs(const DevGrid &g)
+{
+    RowPairs r;
+    r.nxo = g.x_hi - g.x_lo;
+    r.nyp = (g.ny + 1) / 2;
+    r.nby = (r.nyp + 3) / 4;
+    r.nkeys = (long long)((r.nxo + 3) / 4) * r.nby * 16;
+    return r;
+}
+
+__host__ __device__ __forceinline__ void key_rowpair(const RowPairs &r, long long key, int &xo, int &yp)
+{
+    const long long blk = key / 16;
+    const int w = (int)(key % 16);
+    xo = (int)(blk / r.nby) * 4 + w / 4;
+    yp = (int)(blk % r.nby) * 4 + w % 4;
+}
+
+__host__ __device__ __forceinline__ long long v4_tile_capacity(const DevGrid &g, long long n)
+{
+    // every tile holds a non-empty z-slice, and a slice yields at most ceil(n_slice / V4_TP) tiles
+    return n / V4_TP + g.n_owned_cells + 64;
+}
+
+// Local cell of staged row k (ox = k/4 - 1, oy = k%4 - 1 relative to the tile's first
+// row y0 of owned plane xo) at unwrapped z; also the periodic flags of DESIGN.md §4.3.
+struct StagedRow {
+    long long base;   // local cell id of (row, z = 0)
+    int gx, uy;       // unwrapped global x plane and y row
+};
+
+__device__ __forceinline__ StagedRow staged_row(const DevGrid &g, int xo, int y0, int k)
+{
+    const int ox = k / 4 - 1, oy = k % 4 - 1;
+    const int xl = xo + g.ghost_x;
+    const int jx = g.ghost_x ? xl + ox : wrap_i(xl + ox, g.nc[0]);
+    StagedRow r;
+    r.gx = g.x_lo + xo + ox;
+    r.uy = y0 + oy;
+    r.base = ((long long)jx * g.ny + wrap_i(r.uy, g.ny)) * g.nz;
+    return r;
+}
+
+// Per z: particles of the home slice, of the 12 staged rows, and of the 9 rows around
+// each home row (the 27-cell list sizes are sums of three consecutive z).
+struct ZCols {
+    int slice, c12, c9a, c9b;
+};
+
+__device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__ cs, const long long rb[V4_ROWS],
+                                       bool hasB, int z)
+{
+    const int wz = wrap_i(z, g.nz);
+    int n[V4_ROWS];
+#pragma unroll
+    for (int k = 0; k < V4_ROWS; ++k) n[k] = cs[rb[k] + wz + 1] - cs[rb[k] + wz];
+    ZCols c;
+    c.slice = n[5] + (hasB ? n[6] : 0);
+    c.c12 = c.c9a = c.c9b = 0;
+#pragma unroll
+    for (int k = 0; k < V4_ROWS; ++k) {
+        c.c12 += n[k];
+        if (k % 4 <= 2) c.c9a += n[k];
+        if (k % 4 >= 1) c.c9b += n[k];
+    }
+    if (!hasB) c.c9b = 0;
+    return c;
+}
+
+// Greedy cut of one row pair into tiles {key, z_a, z_b, chunk}.  A staged tile
+// (chunk = -1) is a z-range with <= V4_TP home particles, <= V4_MS staged particles,
+// <= V4_ML list entries and <= V4_MAXZ - 2 cells.  A z-slice that cannot be staged on
+// its own becomes ceil(n / V4_TP) global-memory tiles (chunk >= 0).  WRITE = false
+// counts the tiles of each row pair.
+template <bool WRITE>
+__global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, int *__restrict__ off, int4 *tiles,
+                           long long tile_cap, unsigned *status)
+{
+    const RowPairs r = row_pairs(g);
+    for (long long key = blockIdx.x * (long long)blockDim.x + threadIdx.x; key < r.nkeys;
+         key += (long long)gridDim.x * blockDim.x) {
+        int xo, yp;
+        key_rowpair(r, key, xo, yp);
+        int nt = 0;
+        if (xo < r.nxo && yp < r.nyp) {
+            const int y0 = 2 * yp;
+            const bool hasB = y0 + 1 < g.ny;
+            long long rb[V4_ROWS];
+#pragma unroll
+            for (int k = 0; k < V4_ROWS; ++k) rb[k] = staged_row(g, xo, y0, k).base;
+            int pos = WRITE ? off[key] : 0;
+            auto emit = [&](int za, int zb, int chunk) {
+                if (WRITE) {
+                    if (pos < tile_cap) tiles[pos] = make_int4((int)key, za, zb, chunk);
+                    else set_status(status, ST_ECAPACITY);
+                    ++pos;
+                }
+                ++nt;
+            };
+            ZCols cm = zcols(g, cell_start, rb, hasB, -1), c0 = zcols(g, cell_start, rb, hasB, 0);
+            int cs = -1, home = 0, stg = 0, lst = 0, c12_before = 0;
+            for (int z = 0; z < g.nz; ++z) {
+                const ZCols cp = zcols(g, cell_start, rb, hasB, z + 1);
+                const int nb = cm.c9a + c0.c9a + cp.c9a + cm.c9b + c0.c9b + cp.c9b;
+                bool placed = false;
+                if (cs >= 0) {
+                    const int home2 = home + c0.slice, lst2 = lst + nb;
+                    const int stg2 = c12_before + stg + c0.c12 + cp.c12;
+                    if (home2 <= V4_TP && stg2 <= V4_MS && lst2 <= V4_ML && z - cs + 1 <= V4_MAXZ - 2) {
+                        home = home2;
+                        lst = lst2;
+                        stg += c0.c12;
+                        placed = true;
+                    } else {
+                        if (home > 0) emit(cs, z - 1, -1);
+                        cs = -1;
+                    }
+                }
+                if (!placed) {
+                    if (c0.slice > V4_TP || cm.c12 + c0.c12 + cp.c12 > V4_MS || nb > V4_ML) {
+                        for (int k = 0; k * V4_TP < c0.slice; ++k) emit(z, z, k);
+                    } else {
+                        cs = z;
+                        home = c0.slice;
+                        stg = c0.c12;
+                        lst = nb;
+                        c12_before = cm.c12;
+                    }
+                }
+                cm = c0;
+                c0 = cp;
+            }
+            if (cs >= 0 && home > 0) emit(cs, g.nz - 1, -1);
+        }
+        if (!WRITE) off[key] = nt;
+    }
+}
+
+// ---- the engine ------------------------------------------------------------------
+// Block-wide exclusive scan of one int per thread (blockDim.x == V4_TP).
+__device__ __forceinline__ int block_exscan(int v, int *wsum, int &total)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < V4_WARPS; ++k) {
+        const int s = wsum[k];
+        pre += k < w ? s : 0;
+        tot += s;
+    }
+    __syncthreads();
+    total = tot;
+    return pre + x - v;
+}
+
+// Reference per-particle sweep (global memory) for tiles that are not staged.
+template <bool COUNT>
+__device__ __forceinline__ void v4_particle_global(const DevGrid &g, const DevCells &c, const DevOut &o, int i,
+                                                   unsigned cand[4], unsigned hits[4])
+{
+    const int home = c.slot_cell[i];
+    HomeCell hc = home_cell(g, home);
+    IPart p = load_i(g, c, i, hc.corner);
+    Acc a;
+    acc_zero(a);
+    sweep_self<COUNT>(c, p, c.cell_start[home], c.cell_start[home + 1], a, cand[0], hits[0]);
+    for (int ox = -1; ox <= 1; ++ox)
+        for (int oy = -1; oy <= 1; ++oy)
+            for (int oz = -1; oz <= 1; ++oz) {
+                if (!(ox | oy | oz)) continue;
+                int cj, sh[3];
+                if (!neighbour(g, hc, ox, oy, oz, cj, sh)) continue;
+                const int k = kind_of(ox, oy, oz);
+                sweep_pair<COUNT>(g, c, p, cj, ox, oy, oz, sh, a, cand[k], hits[k]);
+            }
+    Final f = finalise(g, p, a, true);
+    const int out = c.perm[i];
+    if (out < o.n_out) {
+        const float rinv = 1.0f / f.rho;
+        o.rho[out] = f.rho;
+        o.wcount[out] = f.wc;
+        o.rho_dh[out] = f.rho_dh;
+        o.wcount_dh[out] = f.wc_dh;
+        o.div_v[out] = f.div * rinv;
+        o.curl_v[out] = f.cx * rinv;
+        o.curl_v[o.n_out + out] = f.cy * rinv;
+        o.curl_v[2 * o.n_out + out] = f.cz * rinv;
+        o.nngb[out] = a.nngb;
+    }
+}
+
+// Packed accumulators; D and curl use v_j - v_i (= -v_ij) so the cross products
+// need no negation: Dn = -sum fac (v_ij . x_ij); R = P - N.
+struct Acc2 {
+    f2 rho, wc, srt, st, Dn, Px, Nx, Py, Ny, Pz, Nz;
+};
+
+// Two interactions (MASK: the odd half may be empty, mk = (1, 0)).
+// M4 in branch-free form: w(x) = u^3 - v^3/2, w'(x) = -3 (u - v)(u + v),
+// u = max(0, 1 - x), v = max(0, 1 - 2x)  (equal to the two-branch form of R1);
+// u - v = min(x, u) is formed without cancellation.
+template <bool MASK>
+__device__ __forceinline__ void interact_pair(f2 Hinv2, f2 dx, f2 dy, f2 dz, f2 m, f2 nvx, f2 nvy, f2 nvz, f2 mk,
+                                              Acc2 &A)
+{
+    f2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    float r2a, r2b;
+    upk(r2, r2a, r2b);
+    // r^2 = 0 (coincident particles): rinv stays finite, x = 0 and w'(0) = 0 make every gradient term 0
+    f2 rinv = pk(rsqrt_fast(fmaxf(r2a, 1e-30f)), rsqrt_fast(fmaxf(r2b, 1e-30f)));
+    f2 x = mul2(mul2(r2, rinv), Hinv2);
+    f2 u = sub2(bc2(1.0f), x);
+    f2 v = fma2(bc2(-2.0f), x, bc2(1.0f));
+    float va, vb, xa, xb, ua, ub;
+    upk(v, va, vb);
+    upk(x, xa, xb);
+    upk(u, ua, ub);
+    v = pk(fmaxf(va, 0.0f), fmaxf(vb, 0.0f));
+    const f2 mn = pk(fminf(xa, ua), fminf(xb, ub));
+    f2 uu = mul2(u, u), vv = mul2(v, v);
+    f2 w = fma2(uu, u, mul2(bc2(-0.5f), mul2(vv, v)));
+    f2 dw = mul2(bc2(-3.0f), mul2(mn, add2(u, v)));
+    if (MASK) {
+        w = mul2(w, mk);
+        dw = mul2(dw, mk);
+        m = mul2(m, mk);
+    }
+    acc_fma2(A.rho, m, w);
+    acc_add2(A.wc, w);
+    f2 t = fma2(x, dw, mul2(bc2(3.0f), w));
+    acc_fma2(A.srt, m, t);
+    acc_add2(A.st, t);
+    f2 nvdx = fma2(nvx, dx, fma2(nvy, dy, mul2(nvz, dz)));
+    f2 fac = mul2(mul2(m, dw), rinv);
+    acc_fma2(A.Dn, fac, nvdx);
+    f2 fx = mul2(fac, nvx), fy = mul2(fac, nvy), fz = mul2(fac, nvz);
+    acc_fma2(A.Px, fz, dy);
+    acc_fma2(A.Nx, fy, dz);
+    acc_fma2(A.Py, fx, dz);
+    acc_fma2(A.Ny, fz, dx);
+    acc_fma2(A.Pz, fy, dx);
+    acc_fma2(A.Nz, fx, dy);
+}
+
+__device__ __forceinline__ int v4_kind(int d)
+{
+    // faces (0,0,1) (0,1,0) (1,0,0); corners (1,+-1,+-1); the rest edges
+    return (d == 0 || d == 2 || d == 8) ? 1 : ((d == 4 || d == 6 || d == 10 || d == 12) ? 3 : 2);
+}
+
+// Shared-memory view of a staged tile (32-bit shared addresses).
+struct V4Stage {
+    unsigned P;               // float4 x, y, z (low-face images pre-shifted by -L), 0
+    unsigned V;               // float4 vx, vy, vz, m
+    unsigned L;               // uint16 staged indices: 27 segments per home cell
+    const int4 *tab;          // {base, count, gstart, flags}: flags bits 0-2 home shift (+L image), 3-5 pre-shifted
+    int nzs;
+};
+
+// Window lengths: the number of leading entries of two staged segments whose
+// projected separation is below Hk; the separation grows along each segment.
+// Segment 0 (+d neighbour, reversed list) is read backwards from storage index f0
+// with sep = (x_j - h0) . d, segment 1 (-d neighbour, reversed list) forwards from
+// f1 with sep = (h1 - x_j) . d.  Galloping from the near end, then bisecting: the
+// exact per-particle bound of P:151-165; the two searches advance in lockstep so
+// their shared-memory loads overlap.
+struct Gallop {
+    int lo, hi, k, step;
+    __device__ __forceinline__ void init(int n)
+    {
+        lo = 0;
+        hi = n;
+        k = 0;
+        step = 1;
+    }
+    __device__ __forceinline__ bool active() const { return lo < hi; }
+    __device__ __forceinline__ int probe() const { return k < hi ? k : (lo + hi) >> 1; }
+    __device__ __forceinline__ void update(bool below)
+    {
+        if (k < hi) {                 // galloping phase: probes 0, 1, 3, 7, ...
+            if (below) {
+                lo = k + 1;
+                k += step;
+                step <<= 1;
+                if (k >= hi) k = 0x7fffffff;
+            } else {
+                hi = k;
+                k = 0x7fffffff;
+            }
+        } else {                      // bisection
+            const int mid = (lo + hi) >> 1;
+            if (below) lo = mid + 1; else hi = mid;
+        }
+    }
+};
+
+__device__ __forceinline__ void v4_windows(const V4Stage &S, int f0, int n0, int f1, int n1, float c0, float c1,
+                                           float c2, float h0x, float h0y, float h0z, float h1x, float h1y, float h1z,
+                                           float Hk, int &len0, int &len1)
+{
+    Gallop A, B;
+    A.init(n0);
+    B.init(n1);
+    while (A.active() || B.active()) {
+        const bool ga = A.active(), gb = B.active();
+        const int ka = A.probe(), kb = B.probe();
+        const unsigned ia = ga ? lds_u16(S.L + 2u * (unsigned)(f0 - ka)) : 0u;
+        const unsigned ib = gb ? lds_u16(S.L + 2u * (unsigned)(f1 + kb)) : 0u;
+        const float4 pa = lds_f4(S.P + 16u * ia), pb = lds_f4(S.P + 16u * ib);
+        const float sa = fmaf(c0, pa.x - h0x, fmaf(c1, pa.y - h0y, c2 * (pa.z - h0z)));
+        const float sb = fmaf(c0, h1x - pb.x, fmaf(c1, h1y - pb.y, c2 * (h1z - pb.z)));
+        if (ga) A.update(sa < Hk);
+        if (gb) B.update(sb < Hk);
+    }
+    len0 = A.lo;
+    len1 = B.lo;
+}
+
+// One lane = one home particle of a staged tile.  lpos: first list entry of its home
+// cell, qh: its staged column, yoff: its row in the tile (0/1).  FRAMES: the tile
+// touches a high box face (some home coordinate must be shifted by -L).
+template <bool COUNT, bool FRAMES>
+__device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCells &c, const DevOut &o,
+                                                   const V4Stage &S, unsigned qbase, bool active, int i, int yoff,
+                                                   int qh, int lpos, unsigned cand[4], unsigned hits[4])
+{
+    const unsigned sQ = qbase + 4u * (threadIdx.x & 31);
+    float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
+    if (active) {
+        const float4 a = c.xyzh[i];
+        const float4 b = c.vm[i];
+        x = a.x; y = a.y; z = a.z;
+        vx = b.x; vy = b.y; vz = b.z; m = b.w;
+        const double H = (double)g.gamma * (double)a.w;   // exact product; H^2, 1/H rounded once
+        H2 = (float)(H * H);
+        Hinv = (float)(1.0 / H);
+        Hd = (float)H + g.delta;
+    }
+    const float xs = x - g.boxf[0], ys = y - g.boxf[1], zs = z - g.boxf[2];   // exact where used (x >= L/2)
+    const float Hd2 = Hd * 1.41421356237309505f, Hd3 = Hd * 1.73205080756887729f;   // (H + delta) sqrt(kind)
+    const f2 Hinv2 = bc2(Hinv);
+    auto scell = [&](int ox, int oy, int oz) { return ((ox + 1) * 4 + oy + yoff + 1) * S.nzs + qh + oz; };
+    const int4 eh = S.tab[scell(0, 0, 0)];
+    const int kh = active ? i - eh.z : -1;                // in-cell index of i
+
+    Acc2 A;
+    A.rho = A.wc = A.srt = A.st = A.Dn = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
+    unsigned head = 0, tail = 0;
+
+    auto home_of = [&](unsigned fl, float &hx, float &hy, float &hz) {
+        hx = (fl & 1u) ? xs : x;
+        hy = (fl & 2u) ? ys : y;
+        hz = (fl & 4u) ? zs : z;
+    };
+    // pop one pair of hits per lane (FINAL: also a single one)
+    auto drain = [&](auto final_tag) {
+        constexpr bool FINAL = decltype(final_tag)::value;
+        const unsigned n = tail - head;
+        if (n >= 2 || (FINAL && n == 1)) {
+            const unsigned e0 = lds_u32(sQ + ((head & (V4_Q - 1)) << 7));
+            const unsigned e1 = (!FINAL || n >= 2) ? lds_u32(sQ + (((head + 1) & (V4_Q - 1)) << 7)) : e0;
+            const unsigned s0 = e0 & 0xffffu, s1 = e1 & 0xffffu;
+            float hx0 = x, hy0 = y, hz0 = z, hx1 = x, hy1 = y, hz1 = z;
+            if (FRAMES) {
+                home_of(e0 >> 16, hx0, hy0, hz0);
+                home_of(e1 >> 16, hx1, hy1, hz1);
+            }
+            const float4 p0 = lds_f4(S.P + 16u * s0), p1 = lds_f4(S.P + 16u * s1);
+            const float4 v0 = lds_f4(S.V + 16u * s0), v1 = lds_f4(S.V + 16u * s1);
+            const f2 mk = pk(1.0f, n >= 2 ? 1.0f : 0.0f);
+            interact_pair<FINAL>(Hinv2, pk(hx0 - p0.x, hx1 - p1.x), pk(hy0 - p0.y, hy1 - p1.y),
+                                 pk(hz0 - p0.z, hz1 - p1.z), pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx),
+                                 pk(v0.y - vy, v1.y - vy), pk(v0.z - vz, v1.z - vz), mk, A);
+            head += (!FINAL || n >= 2) ? 2u : 1u;
+        }
+    };
+
+    int pos = lpos;                                       // this home cell's list segments
+    for (int a = 0; a < 14; ++a) {
+        // a = 0: the self cell (identity segment); a = 1 + d: reversed +d list, then reversed -d list,
+        // so that the lane's two windows (a prefix of +d, a suffix of -d) are contiguous: L[wb, wb + total)
+        int wb = 0, len0 = 0, total = 0, kind = 0;
+        unsigned fl0 = 0, fl1 = 0;
+        if (a == 0) {
+            if (active) {
+                wb = pos;
+                total = eh.y;
+                len0 = total;
+                pos += eh.y;
+            }
+        } else {
+            const int d = a - 1;
+            kind = v4_kind(d);
+            const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+            const float Hk = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
+            if (active) {
+                const int4 ep = S.tab[scell(a0, a1, a2)];
+                const int4 em = S.tab[scell(-a0, -a1, -a2)];
+                const int mid = pos + ep.y;                   // boundary between the two reversed segments
+                pos = mid + em.y;
+                float px = x, py = y, pz = z, mx = x, my = y, mz = z;
+                if (FRAMES) {
+                    fl0 = (unsigned)ep.w & 7u;
+                    fl1 = (unsigned)em.w & 7u;
+                    home_of(fl0, px, py, pz);
+                    home_of(fl1, mx, my, mz);
+                }
+                const float c0 = (float)a0, c1 = (float)a1, c2 = (float)a2;
+                int len1;
+                v4_windows(S, mid - 1, ep.y, mid, em.y, c0, c1, c2, px, py, pz, mx, my, mz, Hk, len0, len1);
+                wb = mid - len0;
+                total = len0 + len1;
+            }
+        }
+        const int trip = __reduce_max_sync(0xffffffffu, total);
+        const int excl = a == 0 ? kh : -1;                                 // i itself in the self cell
+        const unsigned lb = S.L + 2u * (unsigned)wb;
+        for (int t = 0; t < trip; t += 4) {
+            // four candidates: list loads, then positions, then the tests (ILP across candidates)
+            bool ok[4];
+            unsigned sj[4];
+            float4 p[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                ok[u] = t + u < total && t + u != excl;
+                sj[u] = ok[u] ? lds_u16(lb + 2u * (unsigned)(t + u)) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) p[u] = lds_f4(S.P + 16u * sj[u]);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                float hx = x, hy = y, hz = z;
+                unsigned fl = 0;
+                if (FRAMES) {
+                    fl = t + u < len0 ? fl0 : fl1;
+                    home_of(fl, hx, hy, hz);
+                }
+                const float dx = hx - p[u].x, dy = hy - p[u].y, dz = hz - p[u].z;
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (COUNT) cand[kind] += ok[u] ? 1u : 0u;
+                if (ok[u] && r2 < H2) {
+                    sts_u32(sQ + ((tail & (V4_Q - 1)) << 7), FRAMES ? (sj[u] | (fl << 16)) : sj[u]);
+                    ++tail;
+                    if (COUNT) ++hits[kind];
+                }
+            }
+            // at most four pushes per step: keep every queue at <= V4_Q - 5 entries after draining
+            for (;;) {
+                const unsigned n = tail - head;
+                if (!(__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= V4_Q - 4)))
+                    break;
+                drain(std::false_type{});
+            }
+        }
+    }
+    while (__any_sync(0xffffffffu, tail != head)) drain(std::true_type{});
+
+    if (active) {
+        // finalise (self term w(0) = 1/2, t(0) = 3/2), as finalise() in density.cuh
+        const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;
+        const float rho = K3 * fmaf(0.5f, m, sum2(A.rho));
+        const float wc = K3 * (0.5f + sum2(A.wc));
+        const float dh = -K3 * g.gamma * Hinv;
+        const float rho_dh = dh * fmaf(1.5f, m, sum2(A.srt));
+        const float wc_dh = dh * (1.5f + sum2(A.st));
+        const float gf = K3 * Hinv;
+        const float rinv = 1.0f / rho;
+        const int out = c.perm[i];
+        if (out < o.n_out) {
+            o.rho[out] = rho;
+            o.wcount[out] = wc;
+            o.rho_dh[out] = rho_dh;
+            o.wcount_dh[out] = wc_dh;
+            o.div_v[out] = gf * sum2(A.Dn) * rinv;
+            o.curl_v[out] = gf * (sum2(A.Px) - sum2(A.Nx)) * rinv;
+            o.curl_v[o.n_out + out] = gf * (sum2(A.Py) - sum2(A.Ny)) * rinv;
+            o.curl_v[2 * o.n_out + out] = gf * (sum2(A.Pz) - sum2(A.Nz)) * rinv;
+            o.nngb[out] = (int)tail;
+        }
+    }
+}
+
+// Persistent CTAs take tiles in order from an atomic counter.
+template <bool COUNT>
+__global__ void __launch_bounds__(V4_TP, 2) k_density_v4(DevGrid g, DevCells c, DevOut o, sph_stats *st,
+                                                         const int4 *__restrict__ tiles,
+                                                         const int *__restrict__ ntiles_p, int *tile_counter)
+{
+    extern __shared__ __align__(16) unsigned char v4_smem[];
+    float4 *P = reinterpret_cast<float4 *>(v4_smem);
+    float4 *V = P + V4_MS;
+    int4 *tab = reinterpret_cast<int4 *>(V + V4_MS);
+    uint16_t *L = reinterpret_cast<uint16_t *>(tab + V4_MAXCELLS);
+    int *hoff = reinterpret_cast<int *>(L + V4_ML);
+    unsigned *queue = reinterpret_cast<unsigned *>(hoff + V4_MAXH + 4);
+    __shared__ int s_tile, s_wsum[V4_WARPS];
+
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const RowPairs rp = row_pairs(g);
+    const int ntiles = *ntiles_p;
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
+        __syncthreads();
+        const int t = s_tile;
+        if (t >= ntiles) break;
+        const int4 td = tiles[t];
+        int xo, yp;
+        key_rowpair(rp, td.x, xo, yp);
+        const int y0 = 2 * yp;
+        const bool hasB = y0 + 1 < g.ny;
+        const int za = td.y, zb = td.z, chunk = td.w;
+        const long long rowA = ((long long)(xo + g.ghost_x) * g.ny + y0) * g.nz;
+        const int sA = c.cell_start[rowA + za], eA = c.cell_start[rowA + zb + 1];
+        const int sB = hasB ? c.cell_start[rowA + g.nz + za] : 0;
+        const int eB = hasB ? c.cell_start[rowA + g.nz + zb + 1] : 0;
+        const int nA = eA - sA, nH = nA + (eB - sB);
+        const int nzs = zb - za + 3, nzh = zb - za + 1, nh = (hasB ? 2 : 1) * nzh;
+        bool staged = chunk < 0 && nzs <= V4_MAXZ;
+        // a staged neighbour beyond a high face (home shift needed): x plane, y row or z column
+        const bool frames = g.x_lo + xo + 1 >= g.nc[0] || y0 + 2 >= g.ny || zb + 1 >= g.nz;
+
+        if (staged) {
+            // staged cell table: s = row * nzs + col, row = (ox + 1) * 4 + (oy + 1), col = uz - za + 1
+            const int ncs = V4_ROWS * nzs;
+            int cnt[2] = {0, 0};
+            int4 ent[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int s = 2 * threadIdx.x + k;
+                ent[k] = make_int4(0, 0, 0, 0);
+                if (s < ncs) {
+                    const int r = s / nzs, q = s % nzs;
+                    const StagedRow sr = staged_row(g, xo, y0, r);
+                    const int uz = za - 1 + q;
+                    const long long cell = sr.base + wrap_i(uz, g.nz);
+                    const int gs = c.cell_start[cell];
+                    cnt[k] = c.cell_start[cell + 1] - gs;
+                    const unsigned fl = (sr.gx >= g.nc[0] ? 1u : 0u) | (sr.uy >= g.ny ? 2u : 0u) |
+                                        (uz >= g.nz ? 4u : 0u) | (sr.gx < 0 ? 8u : 0u) | (sr.uy < 0 ? 16u : 0u) |
+                                        (uz < 0 ? 32u : 0u);
+                    ent[k] = make_int4(0, cnt[k], gs, (int)fl);
+                }
+            }
+            int total;
+            const int pre = block_exscan(cnt[0] + cnt[1], s_wsum, total);
+            if (2 * threadIdx.x < ncs) {
+                ent[0].x = pre;
+                tab[2 * threadIdx.x] = ent[0];
+            }
+            if (2 * threadIdx.x + 1 < ncs) {
+                ent[1].x = pre + cnt[0];
+                tab[2 * threadIdx.x + 1] = ent[1];
+            }
+            __syncthreads();
+            // list segments of each home cell: self + 13 x (+d, -d) = the 27 cells around it
+            int lsz = 0;
+            if ((int)threadIdx.x < nh) {
+                const int r = threadIdx.x / nzh, q = threadIdx.x % nzh + 1;
+                for (int ox = -1; ox <= 1; ++ox)
+                    for (int oy = -1; oy <= 1; ++oy)
+                        for (int oz = -1; oz <= 1; ++oz) lsz += tab[((ox + 1) * 4 + oy + r + 1) * nzs + q + oz].y;
+            }
+            int ltotal;
+            const int lpre = block_exscan(lsz, s_wsum, ltotal);
+            if ((int)threadIdx.x < nh) hoff[threadIdx.x] = lpre;
+            if (total > V4_MS || ltotal > V4_ML || nh > V4_MAXH) staged = false;   // CTA-uniform
+            __syncthreads();
+            if (staged) {
+                // positions and (v, m): each staged row is one contiguous slot range, split where z wraps
+                for (int r = wl; r < V4_ROWS; r += V4_WARPS) {
+                    const int4 e0 = tab[r * nzs];
+                    const float sx = (e0.w & 8) ? g.boxf[0] : 0.0f;
+                    const float sy = (e0.w & 16) ? g.boxf[1] : 0.0f;
+                    for (int piece = 0; piece < 3; ++piece) {
+                        // piece 0: column 0 if it wraps (uz = -1); 1: the in-box columns; 2: last column if uz = nz
+                        const int q0 = piece == 0 ? 0 : (piece == 1 ? (za == 0 ? 1 : 0) : nzs - 1);
+                        const int q1 = piece == 0 ? (za == 0 ? 1 : 0) : (piece == 1 ? (zb + 1 >= g.nz ? nzs - 1 : nzs) : (zb + 1 >= g.nz ? nzs : nzs - 1));
+                        if (q1 <= q0) continue;
+                        const int4 ea = tab[r * nzs + q0];
+                        const int4 eb = tab[r * nzs + q1 - 1];
+                        const float sz = (ea.w & 32) ? g.boxf[2] : 0.0f;
+                        const int n = eb.x + eb.y - ea.x;
+                        const float4 *gx = c.xyzh + ea.z;
+                        const float4 *gv = c.vm + ea.z;
+#pragma unroll 4
+                        for (int k = lane; k < n; k += 32) {
+                            const float4 p = gx[k];
+                            // exact: a pre-shifted coordinate is >= L/2
+                            P[ea.x + k] = make_float4(p.x - sx, p.y - sy, p.z - sz, 0.0f);
+                            V[ea.x + k] = gv[k];
+                        }
+                    }
+                }
+                // lists: lane k of the warp of home cell h copies segment k (self, then +d / -d
+                // reversed for d = 0..12), at its offset from a warp scan of the segment sizes
+                for (int h = wl; h < nh; h += V4_WARPS) {
+                    const int r = h / nzh, q = h % nzh + 1;
+                    int o0 = 0, o1 = 0, o2 = 0, d = 0;
+                    if (lane >= 1 && lane < 27) {
+                        d = (lane - 1) >> 1;
+                        const int sg = (lane & 1) ? 1 : -1;
+                        o0 = sg * dir_component(d, 0);
+                        o1 = sg * dir_component(d, 1);
+                        o2 = sg * dir_component(d, 2);
+                    }
+                    const int4 e = lane < 27 ? tab[((o0 + 1) * 4 + o1 + r + 1) * nzs + q + o2] : make_int4(0, 0, 0, 0);
+                    int x = e.y;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    const int dst = hoff[h] + x - e.y;
+                    const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
+                    if (lane == 0) {
+                        for (int k = 0; k < e.y; ++k) L[dst + k] = (uint16_t)(e.x + k);
+                    } else {
+#pragma unroll 4
+                        for (int k = 0; k < e.y; ++k) L[dst + e.y - 1 - k] = (uint16_t)(e.x + (int)src[k]);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+
+        if (staged) {
+            const int h = threadIdx.x;
+            const bool active = h < nH;
+            const int i = active ? (h < nA ? sA + h : sB + (h - nA)) : sA;
+            const int yoff = h < nA ? 0 : 1;
+            int qh = 1, lpos = 0;
+            if (active) {
+                const int iz = c.slot_cell[i] % g.nz;
+                qh = iz - za + 1;
+                lpos = hoff[yoff * nzh + iz - za];
+            }
+            const V4Stage S{smem_addr(P), smem_addr(V), smem_addr(L), tab, nzs};
+            const unsigned qb = smem_addr(queue + wl * V4_Q * 32);
+            if (wl * 32 < nH) {
+                if (frames)
+                    v4_particle_staged<COUNT, true>(g, c, o, S, qb, active, i, yoff, qh, lpos, cand, hits);
+                else
+                    v4_particle_staged<COUNT, false>(g, c, o, S, qb, active, i, yoff, qh, lpos, cand, hits);
+            }
+        } else {
+            // global-memory sweep: chunk tiles (a z-slice that cannot be staged) or oversized neighbourhoods
+            const int base = chunk < 0 ? 0 : chunk * V4_TP;
+            const int nAll = chunk < 0 ? nH : min(nH - base, V4_TP);
+            for (int h = threadIdx.x; h < nAll; h += V4_TP) {
+                const int hh = base + h;
+                const int i = hh < nA ? sA + hh : sB + (hh - nA);
+                v4_particle_global<COUNT>(g, c, o, i, cand, hits);
+            }
+        }
+        __syncthreads();
+    }
+    flush_stats<COUNT>(st, cand, hits);
+}
+
+}  // namespace pvsph

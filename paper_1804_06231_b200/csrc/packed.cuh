@@ -5,53 +5,24 @@
 
 namespace pvsph {
 
-typedef unsigned long long f2;
+// Packed pair of fp32 lanes: float2 with the sm_100 FFMA2/FADD2/FMUL2 intrinsics, so that
+// the register allocator sees real pairs (no 64-bit inline-asm copies).
+typedef float2 f2;
 
-__device__ __forceinline__ f2 pk(float a, float b)
-{
-    f2 r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
+__device__ __forceinline__ f2 pk(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ void upk(f2 v, float &a, float &b)
 {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    a = v.x;
+    b = v.y;
 }
-__device__ __forceinline__ f2 as_f2(float2 v) { return pk(v.x, v.y); }
-__device__ __forceinline__ f2 bc2(float a) { return pk(a, a); }
-__device__ __forceinline__ f2 add2(f2 a, f2 b)
-{
-    f2 d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2 sub2(f2 a, f2 b)
-{
-    f2 d;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b)
-{
-    f2 d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c)
-{
-    f2 d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-// acc += a * b and acc += a, updating the accumulator register pair in place
-__device__ __forceinline__ void acc_fma2(f2 &acc, f2 a, f2 b)
-{
-    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(a), "l"(b));
-}
-__device__ __forceinline__ void acc_add2(f2 &acc, f2 a)
-{
-    asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(a));
-}
+__device__ __forceinline__ f2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) { return __ffma2_rn(a, b, c); }
+// acc += a * b and acc += a
+__device__ __forceinline__ void acc_fma2(f2 &acc, f2 a, f2 b) { acc = __ffma2_rn(a, b, acc); }
+__device__ __forceinline__ void acc_add2(f2 &acc, f2 a) { acc = __fadd2_rn(acc, a); }
 // 1/sqrt(x) for normal x > 0 (MUFU.RSQ, no denormal fix-up; callers clamp x >= 1e-30)
 __device__ __forceinline__ float rsqrt_fast(float x)
 {
@@ -59,11 +30,36 @@ __device__ __forceinline__ float rsqrt_fast(float x)
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ float sum2(f2 v)
+__device__ __forceinline__ float sum2(f2 v) { return v.x + v.y; }
+__device__ __forceinline__ f2 zero2() { return make_float2(0.0f, 0.0f); }
+
+}  // namespace pvsph
+
+namespace pvsph {
+
+// 32-bit shared-memory addressing (avoids generic-pointer window arithmetic in hot loops).
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float4 lds_f4(unsigned a)
 {
-    float a, b;
-    upk(v, a, b);
-    return a + b;
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u16(unsigned a)
+{
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned a)
+{
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_u32(unsigned a, unsigned v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 }  // namespace pvsph

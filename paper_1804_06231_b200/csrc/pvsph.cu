@@ -11,7 +11,7 @@
 #include "calib.cuh"
 #include "common.cuh"
 #include "density.cuh"
-#include "density_v3.cuh"
+#include "density_v4.cuh"
 #include "sort.cuh"
 
 using namespace pvsph;
@@ -76,10 +76,10 @@ int make_grid(const sph_grid *gr, DevGrid &g)
 
 bool cells_ok(const sph_cells *c)
 {
-    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->pv && c->slot_cell &&
+    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell &&
            c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
-           ((uintptr_t)c->pv % 16 == 0);
+           ((uintptr_t)c->order % 2 == 0);
 }
 
 DevCells dev_cells(const sph_cells *c)
@@ -91,7 +91,7 @@ DevCells dev_cells(const sph_cells *c)
     d.vm = reinterpret_cast<const float4 *>(c->vm);
     d.perm = c->perm;
     d.cell_hmax = c->cell_hmax;
-    d.pv = c->pv;
+    d.ord = c->order;
     d.slot_cell = c->slot_cell;
     return d;
 }
@@ -120,7 +120,9 @@ DevOut dev_out(const sph_out *o)
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
-    size_t status, cell_of, rank, perm_tmp, count, tile_sum, big_count, big_items, rows, rows_sum, total;
+    size_t status, cell_of, rank, perm_tmp, count, tile_sum, big_count, big_items, rows, rows_sum, tiles, counter,
+        total;
+    long long tile_cap;
 };
 
 Ws ws_layout(const DevGrid &g, long long n)
@@ -145,11 +147,16 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4, 256);
     w.big_items = o;
     o = align_up(o + 8 * (size_t)(n / 64 + 64), 256);
-    const long long nkeys = row_nkeys(g);
+    const long long nkeys = row_pairs(g).nkeys;
     w.rows = o;
     o = align_up(o + 4 * (size_t)(nkeys + 1), 256);
     w.rows_sum = o;
     o = align_up(o + 4 * (size_t)((nkeys + SCAN_TILE - 1) / SCAN_TILE + 1), 256);
+    w.tile_cap = v4_tile_capacity(g, n);
+    w.tiles = o;
+    o = align_up(o + 16 * (size_t)w.tile_cap, 256);
+    w.counter = o;
+    o = align_up(o + 4, 256);
     w.total = o;
     return w;
 }
@@ -264,8 +271,8 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     DevCells c = dev_cells(cells);
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
-        g, c, cells->pv, cell_begin, cell_end, big_items, big_count);
-    k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->pv, big_items, big_count);
+        g, c, cells->order, cell_begin, cell_end, big_items, big_count);
+    k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count);
     return check_launch();
 }
 
@@ -339,22 +346,39 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     }
     Ws w = ws_layout(g, cells->capacity);
     if (ws_bytes < w.total) return SPH_EINVAL;
-    const int nkeys = (int)row_nkeys(g);
+    // tile list (k_v4_tiles): count per row pair -> exclusive scan -> write
+    const long long nkeys = row_pairs(g).nkeys;
     int *rows = at<int>(ws, w.rows), *rows_sum = at<int>(ws, w.rows_sum);
-    k_row_chunks<<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, cells->cell_start, rows, nkeys);
-    const long long ntiles = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
     unsigned *status = at<unsigned>(ws, w.status);
-    k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
-    k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles, rows, nkeys);
-    k_scan_add<<<(int)ntiles, SCAN_T, 0, s>>>(rows, nkeys, rows_sum);
-    const long long rows_total = (long long)(g.x_hi - g.x_lo) * g.ny;
-    const long long warps = (cells->n + 31) / 32 + rows_total + 1;   // >= sum over rows of ceil(slots/32)
-    int blocks = grid_blocks(warps, V3_WARPS, 1 << 30);
+    int4 *tiles = at<int4>(ws, w.tiles);
+    int *counter = at<int>(ws, w.counter);
+    const DevCells dc = dev_cells(cells);
+    k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, rows, tiles, w.tile_cap,
+                                                                       status);
+    const long long ntiles_scan = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_tiles<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
+    k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles_scan, rows, nkeys);
+    k_scan_add<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows_sum);
+    k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, rows, tiles, w.tile_cap,
+                                                                      status);
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(counter, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+    static int blocks_per_sm = 0, sms = 0;
+    if (!blocks_per_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_density_v4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
+        cudaFuncSetAttribute(k_density_v4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_density_v4<false>, V4_TP, V4_SMEM);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int blocks = sms * blocks_per_sm;
     if (stats)
-        k_density_all_v3<true><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), stats, rows, nkeys);
+        k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, dev_out(out), stats, tiles, rows + nkeys, counter);
     else
-        k_density_all_v3<false><<<blocks, V3_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(out), nullptr, rows,
-                                                                 nkeys);
+        k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, dev_out(out), nullptr, tiles, rows + nkeys,
+                                                           counter);
     return check_launch();
 }
 

@@ -5,7 +5,7 @@
 // Key of particle k in cell c along d: fp32( (x_k - corner_c) . d/|d| ),
 // the difference and dot product in fp64.  Order: ascending
 // key, ties by input index perm[k] -- deterministic whatever the slot order.
-// Each entry stores the particle's position and slot (sph_pv_entry).
+// Each list entry is the particle's in-cell index (uint16, include/sph.h).
 //
 // Small cells (n <= SORT_SMALL): one warp per cell, composite 64-bit keys
 // (orderable key << 32 | input index) staged in shared memory, rank by
@@ -35,7 +35,7 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
     corner[2] = (double)iz * g.cl[2];
 }
 
-__global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCells c, sph_pv_entry *pv,
+__global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
                                                                  long long cbeg, long long cend, int2 *big_items,
                                                                  int *big_count)
 {
@@ -92,26 +92,19 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCe
                 r[12] += c12 < comp[12];
             }
             if (mine) {
-                sph_pv_entry ent;
-                ent.x = p.x;
-                ent.y = p.y;
-                ent.z = p.z;
-                ent.j = s0 + lane;
 #pragma unroll
-                for (int d = 0; d < SPH_NDIR; ++d) pv[(long long)d * c.cap + s0 + r[d]] = ent;
+                for (int d = 0; d < SPH_NDIR; ++d) ord[(long long)d * c.cap + s0 + r[d]] = (uint16_t)lane;
             }
             __syncwarp();
             continue;
         }
         double u[PER][3];
-        float4 pos[PER];
         unsigned tie[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             int e = lane + 32 * k;
             if (e < n) {
                 float4 p = c.xyzh[s0 + e];
-                pos[k] = p;
                 u[k][0] = (double)p.x - corner[0];
                 u[k][1] = (double)p.y - corner[1];
                 u[k][2] = (double)p.z - corner[2];
@@ -137,12 +130,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCe
                 if (e < n) {
                     int r = 0;
                     for (int m = 0; m < n; ++m) r += sh[w][m] < comp[k];
-                    sph_pv_entry ent;
-                    ent.x = pos[k].x;
-                    ent.y = pos[k].y;
-                    ent.z = pos[k].z;
-                    ent.j = s0 + e;
-                    pv[(long long)d * c.cap + s0 + r] = ent;
+                    ord[(long long)d * c.cap + s0 + r] = (uint16_t)e;
                 }
             }
             __syncwarp();
@@ -151,7 +139,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCe
 }
 
 // One CTA per (cell, chunk) item; grid-strides over the queued items.
-__global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells c, sph_pv_entry *pv,
+__global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells c, uint16_t *ord,
                                                               const int2 *big_items, const int *big_count)
 {
     __shared__ unsigned long long tile[SORT_BIG_TILE];
@@ -191,14 +179,7 @@ __global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells
                 if (mine)
                     for (int m = 0; m < tn; ++m) r += tile[m] < comp;
             }
-            if (mine) {
-                sph_pv_entry ent;
-                ent.x = p.x;
-                ent.y = p.y;
-                ent.z = p.z;
-                ent.j = s0 + e;
-                pv[(long long)d * c.cap + s0 + r] = ent;
-            }
+            if (mine) ord[(long long)d * c.cap + s0 + r] = (uint16_t)e;
         }
         __syncthreads();
     }

@@ -64,22 +64,19 @@ def test_build_cells_matches_oracle_binning(pv, cfg):
 
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
 def test_sort_cells_orders_keys(pv, cfg):
-    """Each list is a permutation of its cell, carries the particles' positions, and is
-    ascending in the projection (oracle fp64 keys; fp32 rounding allowed, 1e-6 C_l)."""
+    """Each list is a permutation of its cell's in-cell indices and is ascending in the
+    projection (oracle fp64 keys; fp32 rounding allowed, 1e-6 C_l)."""
     p = synth.make(cfg)
     dp = _built(pv, p)
     cs = dp.cells.cell_start.cpu().numpy().astype(np.int64)
     perm = dp.cells.perm[:p.n].cpu().numpy()
-    pos = dp.cells.pv_pos()[:, :p.n].cpu().numpy()
-    slots = dp.cells.pv_slots()[:, :p.n].cpu().numpy()
-    xs = dp.cells.xyzh[:p.n, :3].cpu().numpy()
+    order = dp.cells.order_np()[:, :p.n]
     ref = oracle.cell_keys(p.xyzh, p.nc)            # [13, N] fp64, input order
     Cl = 1.0 / p.nc
     for d in range(13):
-        assert np.array_equal(pos[d], xs[slots[d]])                       # entries carry positions
         for c in range(p.nc ** 3):
             a, b = cs[c], cs[c + 1]
-            sl = slots[d, a:b]
+            sl = a + order[d, a:b]
             assert np.array_equal(np.sort(sl), np.arange(a, b))          # a permutation of the cell
             k = ref[d, perm[sl]]
             assert np.all(np.diff(k) >= -1e-6 * Cl)                     # ascending projection
