@@ -47,16 +47,17 @@
 namespace pvsph {
 
 constexpr int V4_WARPS = 8;
-constexpr int V4_TP = V4_WARPS * 32;     // home particles per tile (upper bound)
-constexpr int V4_Q = 16;                 // queued hits per lane (power of two)
+constexpr int V4_CTAS = 2;               // resident CTAs per SM (launch bounds; smem below fits 2)
+constexpr int V4_TP = V4_WARPS * 32;     // home particles per tile: exactly V4_TP except where a limit cuts
+constexpr int V4_Q = 24;                 // hit stack depth per lane, 2-byte entries
 constexpr int V4_ROWS = 12;              // staged rows: ox in -1..1, oy in -1..2 (relative to the tile's first row)
 constexpr int V4_MAXZ = 32;              // staged cells per row
 constexpr int V4_MAXCELLS = V4_ROWS * V4_MAXZ;
 constexpr int V4_MAXH = 2 * (V4_MAXZ - 2);   // home cells per tile
-constexpr int V4_MS = 2176;              // staged particles
+constexpr int V4_MS = 2400;              // staged particles (< 4096: 12-bit queue entries)
 constexpr int V4_ML = 8192;              // staged list entries (27 segments per home cell)
 constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size_t)V4_ML * 2 +
-                           (size_t)(V4_MAXH + 4) * 4 + (size_t)V4_WARPS * V4_Q * 32 * 4;
+                           (size_t)(V4_MAXH + 4) * 4 + (size_t)V4_WARPS * V4_Q * 32 * 2 + (size_t)V4_MAXZ * 16;
 
 
 // ---- tile list ------------------------------------------------------------------
@@ -134,11 +135,15 @@ __device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__
     return c;
 }
 
-// Greedy cut of one row pair into tiles {key, z_a, z_b, chunk}.  A staged tile
-// (chunk = -1) is a z-range with <= V4_TP home particles, <= V4_MS staged particles,
-// <= V4_ML list entries and <= V4_MAXZ - 2 cells.  A z-slice that cannot be staged on
-// its own becomes ceil(n / V4_TP) global-memory tiles (chunk >= 0).  WRITE = false
-// counts the tiles of each row pair.
+// Cut of one row pair into tiles.  The particles of a row pair are taken in the
+// sequence z = 0, 1, ..., each z-slice listing its row-A cell then its row-B cell.
+// A staged tile is a run of V4_TP consecutive particles of that sequence (fewer
+// where a limit cuts it): at most V4_MS staged neighbours, V4_ML list entries and
+// V4_MAXZ - 2 slices, so every warp of the CTA is full.  Its first and last cells
+// may be shared with the neighbouring tiles.  A slice whose neighbourhood cannot be
+// staged becomes global-memory tiles of <= V4_TP particles.  Descriptor:
+// {key, z_a | z_b << 16, first particle in slice z_a, count (< 0: global-memory)}.
+// The cut depends only on the row pair's own counts (identical on any GPU count).
 template <bool WRITE>
 __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, int *__restrict__ off, int4 *tiles,
                            long long tile_cap, unsigned *status)
@@ -156,48 +161,62 @@ __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, int *_
 #pragma unroll
             for (int k = 0; k < V4_ROWS; ++k) rb[k] = staged_row(g, xo, y0, k).base;
             int pos = WRITE ? off[key] : 0;
-            auto emit = [&](int za, int zb, int chunk) {
+            auto emit = [&](int za, int zb, int first, int cnt) {
                 if (WRITE) {
-                    if (pos < tile_cap) tiles[pos] = make_int4((int)key, za, zb, chunk);
+                    if (pos < tile_cap) tiles[pos] = make_int4((int)key, za | (zb << 16), first, cnt);
                     else set_status(status, ST_ECAPACITY);
                     ++pos;
                 }
                 ++nt;
             };
-            ZCols cm = zcols(g, cell_start, rb, hasB, -1), c0 = zcols(g, cell_start, rb, hasB, 0);
-            int cs = -1, home = 0, stg = 0, lst = 0, c12_before = 0;
-            for (int z = 0; z < g.nz; ++z) {
-                const ZCols cp = zcols(g, cell_start, rb, hasB, z + 1);
+            ZCols cm = zcols(g, cell_start, rb, hasB, -1), c0 = zcols(g, cell_start, rb, hasB, 0),
+                  cp = zcols(g, cell_start, rb, hasB, 1);
+            bool open = false;
+            int tz = 0, tfirst = 0, home = 0, stg = 0, lst = 0;
+            int z = 0, o = 0;                      // next particle: o-th of slice z
+            while (z < g.nz) {
                 const int nb = cm.c9a + c0.c9a + cp.c9a + cm.c9b + c0.c9b + cp.c9b;
-                bool placed = false;
-                if (cs >= 0) {
-                    const int home2 = home + c0.slice, lst2 = lst + nb;
-                    const int stg2 = c12_before + stg + c0.c12 + cp.c12;
-                    if (home2 <= V4_TP && stg2 <= V4_MS && lst2 <= V4_ML && z - cs + 1 <= V4_MAXZ - 2) {
-                        home = home2;
-                        lst = lst2;
-                        stg += c0.c12;
-                        placed = true;
+                bool take = true;
+                if (!open) {
+                    if (cm.c12 + c0.c12 + cp.c12 > V4_MS || nb > V4_ML) {
+                        for (int k = o; k < c0.slice; k += V4_TP) emit(z, z, k, -min(V4_TP, c0.slice - k));
+                        take = false;              // whole slice done
+                        o = c0.slice;
                     } else {
-                        if (home > 0) emit(cs, z - 1, -1);
-                        cs = -1;
-                    }
-                }
-                if (!placed) {
-                    if (c0.slice > V4_TP || cm.c12 + c0.c12 + cp.c12 > V4_MS || nb > V4_ML) {
-                        for (int k = 0; k * V4_TP < c0.slice; ++k) emit(z, z, k);
-                    } else {
-                        cs = z;
-                        home = c0.slice;
-                        stg = c0.c12;
+                        open = true;
+                        tz = z;
+                        tfirst = o;
+                        home = 0;
+                        stg = cm.c12 + c0.c12 + cp.c12;
                         lst = nb;
-                        c12_before = cm.c12;
+                    }
+                } else if (o == 0) {               // the open tile would extend to slice z
+                    if (stg + cp.c12 > V4_MS || lst + nb > V4_ML || z - tz + 1 > V4_MAXZ - 2) {
+                        if (home > 0) emit(tz, z - 1, tfirst, home);
+                        open = false;
+                        continue;                  // start a new tile at slice z
+                    }
+                    stg += cp.c12;
+                    lst += nb;
+                }
+                if (take) {
+                    const int n = min(c0.slice - o, V4_TP - home);
+                    home += n;
+                    o += n;
+                    if (home == V4_TP) {
+                        emit(tz, z, tfirst, home);
+                        open = false;
                     }
                 }
-                cm = c0;
-                c0 = cp;
+                if (o >= c0.slice) {
+                    ++z;
+                    o = 0;
+                    cm = c0;
+                    c0 = cp;
+                    cp = zcols(g, cell_start, rb, hasB, z + 1);
+                }
             }
-            if (cs >= 0 && home > 0) emit(cs, g.nz - 1, -1);
+            if (open && home > 0) emit(tz, g.nz - 1, tfirst, home);
         }
         if (!WRITE) off[key] = nt;
     }
@@ -336,70 +355,41 @@ struct V4Stage {
 // projected separation is below Hk; the separation grows along each segment.
 // Segment 0 (+d neighbour, reversed list) is read backwards from storage index f0
 // with sep = (x_j - h0) . d, segment 1 (-d neighbour, reversed list) forwards from
-// f1 with sep = (h1 - x_j) . d.  Galloping from the near end, then bisecting: the
-// exact per-particle bound of P:151-165; the two searches advance in lockstep so
-// their shared-memory loads overlap.
-struct Gallop {
-    int lo, hi, k, step;
-    __device__ __forceinline__ void init(int n)
-    {
-        lo = 0;
-        hi = n;
-        k = 0;
-        step = 1;
-    }
-    __device__ __forceinline__ bool active() const { return lo < hi; }
-    __device__ __forceinline__ int probe() const { return k < hi ? k : (lo + hi) >> 1; }
-    __device__ __forceinline__ void update(bool below)
-    {
-        if (k < hi) {                 // galloping phase: probes 0, 1, 3, 7, ...
-            if (below) {
-                lo = k + 1;
-                k += step;
-                step <<= 1;
-                if (k >= hi) k = 0x7fffffff;
-            } else {
-                hi = k;
-                k = 0x7fffffff;
-            }
-        } else {                      // bisection
-            const int mid = (lo + hi) >> 1;
-            if (below) lo = mid + 1; else hi = mid;
-        }
-    }
-};
-
-__device__ __forceinline__ void v4_windows(const V4Stage &S, int f0, int n0, int f1, int n1, float c0, float c1,
-                                           float c2, float h0x, float h0y, float h0z, float h1x, float h1y, float h1z,
-                                           float Hk, int &len0, int &len1)
+// f1 with sep = (h1 - x_j) . d.  Branch-free bisection with `top` = the largest
+// power of two <= the warp's longest segment, so every lane runs the same steps:
+// the exact per-particle bound of P:151-165; the two searches are interleaved.
+__device__ __forceinline__ void v4_windows(const V4Stage &S, int top, int f0, int n0, int f1, int n1, float c0,
+                                           float c1, float c2, float h0x, float h0y, float h0z, float h1x,
+                                           float h1y, float h1z, float Hk, int &len0, int &len1)
 {
-    Gallop A, B;
-    A.init(n0);
-    B.init(n1);
-    while (A.active() || B.active()) {
-        const bool ga = A.active(), gb = B.active();
-        const int ka = A.probe(), kb = B.probe();
-        const unsigned ia = ga ? lds_u16(S.L + 2u * (unsigned)(f0 - ka)) : 0u;
-        const unsigned ib = gb ? lds_u16(S.L + 2u * (unsigned)(f1 + kb)) : 0u;
-        const float4 pa = lds_f4(S.P + 16u * ia), pb = lds_f4(S.P + 16u * ib);
-        const float sa = fmaf(c0, pa.x - h0x, fmaf(c1, pa.y - h0y, c2 * (pa.z - h0z)));
-        const float sb = fmaf(c0, h1x - pb.x, fmaf(c1, h1y - pb.y, c2 * (h1z - pb.z)));
-        if (ga) A.update(sa < Hk);
-        if (gb) B.update(sb < Hk);
+    int lo0 = 0, lo1 = 0;
+    for (int st = top; st > 0; st >>= 1) {
+        const int k0 = lo0 + st, k1 = lo1 + st;           // is entry k - 1 inside the window?
+        const bool v0 = k0 <= n0, v1 = k1 <= n1;
+        const unsigned i0 = v0 ? lds_u16(S.L + 2u * (unsigned)(f0 - k0 + 1)) : 0u;
+        const unsigned i1 = v1 ? lds_u16(S.L + 2u * (unsigned)(f1 + k1 - 1)) : 0u;
+        const float4 p0 = lds_f4(S.P + 16u * i0), p1 = lds_f4(S.P + 16u * i1);
+        const float s0 = fmaf(c0, p0.x - h0x, fmaf(c1, p0.y - h0y, c2 * (p0.z - h0z)));
+        const float s1 = fmaf(c0, h1x - p1.x, fmaf(c1, h1y - p1.y, c2 * (h1z - p1.z)));
+        if (v0 && s0 < Hk) lo0 = k0;
+        if (v1 && s1 < Hk) lo1 = k1;
     }
-    len0 = A.lo;
-    len1 = B.lo;
+    len0 = lo0;
+    len1 = lo1;
 }
 
 // One lane = one home particle of a staged tile.  lpos: first list entry of its home
 // cell, qh: its staged column, yoff: its row in the tile (0/1).  FRAMES: the tile
 // touches a high box face (some home coordinate must be shifted by -L).
+// Hits are pushed on a per-lane stack of staged indices in shared memory (slot k of
+// lane l at qbase + 64 k + 2 l: conflict-free); every particle sums its hits in a
+// fixed order, so the result does not depend on the tile or the warp.
 template <bool COUNT, bool FRAMES>
 __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCells &c, const DevOut &o,
                                                    const V4Stage &S, unsigned qbase, bool active, int i, int yoff,
                                                    int qh, int lpos, unsigned cand[4], unsigned hits[4])
 {
-    const unsigned sQ = qbase + 4u * (threadIdx.x & 31);
+    const unsigned sQ = qbase + 2u * (threadIdx.x & 31);
     float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
     if (active) {
         const float4 a = c.xyzh[i];
@@ -420,115 +410,136 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
 
     Acc2 A;
     A.rho = A.wc = A.srt = A.st = A.Dn = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
-    unsigned head = 0, tail = 0;
+    unsigned qp = sQ;                                     // stack top (next free slot)
+    int nngb = 0;
 
     auto home_of = [&](unsigned fl, float &hx, float &hy, float &hz) {
         hx = (fl & 1u) ? xs : x;
         hy = (fl & 2u) ? ys : y;
         hz = (fl & 4u) ? zs : z;
     };
-    // pop one pair of hits per lane (FINAL: also a single one)
+    // pop two hits per lane (FINAL: also a single one)
     auto drain = [&](auto final_tag) {
         constexpr bool FINAL = decltype(final_tag)::value;
-        const unsigned n = tail - head;
+        const unsigned n = (qp - sQ) >> 6;
         if (n >= 2 || (FINAL && n == 1)) {
-            const unsigned e0 = lds_u32(sQ + ((head & (V4_Q - 1)) << 7));
-            const unsigned e1 = (!FINAL || n >= 2) ? lds_u32(sQ + (((head + 1) & (V4_Q - 1)) << 7)) : e0;
-            const unsigned s0 = e0 & 0xffffu, s1 = e1 & 0xffffu;
+            const bool two = !FINAL || n >= 2;
+            const unsigned e0 = lds_u16(qp - 64u);
+            const unsigned e1 = two ? lds_u16(qp - 128u) : e0;
+            qp -= two ? 128u : 64u;
+            nngb += two ? 2 : 1;
+            const unsigned s0 = FRAMES ? (e0 & 0xfffu) : e0, s1 = FRAMES ? (e1 & 0xfffu) : e1;
             float hx0 = x, hy0 = y, hz0 = z, hx1 = x, hy1 = y, hz1 = z;
             if (FRAMES) {
-                home_of(e0 >> 16, hx0, hy0, hz0);
-                home_of(e1 >> 16, hx1, hy1, hz1);
+                home_of(e0 >> 12, hx0, hy0, hz0);
+                home_of(e1 >> 12, hx1, hy1, hz1);
             }
             const float4 p0 = lds_f4(S.P + 16u * s0), p1 = lds_f4(S.P + 16u * s1);
             const float4 v0 = lds_f4(S.V + 16u * s0), v1 = lds_f4(S.V + 16u * s1);
-            const f2 mk = pk(1.0f, n >= 2 ? 1.0f : 0.0f);
+            const f2 mk = pk(1.0f, two ? 1.0f : 0.0f);
             interact_pair<FINAL>(Hinv2, pk(hx0 - p0.x, hx1 - p1.x), pk(hy0 - p0.y, hy1 - p1.y),
                                  pk(hz0 - p0.z, hz1 - p1.z), pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx),
                                  pk(v0.y - vy, v1.y - vy), pk(v0.z - vz, v1.z - vz), mk, A);
-            head += (!FINAL || n >= 2) ? 2u : 1u;
+        }
+    };
+    // keep every stack at <= V4_Q - 9 entries (8 pushes follow before the next check)
+    auto drain_check = [&]() {
+        for (;;) {
+            const unsigned n = (qp - sQ) >> 6;
+            if (!(__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= V4_Q - 8)))
+                break;
+            drain(std::false_type{});
+        }
+    };
+    // candidates t .. t+3 of the window L[lb + ...] (SELF: the home cell, staged index base + t, minus i)
+    auto step4 = [&](auto self_tag, unsigned lb, int base, int t, int total, int len0, unsigned fl0, unsigned fl1,
+                     int kind) {
+        constexpr bool SELF = decltype(self_tag)::value;
+        bool ok[4];
+        unsigned sj[4];
+        float4 p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            ok[u] = t + u < total && (!SELF || t + u != kh);
+            if (SELF) {
+                sj[u] = (unsigned)(base + (ok[u] ? t + u : 0));
+            } else {
+                const unsigned e = lds_u16(lb + 2u * (unsigned)(t + u));   // in the segment or just past it
+                sj[u] = ok[u] ? e : 0u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) p[u] = lds_f4(S.P + 16u * sj[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float hx = x, hy = y, hz = z;
+            unsigned fl = 0;
+            if (FRAMES && !SELF) {
+                fl = t + u < len0 ? fl0 : fl1;
+                home_of(fl, hx, hy, hz);
+            }
+            const float dx = hx - p[u].x, dy = hy - p[u].y, dz = hz - p[u].z;
+            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (COUNT) cand[kind] += ok[u] ? 1u : 0u;
+            if (ok[u] && r2 < H2) {
+                sts_u16(qp, FRAMES ? (sj[u] | (fl << 12)) : sj[u]);
+                qp += 64u;
+                if (COUNT) ++hits[kind];
+            }
         }
     };
 
-    int pos = lpos;                                       // this home cell's list segments
-    for (int a = 0; a < 14; ++a) {
-        // a = 0: the self cell (identity segment); a = 1 + d: reversed +d list, then reversed -d list,
-        // so that the lane's two windows (a prefix of +d, a suffix of -d) are contiguous: L[wb, wb + total)
-        int wb = 0, len0 = 0, total = 0, kind = 0;
-        unsigned fl0 = 0, fl1 = 0;
-        if (a == 0) {
-            if (active) {
-                wb = pos;
-                total = eh.y;
-                len0 = total;
-                pos += eh.y;
-            }
-        } else {
-            const int d = a - 1;
-            kind = v4_kind(d);
-            const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
-            const float Hk = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
-            if (active) {
-                const int4 ep = S.tab[scell(a0, a1, a2)];
-                const int4 em = S.tab[scell(-a0, -a1, -a2)];
-                const int mid = pos + ep.y;                   // boundary between the two reversed segments
-                pos = mid + em.y;
-                float px = x, py = y, pz = z, mx = x, my = y, mz = z;
-                if (FRAMES) {
-                    fl0 = (unsigned)ep.w & 7u;
-                    fl1 = (unsigned)em.w & 7u;
-                    home_of(fl0, px, py, pz);
-                    home_of(fl1, mx, my, mz);
-                }
-                const float c0 = (float)a0, c1 = (float)a1, c2 = (float)a2;
-                int len1;
-                v4_windows(S, mid - 1, ep.y, mid, em.y, c0, c1, c2, px, py, pz, mx, my, mz, Hk, len0, len1);
-                wb = mid - len0;
-                total = len0 + len1;
-            }
-        }
+    // the self cell: all j != i of the home cell
+    {
+        const int total = active ? eh.y : 0;
         const int trip = __reduce_max_sync(0xffffffffu, total);
-        const int excl = a == 0 ? kh : -1;                                 // i itself in the self cell
-        const unsigned lb = S.L + 2u * (unsigned)wb;
-        for (int t = 0; t < trip; t += 4) {
-            // four candidates: list loads, then positions, then the tests (ILP across candidates)
-            bool ok[4];
-            unsigned sj[4];
-            float4 p[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                ok[u] = t + u < total && t + u != excl;
-                sj[u] = ok[u] ? lds_u16(lb + 2u * (unsigned)(t + u)) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) p[u] = lds_f4(S.P + 16u * sj[u]);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                float hx = x, hy = y, hz = z;
-                unsigned fl = 0;
-                if (FRAMES) {
-                    fl = t + u < len0 ? fl0 : fl1;
-                    home_of(fl, hx, hy, hz);
-                }
-                const float dx = hx - p[u].x, dy = hy - p[u].y, dz = hz - p[u].z;
-                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                if (COUNT) cand[kind] += ok[u] ? 1u : 0u;
-                if (ok[u] && r2 < H2) {
-                    sts_u32(sQ + ((tail & (V4_Q - 1)) << 7), FRAMES ? (sj[u] | (fl << 16)) : sj[u]);
-                    ++tail;
-                    if (COUNT) ++hits[kind];
-                }
-            }
-            // at most four pushes per step: keep every queue at <= V4_Q - 5 entries after draining
-            for (;;) {
-                const unsigned n = tail - head;
-                if (!(__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= V4_Q - 4)))
-                    break;
-                drain(std::false_type{});
-            }
+        for (int t = 0; t < trip; t += 8) {
+            step4(std::true_type{}, 0u, eh.x, t, total, total, 0u, 0u, 0);
+            step4(std::true_type{}, 0u, eh.x, t + 4, total, total, 0u, 0u, 0);
+            drain_check();
         }
     }
-    while (__any_sync(0xffffffffu, tail != head)) drain(std::true_type{});
+    int pos = lpos + eh.y;                                // this home cell's direction segments
+    for (int d = 0; d < 13; ++d) {
+        // reversed +d list, then reversed -d list, so that the lane's two windows (a prefix
+        // of +d, a suffix of -d) are contiguous: L[wb, wb + total)
+        int wb = 0, len0 = 0, total = 0;
+        unsigned fl0 = 0, fl1 = 0;
+        const int kind = v4_kind(d);
+        const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+        const float Hk = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
+        int4 ep = make_int4(0, 0, 0, 0), em = make_int4(0, 0, 0, 0);
+        if (active) {
+            ep = S.tab[scell(a0, a1, a2)];
+            em = S.tab[scell(-a0, -a1, -a2)];
+        }
+        const int nmax = __reduce_max_sync(0xffffffffu, max(ep.y, em.y));
+        const int top = nmax > 0 ? 1 << (31 - __clz(nmax)) : 0;
+        if (active) {
+            const int mid = pos + ep.y;                   // boundary between the two reversed segments
+            pos = mid + em.y;
+            float px = x, py = y, pz = z, mx = x, my = y, mz = z;
+            if (FRAMES) {
+                fl0 = (unsigned)ep.w & 7u;
+                fl1 = (unsigned)em.w & 7u;
+                home_of(fl0, px, py, pz);
+                home_of(fl1, mx, my, mz);
+            }
+            int len1;
+            v4_windows(S, top, mid - 1, ep.y, mid, em.y, (float)a0, (float)a1, (float)a2, px, py, pz, mx, my, mz,
+                       Hk, len0, len1);
+            wb = mid - len0;
+            total = len0 + len1;
+        }
+        const int trip = __reduce_max_sync(0xffffffffu, total);
+        const unsigned lb = S.L + 2u * (unsigned)wb;
+        for (int t = 0; t < trip; t += 8) {
+            step4(std::false_type{}, lb, 0, t, total, len0, fl0, fl1, kind);
+            step4(std::false_type{}, lb, 0, t + 4, total, len0, fl0, fl1, kind);
+            drain_check();
+        }
+    }
+    while (__any_sync(0xffffffffu, qp != sQ)) drain(std::true_type{});
 
     if (active) {
         // finalise (self term w(0) = 1/2, t(0) = 3/2), as finalise() in density.cuh
@@ -550,14 +561,14 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
             o.curl_v[out] = gf * (sum2(A.Px) - sum2(A.Nx)) * rinv;
             o.curl_v[o.n_out + out] = gf * (sum2(A.Py) - sum2(A.Ny)) * rinv;
             o.curl_v[2 * o.n_out + out] = gf * (sum2(A.Pz) - sum2(A.Nz)) * rinv;
-            o.nngb[out] = (int)tail;
+            o.nngb[out] = nngb;
         }
     }
 }
 
 // Persistent CTAs take tiles in order from an atomic counter.
 template <bool COUNT>
-__global__ void __launch_bounds__(V4_TP, 2) k_density_v4(DevGrid g, DevCells c, DevOut o, sph_stats *st,
+__global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCells c, DevOut o, sph_stats *st,
                                                          const int4 *__restrict__ tiles,
                                                          const int *__restrict__ ntiles_p, int *tile_counter)
 {
@@ -567,7 +578,8 @@ __global__ void __launch_bounds__(V4_TP, 2) k_density_v4(DevGrid g, DevCells c, 
     int4 *tab = reinterpret_cast<int4 *>(V + V4_MS);
     uint16_t *L = reinterpret_cast<uint16_t *>(tab + V4_MAXCELLS);
     int *hoff = reinterpret_cast<int *>(L + V4_ML);
-    unsigned *queue = reinterpret_cast<unsigned *>(hoff + V4_MAXH + 4);
+    uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_MAXH + 4);
+    int4 *seq = reinterpret_cast<int4 *>(queue + V4_WARPS * V4_Q * 32);
     __shared__ int s_tile, s_wsum[V4_WARPS];
 
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -585,19 +597,47 @@ __global__ void __launch_bounds__(V4_TP, 2) k_density_v4(DevGrid g, DevCells c, 
         key_rowpair(rp, td.x, xo, yp);
         const int y0 = 2 * yp;
         const bool hasB = y0 + 1 < g.ny;
-        const int za = td.y, zb = td.z, chunk = td.w;
+        const int za = td.y & 0xffff, zb = td.y >> 16, first = td.z, cnt = td.w;
         const long long rowA = ((long long)(xo + g.ghost_x) * g.ny + y0) * g.nz;
-        const int sA = c.cell_start[rowA + za], eA = c.cell_start[rowA + zb + 1];
-        const int sB = hasB ? c.cell_start[rowA + g.nz + za] : 0;
-        const int eB = hasB ? c.cell_start[rowA + g.nz + zb + 1] : 0;
-        const int nA = eA - sA, nH = nA + (eB - sB);
         const int nzs = zb - za + 3, nzh = zb - za + 1, nh = (hasB ? 2 : 1) * nzh;
-        bool staged = chunk < 0 && nzs <= V4_MAXZ;
+        bool staged = cnt > 0 && nzs <= V4_MAXZ;
         // a staged neighbour beyond a high face (home shift needed): x plane, y row or z column
         const bool frames = g.x_lo + xo + 1 >= g.nc[0] || y0 + 2 >= g.ny || zb + 1 >= g.nz;
+        // home slices: {A start, A count, B start, first sequence index}
+        if ((int)threadIdx.x < nzh) {
+            const long long ca = rowA + za + threadIdx.x;
+            const int a0 = c.cell_start[ca], a1 = c.cell_start[ca + 1];
+            const int b0 = hasB ? c.cell_start[ca + g.nz] : 0, b1 = hasB ? c.cell_start[ca + g.nz + 1] : 0;
+            seq[threadIdx.x] = make_int4(a0, a1 - a0, b0, (a1 - a0) + (b1 - b0));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int acc = 0;
+            for (int k = 0; k < nzh; ++k) {
+                const int n = seq[k].w;
+                seq[k].w = acc;
+                acc += n;
+            }
+        }
+        __syncthreads();
+        // home particle of thread h: sequence index first + h from slice za on
+        auto home_slot = [&](int h, int &slot, int &yo, int &tz) {
+            const int q = first + h;
+            int lo = 0, hi = nzh - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (seq[mid].w <= q) lo = mid; else hi = mid - 1;
+            }
+            const int4 e = seq[lo];
+            const int loc = q - e.w;
+            yo = loc < e.y ? 0 : 1;
+            slot = yo == 0 ? e.x + loc : e.z + (loc - e.y);
+            tz = lo;
+        };
 
         if (staged) {
             // staged cell table: s = row * nzs + col, row = (ox + 1) * 4 + (oy + 1), col = uz - za + 1
+            static_assert(V4_MAXCELLS <= 2 * V4_TP, "two table entries per thread");
             const int ncs = V4_ROWS * nzs;
             int cnt[2] = {0, 0};
             int4 ent[2];
@@ -702,30 +742,28 @@ __global__ void __launch_bounds__(V4_TP, 2) k_density_v4(DevGrid g, DevCells c, 
 
         if (staged) {
             const int h = threadIdx.x;
-            const bool active = h < nH;
-            const int i = active ? (h < nA ? sA + h : sB + (h - nA)) : sA;
-            const int yoff = h < nA ? 0 : 1;
-            int qh = 1, lpos = 0;
+            const bool active = h < cnt;
+            int i = 0, yoff = 0, tz = 0, lpos = 0;
             if (active) {
-                const int iz = c.slot_cell[i] % g.nz;
-                qh = iz - za + 1;
-                lpos = hoff[yoff * nzh + iz - za];
+                home_slot(h, i, yoff, tz);
+                lpos = hoff[yoff * nzh + tz];
+            } else {
+                i = seq[0].x;
             }
             const V4Stage S{smem_addr(P), smem_addr(V), smem_addr(L), tab, nzs};
             const unsigned qb = smem_addr(queue + wl * V4_Q * 32);
-            if (wl * 32 < nH) {
+            if (wl * 32 < cnt) {
                 if (frames)
-                    v4_particle_staged<COUNT, true>(g, c, o, S, qb, active, i, yoff, qh, lpos, cand, hits);
+                    v4_particle_staged<COUNT, true>(g, c, o, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
                 else
-                    v4_particle_staged<COUNT, false>(g, c, o, S, qb, active, i, yoff, qh, lpos, cand, hits);
+                    v4_particle_staged<COUNT, false>(g, c, o, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
             }
         } else {
-            // global-memory sweep: chunk tiles (a z-slice that cannot be staged) or oversized neighbourhoods
-            const int base = chunk < 0 ? 0 : chunk * V4_TP;
-            const int nAll = chunk < 0 ? nH : min(nH - base, V4_TP);
-            for (int h = threadIdx.x; h < nAll; h += V4_TP) {
-                const int hh = base + h;
-                const int i = hh < nA ? sA + hh : sB + (hh - nA);
+            // global-memory sweep: a slice that cannot be staged, or a tile whose check failed
+            const int ntot = cnt > 0 ? cnt : -cnt;
+            for (int h = threadIdx.x; h < ntot; h += V4_TP) {
+                int i, yo, tz;
+                home_slot(h, i, yo, tz);
                 v4_particle_global<COUNT>(g, c, o, i, cand, hits);
             }
         }
