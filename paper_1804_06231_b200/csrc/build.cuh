@@ -2,15 +2,18 @@
 //
 //   k_bin          : validate, fp64 bin, atomic slot rank within the cell, cell_hmax
 //   k_scan_*       : exclusive scan of the per-cell counts -> cell_start
-//   k_scatter_perm : perm_tmp[cell_start[cell] + rank] = input index
-//   k_stable_*     : sort each cell's input indices ascending (the atomic ranks
-//                    arrive in any order) -> perm: in-cell order = input order
-//   k_gather       : xyzh, vm in cell order
+//   k_scatter_rec  : the particle's 32-byte record (x, y, z, h, vx, vy, vz, m) and
+//                    input index to slot cell_start[cell] + rank (one full
+//                    sector per particle: no read-modify-write at random slots)
+//   k_stable_*     : per cell, sort the records by input index (the atomic ranks
+//                    arrive in any order) -> xyzh, vm, perm, slot_cell with the
+//                    in-cell order = input order, all reads/writes coalesced
 //
 // Stable in-cell order makes everything downstream deterministic and, with
 // slab ghosts received in the sender's cell order, identical across GPU
-// counts.  HBM traffic ~ 32 (read) + 12 (cell/rank/
-// count) + 12 (scatter) + 8 (stable) + 4+32+32 (gather) ~ 130 B/particle.
+// counts.  HBM traffic per particle ~ 32 (read) + 8
+// (cell/rank) + 40 (re-read) + 36 + 32 (scattered record + index sector) +
+// 36 (stable read) + 40 (write) ~ 225 B.
 #pragma once
 
 #include "common.cuh"
@@ -146,13 +149,28 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_add(int *__restrict__ start, lo
         if (base + k < n) start[base + k] += add;
 }
 
-__global__ void k_scatter_perm(long long n_total, const int *__restrict__ cell_of, const int *__restrict__ rank,
-                               const int *__restrict__ start, int *__restrict__ perm_tmp)
+struct alignas(32) ParticleRec {
+    float4 xyzh, vm;
+};
+
+__global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of, const int *__restrict__ rank,
+                              const int *__restrict__ start, const float4 *__restrict__ xyzh_in,
+                              const float4 *__restrict__ vm_in, ParticleRec *__restrict__ rec,
+                              int *__restrict__ idx_tmp)
 {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
          p += (long long)gridDim.x * blockDim.x) {
-        int c = cell_of[p];
-        if (c >= 0) perm_tmp[start[c] + rank[p]] = (int)p;
+        const int c = __ldcs(cell_of + p);
+        if (c >= 0) {
+            const int slot = start[c] + __ldcs(rank + p);
+            const float4 a = __ldcs(xyzh_in + p), b = __ldcs(vm_in + p);
+            // one 256-bit store (STG.256): the whole 32-byte sector at once, no read-modify-write
+            // (evict-first: the scattered stream must not push cell_start out of L2)
+            asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + slot), "f"(a.x),
+                         "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                         : "memory");
+            __stcs(idx_tmp + slot, (int)p);
+        }
     }
 }
 
@@ -162,23 +180,33 @@ constexpr int STABLE_BIG_CHUNK = 256;
 constexpr int STABLE_BIG_TILE = 4096;
 
 // One warp per cell of <= STABLE_SMALL particles: rank each input index among the
-// cell's (all distinct) and place it.  Larger cells are queued as (cell, chunk).
+// cell's (all distinct) and move its record there.  Larger cells are queued as
+// (cell, chunk).  slot_cell is written for every slot.
+__device__ __forceinline__ void stable_place(int s0, int e, int r, const ParticleRec *__restrict__ rec,
+                                             const int *__restrict__ idx_tmp, float4 *__restrict__ xyzh,
+                                             float4 *__restrict__ vm, int *__restrict__ perm)
+{
+    const ParticleRec q = rec[s0 + e];
+    xyzh[s0 + r] = q.xyzh;
+    vm[s0 + r] = q.vm;
+    perm[s0 + r] = idx_tmp[s0 + e];
+}
+
 __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
-                                                                    const int *__restrict__ perm_tmp,
-                                                                    int *__restrict__ perm, int2 *big_items,
-                                                                    int *big_count)
+                                                                    const int *__restrict__ idx_tmp,
+                                                                    const ParticleRec *__restrict__ rec,
+                                                                    float4 *__restrict__ xyzh, float4 *__restrict__ vm,
+                                                                    int *__restrict__ perm, int *__restrict__ slot_cell,
+                                                                    int2 *big_items, int *big_count)
 {
     __shared__ int sh[STABLE_WARPS][STABLE_SMALL];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     constexpr int PER = STABLE_SMALL / 32;
     for (long long cell = (long long)blockIdx.x * STABLE_WARPS + w; cell < ncell;
          cell += (long long)gridDim.x * STABLE_WARPS) {
-        int s0 = start[cell];
-        int n = start[cell + 1] - s0;
-        if (n <= 1) {
-            if (n == 1 && lane == 0) perm[s0] = perm_tmp[s0];
-            continue;
-        }
+        const int s0 = start[cell];
+        const int n = start[cell + 1] - s0;
+        for (int e = lane; e < n; e += 32) slot_cell[s0 + e] = (int)cell;
         if (n > STABLE_SMALL) {
             if (lane == 0) {
                 int nch = (n + STABLE_BIG_CHUNK - 1) / STABLE_BIG_CHUNK;
@@ -190,18 +218,18 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         int v[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            int e = lane + 32 * k;
-            v[k] = e < n ? perm_tmp[s0 + e] : 0;
+            const int e = lane + 32 * k;
+            v[k] = e < n ? idx_tmp[s0 + e] : 0;
             if (e < n) sh[w][e] = v[k];
         }
         __syncwarp();
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
-            int e = lane + 32 * k;
+            const int e = lane + 32 * k;
             if (e < n) {
                 int r = 0;
                 for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
-                perm[s0 + r] = v[k];
+                stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm);
             }
         }
         __syncwarp();
@@ -209,7 +237,9 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
 }
 
 __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__restrict__ start,
-                                                                  const int *__restrict__ perm_tmp,
+                                                                  const int *__restrict__ idx_tmp,
+                                                                  const ParticleRec *__restrict__ rec,
+                                                                  float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                   int *__restrict__ perm, const int2 *big_items,
                                                                   const int *big_count)
 {
@@ -221,34 +251,20 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
         int n = start[item.x + 1] - s0;
         int e = item.y * STABLE_BIG_CHUNK + threadIdx.x;
         bool mine = e < n;
-        int v = mine ? perm_tmp[s0 + e] : 0;
+        int v = mine ? idx_tmp[s0 + e] : 0;
         int r = 0;
         for (int t0 = 0; t0 < n; t0 += STABLE_BIG_TILE) {
             int tn = min(STABLE_BIG_TILE, n - t0);
             __syncthreads();
-            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = perm_tmp[s0 + t0 + m];
+            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = idx_tmp[s0 + t0 + m];
             __syncthreads();
             if (mine)
                 for (int m = 0; m < tn; ++m) r += tile[m] < v;
         }
-        if (mine) perm[s0 + r] = v;
+        if (mine) stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm);
         __syncthreads();
     }
 }
 
-__global__ void k_gather(long long n_total, const int *__restrict__ start_end, const int *__restrict__ perm,
-                         const int *__restrict__ cell_of, const float4 *__restrict__ xyzh_in,
-                         const float4 *__restrict__ vm_in, float4 *__restrict__ xyzh_s, float4 *__restrict__ vm_s,
-                         int *__restrict__ slot_cell)
-{
-    const long long n_valid = *start_end;   // cell_start[ncell]: particles actually binned
-    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_valid && k < n_total;
-         k += (long long)gridDim.x * blockDim.x) {
-        int p = perm[k];
-        xyzh_s[k] = xyzh_in[p];
-        vm_s[k] = vm_in[p];
-        slot_cell[k] = cell_of[p];
-    }
-}
 
 }  // namespace pvsph

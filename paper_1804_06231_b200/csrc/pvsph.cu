@@ -120,8 +120,8 @@ DevOut dev_out(const sph_out *o)
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
-    size_t status, cell_of, rank, perm_tmp, count, tile_sum, big_count, big_items, rows, rows_sum, tiles, counter,
-        total;
+    size_t status, cell_of, rank, perm_tmp, rec, count, tile_sum, big_count, big_items, rows, rows_sum, tiles,
+        counter, total;
     long long tile_cap;
 };
 
@@ -138,6 +138,8 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
     w.perm_tmp = o;
     o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
+    w.rec = o;
+    o = align_up(o + 32 * (size_t)(n > 0 ? n : 1), 256);
     w.count = o;
     o = align_up(o + 4 * (size_t)(ncell + 1), 256);
     long long ntiles = (ncell + SCAN_TILE - 1) / SCAN_TILE;
@@ -239,14 +241,14 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     int2 *big_items = at<int2>(ws, w.big_items);
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     if (n > 0) {
-        k_scatter_perm<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cell_of, rank, cells->cell_start, perm_tmp);
+        ParticleRec *rec = at<ParticleRec>(ws, w.rec);
+        k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cell_of, rank, cells->cell_start, xin, vin,
+                                                                    rec, perm_tmp);
+        float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, perm_tmp, cells->perm, big_items, big_count);
-        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, cells->perm, big_items,
-                                                          big_count);
-        k_gather<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cells->cell_start + g.ncell, cells->perm, cell_of,
-                                                               xin, vin, reinterpret_cast<float4 *>(cells->xyzh),
-                                                               reinterpret_cast<float4 *>(cells->vm), cells->slot_cell);
+            g.ncell, cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, cells->slot_cell, big_items, big_count);
+        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, rec, xs, vs, cells->perm,
+                                                          big_items, big_count);
     }
     cells->n = n;
     return check_launch();

@@ -7,18 +7,18 @@
 // key, ties by input index perm[k] -- deterministic whatever the slot order.
 // Each list entry is the particle's in-cell index (uint16, include/sph.h).
 //
-// Small cells (n <= SORT_SMALL): one warp per cell, composite 64-bit keys
-// (orderable key << 32 | input index) staged in shared memory, rank by
-// counting.  Larger cells are queued as (cell, chunk) items and ranked by
-// k_sort_big, one CTA per chunk of SORT_BIG_CHUNK elements, streaming the
-// cell's composites through shared-memory tiles.
+// Small cells (n <= SORT_SMALL = 32): one warp per cell, one particle per lane,
+// 32-bit composites (quantised fp32 key, in-cell index) ranked by counting.
+// Larger cells are queued as (cell, chunk) items and ranked by k_sort_big, one
+// CTA per chunk of SORT_BIG_CHUNK elements, streaming the cell's 64-bit
+// composites (orderable fp32 key << 32 | input index) through shared memory.
 #pragma once
 
 #include "common.cuh"
 
 namespace pvsph {
 
-constexpr int SORT_SMALL = 128;
+constexpr int SORT_SMALL = 32;
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_BIG_CHUNK = 256;
 constexpr int SORT_BIG_TILE = 2048;
@@ -35,17 +35,16 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
     corner[2] = (double)iz * g.cl[2];
 }
 
-__global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
-                                                                 long long cbeg, long long cend, int2 *big_items,
-                                                                 int *big_count)
+__global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
+                                                                    long long cbeg, long long cend, int2 *big_items,
+                                                                    int *big_count)
 {
-    __shared__ unsigned long long sh[SORT_WARPS][2 * SORT_SMALL];   // >= 32 x 16 u32 for the fast path
+    __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    constexpr int PER = SORT_SMALL / 32;
     for (long long cell = cbeg + (long long)blockIdx.x * SORT_WARPS + w; cell < cend;
          cell += (long long)gridDim.x * SORT_WARPS) {
-        int s0 = c.cell_start[cell];
-        int n = c.cell_start[cell + 1] - s0;
+        const int s0 = c.cell_start[cell];
+        const int n = c.cell_start[cell + 1] - s0;
         if (n == 0) continue;
         if (n > SORT_SMALL) {
             if (lane == 0) {
@@ -57,84 +56,50 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_small(DevGrid g, DevCe
         }
         double corner[3];
         cell_corner(g, cell, corner);
-        if (n <= 32) {
-            // Fast path, one particle per lane, all 13 directions ranked in one pass over the
-            // cell: composite = quantised key (25 bits) << 7 | in-cell index (the slot order is
-            // the input order, so equal keys keep input order).  The quantum 2 sqrt(3) C_l / 2^25
-            // (~1e-7 C_l) is far below the window margin delta = 2^-16 C_l.
-            unsigned *S = reinterpret_cast<unsigned *>(sh[w]);   // [32][16] composites
-            const bool mine = lane < n;
-            float4 p = mine ? c.xyzh[s0 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-            const double u0 = (double)p.x - corner[0], u1 = (double)p.y - corner[1], u2 = (double)p.z - corner[2];
-            const double cmax = 1.7320508075688772 * fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
-            const double scale = 33554432.0 / (2.0 * cmax);      // 2^25 over the key range
-            unsigned comp[SPH_NDIR];
+        // One particle per lane, all 13 directions ranked in one pass over the cell:
+        // composite = quantised key (25 bits) << 7 | in-cell index (the slot order is the
+        // input order, so equal keys keep input order).  The fp32 key error (< 1e-6 C_l)
+        // and the quantum 2 sqrt(3) C_l / 2^25 (~1e-7 C_l) are far below the window margin
+        // delta = 2^-16 C_l; the density sweeps tolerate that much disorder.
+        unsigned *S = sh[w];
+        const bool mine = lane < n;
+        const float4 p = mine ? c.xyzh[s0 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        // cell-local coordinates in fp32: x - fp32(corner) is exact (Sterbenz) unless both are
+        // within a cell of 0, where the error is below ulp(C_l)
+        const float u0 = p.x - (float)corner[0], u1 = p.y - (float)corner[1], u2 = p.z - (float)corner[2];
+        const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
+        const float scale = 33554432.0f / (2.0f * cmax);     // 2^25 over the key range
+        unsigned comp[SPH_NDIR];
 #pragma unroll
-            for (int d = 0; d < SPH_NDIR; ++d) {
-                double key = (double)pv_key(u0, u1, u2, d);
-                double qk = floor((key + cmax) * scale);
-                qk = fmin(fmax(qk, 0.0), 33554431.0);
-                comp[d] = ((unsigned)qk << 7) | (unsigned)lane;
-                if (mine) S[lane * 16 + d] = comp[d];
-            }
-            __syncwarp();
-            unsigned r[SPH_NDIR];
-#pragma unroll
-            for (int d = 0; d < SPH_NDIR; ++d) r[d] = 0;
-            for (int m = 0; m < n; ++m) {
-                const uint4 c0 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 0]);
-                const uint4 c1 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 4]);
-                const uint4 c2 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 8]);
-                const unsigned c12 = S[m * 16 + 12];
-                r[0] += c0.x < comp[0]; r[1] += c0.y < comp[1]; r[2] += c0.z < comp[2]; r[3] += c0.w < comp[3];
-                r[4] += c1.x < comp[4]; r[5] += c1.y < comp[5]; r[6] += c1.z < comp[6]; r[7] += c1.w < comp[7];
-                r[8] += c2.x < comp[8]; r[9] += c2.y < comp[9]; r[10] += c2.z < comp[10]; r[11] += c2.w < comp[11];
-                r[12] += c12 < comp[12];
-            }
-            if (mine) {
-#pragma unroll
-                for (int d = 0; d < SPH_NDIR; ++d) ord[(long long)d * c.cap + s0 + r[d]] = (uint16_t)lane;
-            }
-            __syncwarp();
-            continue;
-        }
-        double u[PER][3];
-        unsigned tie[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            int e = lane + 32 * k;
-            if (e < n) {
-                float4 p = c.xyzh[s0 + e];
-                u[k][0] = (double)p.x - corner[0];
-                u[k][1] = (double)p.y - corner[1];
-                u[k][2] = (double)p.z - corner[2];
-                tie[k] = (unsigned)c.perm[s0 + e];
-            }
-        }
         for (int d = 0; d < SPH_NDIR; ++d) {
-            float key[PER];
-            unsigned long long comp[PER];
-#pragma unroll
-            for (int k = 0; k < PER; ++k) {
-                int e = lane + 32 * k;
-                if (e < n) {
-                    key[k] = pv_key(u[k][0], u[k][1], u[k][2], d);
-                    comp[k] = ((unsigned long long)float_order(key[k]) << 32) | tie[k];
-                    sh[w][e] = comp[k];
-                }
-            }
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < PER; ++k) {
-                int e = lane + 32 * k;
-                if (e < n) {
-                    int r = 0;
-                    for (int m = 0; m < n; ++m) r += sh[w][m] < comp[k];
-                    ord[(long long)d * c.cap + s0 + r] = (uint16_t)e;
-                }
-            }
-            __syncwarp();
+            const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+            const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
+            const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
+            const float key = ((float)a0 * u0 + (float)a1 * u1 + (float)a2 * u2) * inv;
+            float qk = floorf((key + cmax) * scale);
+            qk = fminf(fmaxf(qk, 0.0f), 33554431.0f);
+            comp[d] = ((unsigned)qk << 7) | (unsigned)lane;
+            if (mine) S[lane * 16 + d] = comp[d];
         }
+        __syncwarp();
+        unsigned r[SPH_NDIR];
+#pragma unroll
+        for (int d = 0; d < SPH_NDIR; ++d) r[d] = 0;
+        for (int m = 0; m < n; ++m) {
+            const uint4 c0 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 0]);
+            const uint4 c1 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 4]);
+            const uint4 c2 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 8]);
+            const unsigned c12 = S[m * 16 + 12];
+            r[0] += c0.x < comp[0]; r[1] += c0.y < comp[1]; r[2] += c0.z < comp[2]; r[3] += c0.w < comp[3];
+            r[4] += c1.x < comp[4]; r[5] += c1.y < comp[5]; r[6] += c1.z < comp[6]; r[7] += c1.w < comp[7];
+            r[8] += c2.x < comp[8]; r[9] += c2.y < comp[9]; r[10] += c2.z < comp[10]; r[11] += c2.w < comp[11];
+            r[12] += c12 < comp[12];
+        }
+        if (mine) {
+#pragma unroll
+            for (int d = 0; d < SPH_NDIR; ++d) ord[(long long)d * c.cap + s0 + r[d]] = (uint16_t)lane;
+        }
+        __syncwarp();
     }
 }
 
