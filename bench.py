@@ -290,7 +290,7 @@ def run_ours(args):
     flops = FLOP_CAND * cand_sum + FLOP_HIT * hit_sum          # this rank's density launch
     achieved = flops / (dens_ms_local * 1e-3) / 1e12
     traffic = _profile_traffic()
-    roof = {"bound": "alu", "kernel": "k_density_all", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+    roof = {"bound": "alu", "kernel": "k_density_v4 (sph_density_all incl. its tile list)", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
             "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §6.2)",
             "traffic": (traffic or {}).get(args.config) if traffic else None,

@@ -106,6 +106,9 @@ typedef struct sph_grid {
  *   perm[capacity]          slot -> input index
  *   cell_hmax[ncell]        max h in each cell
  *   slot_cell[capacity]     local cell of each slot (written by build)
+ *   slot_of[capacity]       slot of each input index (written by build; the
+ *                           inverse of perm, used to return outputs in input
+ *                           order with a coalesced gather)
  *   order[SPH_NDIR * capacity] sorted lists (uint16 in-cell indices):
  *                           direction d, cell c at
  *                           order[d * capacity + cell_start[c] ...]
@@ -121,6 +124,7 @@ typedef struct sph_cells {
     float *cell_hmax;
     uint16_t *order;
     int32_t *slot_cell;
+    int32_t *slot_of;
 } sph_cells;
 
 /* Outputs, each an array of n_out elements indexed by INPUT index (only

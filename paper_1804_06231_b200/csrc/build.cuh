@@ -184,12 +184,15 @@ constexpr int STABLE_BIG_TILE = 4096;
 // (cell, chunk).  slot_cell is written for every slot.
 __device__ __forceinline__ void stable_place(int s0, int e, int r, const ParticleRec *__restrict__ rec,
                                              const int *__restrict__ idx_tmp, float4 *__restrict__ xyzh,
-                                             float4 *__restrict__ vm, int *__restrict__ perm)
+                                             float4 *__restrict__ vm, int *__restrict__ perm,
+                                             int *__restrict__ slot_of)
 {
     const ParticleRec q = rec[s0 + e];
+    const int idx = idx_tmp[s0 + e];
     xyzh[s0 + r] = q.xyzh;
     vm[s0 + r] = q.vm;
-    perm[s0 + r] = idx_tmp[s0 + e];
+    perm[s0 + r] = idx;
+    slot_of[idx] = s0 + r;
 }
 
 __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
@@ -197,7 +200,8 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     const ParticleRec *__restrict__ rec,
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
-                                                                    int2 *big_items, int *big_count)
+                                                                    int *__restrict__ slot_of, int2 *big_items,
+                                                                    int *big_count)
 {
     __shared__ int sh[STABLE_WARPS][STABLE_SMALL];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             if (e < n) {
                 int r = 0;
                 for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
-                stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm);
+                stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, slot_of);
             }
         }
         __syncwarp();
@@ -240,8 +244,8 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
                                                                   const int *__restrict__ idx_tmp,
                                                                   const ParticleRec *__restrict__ rec,
                                                                   float4 *__restrict__ xyzh, float4 *__restrict__ vm,
-                                                                  int *__restrict__ perm, const int2 *big_items,
-                                                                  const int *big_count)
+                                                                  int *__restrict__ perm, int *__restrict__ slot_of,
+                                                                  const int2 *big_items, const int *big_count)
 {
     __shared__ int tile[STABLE_BIG_TILE];
     const int nitems = *big_count;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
             if (mine)
                 for (int m = 0; m < tn; ++m) r += tile[m] < v;
         }
-        if (mine) stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm);
+        if (mine) stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, slot_of);
         __syncthreads();
     }
 }

@@ -60,6 +60,43 @@ constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size
                            (size_t)(V4_MAXH + 4) * 4 + (size_t)V4_WARPS * V4_Q * 32 * 2 + (size_t)V4_MAXZ * 16;
 
 
+// Results of one particle in slot (cell) order: rho, wcount, rho_dh, wcount_dh, div_v,
+// curl_v (3), nngb (int bits), padding.  48 bytes = two 32-byte sectors, so the final
+// input-order gather (k_unpermute) reads two sectors per particle instead of the nine
+// read-modify-write sectors of scattered 4-byte stores.
+struct alignas(16) OutRec {
+    float4 a, b, c;
+};
+
+__device__ __forceinline__ void store_rec(OutRec *orec, int slot, float rho, float wc, float rho_dh, float wc_dh,
+                                          float div, float cx, float cy, float cz, int nngb)
+{
+    float4 *q = reinterpret_cast<float4 *>(orec + slot);
+    q[0] = make_float4(rho, wc, rho_dh, wc_dh);
+    q[1] = make_float4(div, cx, cy, cz);
+    q[2] = make_float4(__int_as_float(nngb), 0.0f, 0.0f, 0.0f);
+}
+
+// out[p] = record of slot_of[p] for the first n_out input indices (coalesced writes,
+// one 48-byte gather per particle).
+__global__ void k_unpermute(DevOut o, const int *__restrict__ slot_of, const OutRec *__restrict__ orec)
+{
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < o.n_out;
+         p += (long long)gridDim.x * blockDim.x) {
+        const float4 *q = reinterpret_cast<const float4 *>(orec + slot_of[p]);
+        const float4 a = q[0], b = q[1], c = q[2];
+        o.rho[p] = a.x;
+        o.wcount[p] = a.y;
+        o.rho_dh[p] = a.z;
+        o.wcount_dh[p] = a.w;
+        o.div_v[p] = b.x;
+        o.curl_v[p] = b.y;
+        o.curl_v[o.n_out + p] = b.z;
+        o.curl_v[2 * o.n_out + p] = b.w;
+        o.nngb[p] = __float_as_int(c.x);
+    }
+}
+
 // ---- tile list ------------------------------------------------------------------
 struct RowPairs {
     int nxo, nyp, nby;
@@ -249,7 +286,7 @@ __device__ __forceinline__ int block_exscan(int v, int *wsum, int &total)
 
 // Reference per-particle sweep (global memory) for tiles that are not staged.
 template <bool COUNT>
-__device__ __forceinline__ void v4_particle_global(const DevGrid &g, const DevCells &c, const DevOut &o, int i,
+__device__ __forceinline__ void v4_particle_global(const DevGrid &g, const DevCells &c, OutRec *orec, int i,
                                                    unsigned cand[4], unsigned hits[4])
 {
     const int home = c.slot_cell[i];
@@ -268,19 +305,8 @@ __device__ __forceinline__ void v4_particle_global(const DevGrid &g, const DevCe
                 sweep_pair<COUNT>(g, c, p, cj, ox, oy, oz, sh, a, cand[k], hits[k]);
             }
     Final f = finalise(g, p, a, true);
-    const int out = c.perm[i];
-    if (out < o.n_out) {
-        const float rinv = 1.0f / f.rho;
-        o.rho[out] = f.rho;
-        o.wcount[out] = f.wc;
-        o.rho_dh[out] = f.rho_dh;
-        o.wcount_dh[out] = f.wc_dh;
-        o.div_v[out] = f.div * rinv;
-        o.curl_v[out] = f.cx * rinv;
-        o.curl_v[o.n_out + out] = f.cy * rinv;
-        o.curl_v[2 * o.n_out + out] = f.cz * rinv;
-        o.nngb[out] = a.nngb;
-    }
+    const float rinv = 1.0f / f.rho;
+    store_rec(orec, i, f.rho, f.wc, f.rho_dh, f.wc_dh, f.div * rinv, f.cx * rinv, f.cy * rinv, f.cz * rinv, a.nngb);
 }
 
 // Packed accumulators; D and curl use v_j - v_i (= -v_ij) so the cross products
@@ -358,24 +384,52 @@ struct V4Stage {
 // f1 with sep = (h1 - x_j) . d.  Branch-free bisection with `top` = the largest
 // power of two <= the warp's longest segment, so every lane runs the same steps:
 // the exact per-particle bound of P:151-165; the two searches are interleaved.
-__device__ __forceinline__ void v4_windows(const V4Stage &S, int top, int f0, int n0, int f1, int n1, float c0,
-                                           float c1, float c2, float h0x, float h0y, float h0z, float h1x,
-                                           float h1y, float h1z, float Hk, int &len0, int &len1)
+template <int D>
+__device__ __forceinline__ float v4_dot(float dx, float dy, float dz)
+{
+    // d . (dx, dy, dz) with the canonical direction's components (+1, -1 or 0) folded in
+    constexpr int a0 = D == 0 ? 0 : (D <= 3 ? 0 : 1);
+    constexpr int a1 = D == 0 ? 0 : (D <= 3 ? 1 : (D - 4) / 3 - 1);
+    constexpr int a2 = D == 0 ? 1 : (D <= 3 ? D - 2 : (D - 4) % 3 - 1);
+    float s = 0.0f;
+    bool any = false;
+    if (a0 != 0) { s = a0 > 0 ? dx : -dx; any = true; }
+    if (a1 != 0) { s = any ? (a1 > 0 ? s + dy : s - dy) : (a1 > 0 ? dy : -dy); any = true; }
+    if (a2 != 0) { s = any ? (a2 > 0 ? s + dz : s - dz) : (a2 > 0 ? dz : -dz); }
+    return s;
+}
+
+template <int D>
+__device__ __forceinline__ void v4_windows_d(const V4Stage &S, int top, int f0, int n0, int f1, int n1, float h0x,
+                                             float h0y, float h0z, float h1x, float h1y, float h1z, float Hk,
+                                             int &len0, int &len1)
 {
     int lo0 = 0, lo1 = 0;
     for (int st = top; st > 0; st >>= 1) {
         const int k0 = lo0 + st, k1 = lo1 + st;           // is entry k - 1 inside the window?
         const bool v0 = k0 <= n0, v1 = k1 <= n1;
-        const unsigned i0 = v0 ? lds_u16(S.L + 2u * (unsigned)(f0 - k0 + 1)) : 0u;
-        const unsigned i1 = v1 ? lds_u16(S.L + 2u * (unsigned)(f1 + k1 - 1)) : 0u;
-        const float4 p0 = lds_f4(S.P + 16u * i0), p1 = lds_f4(S.P + 16u * i1);
-        const float s0 = fmaf(c0, p0.x - h0x, fmaf(c1, p0.y - h0y, c2 * (p0.z - h0z)));
-        const float s1 = fmaf(c0, h1x - p1.x, fmaf(c1, h1y - p1.y, c2 * (h1z - p1.z)));
+        const unsigned i0 = v0 ? ldsr_u16(S.L + 2u * (unsigned)(f0 - k0 + 1)) : 0u;
+        const unsigned i1 = v1 ? ldsr_u16(S.L + 2u * (unsigned)(f1 + k1 - 1)) : 0u;
+        const float4 p0 = ldsr_f4(S.P + 16u * i0), p1 = ldsr_f4(S.P + 16u * i1);
+        const float s0 = v4_dot<D>(p0.x - h0x, p0.y - h0y, p0.z - h0z);
+        const float s1 = v4_dot<D>(h1x - p1.x, h1y - p1.y, h1z - p1.z);
         if (v0 && s0 < Hk) lo0 = k0;
         if (v1 && s1 < Hk) lo1 = k1;
     }
     len0 = lo0;
     len1 = lo1;
+}
+
+__device__ __forceinline__ void v4_windows(const V4Stage &S, int d, int top, int f0, int n0, int f1, int n1,
+                                           float h0x, float h0y, float h0z, float h1x, float h1y, float h1z, float Hk,
+                                           int &len0, int &len1)
+{
+#define V4W(D) case D: v4_windows_d<D>(S, top, f0, n0, f1, n1, h0x, h0y, h0z, h1x, h1y, h1z, Hk, len0, len1); break;
+    switch (d) {
+        V4W(0) V4W(1) V4W(2) V4W(3) V4W(4) V4W(5) V4W(6) V4W(7) V4W(8) V4W(9) V4W(10) V4W(11) V4W(12)
+    default: len0 = len1 = 0;
+    }
+#undef V4W
 }
 
 // One lane = one home particle of a staged tile.  lpos: first list entry of its home
@@ -385,10 +439,13 @@ __device__ __forceinline__ void v4_windows(const V4Stage &S, int top, int f0, in
 // lane l at qbase + 64 k + 2 l: conflict-free); every particle sums its hits in a
 // fixed order, so the result does not depend on the tile or the warp.
 template <bool COUNT, bool FRAMES>
-__device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCells &c, const DevOut &o,
+__device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCells &c, OutRec *orec,
                                                    const V4Stage &S, unsigned qbase, bool active, int i, int yoff,
                                                    int qh, int lpos, unsigned cand[4], unsigned hits[4])
 {
+#ifdef PVSPH_STAGE_ONLY
+    return;
+#endif
     const unsigned sQ = qbase + 2u * (threadIdx.x & 31);
     float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
     if (active) {
@@ -434,8 +491,8 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
                 home_of(e0 >> 12, hx0, hy0, hz0);
                 home_of(e1 >> 12, hx1, hy1, hz1);
             }
-            const float4 p0 = lds_f4(S.P + 16u * s0), p1 = lds_f4(S.P + 16u * s1);
-            const float4 v0 = lds_f4(S.V + 16u * s0), v1 = lds_f4(S.V + 16u * s1);
+            const float4 p0 = ldsr_f4(S.P + 16u * s0), p1 = ldsr_f4(S.P + 16u * s1);
+            const float4 v0 = ldsr_f4(S.V + 16u * s0), v1 = ldsr_f4(S.V + 16u * s1);
             const f2 mk = pk(1.0f, two ? 1.0f : 0.0f);
             interact_pair<FINAL>(Hinv2, pk(hx0 - p0.x, hx1 - p1.x), pk(hy0 - p0.y, hy1 - p1.y),
                                  pk(hz0 - p0.z, hz1 - p1.z), pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx),
@@ -464,12 +521,12 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
             if (SELF) {
                 sj[u] = (unsigned)(base + (ok[u] ? t + u : 0));
             } else {
-                const unsigned e = lds_u16(lb + 2u * (unsigned)(t + u));   // in the segment or just past it
+                const unsigned e = ldsr_u16(lb + 2u * (unsigned)(t + u));   // in the segment or just past it
                 sj[u] = ok[u] ? e : 0u;
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) p[u] = lds_f4(S.P + 16u * sj[u]);
+        for (int u = 0; u < 4; ++u) p[u] = ldsr_f4(S.P + 16u * sj[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             float hx = x, hy = y, hz = z;
@@ -526,8 +583,7 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
                 home_of(fl1, mx, my, mz);
             }
             int len1;
-            v4_windows(S, top, mid - 1, ep.y, mid, em.y, (float)a0, (float)a1, (float)a2, px, py, pz, mx, my, mz,
-                       Hk, len0, len1);
+            v4_windows(S, d, top, mid - 1, ep.y, mid, em.y, px, py, pz, mx, my, mz, Hk, len0, len1);
             wb = mid - len0;
             total = len0 + len1;
         }
@@ -551,24 +607,54 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
         const float wc_dh = dh * (1.5f + sum2(A.st));
         const float gf = K3 * Hinv;
         const float rinv = 1.0f / rho;
-        const int out = c.perm[i];
-        if (out < o.n_out) {
-            o.rho[out] = rho;
-            o.wcount[out] = wc;
-            o.rho_dh[out] = rho_dh;
-            o.wcount_dh[out] = wc_dh;
-            o.div_v[out] = gf * sum2(A.Dn) * rinv;
-            o.curl_v[out] = gf * (sum2(A.Px) - sum2(A.Nx)) * rinv;
-            o.curl_v[o.n_out + out] = gf * (sum2(A.Py) - sum2(A.Ny)) * rinv;
-            o.curl_v[2 * o.n_out + out] = gf * (sum2(A.Pz) - sum2(A.Nz)) * rinv;
-            o.nngb[out] = nngb;
-        }
+        store_rec(orec, i, rho, wc, rho_dh, wc_dh, gf * sum2(A.Dn) * rinv, gf * (sum2(A.Px) - sum2(A.Nx)) * rinv,
+                  gf * (sum2(A.Py) - sum2(A.Ny)) * rinv, gf * (sum2(A.Pz) - sum2(A.Nz)) * rinv, nngb);
     }
 }
 
-// Persistent CTAs take tiles in order from an atomic counter.
+// Staged cell s of a tile (s = row * nzs + col; row = (ox + 1) * 4 + (oy + 1) relative to
+// the tile's first row, col = uz - z_a + 1): local cell id and periodic flags (bits 0-2
+// home shift for a +L image, bits 3-5 pre-shift of a -L image).
+struct TileGeom {
+    int xo, y0, za, zb, first, cnt, nzs, nzh, nh;
+    bool hasB, staged, frames;
+};
+
+__device__ __forceinline__ TileGeom tile_geom(const DevGrid &g, const RowPairs &rp, int4 td)
+{
+    TileGeom t;
+    int yp;
+    key_rowpair(rp, td.x, t.xo, yp);
+    t.y0 = 2 * yp;
+    t.hasB = t.y0 + 1 < g.ny;
+    t.za = td.y & 0xffff;
+    t.zb = td.y >> 16;
+    t.first = td.z;
+    t.cnt = td.w;
+    t.nzs = t.zb - t.za + 3;
+    t.nzh = t.zb - t.za + 1;
+    t.nh = (t.hasB ? 2 : 1) * t.nzh;
+    t.staged = t.cnt > 0 && t.nzs <= V4_MAXZ;
+    // a staged neighbour beyond a high face (home shift needed): x plane, y row or z column
+    t.frames = g.x_lo + t.xo + 1 >= g.nc[0] || t.y0 + 2 >= g.ny || t.zb + 1 >= g.nz;
+    return t;
+}
+
+__device__ __forceinline__ long long staged_cell(const DevGrid &g, const TileGeom &t, int s, unsigned &fl)
+{
+    const int r = s / t.nzs, q = s % t.nzs;
+    const StagedRow sr = staged_row(g, t.xo, t.y0, r);
+    const int uz = t.za - 1 + q;
+    fl = (sr.gx >= g.nc[0] ? 1u : 0u) | (sr.uy >= g.ny ? 2u : 0u) | (uz >= g.nz ? 4u : 0u) | (sr.gx < 0 ? 8u : 0u) |
+         (sr.uy < 0 ? 16u : 0u) | (uz < 0 ? 32u : 0u);
+    return sr.base + wrap_i(uz, g.nz);
+}
+
+// Persistent CTAs take tiles in order from an atomic counter.  The next tile's
+// descriptor and the cell counts of its staged neighbourhood are fetched while the
+// current tile computes, so staging starts without a global-memory round trip.
 template <bool COUNT>
-__global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCells c, DevOut o, sph_stats *st,
+__global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCells c, OutRec *orec, sph_stats *st,
                                                          const int4 *__restrict__ tiles,
                                                          const int *__restrict__ ntiles_p, int *tile_counter)
 {
@@ -580,121 +666,125 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     int *hoff = reinterpret_cast<int *>(L + V4_ML);
     uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_MAXH + 4);
     int4 *seq = reinterpret_cast<int4 *>(queue + V4_WARPS * V4_Q * 32);
-    __shared__ int s_tile, s_wsum[V4_WARPS];
+    __shared__ int4 s_next;
+    __shared__ int s_wsum[V4_WARPS];
+    static_assert(V4_MAXCELLS <= 2 * V4_TP, "two table entries per thread");
 
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const RowPairs rp = row_pairs(g);
     const int ntiles = *ntiles_p;
     unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    const int4 kEnd = make_int4(-1, 0, 0, 0);
 
-    for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1);
-        __syncthreads();
-        const int t = s_tile;
-        if (t >= ntiles) break;
-        const int4 td = tiles[t];
-        int xo, yp;
-        key_rowpair(rp, td.x, xo, yp);
-        const int y0 = 2 * yp;
-        const bool hasB = y0 + 1 < g.ny;
-        const int za = td.y & 0xffff, zb = td.y >> 16, first = td.z, cnt = td.w;
-        const long long rowA = ((long long)(xo + g.ghost_x) * g.ny + y0) * g.nz;
-        const int nzs = zb - za + 3, nzh = zb - za + 1, nh = (hasB ? 2 : 1) * nzh;
-        bool staged = cnt > 0 && nzs <= V4_MAXZ;
-        // a staged neighbour beyond a high face (home shift needed): x plane, y row or z column
-        const bool frames = g.x_lo + xo + 1 >= g.nc[0] || y0 + 2 >= g.ny || zb + 1 >= g.nz;
-        // home slices: {A start, A count, B start, first sequence index}
-        if ((int)threadIdx.x < nzh) {
-            const long long ca = rowA + za + threadIdx.x;
-            const int a0 = c.cell_start[ca], a1 = c.cell_start[ca + 1];
-            const int b0 = hasB ? c.cell_start[ca + g.nz] : 0, b1 = hasB ? c.cell_start[ca + g.nz + 1] : 0;
-            seq[threadIdx.x] = make_int4(a0, a1 - a0, b0, (a1 - a0) + (b1 - b0));
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int acc = 0;
-            for (int k = 0; k < nzh; ++k) {
-                const int n = seq[k].w;
-                seq[k].w = acc;
-                acc += n;
+    // prefetch of a tile's staged-cell counts: thread owns table entries 2 tid, 2 tid + 1
+    int pf_start[2] = {0, 0}, pf_end[2] = {0, 0};
+    auto prefetch = [&](int4 td) {
+        if (td.x < 0) return;
+        const TileGeom t = tile_geom(g, rp, td);
+        if (!t.staged) return;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int s = 2 * threadIdx.x + k;
+            if (s < V4_ROWS * t.nzs) {
+                unsigned fl;
+                const long long cell = staged_cell(g, t, s, fl);
+                pf_start[k] = c.cell_start[cell];
+                pf_end[k] = c.cell_start[cell + 1];
             }
         }
-        __syncthreads();
-        // home particle of thread h: sequence index first + h from slice za on
-        auto home_slot = [&](int h, int &slot, int &yo, int &tz) {
-            const int q = first + h;
-            int lo = 0, hi = nzh - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (seq[mid].w <= q) lo = mid; else hi = mid - 1;
-            }
-            const int4 e = seq[lo];
-            const int loc = q - e.w;
-            yo = loc < e.y ? 0 : 1;
-            slot = yo == 0 ? e.x + loc : e.z + (loc - e.y);
-            tz = lo;
-        };
+    };
+    if (threadIdx.x == 0) {
+        const int t0 = atomicAdd(tile_counter, 1);
+        s_next = t0 < ntiles ? tiles[t0] : kEnd;
+    }
+    __syncthreads();
+    int4 td = s_next;
+    prefetch(td);
 
+    while (td.x >= 0) {
+        __syncthreads();                                  // s_next consumed by every thread
+        if (threadIdx.x == 0) {                           // claim the next tile early
+            const int t1 = atomicAdd(tile_counter, 1);
+            s_next = t1 < ntiles ? tiles[t1] : kEnd;
+        }
+        const TileGeom T = tile_geom(g, rp, td);
+        bool staged = T.staged;
         if (staged) {
-            // staged cell table: s = row * nzs + col, row = (ox + 1) * 4 + (oy + 1), col = uz - za + 1
-            static_assert(V4_MAXCELLS <= 2 * V4_TP, "two table entries per thread");
-            const int ncs = V4_ROWS * nzs;
-            int cnt[2] = {0, 0};
+            // staged cell table from the prefetched counts
+            const int ncs = V4_ROWS * T.nzs;
+            int cnt2[2] = {0, 0};
             int4 ent[2];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
                 const int s = 2 * threadIdx.x + k;
                 ent[k] = make_int4(0, 0, 0, 0);
                 if (s < ncs) {
-                    const int r = s / nzs, q = s % nzs;
-                    const StagedRow sr = staged_row(g, xo, y0, r);
-                    const int uz = za - 1 + q;
-                    const long long cell = sr.base + wrap_i(uz, g.nz);
-                    const int gs = c.cell_start[cell];
-                    cnt[k] = c.cell_start[cell + 1] - gs;
-                    const unsigned fl = (sr.gx >= g.nc[0] ? 1u : 0u) | (sr.uy >= g.ny ? 2u : 0u) |
-                                        (uz >= g.nz ? 4u : 0u) | (sr.gx < 0 ? 8u : 0u) | (sr.uy < 0 ? 16u : 0u) |
-                                        (uz < 0 ? 32u : 0u);
-                    ent[k] = make_int4(0, cnt[k], gs, (int)fl);
+                    unsigned fl;
+                    staged_cell(g, T, s, fl);
+                    cnt2[k] = pf_end[k] - pf_start[k];
+                    ent[k] = make_int4(0, cnt2[k], pf_start[k], (int)fl);
                 }
             }
             int total;
-            const int pre = block_exscan(cnt[0] + cnt[1], s_wsum, total);
+            const int pre = block_exscan(cnt2[0] + cnt2[1], s_wsum, total);
             if (2 * threadIdx.x < ncs) {
                 ent[0].x = pre;
                 tab[2 * threadIdx.x] = ent[0];
             }
             if (2 * threadIdx.x + 1 < ncs) {
-                ent[1].x = pre + cnt[0];
+                ent[1].x = pre + cnt2[0];
                 tab[2 * threadIdx.x + 1] = ent[1];
             }
             __syncthreads();
-            // list segments of each home cell: self + 13 x (+d, -d) = the 27 cells around it
+            // list sizes of the home cells (27 neighbours each) and the home slices
             int lsz = 0;
-            if ((int)threadIdx.x < nh) {
-                const int r = threadIdx.x / nzh, q = threadIdx.x % nzh + 1;
+            if ((int)threadIdx.x < T.nh) {
+                const int r = threadIdx.x / T.nzh, q = threadIdx.x % T.nzh + 1;
+#pragma unroll
                 for (int ox = -1; ox <= 1; ++ox)
+#pragma unroll
                     for (int oy = -1; oy <= 1; ++oy)
-                        for (int oz = -1; oz <= 1; ++oz) lsz += tab[((ox + 1) * 4 + oy + r + 1) * nzs + q + oz].y;
+#pragma unroll
+                        for (int oz = -1; oz <= 1; ++oz) lsz += tab[((ox + 1) * 4 + oy + r + 1) * T.nzs + q + oz].y;
+            }
+            if (wl == V4_WARPS - 1) {
+                // slice k: {A start, A count, B start, first sequence index}, k < nzh <= 30
+                int4 sl = make_int4(0, 0, 0, 0);
+                int ns = 0;
+                if (lane < T.nzh) {
+                    const int4 ea = tab[5 * T.nzs + lane + 1];
+                    const int4 eb = tab[6 * T.nzs + lane + 1];
+                    sl = make_int4(ea.z, ea.y, eb.z, 0);
+                    ns = ea.y + (T.hasB ? eb.y : 0);
+                }
+                int x = ns;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o2);
+                    if (lane >= o2) x += y;
+                }
+                sl.w = x - ns;
+                if (lane < T.nzh) seq[lane] = sl;
             }
             int ltotal;
             const int lpre = block_exscan(lsz, s_wsum, ltotal);
-            if ((int)threadIdx.x < nh) hoff[threadIdx.x] = lpre;
-            if (total > V4_MS || ltotal > V4_ML || nh > V4_MAXH) staged = false;   // CTA-uniform
+            if ((int)threadIdx.x < T.nh) hoff[threadIdx.x] = lpre;
+            if (total > V4_MS || ltotal > V4_ML || T.nh > V4_MAXH) staged = false;   // CTA-uniform
             __syncthreads();
             if (staged) {
                 // positions and (v, m): each staged row is one contiguous slot range, split where z wraps
                 for (int r = wl; r < V4_ROWS; r += V4_WARPS) {
-                    const int4 e0 = tab[r * nzs];
+                    const int4 e0 = tab[r * T.nzs];
                     const float sx = (e0.w & 8) ? g.boxf[0] : 0.0f;
                     const float sy = (e0.w & 16) ? g.boxf[1] : 0.0f;
                     for (int piece = 0; piece < 3; ++piece) {
                         // piece 0: column 0 if it wraps (uz = -1); 1: the in-box columns; 2: last column if uz = nz
-                        const int q0 = piece == 0 ? 0 : (piece == 1 ? (za == 0 ? 1 : 0) : nzs - 1);
-                        const int q1 = piece == 0 ? (za == 0 ? 1 : 0) : (piece == 1 ? (zb + 1 >= g.nz ? nzs - 1 : nzs) : (zb + 1 >= g.nz ? nzs : nzs - 1));
+                        const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
+                        const int q0 = piece == 0 ? 0 : (piece == 1 ? (wlo ? 1 : 0) : T.nzs - 1);
+                        const int q1 = piece == 0 ? (wlo ? 1 : 0) : (piece == 1 ? (whi ? T.nzs - 1 : T.nzs) : (whi ? T.nzs : T.nzs - 1));
                         if (q1 <= q0) continue;
-                        const int4 ea = tab[r * nzs + q0];
-                        const int4 eb = tab[r * nzs + q1 - 1];
+                        const int4 ea = tab[r * T.nzs + q0];
+                        const int4 eb = tab[r * T.nzs + q1 - 1];
                         const float sz = (ea.w & 32) ? g.boxf[2] : 0.0f;
                         const int n = eb.x + eb.y - ea.x;
                         const float4 *gx = c.xyzh + ea.z;
@@ -708,10 +798,10 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                         }
                     }
                 }
-                // lists: lane k of the warp of home cell h copies segment k (self, then +d / -d
-                // reversed for d = 0..12), at its offset from a warp scan of the segment sizes
-                for (int h = wl; h < nh; h += V4_WARPS) {
-                    const int r = h / nzh, q = h % nzh + 1;
+                // lists: warp per home cell; segment k (self, then +d / -d reversed for d = 0..12)
+                // at its offset from a warp scan; lanes copy an element each, 9 segments in flight
+                for (int h = wl; h < T.nh; h += V4_WARPS) {
+                    const int r = h / T.nzh, q = h % T.nzh + 1;
                     int o0 = 0, o1 = 0, o2 = 0, d = 0;
                     if (lane >= 1 && lane < 27) {
                         d = (lane - 1) >> 1;
@@ -720,54 +810,94 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                         o1 = sg * dir_component(d, 1);
                         o2 = sg * dir_component(d, 2);
                     }
-                    const int4 e = lane < 27 ? tab[((o0 + 1) * 4 + o1 + r + 1) * nzs + q + o2] : make_int4(0, 0, 0, 0);
+                    const int4 e = lane < 27 ? tab[((o0 + 1) * 4 + o1 + r + 1) * T.nzs + q + o2] : make_int4(0, 0, 0, 0);
                     int x = e.y;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {
                         const int y = __shfl_up_sync(0xffffffffu, x, o);
                         if (lane >= o) x += y;
                     }
-                    const int dst = hoff[h] + x - e.y;
-                    const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
-                    if (lane == 0) {
-                        for (int k = 0; k < e.y; ++k) L[dst + k] = (uint16_t)(e.x + k);
-                    } else {
-#pragma unroll 4
-                        for (int k = 0; k < e.y; ++k) L[dst + e.y - 1 - k] = (uint16_t)(e.x + (int)src[k]);
+                    const int dst = hoff[h] + x - e.y;                 // segment's first list entry
+#ifndef PVSPH_NO_LISTS
+                    if (lane < 27) {
+                        if (lane == 0) {
+                            for (int k = 0; k < e.y; ++k) L[dst + k] = (uint16_t)(e.x + k);
+                        } else {
+                            // reversed; 16 independent loads in flight per lane
+                            const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
+                            for (int k0 = 0; k0 < e.y; k0 += 16) {
+                                unsigned v[16];
+#pragma unroll
+                                for (int u = 0; u < 16; ++u) v[u] = k0 + u < e.y ? (unsigned)src[k0 + u] : 0u;
+#pragma unroll
+                                for (int u = 0; u < 16; ++u)
+                                    if (k0 + u < e.y) L[dst + e.y - 1 - (k0 + u)] = (uint16_t)(e.x + (int)v[u]);
+                            }
+                        }
                     }
+#endif
                 }
                 __syncthreads();
             }
         }
+        // the next tile: descriptor published by thread 0 (visible after the barrier above, or
+        // the one below for unstaged tiles); its counts are fetched while this tile computes
+        __syncthreads();
+        const int4 td_next = s_next;
+        prefetch(td_next);
 
+        // home particle of thread h: sequence index first + h from slice za on
+        auto home_slot = [&](int h, int &slot, int &yo, int &tz) {
+            const int qq = T.first + h;
+            int lo = 0, hi = T.nzh - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (seq[mid].w <= qq) lo = mid; else hi = mid - 1;
+            }
+            const int4 e = seq[lo];
+            const int loc = qq - e.w;
+            yo = loc < e.y ? 0 : 1;
+            slot = yo == 0 ? e.x + loc : e.z + (loc - e.y);
+            tz = lo;
+        };
         if (staged) {
             const int h = threadIdx.x;
-            const bool active = h < cnt;
+            const bool active = h < T.cnt;
             int i = 0, yoff = 0, tz = 0, lpos = 0;
             if (active) {
                 home_slot(h, i, yoff, tz);
-                lpos = hoff[yoff * nzh + tz];
+                lpos = hoff[yoff * T.nzh + tz];
             } else {
                 i = seq[0].x;
             }
-            const V4Stage S{smem_addr(P), smem_addr(V), smem_addr(L), tab, nzs};
+            const V4Stage S{smem_addr(P), smem_addr(V), smem_addr(L), tab, T.nzs};
             const unsigned qb = smem_addr(queue + wl * V4_Q * 32);
-            if (wl * 32 < cnt) {
-                if (frames)
-                    v4_particle_staged<COUNT, true>(g, c, o, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
+            if (wl * 32 < T.cnt) {
+                if (T.frames)
+                    v4_particle_staged<COUNT, true>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
                 else
-                    v4_particle_staged<COUNT, false>(g, c, o, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
+                    v4_particle_staged<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
             }
         } else {
             // global-memory sweep: a slice that cannot be staged, or a tile whose check failed
-            const int ntot = cnt > 0 ? cnt : -cnt;
+            const long long rowA = ((long long)(T.xo + g.ghost_x) * g.ny + T.y0) * g.nz;
+            const int ntot = T.cnt > 0 ? T.cnt : -T.cnt;
             for (int h = threadIdx.x; h < ntot; h += V4_TP) {
-                int i, yo, tz;
-                home_slot(h, i, yo, tz);
-                v4_particle_global<COUNT>(g, c, o, i, cand, hits);
+                // slices from z_a on: row-A cell then row-B cell
+                int qq = T.first + h, z = T.za, slot = 0;
+                for (;; ++z) {
+                    const long long ca = rowA + z;
+                    const int a0 = c.cell_start[ca], na = c.cell_start[ca + 1] - a0;
+                    const int b0 = T.hasB ? c.cell_start[ca + g.nz] : 0;
+                    const int nb = T.hasB ? c.cell_start[ca + g.nz + 1] - b0 : 0;
+                    if (qq < na) { slot = a0 + qq; break; }
+                    if (qq < na + nb) { slot = b0 + (qq - na); break; }
+                    qq -= na + nb;
+                }
+                v4_particle_global<COUNT>(g, c, orec, slot, cand, hits);
             }
         }
-        __syncthreads();
+        td = td_next;
     }
     flush_stats<COUNT>(st, cand, hits);
 }

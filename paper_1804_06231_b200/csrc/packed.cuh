@@ -51,6 +51,21 @@ __device__ __forceinline__ unsigned lds_u16(unsigned a)
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
     return v;
 }
+// Loads of shared data that is read-only while the warp computes (no volatile: the
+// compiler may schedule them early; their addresses derive from values loaded after
+// the staging barrier, which anchors them after it).
+__device__ __forceinline__ float4 ldsr_f4(unsigned a)
+{
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned ldsr_u16(unsigned a)
+{
+    unsigned short v;
+    asm("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ unsigned lds_u32(unsigned a)
 {
     unsigned v;

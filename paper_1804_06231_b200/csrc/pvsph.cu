@@ -76,7 +76,7 @@ int make_grid(const sph_grid *gr, DevGrid &g)
 
 bool cells_ok(const sph_cells *c)
 {
-    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell &&
+    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell && c->slot_of &&
            c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
            ((uintptr_t)c->order % 2 == 0);
@@ -93,6 +93,7 @@ DevCells dev_cells(const sph_cells *c)
     d.cell_hmax = c->cell_hmax;
     d.ord = c->order;
     d.slot_cell = c->slot_cell;
+    d.slot_of = c->slot_of;
     return d;
 }
 
@@ -120,7 +121,7 @@ DevOut dev_out(const sph_out *o)
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
-    size_t status, cell_of, rank, perm_tmp, rec, count, tile_sum, big_count, big_items, rows, rows_sum, tiles,
+    size_t status, cell_of, rank, perm_tmp, rec, orec, count, tile_sum, big_count, big_items, rows, rows_sum, tiles,
         counter, total;
     long long tile_cap;
 };
@@ -140,6 +141,8 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
     w.rec = o;
     o = align_up(o + 32 * (size_t)(n > 0 ? n : 1), 256);
+    w.orec = o;
+    o = align_up(o + sizeof(OutRec) * (size_t)(n > 0 ? n : 1), 256);
     w.count = o;
     o = align_up(o + 4 * (size_t)(ncell + 1), 256);
     long long ntiles = (ncell + SCAN_TILE - 1) / SCAN_TILE;
@@ -246,9 +249,10 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
                                                                     rec, perm_tmp);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, cells->slot_cell, big_items, big_count);
+            g.ncell, cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, cells->slot_cell, cells->slot_of, big_items,
+            big_count);
         k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, rec, xs, vs, cells->perm,
-                                                          big_items, big_count);
+                                                          cells->slot_of, big_items, big_count);
     }
     cells->n = n;
     return check_launch();
@@ -376,11 +380,13 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
     const int blocks = sms * blocks_per_sm;
+    OutRec *orec = at<OutRec>(ws, w.orec);
     if (stats)
-        k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, dev_out(out), stats, tiles, rows + nkeys, counter);
+        k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter);
     else
-        k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, dev_out(out), nullptr, tiles, rows + nkeys,
-                                                           counter);
+        k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter);
+    if (out->n_out > 0)
+        k_unpermute<<<grid_blocks(out->n_out, 256, 148 * 16), 256, 0, s>>>(dev_out(out), dc.slot_of, orec);
     return check_launch();
 }
 

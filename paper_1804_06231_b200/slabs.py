@@ -29,9 +29,9 @@ import torch
 
 from . import api as pv
 
-BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_perm, k_stable_small/big, k_gather
+BUILD_LAUNCHES = 7      # k_bin, 3 scan kernels, k_scatter_rec, k_stable_small/big
 SORT_LAUNCHES = 2       # k_sort_small, k_sort_big
-DENSITY_LAUNCHES = 5    # k_row_chunks, 3 scan kernels, k_density_all
+DENSITY_LAUNCHES = 7    # k_v4_tiles (count), 3 scan kernels, k_v4_tiles (write), k_density_v4, k_unpermute
 
 
 def slab_bounds(nc: int, world: int, rank: int) -> tuple[int, int]:
