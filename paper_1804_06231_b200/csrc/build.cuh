@@ -22,7 +22,8 @@ namespace pvsph {
 
 __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float4 *__restrict__ xyzh_in,
                       const float4 *__restrict__ vm_in, int *__restrict__ cell_of, int *__restrict__ rank,
-                      int *__restrict__ count, float *__restrict__ cell_hmax, unsigned *status)
+                      int *__restrict__ count, float *__restrict__ cell_hmax, int *__restrict__ slot_of,
+                      unsigned *status)
 {
     double clmin = fmin(g.cl[0], fmin(g.cl[1], g.cl[2]));
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
@@ -63,6 +64,7 @@ __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float
             }
         }
         cell_of[p] = cell;
+        if (cell < 0) slot_of[p] = -1;   // rejected input: no slot (k_unpermute leaves its outputs alone)
     }
 }
 

@@ -83,7 +83,9 @@ __global__ void k_unpermute(DevOut o, const int *__restrict__ slot_of, const Out
 {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < o.n_out;
          p += (long long)gridDim.x * blockDim.x) {
-        const float4 *q = reinterpret_cast<const float4 *>(orec + slot_of[p]);
+        const int sl = slot_of[p];
+        if (sl < 0) continue;                    // input rejected by sph_build_cells (status word set)
+        const float4 *q = reinterpret_cast<const float4 *>(orec + sl);
         const float4 a = q[0], b = q[1], c = q[2];
         o.rho[p] = a.x;
         o.wcount[p] = a.y;

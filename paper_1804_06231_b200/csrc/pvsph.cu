@@ -233,7 +233,7 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     const float4 *vin = reinterpret_cast<const float4 *>(vm_in);
     if (n > 0) {
         k_bin<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n_own, n, xin, vin, cell_of, rank, count,
-                                                            cells->cell_hmax, status);
+                                                            cells->cell_hmax, cells->slot_of, status);
     }
     long long ntiles = (g.ncell + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(count, g.ncell, cells->cell_start, tile_sum, status);
