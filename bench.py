@@ -110,34 +110,36 @@ def _profile_traffic():
 # CPU baseline: the oracle's cell list on a bounded sample
 # ---------------------------------------------------------------------------
 def _oracle_rate(p, seconds: float, rng):
-    """Time oracle_celllist on two random target samples of p; the difference removes the
-    one-off binning of all N particles, which a full run amortises over N targets.
-    Returns (interactions/s for a full run, n_targets, description)."""
+    """Time oracle_celllist on two bounded random target samples of p.  Each call bins all
+    N particles once (a fixed cost) and then evaluates its targets; the difference of the
+    two calls gives the per-target cost, the rest is the binning.  The rate is that of a
+    full pass (binning once + all N targets).  Returns (interactions/s, n_targets, text)."""
     import oracle
-    n1 = 1000
-    t1 = rng.choice(p.n, n1, replace=False)
+    if p.n <= 1_000_000:                       # small sets: one full pass
+        t0 = time.perf_counter()
+        r = oracle.celllist(p.xyzh, p.vm, p.nc)
+        dt = time.perf_counter() - t0
+        return (float(r["nngb"].sum()) / dt, p.n,
+                f"oracle_celllist (fp64, OpenMP), one full pass over {p.name} (N={p.n}): {dt:.2f} s")
+    n_a = 50_000
+    ta = np.sort(rng.choice(p.n, n_a, replace=False))
     t0 = time.perf_counter()
-    r1 = oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(t1))
-    d1 = time.perf_counter() - t0
-    # second sample sized for ~`seconds` of target work (probe slope from a 2x sample)
-    t2 = rng.choice(p.n, 2 * n1, replace=False)
+    oracle.celllist(p.xyzh, p.vm, p.nc, targets=ta)
+    d_a = time.perf_counter() - t0
+    # second sample: about `seconds` of target work, from a rough per-target estimate, capped
+    rough = max(d_a / n_a, 2e-7) if p.n <= 4 * n_a else 2e-6
+    n_b = int(min(p.n, max(4 * n_a, seconds / rough)))
+    tb = np.sort(rng.choice(p.n, n_b, replace=False))
     t0 = time.perf_counter()
-    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(t2))
-    d2 = time.perf_counter() - t0
-    slope = max((d2 - d1) / n1, 1e-9)
-    n_s = int(min(p.n, max(4 * n1, seconds / slope)))
-    ts = rng.choice(p.n, n_s, replace=False)
-    t0 = time.perf_counter()
-    rs = oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(ts))
-    ds = time.perf_counter() - t0
-    per_target = (ds - d1) / (n_s - n1)
-    t_bin = max(0.0, d1 - n1 * per_target)
-    inter_per_target = float(rs["nngb"].sum()) / n_s
+    rb = oracle.celllist(p.xyzh, p.vm, p.nc, targets=tb)
+    d_b = time.perf_counter() - t0
+    per_target = max(d_b - d_a, 1e-9) / max(n_b - n_a, 1)
+    t_bin = max(0.0, d_a - n_a * per_target)
+    inter_per_target = float(rb["nngb"].sum()) / n_b
     rate = inter_per_target * p.n / (t_bin + per_target * p.n)
-    desc = (f"oracle_celllist (fp64, OpenMP) timed on {n1} and {n_s} random targets of {p.name} (N={p.n}); "
-            f"per-target {per_target * 1e6:.2f} us, binning {t_bin:.2f} s, extrapolated to all N")
-    del r1
-    return rate, n_s, desc
+    desc = (f"oracle_celllist (fp64, OpenMP) timed on {n_a} and {n_b} random targets of {p.name} (N={p.n}); "
+            f"per-target {per_target * 1e6:.2f} us, binning {t_bin:.2f} s, extrapolated to a full pass over all N")
+    return rate, n_b, desc
 
 
 def cpu_baseline(p, seconds: float):
@@ -158,16 +160,21 @@ def run_reference(args):
     p = synth.make(args.config)
     per_step = max(5.0, 90.0 / max(1, args.steps + args.warmup))
     rng = np.random.default_rng(7)
-    # one-off cost of the call (binning all N), measured with a 1000-target call
-    n1 = 1000
+    # one-off cost of a call (binning all N) and the per-target cost, from two bounded calls
+    # (small sets: every step is a full pass)
+    n_a = min(p.n, 50_000)
     t0 = time.perf_counter()
-    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(rng.choice(p.n, n1, replace=False)))
-    d1 = time.perf_counter() - t0
+    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(rng.choice(p.n, n_a, replace=False)))
+    d_a = time.perf_counter() - t0
+    n_b = min(p.n, 20 * n_a)
     t0 = time.perf_counter()
-    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(rng.choice(p.n, 2 * n1, replace=False)))
-    slope = max((time.perf_counter() - t0 - d1) / n1, 1e-9)
-    t_bin = max(0.0, d1 - n1 * slope)
-    n_s = int(min(p.n, max(4 * n1, per_step / slope)))
+    oracle.celllist(p.xyzh, p.vm, p.nc, targets=np.sort(rng.choice(p.n, n_b, replace=False)))
+    d_b = time.perf_counter() - t0
+    slope = max(d_b - d_a, 1e-9) / max(n_b - n_a, 1)
+    t_bin = max(0.0, d_a - n_a * slope)
+    n_s = int(min(p.n, max(n_a, per_step / slope)))
+    if n_b >= p.n:
+        n_s, t_bin = p.n, 0.0
     times, rates = [], []
     for s in range(args.warmup + args.steps):
         tgt = np.sort(rng.choice(p.n, n_s, replace=False))
