@@ -7,7 +7,9 @@
 //                    sector per particle: no read-modify-write at random slots)
 //   k_stable_*     : per cell, sort the records by input index (the atomic ranks
 //                    arrive in any order) -> xyzh, vm, perm, slot_cell with the
-//                    in-cell order = input order, all reads/writes coalesced
+//                    in-cell order = input order, all reads/writes coalesced;
+//                    fin[scatter slot] = final slot
+//   k_slot_of      : slot_of[input] = fin[scatter slot] (gather, coalesced writes)
 //
 // Stable in-cell order makes everything downstream deterministic and, with
 // slab ghosts received in the sender's cell order, identical across GPU
@@ -22,8 +24,7 @@ namespace pvsph {
 
 __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float4 *__restrict__ xyzh_in,
                       const float4 *__restrict__ vm_in, int *__restrict__ cell_of, int *__restrict__ rank,
-                      int *__restrict__ count, float *__restrict__ cell_hmax, int *__restrict__ slot_of,
-                      unsigned *status)
+                      int *__restrict__ count, float *__restrict__ cell_hmax, unsigned *status)
 {
     double clmin = fmin(g.cl[0], fmin(g.cl[1], g.cl[2]));
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
@@ -64,7 +65,6 @@ __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float
             }
         }
         cell_of[p] = cell;
-        if (cell < 0) slot_of[p] = -1;   // rejected input: no slot (k_unpermute leaves its outputs alone)
     }
 }
 
@@ -155,7 +155,7 @@ struct alignas(32) ParticleRec {
     float4 xyzh, vm;
 };
 
-__global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of, const int *__restrict__ rank,
+__global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of, int *__restrict__ rank,
                               const int *__restrict__ start, const float4 *__restrict__ xyzh_in,
                               const float4 *__restrict__ vm_in, ParticleRec *__restrict__ rec,
                               int *__restrict__ idx_tmp)
@@ -163,8 +163,10 @@ __global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
          p += (long long)gridDim.x * blockDim.x) {
         const int c = __ldcs(cell_of + p);
+        if (c < 0) rank[p] = -1;                 // rejected input: no slot
         if (c >= 0) {
-            const int slot = start[c] + __ldcs(rank + p);
+            const int slot = start[c] + rank[p];
+            rank[p] = slot;                      // the scatter slot, for slot_of (k_slot_of)
             const float4 a = __ldcs(xyzh_in + p), b = __ldcs(vm_in + p);
             // one 256-bit store (STG.256): the whole 32-byte sector at once, no read-modify-write
             // (evict-first: the scattered stream must not push cell_start out of L2)
@@ -187,14 +189,26 @@ constexpr int STABLE_BIG_TILE = 4096;
 __device__ __forceinline__ void stable_place(int s0, int e, int r, const ParticleRec *__restrict__ rec,
                                              const int *__restrict__ idx_tmp, float4 *__restrict__ xyzh,
                                              float4 *__restrict__ vm, int *__restrict__ perm,
-                                             int *__restrict__ slot_of)
+                                             int *__restrict__ fin)
 {
     const ParticleRec q = rec[s0 + e];
     const int idx = idx_tmp[s0 + e];
     xyzh[s0 + r] = q.xyzh;
     vm[s0 + r] = q.vm;
     perm[s0 + r] = idx;
-    slot_of[idx] = s0 + r;
+    fin[s0 + e] = s0 + r;                        // scatter slot -> final slot (coalesced)
+}
+
+// slot_of[p] = final slot of input p: fin[scatter slot] (a gathered read instead of a
+// scattered read-modify-write store per particle).
+__global__ void k_slot_of(long long n_total, const int *__restrict__ scat, const int *__restrict__ fin,
+                          int *__restrict__ slot_of)
+{
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
+         p += (long long)gridDim.x * blockDim.x) {
+        const int t = __ldcs(scat + p);
+        slot_of[p] = t >= 0 ? fin[t] : -1;
+    }
 }
 
 __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
@@ -202,7 +216,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     const ParticleRec *__restrict__ rec,
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
-                                                                    int *__restrict__ slot_of, int2 *big_items,
+                                                                    int *__restrict__ fin, int2 *big_items,
                                                                     int *big_count)
 {
     __shared__ int sh[STABLE_WARPS][STABLE_SMALL];
@@ -235,7 +249,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             if (e < n) {
                 int r = 0;
                 for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
-                stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, slot_of);
+                stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, fin);
             }
         }
         __syncwarp();
@@ -246,7 +260,7 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
                                                                   const int *__restrict__ idx_tmp,
                                                                   const ParticleRec *__restrict__ rec,
                                                                   float4 *__restrict__ xyzh, float4 *__restrict__ vm,
-                                                                  int *__restrict__ perm, int *__restrict__ slot_of,
+                                                                  int *__restrict__ perm, int *__restrict__ fin,
                                                                   const int2 *big_items, const int *big_count)
 {
     __shared__ int tile[STABLE_BIG_TILE];
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
             if (mine)
                 for (int m = 0; m < tn; ++m) r += tile[m] < v;
         }
-        if (mine) stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, slot_of);
+        if (mine) stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, fin);
         __syncthreads();
     }
 }

@@ -78,24 +78,45 @@ __device__ __forceinline__ void store_rec(OutRec *orec, int slot, float rho, flo
 }
 
 // out[p] = record of slot_of[p] for the first n_out input indices (coalesced writes,
-// one 48-byte gather per particle).
-__global__ void k_unpermute(DevOut o, const int *__restrict__ slot_of, const OutRec *__restrict__ orec)
+// one 48-byte gather per particle; UNPERM_ILP independent gathers in flight per thread).
+constexpr int UNPERM_ILP = 4;
+
+__global__ void __launch_bounds__(256) k_unpermute(DevOut o, const int *__restrict__ slot_of,
+                                                    const OutRec *__restrict__ orec)
 {
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < o.n_out;
-         p += (long long)gridDim.x * blockDim.x) {
-        const int sl = slot_of[p];
-        if (sl < 0) continue;                    // input rejected by sph_build_cells (status word set)
-        const float4 *q = reinterpret_cast<const float4 *>(orec + sl);
-        const float4 a = q[0], b = q[1], c = q[2];
-        o.rho[p] = a.x;
-        o.wcount[p] = a.y;
-        o.rho_dh[p] = a.z;
-        o.wcount_dh[p] = a.w;
-        o.div_v[p] = b.x;
-        o.curl_v[p] = b.y;
-        o.curl_v[o.n_out + p] = b.z;
-        o.curl_v[2 * o.n_out + p] = b.w;
-        o.nngb[p] = __float_as_int(c.x);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long p0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; p0 < o.n_out;
+         p0 += stride * UNPERM_ILP) {
+        float4 a[UNPERM_ILP], b[UNPERM_ILP], c[UNPERM_ILP];
+        int sl[UNPERM_ILP];
+#pragma unroll
+        for (int u = 0; u < UNPERM_ILP; ++u) {
+            const long long p = p0 + u * stride;
+            sl[u] = p < o.n_out ? __ldcs(slot_of + p) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < UNPERM_ILP; ++u) {
+            if (sl[u] >= 0) {            // < 0: input rejected by sph_build_cells (status word set)
+                const float4 *q = reinterpret_cast<const float4 *>(orec + sl[u]);
+                a[u] = __ldcs(q);
+                b[u] = __ldcs(q + 1);
+                c[u] = __ldcs(q + 2);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UNPERM_ILP; ++u) {
+            const long long p = p0 + u * stride;
+            if (sl[u] < 0) continue;
+            __stcs(o.rho + p, a[u].x);
+            __stcs(o.wcount + p, a[u].y);
+            __stcs(o.rho_dh + p, a[u].z);
+            __stcs(o.wcount_dh + p, a[u].w);
+            __stcs(o.div_v + p, b[u].x);
+            __stcs(o.curl_v + p, b[u].y);
+            __stcs(o.curl_v + o.n_out + p, b[u].z);
+            __stcs(o.curl_v + 2 * o.n_out + p, b[u].w);
+            __stcs(o.nngb + p, __float_as_int(c[u].x));
+        }
     }
 }
 

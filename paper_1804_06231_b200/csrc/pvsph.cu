@@ -233,7 +233,7 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     const float4 *vin = reinterpret_cast<const float4 *>(vm_in);
     if (n > 0) {
         k_bin<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n_own, n, xin, vin, cell_of, rank, count,
-                                                            cells->cell_hmax, cells->slot_of, status);
+                                                            cells->cell_hmax, status);
     }
     long long ntiles = (g.ncell + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(count, g.ncell, cells->cell_start, tile_sum, status);
@@ -248,11 +248,13 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cell_of, rank, cells->cell_start, xin, vin,
                                                                     rec, perm_tmp);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
+        int *fin = cell_of;                       // cell_of is dead after k_scatter_rec
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, cells->slot_cell, cells->slot_of, big_items,
+            g.ncell, cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, cells->slot_cell, fin, big_items,
             big_count);
-        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, rec, xs, vs, cells->perm,
-                                                          cells->slot_of, big_items, big_count);
+        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, fin,
+                                                          big_items, big_count);
+        k_slot_of<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, rank, fin, cells->slot_of);
     }
     cells->n = n;
     return check_launch();
