@@ -51,13 +51,15 @@ constexpr int V4_CTAS = 2;               // resident CTAs per SM (launch bounds;
 constexpr int V4_TP = V4_WARPS * 32;     // home particles per tile: exactly V4_TP except where a limit cuts
 constexpr int V4_Q = 24;                 // hit stack depth per lane, 2-byte entries
 constexpr int V4_ROWS = 12;              // staged rows: ox in -1..1, oy in -1..2 (relative to the tile's first row)
-constexpr int V4_MAXZ = 32;              // staged cells per row
+constexpr int V4_MAXZ = 21;              // staged cells per row (tiles span <= 19 slices)
 constexpr int V4_MAXCELLS = V4_ROWS * V4_MAXZ;
 constexpr int V4_MAXH = 2 * (V4_MAXZ - 2);   // home cells per tile
 constexpr int V4_MS = 2400;              // staged particles (< 4096: 12-bit queue entries)
 constexpr int V4_ML = 8192;              // staged list entries (27 segments per home cell)
-constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size_t)V4_ML * 2 +
-                           (size_t)(V4_MAXH + 4) * 4 + (size_t)V4_WARPS * V4_Q * 32 * 2 + (size_t)V4_MAXZ * 16;
+constexpr int V4_HOFF = (V4_MAXH + 4 + 3) / 4 * 4;      // ints, keeps the following arrays 16-byte aligned
+constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size_t)V4_ML * 2 + (size_t)V4_HOFF * 4 +
+                           (size_t)V4_WARPS * V4_Q * 32 * 2 + (size_t)V4_MAXZ * 16;
+static_assert(V4_ML % 8 == 0 && (V4_WARPS * V4_Q * 32 * 2) % 16 == 0, "16-byte aligned shared arrays");
 
 
 // Results of one particle in slot (cell) order: rho, wcount, rho_dh, wcount_dh, div_v,
@@ -119,6 +121,16 @@ __global__ void __launch_bounds__(256) k_unpermute(DevOut o, const int *__restri
         }
     }
 }
+
+// ---- optional phase timing (compile with -DPVSPH_PHASE_TIMING; profiling only) --------
+#ifdef PVSPH_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[12];   // 0 stage, 1 search, 2 sweep, 3 drain, 4 final drain, 5 barrier
+#define PH_T0(v) long long v = clock64();
+#define PH_ADD(k, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[k], (unsigned long long)(clock64() - (v))); } while (0)
+#else
+#define PH_T0(v)
+#define PH_ADD(k, v) do { } while (0)
+#endif
 
 // ---- tile list ------------------------------------------------------------------
 struct RowPairs {
@@ -466,9 +478,6 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
                                                    const V4Stage &S, unsigned qbase, bool active, int i, int yoff,
                                                    int qh, int lpos, unsigned cand[4], unsigned hits[4])
 {
-#ifdef PVSPH_STAGE_ONLY
-    return;
-#endif
     const unsigned sQ = qbase + 2u * (threadIdx.x & 31);
     float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
     if (active) {
@@ -528,7 +537,9 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
             const unsigned n = (qp - sQ) >> 6;
             if (!(__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 || __any_sync(0xffffffffu, n >= V4_Q - 8)))
                 break;
+            PH_T0(td0)
             drain(std::false_type{});
+            PH_ADD(3, td0);
         }
     };
     // candidates t .. t+3 of the window L[lb + ...] (SELF: the home cell, staged index base + t, minus i)
@@ -579,7 +590,7 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
             drain_check();
         }
     }
-    int pos = lpos + eh.y;                                // this home cell's direction segments
+    int pos = lpos;                                       // this home cell's direction segments
     for (int d = 0; d < 13; ++d) {
         // reversed +d list, then reversed -d list, so that the lane's two windows (a prefix
         // of +d, a suffix of -d) are contiguous: L[wb, wb + total)
@@ -606,19 +617,25 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
                 home_of(fl1, mx, my, mz);
             }
             int len1;
+            PH_T0(ts0)
             v4_windows(S, d, top, mid - 1, ep.y, mid, em.y, px, py, pz, mx, my, mz, Hk, len0, len1);
+            PH_ADD(1, ts0);
             wb = mid - len0;
             total = len0 + len1;
         }
         const int trip = __reduce_max_sync(0xffffffffu, total);
         const unsigned lb = S.L + 2u * (unsigned)wb;
+        PH_T0(tw0)
         for (int t = 0; t < trip; t += 8) {
             step4(std::false_type{}, lb, 0, t, total, len0, fl0, fl1, kind);
             step4(std::false_type{}, lb, 0, t + 4, total, len0, fl0, fl1, kind);
             drain_check();
         }
+        PH_ADD(2, tw0);
     }
+    PH_T0(tf0)
     while (__any_sync(0xffffffffu, qp != sQ)) drain(std::true_type{});
+    PH_ADD(4, tf0);
 
     if (active) {
         // finalise (self term w(0) = 1/2, t(0) = 3/2), as finalise() in density.cuh
@@ -687,7 +704,7 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     int4 *tab = reinterpret_cast<int4 *>(V + V4_MS);
     uint16_t *L = reinterpret_cast<uint16_t *>(tab + V4_MAXCELLS);
     int *hoff = reinterpret_cast<int *>(L + V4_ML);
-    uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_MAXH + 4);
+    uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_HOFF);
     int4 *seq = reinterpret_cast<int4 *>(queue + V4_WARPS * V4_Q * 32);
     __shared__ int4 s_next;
     __shared__ int s_wsum[V4_WARPS];
@@ -725,7 +742,10 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     prefetch(td);
 
     while (td.x >= 0) {
+        PH_T0(tb0)
         __syncthreads();                                  // s_next consumed by every thread
+        PH_ADD(5, tb0);
+        PH_T0(tst0)
         if (threadIdx.x == 0) {                           // claim the next tile early
             const int t1 = atomicAdd(tile_counter, 1);
             s_next = t1 < ntiles ? tiles[t1] : kEnd;
@@ -748,30 +768,30 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                     ent[k] = make_int4(0, cnt2[k], pf_start[k], (int)fl);
                 }
             }
-            int total;
-            const int pre = block_exscan(cnt2[0] + cnt2[1], s_wsum, total);
-            if (2 * threadIdx.x < ncs) {
-                ent[0].x = pre;
-                tab[2 * threadIdx.x] = ent[0];
-            }
-            if (2 * threadIdx.x + 1 < ncs) {
-                ent[1].x = pre + cnt2[0];
-                tab[2 * threadIdx.x + 1] = ent[1];
-            }
+            // counts first; bases and list offsets then come from ONE block scan of packed
+            // (particles | list entries << 16) values (both totals < 2^16: V4_MS, V4_ML)
+            if (2 * threadIdx.x < ncs) tab[2 * threadIdx.x] = ent[0];
+            if (2 * threadIdx.x + 1 < ncs) tab[2 * threadIdx.x + 1] = ent[1];
             __syncthreads();
-            // list sizes of the home cells (27 neighbours each) and the home slices
-            int lsz = 0;
-            if ((int)threadIdx.x < T.nh) {
-                const int r = threadIdx.x / T.nzh, q = threadIdx.x % T.nzh + 1;
+            // list segments: for home cell h, segment k = 2 d (+d neighbour) or 2 d + 1 (-d),
+            // d = 0..12; global segment g = 26 h + k (4 per thread, consecutive)
+            static_assert(26 * V4_MAXH <= 4 * V4_TP, "four list segments per thread");
+            static_assert(V4_MS < 65536 && V4_ML < 65536, "packed scan");
+            const int nseg = 26 * T.nh;
+            int ssz[4];
 #pragma unroll
-                for (int ox = -1; ox <= 1; ++ox)
-#pragma unroll
-                    for (int oy = -1; oy <= 1; ++oy)
-#pragma unroll
-                        for (int oz = -1; oz <= 1; ++oz) lsz += tab[((ox + 1) * 4 + oy + r + 1) * T.nzs + q + oz].y;
+            for (int j = 0; j < 4; ++j) {
+                const int gseg = 4 * threadIdx.x + j;
+                ssz[j] = 0;
+                if (gseg < nseg) {
+                    const int h = gseg / 26, k = gseg % 26, d = k >> 1, sg = (k & 1) ? -1 : 1;
+                    const int r = h / T.nzh, q = h % T.nzh + 1;
+                    ssz[j] = tab[((sg * dir_component(d, 0) + 1) * 4 + sg * dir_component(d, 1) + r + 1) * T.nzs + q +
+                                 sg * dir_component(d, 2)].y;
+                }
             }
             if (wl == V4_WARPS - 1) {
-                // slice k: {A start, A count, B start, first sequence index}, k < nzh <= 30
+                // slice k: {A start, A count, B start, first sequence index}, k < nzh
                 int4 sl = make_int4(0, 0, 0, 0);
                 int ns = 0;
                 if (lane < T.nzh) {
@@ -789,83 +809,87 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                 sl.w = x - ns;
                 if (lane < T.nzh) seq[lane] = sl;
             }
-            int ltotal;
-            const int lpre = block_exscan(lsz, s_wsum, ltotal);
-            if ((int)threadIdx.x < T.nh) hoff[threadIdx.x] = lpre;
+            int ptot;
+            PH_T0(tsc0)
+            const int pp = block_exscan((cnt2[0] + cnt2[1]) | ((ssz[0] + ssz[1] + ssz[2] + ssz[3]) << 16), s_wsum, ptot);
+            PH_ADD(8, tsc0);
+            const int total = ptot & 0xffff, ltotal = ptot >> 16;
+            const int pre = pp & 0xffff;
+            int lpre = pp >> 16;
+            if (2 * threadIdx.x < ncs) tab[2 * threadIdx.x].x = pre;
+            if (2 * threadIdx.x + 1 < ncs) tab[2 * threadIdx.x + 1].x = pre + cnt2[0];
+            int *segoff = reinterpret_cast<int *>(queue);        // scratch: the hit stacks are idle now
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int gseg = 4 * threadIdx.x + j;
+                if (gseg < nseg) {
+                    segoff[gseg] = lpre;
+                    if (gseg % 26 == 0) hoff[gseg / 26] = lpre;
+                }
+                lpre += ssz[j];
+            }
             if (total > V4_MS || ltotal > V4_ML || T.nh > V4_MAXH) staged = false;   // CTA-uniform
             __syncthreads();
             if (staged) {
-                // positions and (v, m): each staged row is one contiguous slot range, split where z wraps
-                for (int r = wl; r < V4_ROWS; r += V4_WARPS) {
+                // positions and (v, m): warp w copies staged particles [w T / 8, (w + 1) T / 8); each
+                // staged row is one contiguous slot range, split where z wraps
+                PH_T0(tpv0)
+                const int lo = (int)((long long)total * wl / V4_WARPS), hi = (int)((long long)total * (wl + 1) / V4_WARPS);
+                const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
+                for (int r = 0; r < V4_ROWS; ++r) {
+                    const int rb = tab[r * T.nzs].x, re = tab[r * T.nzs + T.nzs - 1].x + tab[r * T.nzs + T.nzs - 1].y;
+                    if (re <= lo || rb >= hi) continue;
                     const int4 e0 = tab[r * T.nzs];
                     const float sx = (e0.w & 8) ? g.boxf[0] : 0.0f;
                     const float sy = (e0.w & 16) ? g.boxf[1] : 0.0f;
                     for (int piece = 0; piece < 3; ++piece) {
                         // piece 0: column 0 if it wraps (uz = -1); 1: the in-box columns; 2: last column if uz = nz
-                        const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
                         const int q0 = piece == 0 ? 0 : (piece == 1 ? (wlo ? 1 : 0) : T.nzs - 1);
                         const int q1 = piece == 0 ? (wlo ? 1 : 0) : (piece == 1 ? (whi ? T.nzs - 1 : T.nzs) : (whi ? T.nzs : T.nzs - 1));
                         if (q1 <= q0) continue;
                         const int4 ea = tab[r * T.nzs + q0];
                         const int4 eb = tab[r * T.nzs + q1 - 1];
                         const float sz = (ea.w & 32) ? g.boxf[2] : 0.0f;
-                        const int n = eb.x + eb.y - ea.x;
-                        const float4 *gx = c.xyzh + ea.z;
-                        const float4 *gv = c.vm + ea.z;
+                        const int b0 = max(ea.x, lo), b1 = min(eb.x + eb.y, hi);
+                        const float4 *gx = c.xyzh + (ea.z - ea.x);
+                        const float4 *gv = c.vm + (ea.z - ea.x);
 #pragma unroll 4
-                        for (int k = lane; k < n; k += 32) {
+                        for (int k = b0 + lane; k < b1; k += 32) {
                             const float4 p = gx[k];
                             // exact: a pre-shifted coordinate is >= L/2
-                            P[ea.x + k] = make_float4(p.x - sx, p.y - sy, p.z - sz, 0.0f);
-                            V[ea.x + k] = gv[k];
+                            P[k] = make_float4(p.x - sx, p.y - sy, p.z - sz, 0.0f);
+                            V[k] = gv[k];
                         }
                     }
                 }
-                // lists: warp per home cell; segment k (self, then +d / -d reversed for d = 0..12)
-                // at its offset from a warp scan; lanes copy an element each, 9 segments in flight
-                for (int h = wl; h < T.nh; h += V4_WARPS) {
+                PH_ADD(6, tpv0);
+                PH_T0(tl0)
+                // list segments, strided over the threads (balanced): the sorted list reversed,
+                // entries turned into staged indices; 16 independent loads in flight
+                for (int gseg = threadIdx.x; gseg < nseg; gseg += V4_TP) {
+                    const int h = gseg / 26, k = gseg % 26, d = k >> 1, sg = (k & 1) ? -1 : 1;
                     const int r = h / T.nzh, q = h % T.nzh + 1;
-                    int o0 = 0, o1 = 0, o2 = 0, d = 0;
-                    if (lane >= 1 && lane < 27) {
-                        d = (lane - 1) >> 1;
-                        const int sg = (lane & 1) ? 1 : -1;
-                        o0 = sg * dir_component(d, 0);
-                        o1 = sg * dir_component(d, 1);
-                        o2 = sg * dir_component(d, 2);
-                    }
-                    const int4 e = lane < 27 ? tab[((o0 + 1) * 4 + o1 + r + 1) * T.nzs + q + o2] : make_int4(0, 0, 0, 0);
-                    int x = e.y;
+                    const int4 e = tab[((sg * dir_component(d, 0) + 1) * 4 + sg * dir_component(d, 1) + r + 1) * T.nzs + q +
+                                       sg * dir_component(d, 2)];
+                    const int dst = segoff[gseg];
+                    const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
+                    for (int k0 = 0; k0 < e.y; k0 += 16) {
+                        unsigned v[16];
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= o) x += y;
-                    }
-                    const int dst = hoff[h] + x - e.y;                 // segment's first list entry
-#ifndef PVSPH_NO_LISTS
-                    if (lane < 27) {
-                        if (lane == 0) {
-                            for (int k = 0; k < e.y; ++k) L[dst + k] = (uint16_t)(e.x + k);
-                        } else {
-                            // reversed; 16 independent loads in flight per lane
-                            const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
-                            for (int k0 = 0; k0 < e.y; k0 += 16) {
-                                unsigned v[16];
+                        for (int u = 0; u < 16; ++u) v[u] = k0 + u < e.y ? (unsigned)__ldg(src + k0 + u) : 0u;
 #pragma unroll
-                                for (int u = 0; u < 16; ++u) v[u] = k0 + u < e.y ? (unsigned)src[k0 + u] : 0u;
-#pragma unroll
-                                for (int u = 0; u < 16; ++u)
-                                    if (k0 + u < e.y) L[dst + e.y - 1 - (k0 + u)] = (uint16_t)(e.x + (int)v[u]);
-                            }
-                        }
+                        for (int u = 0; u < 16; ++u)
+                            if (k0 + u < e.y) L[dst + e.y - 1 - (k0 + u)] = (uint16_t)(e.x + (int)v[u]);
                     }
-#endif
                 }
+                PH_ADD(7, tl0);
                 __syncthreads();
             }
         }
         // the next tile: descriptor published by thread 0 (visible after the barrier above, or
         // the one below for unstaged tiles); its counts are fetched while this tile computes
         __syncthreads();
+        PH_ADD(0, tst0);
         const int4 td_next = s_next;
         prefetch(td_next);
 

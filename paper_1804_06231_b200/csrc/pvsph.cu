@@ -409,6 +409,19 @@ int sph_status(void *ws, void *stream)
     return SPH_OK;
 }
 
+#ifdef PVSPH_PHASE_TIMING
+int sph_debug_phase_cycles(unsigned long long *out8, int reset)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out8, g_phase_cycles, 12 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return SPH_OK;
+}
+#endif
+
 int sph_calibrate(int mode, int blocks, int threads, int iters, float *out, void *stream)
 {
     if (mode < 0 || mode > 2 || blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out) return SPH_EINVAL;
