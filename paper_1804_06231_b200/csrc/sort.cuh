@@ -19,6 +19,9 @@
 namespace pvsph {
 
 constexpr int SORT_SMALL = 32;
+constexpr int SORT_HUGE = 1024;         // cells above: one CTA sorts each direction (bitonic, shared memory)
+constexpr int SORT_HUGE_MAX = 16384;    // cells above: chunked ranking again (k_sort_big)
+constexpr int SORT_HUGE_T = 1024;
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_BIG_CHUNK = 256;
 constexpr int SORT_BIG_TILE = 2048;
@@ -37,7 +40,7 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
 
 __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
                                                                     long long cbeg, long long cend, int2 *big_items,
-                                                                    int *big_count)
+                                                                    int *big_count, int *huge_items, int *huge_count)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -46,6 +49,10 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const int s0 = c.cell_start[cell];
         const int n = c.cell_start[cell + 1] - s0;
         if (n == 0) continue;
+        if (n > SORT_HUGE && n <= SORT_HUGE_MAX) {
+            if (lane == 0) huge_items[atomicAdd(huge_count, 1)] = (int)cell;
+            continue;
+        }
         if (n > SORT_SMALL) {
             if (lane == 0) {
                 int nch = (n + SORT_BIG_CHUNK - 1) / SORT_BIG_CHUNK;
@@ -100,6 +107,55 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             for (int d = 0; d < SPH_NDIR; ++d) ord[(long long)d * c.cap + s0 + r[d]] = (uint16_t)lane;
         }
         __syncwarp();
+    }
+}
+
+// One CTA per cell of SORT_HUGE < n <= SORT_HUGE_MAX particles (clustered data): for each
+// direction the 64-bit composites (orderable fp32 key << 32 | in-cell index; in-cell order is
+// the input order) are bitonic-sorted in shared memory, O(n log^2 n) instead of O(n^2).
+__global__ void __launch_bounds__(SORT_HUGE_T) k_sort_huge(DevGrid g, DevCells c, uint16_t *ord,
+                                                          const int *huge_items, const int *huge_count)
+{
+    extern __shared__ unsigned long long hs[];           // SORT_HUGE_MAX composites
+    const int nitems = *huge_count;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const long long cell = huge_items[it];
+        const int s0 = c.cell_start[cell];
+        const int n = c.cell_start[cell + 1] - s0;
+        int P = 1;
+        while (P < n) P <<= 1;
+        double corner[3];
+        cell_corner(g, cell, corner);
+        for (int d = 0; d < SPH_NDIR; ++d) {
+            for (int e = threadIdx.x; e < P; e += SORT_HUGE_T) {
+                unsigned long long comp = ~0ull;
+                if (e < n) {
+                    const float4 p = c.xyzh[s0 + e];
+                    const float key = pv_key((double)p.x - corner[0], (double)p.y - corner[1], (double)p.z - corner[2], d);
+                    comp = ((unsigned long long)float_order(key) << 32) | (unsigned)e;
+                }
+                hs[e] = comp;
+            }
+            __syncthreads();
+            for (int k = 2; k <= P; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int i = threadIdx.x; i < P; i += SORT_HUGE_T) {
+                        const int ixj = i ^ j;
+                        if (ixj > i) {
+                            const unsigned long long a = hs[i], b = hs[ixj];
+                            if ((a > b) == ((i & k) == 0)) {
+                                hs[i] = b;
+                                hs[ixj] = a;
+                            }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int k = threadIdx.x; k < n; k += SORT_HUGE_T)
+                ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
+            __syncthreads();
+        }
     }
 }
 

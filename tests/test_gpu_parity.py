@@ -285,6 +285,46 @@ def test_cell_occupancy_tile_boundaries(pv, occ):
     compare(run(pv, xyzh, vm, nc), oracle.bruteforce(xyzh, vm), None, f"occ{occ}")
 
 
+@pytest.mark.parametrize("occ", [33, 1025, 2000, 16384, 16385])
+def test_sort_big_cells(pv, occ):
+    """Sorted lists of one dense cell on every sort path: chunked ranking (~35), shared-memory
+    bitonic sort (~1025 .. ~16384), chunked ranking again above it (16385 + background).  Each list is a
+    permutation of the cell, ascending in the oracle's fp64 projection (fp32 rounding allowed),
+    equal fp32 keys in input order."""
+    rng = np.random.default_rng(occ)
+    nc = 3
+    Cl = 1.0 / nc
+    n_bg = 20
+    xyzh = np.zeros((n_bg + occ, 4), np.float32)
+    xyzh[:n_bg, :3] = rng.integers(0, 2 ** 24, size=(n_bg, 3)) / 2 ** 24
+    xyzh[n_bg:, :3] = np.floor((1 + rng.random((occ, 3))) * Cl * 2 ** 24) / 2 ** 24   # all in cell (1,1,1)
+    xyzh[:, 3] = 0.5 * Cl / synth.GAMMA
+    vm = np.zeros_like(xyzh)
+    vm[:, 3] = 1.0 / (n_bg + occ)
+    x, v = torch.from_numpy(xyzh).cuda(), torch.from_numpy(vm).cuda()
+    dp = pv.DensityPass(nc, xyzh.shape[0])
+    pv.sph_build_cells(dp.grid, x, v, dp.cells, dp.ws)
+    pv.sph_sort_cells(dp.grid, dp.cells, dp.ws)
+    dp.check()
+    n = xyzh.shape[0]
+    cs = dp.cells.cell_start.cpu().numpy().astype(np.int64)
+    perm = dp.cells.perm[:n].cpu().numpy()
+    order = dp.cells.order_np()[:, :n]
+    ref = oracle.cell_keys(xyzh, nc)
+    c = (1 * nc + 1) * nc + 1
+    a, b = cs[c], cs[c + 1]
+    assert b - a >= occ                              # plus the background particles that fall in it
+    for d in range(13):
+        sl = a + order[d, a:b]
+        assert np.array_equal(np.sort(sl), np.arange(a, b))
+        k = ref[d, perm[sl]]
+        assert np.all(np.diff(k) >= -1e-6 * Cl)
+        k32 = k.astype(np.float32)
+        tie = perm[sl]
+        same = k32[1:] == k32[:-1]
+        assert np.all(tie[1:][same] > tie[:-1][same])
+
+
 def test_on_axis_near_cutoff_pairs(pv):
     """Adversarial pairs at r = H (1 - 10^-k) along face/edge/corner axes, across the periodic boundary."""
     nc = 5
