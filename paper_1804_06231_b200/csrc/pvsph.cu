@@ -123,7 +123,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 struct Ws {
     size_t status, cell_of, rank, perm_tmp, rec, orec, count, tile_sum, big_count, big_items, huge_count,
         huge_items, rows, rows_sum, tiles, counter, total;
-    long long tile_cap;
+    long long tile_cap, huge_cap;
 };
 
 Ws ws_layout(const DevGrid &g, long long n)
@@ -152,10 +152,11 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4, 256);
     w.big_items = o;                     // (cell, chunk) items: cells of > 32 particles, chunks of 256
     o = align_up(o + 8 * (size_t)(n / 32 + 64), 256);
-    w.huge_count = o;
-    o = align_up(o + 4, 256);
-    w.huge_items = o;                    // cells of > SORT_HUGE particles
-    o = align_up(o + 4 * (size_t)(n / SORT_HUGE + 64), 256);
+    w.huge_count = o;                    // [medium, huge]
+    o = align_up(o + 8, 256);
+    w.huge_items = o;                    // cells of > SORT_MED particles (medium from the front, huge from the back)
+    w.huge_cap = n / SORT_MED + 64;
+    o = align_up(o + 4 * (size_t)w.huge_cap, 256);
     const long long nkeys = row_pairs(g).nkeys;
     w.rows = o;
     o = align_up(o + 4 * (size_t)(nkeys + 1), 256);
@@ -283,17 +284,21 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     int *huge_count = at<int>(ws, w.huge_count);
     int *huge_items = at<int>(ws, w.huge_items);
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
-    if ((e = cudaMemsetAsync(huge_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemsetAsync(huge_count, 0, 8, s)) != cudaSuccess) return cuda_fail(e);
     DevCells c = dev_cells(cells);
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
-        g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count);
+        g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap);
     k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count);
     static bool huge_attr = false;
     if (!huge_attr) {
-        cudaFuncSetAttribute(k_sort_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_HUGE_MAX * 8);
+        cudaFuncSetAttribute(k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_HUGE_MAX * 8);
         huge_attr = true;
     }
-    k_sort_huge<<<148, SORT_HUGE_T, SORT_HUGE_MAX * 8, s>>>(g, c, cells->order, huge_items, huge_count);
+    k_sort_bitonic<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, SORT_MED_MAX * 8, s>>>(
+        g, c, cells->order, huge_items, huge_count, (int)w.huge_cap);
+    k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, SORT_HUGE_MAX * 8, s>>>(
+        g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap);
     return check_launch();
 }
 

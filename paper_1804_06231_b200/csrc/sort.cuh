@@ -19,8 +19,10 @@
 namespace pvsph {
 
 constexpr int SORT_SMALL = 32;
-constexpr int SORT_HUGE = 1024;         // cells above: one CTA sorts each direction (bitonic, shared memory)
-constexpr int SORT_HUGE_MAX = 16384;    // cells above: chunked ranking again (k_sort_big)
+constexpr int SORT_MED = 128;           // cells above: one CTA sorts each direction (bitonic, shared memory)
+constexpr int SORT_MED_MAX = 2048;      //   medium tier: 256 threads, 16 KB shared memory
+constexpr int SORT_MED_T = 256;
+constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 1024 threads, 128 KB; above it chunked ranking again
 constexpr int SORT_HUGE_T = 1024;
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_BIG_CHUNK = 256;
@@ -40,7 +42,8 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
 
 __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
                                                                     long long cbeg, long long cend, int2 *big_items,
-                                                                    int *big_count, int *huge_items, int *huge_count)
+                                                                    int *big_count, int *huge_items, int *huge_count,
+                                                                    int huge_cap)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -49,8 +52,12 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const int s0 = c.cell_start[cell];
         const int n = c.cell_start[cell + 1] - s0;
         if (n == 0) continue;
-        if (n > SORT_HUGE && n <= SORT_HUGE_MAX) {
-            if (lane == 0) huge_items[atomicAdd(huge_count, 1)] = (int)cell;
+        if (n > SORT_MED && n <= SORT_HUGE_MAX) {
+            // medium cells from the front of the list, huge ones from the back (k_sort_bitonic)
+            if (lane == 0) {
+                if (n <= SORT_MED_MAX) huge_items[atomicAdd(&huge_count[0], 1)] = (int)cell;
+                else huge_items[huge_cap - 1 - atomicAdd(&huge_count[1], 1)] = (int)cell;
+            }
             continue;
         }
         if (n > SORT_SMALL) {
@@ -110,16 +117,18 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
     }
 }
 
-// One CTA per cell of SORT_HUGE < n <= SORT_HUGE_MAX particles (clustered data): for each
-// direction the 64-bit composites (orderable fp32 key << 32 | in-cell index; in-cell order is
-// the input order) are bitonic-sorted in shared memory, O(n log^2 n) instead of O(n^2).
-__global__ void __launch_bounds__(SORT_HUGE_T) k_sort_huge(DevGrid g, DevCells c, uint16_t *ord,
-                                                          const int *huge_items, const int *huge_count)
+// One CTA per cell of SORT_MED < n <= MAXN particles (clustered data): for each direction the
+// 64-bit composites (orderable fp32 key << 32 | in-cell index; in-cell order is the input
+// order) are bitonic-sorted in shared memory, O(n log^2 n) instead of O(n^2).  FROM_BACK:
+// the items are stored from the back of the list (huge tier).
+template <int MAXN, int T, bool FROM_BACK>
+__global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint16_t *ord, const int *items,
+                                                   const int *count, int cap)
 {
-    extern __shared__ unsigned long long hs[];           // SORT_HUGE_MAX composites
-    const int nitems = *huge_count;
+    extern __shared__ unsigned long long hs[];           // MAXN composites
+    const int nitems = *count;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const long long cell = huge_items[it];
+        const long long cell = items[FROM_BACK ? cap - 1 - it : it];
         const int s0 = c.cell_start[cell];
         const int n = c.cell_start[cell + 1] - s0;
         int P = 1;
@@ -127,7 +136,7 @@ __global__ void __launch_bounds__(SORT_HUGE_T) k_sort_huge(DevGrid g, DevCells c
         double corner[3];
         cell_corner(g, cell, corner);
         for (int d = 0; d < SPH_NDIR; ++d) {
-            for (int e = threadIdx.x; e < P; e += SORT_HUGE_T) {
+            for (int e = threadIdx.x; e < P; e += T) {
                 unsigned long long comp = ~0ull;
                 if (e < n) {
                     const float4 p = c.xyzh[s0 + e];
@@ -139,7 +148,7 @@ __global__ void __launch_bounds__(SORT_HUGE_T) k_sort_huge(DevGrid g, DevCells c
             __syncthreads();
             for (int k = 2; k <= P; k <<= 1) {
                 for (int j = k >> 1; j > 0; j >>= 1) {
-                    for (int i = threadIdx.x; i < P; i += SORT_HUGE_T) {
+                    for (int i = threadIdx.x; i < P; i += T) {
                         const int ixj = i ^ j;
                         if (ixj > i) {
                             const unsigned long long a = hs[i], b = hs[ixj];
@@ -152,8 +161,7 @@ __global__ void __launch_bounds__(SORT_HUGE_T) k_sort_huge(DevGrid g, DevCells c
                     __syncthreads();
                 }
             }
-            for (int k = threadIdx.x; k < n; k += SORT_HUGE_T)
-                ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
+            for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
             __syncthreads();
         }
     }

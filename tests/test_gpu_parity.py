@@ -285,7 +285,7 @@ def test_cell_occupancy_tile_boundaries(pv, occ):
     compare(run(pv, xyzh, vm, nc), oracle.bruteforce(xyzh, vm), None, f"occ{occ}")
 
 
-@pytest.mark.parametrize("occ", [33, 1025, 2000, 16384, 16385])
+@pytest.mark.parametrize("occ", [33, 200, 1025, 2000, 16384, 16385])
 def test_sort_big_cells(pv, occ):
     """Sorted lists of one dense cell on every sort path: chunked ranking (~35), shared-memory
     bitonic sort (~1025 .. ~16384), chunked ranking again above it (16385 + background).  Each list is a
