@@ -455,6 +455,49 @@ __device__ __forceinline__ void v4_windows_d(const V4Stage &S, int top, int f0, 
     len1 = lo1;
 }
 
+// Windows of two directions D0, D1 at once: four independent bisections in lockstep.
+template <int D0, int D1>
+__device__ __forceinline__ void v4_windows2_d(const V4Stage &S, int top, const int f[4], const int n[4],
+                                              const float h[4][3], const float Hk[2], int len[4])
+{
+    int lo[4] = {0, 0, 0, 0};
+    for (int st = top; st > 0; st >>= 1) {
+        unsigned idx[4];
+        bool v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int kk = lo[k] + st;
+            v[k] = kk <= n[k];
+            // segments 0, 2 (+d) read backwards from f, segments 1, 3 (-d) forwards
+            idx[k] = v[k] ? ldsr_u16(S.L + 2u * (unsigned)((k & 1) ? f[k] + kk - 1 : f[k] - kk + 1)) : 0u;
+        }
+        float4 p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = ldsr_f4(S.P + 16u * idx[k]);
+        const float s0 = v4_dot<D0>(p[0].x - h[0][0], p[0].y - h[0][1], p[0].z - h[0][2]);
+        const float s1 = v4_dot<D0>(h[1][0] - p[1].x, h[1][1] - p[1].y, h[1][2] - p[1].z);
+        const float s2 = v4_dot<D1>(p[2].x - h[2][0], p[2].y - h[2][1], p[2].z - h[2][2]);
+        const float s3 = v4_dot<D1>(h[3][0] - p[3].x, h[3][1] - p[3].y, h[3][2] - p[3].z);
+        if (v[0] && s0 < Hk[0]) lo[0] += st;
+        if (v[1] && s1 < Hk[0]) lo[1] += st;
+        if (v[2] && s2 < Hk[1]) lo[2] += st;
+        if (v[3] && s3 < Hk[1]) lo[3] += st;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) len[k] = lo[k];
+}
+
+__device__ __forceinline__ void v4_windows2(const V4Stage &S, int dpair, int top, const int f[4], const int n[4],
+                                            const float h[4][3], const float Hk[2], int len[4])
+{
+#define V4W2(P) case P: v4_windows2_d<2 * P, 2 * P + 1>(S, top, f, n, h, Hk, len); break;
+    switch (dpair) {
+        V4W2(0) V4W2(1) V4W2(2) V4W2(3) V4W2(4) V4W2(5)
+    default: len[0] = len[1] = len[2] = len[3] = 0;
+    }
+#undef V4W2
+}
+
 __device__ __forceinline__ void v4_windows(const V4Stage &S, int d, int top, int f0, int n0, int f1, int n1,
                                            float h0x, float h0y, float h0z, float h1x, float h1y, float h1z, float Hk,
                                            int &len0, int &len1)
@@ -591,47 +634,82 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
         }
     }
     int pos = lpos;                                       // this home cell's direction segments
-    for (int d = 0; d < 13; ++d) {
-        // reversed +d list, then reversed -d list, so that the lane's two windows (a prefix
-        // of +d, a suffix of -d) are contiguous: L[wb, wb + total)
-        int wb = 0, len0 = 0, total = 0;
-        unsigned fl0 = 0, fl1 = 0;
-        const int kind = v4_kind(d);
-        const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
-        const float Hk = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
-        int4 ep = make_int4(0, 0, 0, 0), em = make_int4(0, 0, 0, 0);
-        if (active) {
-            ep = S.tab[scell(a0, a1, a2)];
-            em = S.tab[scell(-a0, -a1, -a2)];
+    // reversed +d list, then reversed -d list, so that the lane's two windows (a prefix of +d,
+    // a suffix of -d) are contiguous: L[wb, wb + total); directions in pairs for the searches
+    for (int d0 = 0; d0 < 13; d0 += 2) {
+        const int nd = d0 + 1 < 13 ? 2 : 1;
+        int wbv[2] = {0, 0}, len0v[2] = {0, 0}, totv[2] = {0, 0};
+        unsigned fl0v[2] = {0, 0}, fl1v[2] = {0, 0};
+        int f[4] = {0, 0, 0, 0}, nn[4] = {0, 0, 0, 0};
+        float hh[4][3];
+        float Hkv[2] = {0.0f, 0.0f};
+        int nmax = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int d = d0 + k;
+            hh[2 * k][0] = hh[2 * k + 1][0] = x;
+            hh[2 * k][1] = hh[2 * k + 1][1] = y;
+            hh[2 * k][2] = hh[2 * k + 1][2] = z;
+            if (k < nd) {
+                const int kind = v4_kind(d);
+                Hkv[k] = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
+                if (active) {
+                    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                    const int4 ep = S.tab[scell(a0, a1, a2)];
+                    const int4 em = S.tab[scell(-a0, -a1, -a2)];
+                    const int mid = pos + ep.y;           // boundary between the two reversed segments
+                    pos = mid + em.y;
+                    f[2 * k] = mid - 1;
+                    f[2 * k + 1] = mid;
+                    nn[2 * k] = ep.y;
+                    nn[2 * k + 1] = em.y;
+                    wbv[k] = mid;
+                    nmax = max(nmax, max(ep.y, em.y));
+                    if (FRAMES) {
+                        fl0v[k] = (unsigned)ep.w & 7u;
+                        fl1v[k] = (unsigned)em.w & 7u;
+                        home_of(fl0v[k], hh[2 * k][0], hh[2 * k][1], hh[2 * k][2]);
+                        home_of(fl1v[k], hh[2 * k + 1][0], hh[2 * k + 1][1], hh[2 * k + 1][2]);
+                    }
+                }
+            }
         }
-        const int nmax = __reduce_max_sync(0xffffffffu, max(ep.y, em.y));
+        nmax = __reduce_max_sync(0xffffffffu, nmax);
         const int top = nmax > 0 ? 1 << (31 - __clz(nmax)) : 0;
         if (active) {
-            const int mid = pos + ep.y;                   // boundary between the two reversed segments
-            pos = mid + em.y;
-            float px = x, py = y, pz = z, mx = x, my = y, mz = z;
-            if (FRAMES) {
-                fl0 = (unsigned)ep.w & 7u;
-                fl1 = (unsigned)em.w & 7u;
-                home_of(fl0, px, py, pz);
-                home_of(fl1, mx, my, mz);
-            }
-            int len1;
+            int len[4];
             PH_T0(ts0)
-            v4_windows(S, d, top, mid - 1, ep.y, mid, em.y, px, py, pz, mx, my, mz, Hk, len0, len1);
+            if (nd == 2) {
+                v4_windows2(S, d0 >> 1, top, f, nn, hh, Hkv, len);
+            } else {
+                v4_windows(S, d0, top, f[0], nn[0], f[1], nn[1], hh[0][0], hh[0][1], hh[0][2], hh[1][0], hh[1][1],
+                           hh[1][2], Hkv[0], len[0], len[1]);
+                len[2] = len[3] = 0;
+            }
             PH_ADD(1, ts0);
-            wb = mid - len0;
-            total = len0 + len1;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                len0v[k] = len[2 * k];
+                totv[k] = len[2 * k] + len[2 * k + 1];
+                wbv[k] -= len[2 * k];
+            }
         }
-        const int trip = __reduce_max_sync(0xffffffffu, total);
-        const unsigned lb = S.L + 2u * (unsigned)wb;
-        PH_T0(tw0)
-        for (int t = 0; t < trip; t += 8) {
-            step4(std::false_type{}, lb, 0, t, total, len0, fl0, fl1, kind);
-            step4(std::false_type{}, lb, 0, t + 4, total, len0, fl0, fl1, kind);
-            drain_check();
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (k >= nd) break;
+            const int kind = v4_kind(d0 + k);
+            const int total = totv[k], len0 = len0v[k];
+            const unsigned fl0 = fl0v[k], fl1 = fl1v[k];
+            const int trip = __reduce_max_sync(0xffffffffu, total);
+            const unsigned lb = S.L + 2u * (unsigned)wbv[k];
+            PH_T0(tw0)
+            for (int t = 0; t < trip; t += 8) {
+                step4(std::false_type{}, lb, 0, t, total, len0, fl0, fl1, kind);
+                step4(std::false_type{}, lb, 0, t + 4, total, len0, fl0, fl1, kind);
+                drain_check();
+            }
+            PH_ADD(2, tw0);
         }
-        PH_ADD(2, tw0);
     }
     PH_T0(tf0)
     while (__any_sync(0xffffffffu, qp != sQ)) drain(std::true_type{});
