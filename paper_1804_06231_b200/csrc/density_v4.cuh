@@ -786,6 +786,9 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     int4 *seq = reinterpret_cast<int4 *>(queue + V4_WARPS * V4_Q * 32);
     __shared__ int4 s_next;
     __shared__ int s_wsum[V4_WARPS];
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const unsigned mbar = smem_addr(&s_mbar);
+    unsigned mbar_phase = 0;
     static_assert(V4_MAXCELLS <= 2 * V4_TP, "two table entries per thread");
 
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -814,6 +817,8 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     if (threadIdx.x == 0) {
         const int t0 = atomicAdd(tile_counter, 1);
         s_next = t0 < ntiles ? tiles[t0] : kEnd;
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     int4 td = s_next;
@@ -909,35 +914,25 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
             if (total > V4_MS || ltotal > V4_ML || T.nh > V4_MAXH) staged = false;   // CTA-uniform
             __syncthreads();
             if (staged) {
-                // positions and (v, m): warp w copies staged particles [w T / 8, (w + 1) T / 8); each
-                // staged row is one contiguous slot range, split where z wraps
+                // positions and (v, m): bulk copies (the TMA engine) of each staged row's contiguous
+                // slot ranges (split where z wraps), issued by warp 0 and overlapped with the list copy
                 PH_T0(tpv0)
-                const int lo = (int)((long long)total * wl / V4_WARPS), hi = (int)((long long)total * (wl + 1) / V4_WARPS);
-                const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
-                for (int r = 0; r < V4_ROWS; ++r) {
-                    const int rb = tab[r * T.nzs].x, re = tab[r * T.nzs + T.nzs - 1].x + tab[r * T.nzs + T.nzs - 1].y;
-                    if (re <= lo || rb >= hi) continue;
-                    const int4 e0 = tab[r * T.nzs];
-                    const float sx = (e0.w & 8) ? g.boxf[0] : 0.0f;
-                    const float sy = (e0.w & 16) ? g.boxf[1] : 0.0f;
-                    for (int piece = 0; piece < 3; ++piece) {
+                if (wl == 0) {
+                    if (lane == 0) mbar_expect_tx(mbar, (unsigned)total * 32u);
+                    __syncwarp();
+                    const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
+                    for (int job = lane; job < V4_ROWS * 3; job += 32) {
+                        const int r = job / 3, piece = job % 3;
                         // piece 0: column 0 if it wraps (uz = -1); 1: the in-box columns; 2: last column if uz = nz
                         const int q0 = piece == 0 ? 0 : (piece == 1 ? (wlo ? 1 : 0) : T.nzs - 1);
                         const int q1 = piece == 0 ? (wlo ? 1 : 0) : (piece == 1 ? (whi ? T.nzs - 1 : T.nzs) : (whi ? T.nzs : T.nzs - 1));
                         if (q1 <= q0) continue;
                         const int4 ea = tab[r * T.nzs + q0];
                         const int4 eb = tab[r * T.nzs + q1 - 1];
-                        const float sz = (ea.w & 32) ? g.boxf[2] : 0.0f;
-                        const int b0 = max(ea.x, lo), b1 = min(eb.x + eb.y, hi);
-                        const float4 *gx = c.xyzh + (ea.z - ea.x);
-                        const float4 *gv = c.vm + (ea.z - ea.x);
-#pragma unroll 4
-                        for (int k = b0 + lane; k < b1; k += 32) {
-                            const float4 p = gx[k];
-                            // exact: a pre-shifted coordinate is >= L/2
-                            P[k] = make_float4(p.x - sx, p.y - sy, p.z - sz, 0.0f);
-                            V[k] = gv[k];
-                        }
+                        const unsigned bytes = (unsigned)(eb.x + eb.y - ea.x) * 16u;
+                        if (bytes == 0) continue;
+                        bulk_g2s(smem_addr(P + ea.x), c.xyzh + ea.z, bytes, mbar);
+                        bulk_g2s(smem_addr(V + ea.x), c.vm + ea.z, bytes, mbar);
                     }
                 }
                 PH_ADD(6, tpv0);
@@ -961,6 +956,26 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                     }
                 }
                 PH_ADD(7, tl0);
+                mbar_wait(mbar, mbar_phase);
+                mbar_phase ^= 1u;
+                if (T.za == 0 || T.y0 == 0 || g.x_lo + T.xo == 0) {
+                    __syncthreads();
+                    // staged cells of a -L periodic image (flags 3-5): x_j - L, exact (x_j >= L/2)
+                    for (int sc = wl; sc < V4_ROWS * T.nzs; sc += V4_WARPS) {
+                        const int4 e = tab[sc];
+                        if (!(e.w & 56)) continue;
+                        const float sx = (e.w & 8) ? g.boxf[0] : 0.0f;
+                        const float sy = (e.w & 16) ? g.boxf[1] : 0.0f;
+                        const float sz = (e.w & 32) ? g.boxf[2] : 0.0f;
+                        for (int k = lane; k < e.y; k += 32) {
+                            float4 q = P[e.x + k];
+                            q.x -= sx;
+                            q.y -= sy;
+                            q.z -= sz;
+                            P[e.x + k] = q;
+                        }
+                    }
+                }
                 __syncthreads();
             }
         }
