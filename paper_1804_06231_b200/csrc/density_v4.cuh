@@ -623,6 +623,44 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
         }
     };
 
+    // candidates t .. t+3 of two consecutive windows (directions d0, d0 + 1 of a pair):
+    // L[lb0 ...] for the first tot0, then L[lb1 ...]
+    auto step4pair = [&](int t, unsigned lb0, int tot0, int len00, unsigned fl00, unsigned fl10, int kind0,
+                         unsigned lb1, int tot1, int len01, unsigned fl01, unsigned fl11, int kind1) {
+        bool ok[4], in0[4];
+        unsigned sj[4];
+        float4 p[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int tt = t + u;
+            in0[u] = tt < tot0;
+            ok[u] = tt < tot0 + tot1;
+            const unsigned e = ldsr_u16(in0[u] ? lb0 + 2u * (unsigned)tt : lb1 + 2u * (unsigned)(tt - tot0));
+            sj[u] = ok[u] ? e : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) p[u] = ldsr_f4(S.P + 16u * sj[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float hx = x, hy = y, hz = z;
+            unsigned fl = 0;
+            if (FRAMES) {
+                const int tt = t + u;
+                fl = in0[u] ? (tt < len00 ? fl00 : fl10) : (tt - tot0 < len01 ? fl01 : fl11);
+                home_of(fl, hx, hy, hz);
+            }
+            const float dx = hx - p[u].x, dy = hy - p[u].y, dz = hz - p[u].z;
+            const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            const int kind = in0[u] ? kind0 : kind1;
+            if (COUNT) cand[kind] += ok[u] ? 1u : 0u;
+            if (ok[u] && r2 < H2) {
+                sts_u16(qp, FRAMES ? (sj[u] | (fl << 12)) : sj[u]);
+                qp += 64u;
+                if (COUNT) ++hits[kind];
+            }
+        }
+    };
+
     // the self cell: all j != i of the home cell
     {
         const int total = active ? eh.y : 0;
@@ -694,22 +732,19 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
                 wbv[k] -= len[2 * k];
             }
         }
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            if (k >= nd) break;
-            const int kind = v4_kind(d0 + k);
-            const int total = totv[k], len0 = len0v[k];
-            const unsigned fl0 = fl0v[k], fl1 = fl1v[k];
-            const int trip = __reduce_max_sync(0xffffffffu, total);
-            const unsigned lb = S.L + 2u * (unsigned)wbv[k];
-            PH_T0(tw0)
-            for (int t = 0; t < trip; t += 8) {
-                step4(std::false_type{}, lb, 0, t, total, len0, fl0, fl1, kind);
-                step4(std::false_type{}, lb, 0, t + 4, total, len0, fl0, fl1, kind);
-                drain_check();
-            }
-            PH_ADD(2, tw0);
+        // one sweep over both directions' windows (one trip count for the pair)
+        const int kind0 = v4_kind(d0), kind1 = nd == 2 ? v4_kind(d0 + 1) : 0;
+        const int trip = __reduce_max_sync(0xffffffffu, totv[0] + totv[1]);
+        const unsigned lb0 = S.L + 2u * (unsigned)wbv[0], lb1 = S.L + 2u * (unsigned)wbv[1];
+        PH_T0(tw0)
+        for (int t = 0; t < trip; t += 8) {
+            step4pair(t, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1, totv[1], len0v[1], fl0v[1], fl1v[1],
+                      kind1);
+            step4pair(t + 4, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1, totv[1], len0v[1], fl0v[1],
+                      fl1v[1], kind1);
+            drain_check();
         }
+        PH_ADD(2, tw0);
     }
     PH_T0(tf0)
     while (__any_sync(0xffffffffu, qp != sQ)) drain(std::true_type{});
