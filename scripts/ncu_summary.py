@@ -92,10 +92,11 @@ def launches(path):
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     t = defaultdict(list)
     unit = None
     for r in rows[hdr + 1:]:
-        if len(r) > vi:
+        if len(r) > vi and (mi is None or r[mi] == "gpu__time_duration.sum"):
             t[r[ki].split("(")[0][:70]].append(float(r[vi].replace(",", "")))
             unit = r[ui]
     total = sum(sum(v) for v in t.values())
