@@ -2,9 +2,9 @@
 //
 //   k_bin          : validate, fp64 bin, atomic slot rank within the cell, cell_hmax
 //   k_scan_*       : exclusive scan of the per-cell counts -> cell_start
-//   k_scatter_rec  : the particle's 32-byte record (x, y, z, h, vx, vy, vz, m) and
-//                    input index to slot cell_start[cell] + rank (one full
-//                    sector per particle: no read-modify-write at random slots)
+//   k_scatter_rec  : the particle's 64-byte record (x, y, z, h, vx, vy, vz, m,
+//                    input index) to slot cell_start[cell] + rank (two full
+//                    sectors per particle: no read-modify-write at random slots)
 //   k_stable_*     : per cell, sort the records by input index (the atomic ranks
 //                    arrive in any order) -> xyzh, vm, perm, slot_cell with the
 //                    in-cell order = input order, all reads/writes coalesced;
@@ -14,8 +14,8 @@
 // Stable in-cell order makes everything downstream deterministic and, with
 // slab ghosts received in the sender's cell order, identical across GPU
 // counts.  HBM traffic per particle ~ 32 (read) + 8
-// (cell/rank) + 40 (re-read) + 36 + 32 (scattered record + index sector) +
-// 36 (stable read) + 40 (write) ~ 225 B.
+// (cell/rank) + 40 (re-read) + 64 (scattered 64-byte record: two full sectors) +
+// 64 (stable read) + 44 (write) + slot_of gather ~ 300 B (random-access granularity).
 #pragma once
 
 #include "common.cuh"
@@ -151,14 +151,16 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_add(int *__restrict__ start, lo
         if (base + k < n) start[base + k] += add;
 }
 
-struct alignas(32) ParticleRec {
+// 64-byte scatter record: the particle's 8 floats and its input index, written as two full
+// 32-byte sectors (two 256-bit stores) so a random slot costs no read-modify-write.
+struct alignas(64) ParticleRec {
     float4 xyzh, vm;
+    int idx, pad[7];
 };
 
 __global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of, int *__restrict__ rank,
                               const int *__restrict__ start, const float4 *__restrict__ xyzh_in,
-                              const float4 *__restrict__ vm_in, ParticleRec *__restrict__ rec,
-                              int *__restrict__ idx_tmp)
+                              const float4 *__restrict__ vm_in, ParticleRec *__restrict__ rec)
 {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
          p += (long long)gridDim.x * blockDim.x) {
@@ -173,7 +175,9 @@ __global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of
             asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + slot), "f"(a.x),
                          "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
                          : "memory");
-            __stcs(idx_tmp + slot, (int)p);
+            asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %2, %2, %2, %2, %2, %2};" ::"l"(&rec[slot].idx),
+                         "r"((int)p), "r"(0)
+                         : "memory");
         }
     }
 }
@@ -187,14 +191,14 @@ constexpr int STABLE_BIG_TILE = 4096;
 // cell's (all distinct) and move its record there.  Larger cells are queued as
 // (cell, chunk).  slot_cell is written for every slot.
 __device__ __forceinline__ void stable_place(int s0, int e, int r, const ParticleRec *__restrict__ rec,
-                                             const int *__restrict__ idx_tmp, float4 *__restrict__ xyzh,
+                                             float4 *__restrict__ xyzh,
                                              float4 *__restrict__ vm, int *__restrict__ perm,
                                              int *__restrict__ fin)
 {
-    const ParticleRec q = rec[s0 + e];
-    const int idx = idx_tmp[s0 + e];
-    xyzh[s0 + r] = q.xyzh;
-    vm[s0 + r] = q.vm;
+    const float4 qx = rec[s0 + e].xyzh, qv = rec[s0 + e].vm;
+    const int idx = rec[s0 + e].idx;
+    xyzh[s0 + r] = qx;
+    vm[s0 + r] = qv;
     perm[s0 + r] = idx;
     fin[s0 + e] = s0 + r;                        // scatter slot -> final slot (coalesced)
 }
@@ -212,7 +216,6 @@ __global__ void k_slot_of(long long n_total, const int *__restrict__ scat, const
 }
 
 __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
-                                                                    const int *__restrict__ idx_tmp,
                                                                     const ParticleRec *__restrict__ rec,
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int e = lane + 32 * k;
-            v[k] = e < n ? idx_tmp[s0 + e] : 0;
+            v[k] = e < n ? rec[s0 + e].idx : 0;
             if (e < n) sh[w][e] = v[k];
         }
         __syncwarp();
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             if (e < n) {
                 int r = 0;
                 for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
-                stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, fin);
+                stable_place(s0, e, r, rec, xyzh, vm, perm, fin);
             }
         }
         __syncwarp();
@@ -257,7 +260,6 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
 }
 
 __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__restrict__ start,
-                                                                  const int *__restrict__ idx_tmp,
                                                                   const ParticleRec *__restrict__ rec,
                                                                   float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                   int *__restrict__ perm, int *__restrict__ fin,
@@ -271,17 +273,17 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
         int n = start[item.x + 1] - s0;
         int e = item.y * STABLE_BIG_CHUNK + threadIdx.x;
         bool mine = e < n;
-        int v = mine ? idx_tmp[s0 + e] : 0;
+        int v = mine ? rec[s0 + e].idx : 0;
         int r = 0;
         for (int t0 = 0; t0 < n; t0 += STABLE_BIG_TILE) {
             int tn = min(STABLE_BIG_TILE, n - t0);
             __syncthreads();
-            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = idx_tmp[s0 + t0 + m];
+            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = rec[s0 + t0 + m].idx;
             __syncthreads();
             if (mine)
                 for (int m = 0; m < tn; ++m) r += tile[m] < v;
         }
-        if (mine) stable_place(s0, e, r, rec, idx_tmp, xyzh, vm, perm, fin);
+        if (mine) stable_place(s0, e, r, rec, xyzh, vm, perm, fin);
         __syncthreads();
     }
 }

@@ -121,7 +121,7 @@ DevOut dev_out(const sph_out *o)
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
-    size_t status, cell_of, rank, perm_tmp, rec, orec, count, tile_sum, big_count, big_items, huge_count,
+    size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
         huge_items, rows, rows_sum, tiles, counter, total;
     long long tile_cap, huge_cap;
 };
@@ -137,10 +137,8 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
     w.rank = o;
     o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
-    w.perm_tmp = o;
-    o = align_up(o + 4 * (size_t)(n > 0 ? n : 1), 256);
     w.rec = o;
-    o = align_up(o + 32 * (size_t)(n > 0 ? n : 1), 256);
+    o = align_up(o + sizeof(ParticleRec) * (size_t)(n > 0 ? n : 1), 256);
     w.orec = o;
     o = align_up(o + sizeof(OutRec) * (size_t)(n > 0 ? n : 1), 256);
     w.count = o;
@@ -244,20 +242,19 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(count, g.ncell, cells->cell_start, tile_sum, status);
     k_scan_sums<<<1, SCAN_T, 0, s>>>(tile_sum, ntiles, cells->cell_start, g.ncell);
     k_scan_add<<<(int)ntiles, SCAN_T, 0, s>>>(cells->cell_start, g.ncell, tile_sum);
-    int *perm_tmp = at<int>(ws, w.perm_tmp);
     int *big_count = at<int>(ws, w.big_count);
     int2 *big_items = at<int2>(ws, w.big_items);
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     if (n > 0) {
         ParticleRec *rec = at<ParticleRec>(ws, w.rec);
         k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cell_of, rank, cells->cell_start, xin, vin,
-                                                                    rec, perm_tmp);
+                                                                    rec);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
         int *fin = cell_of;                       // cell_of is dead after k_scatter_rec
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, cells->slot_cell, fin, big_items,
+            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, fin, big_items,
             big_count);
-        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, perm_tmp, rec, xs, vs, cells->perm, fin,
+        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, fin,
                                                           big_items, big_count);
         k_slot_of<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, rank, fin, cells->slot_of);
     }
