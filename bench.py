@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--levels", type=int, default=0,
+                    help="level passes (DESIGN.md §4.5); 0 = auto: 3 for the clustered c4, else 1")
     return ap.parse_args()
 
 
@@ -227,7 +229,9 @@ def run_ours(args):
         part = slabs.Slab.from_config(args.config, rank, world)
     t_gen = time.perf_counter() - t_gen
 
-    runner = slabs.SlabRunner(part, dist=dist)
+    nlev = args.levels or (3 if args.config == "c4" and world == 1 else 1)
+    levels = pv.level_grids(part.pset.xyzh[:, 3], part.nc, max_levels=nlev) if nlev > 1 else None
+    runner = slabs.SlabRunner(part, dist=dist, levels=levels)
     runner.upload()
     stream = torch.cuda.current_stream()
 
@@ -314,6 +318,7 @@ def run_ours(args):
                 "config": {"workload": f"{args.config} (BASELINE.json configs, DESIGN.md §3)",
                            "n_particles": part.n_global, "cells": f"{part.nc}^3",
                            "parallelism": f"x-slab{world}" if world > 1 else "single",
+                           "level_grids": [lv[0] for lv in runner.levels],
                            "l2": "inputs (>= 4 GB at c5) larger than L2; no flush",
                            "step": "ghost exchange + build_cells + sort_cells + density_all"},
                 "interactions_per_step": tot_inter, "candidates_per_step": tot_cand,

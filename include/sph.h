@@ -84,6 +84,11 @@ typedef struct sph_grid {
     int32_t reserved;   /* must be 0                                        */
     double box[3];      /* periodic box lengths (> 0)                       */
     float gamma;        /* support / smoothing length (1.825742)            */
+    float h_home_min;   /* level passes: if h_home_max > 0, */
+    float h_home_max;   /*   only particles with h_home_min < h <= h_home_max */
+                        /*   are HOME (outputs computed) on this grid; the  */
+                        /*   others are binned as neighbour sources only    */
+                        /*   and may have gamma*h > C_l.  0, 0: all home.   */
     float reserved2;    /* must be 0                                        */
 } sph_grid;
 
@@ -108,7 +113,10 @@ typedef struct sph_grid {
  *   slot_cell[capacity]     local cell of each slot (written by build)
  *   slot_of[capacity]       slot of each input index (written by build; the
  *                           inverse of perm, used to return outputs in input
- *                           order with a coalesced gather)
+ *                           order with a coalesced gather); -1 for an input
+ *                           that is rejected or not home on this grid
+ *   cell_nhome[ncell]       home particles of each cell; they occupy the first
+ *                           cell_nhome[c] slots of the cell (written by build)
  *   order[SPH_NDIR * capacity] sorted lists (uint16 in-cell indices):
  *                           direction d, cell c at
  *                           order[d * capacity + cell_start[c] ...]
@@ -125,6 +133,7 @@ typedef struct sph_cells {
     uint16_t *order;
     int32_t *slot_cell;
     int32_t *slot_of;
+    int32_t *cell_nhome;
 } sph_cells;
 
 /* Outputs, each an array of n_out elements indexed by INPUT index (only
@@ -150,7 +159,9 @@ int64_t sph_ncell(const sph_grid *grid);
 size_t sph_workspace_bytes(const sph_grid *grid, int64_t n_total);
 
 /* Bin particles into cells and write the cell-sorted SoA
- * arrays, perm, cell_start, cell_hmax and cells->n = n_own + n_ghost.
+ * arrays, perm, cell_start, cell_hmax, cell_nhome, slot_of and cells->n =
+ * n_own + n_ghost.  Within a cell, home particles come first, each group in
+ * input order.
  * Inputs xyzh_in/vm_in hold n_own owned particles followed by n_ghost
  * ghost particles (float4 each, device).  Owned particles must lie in the
  * rank's owned planes, ghosts in its ghost planes (n_ghost > 0 needs
@@ -165,7 +176,9 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
 int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end,
                    void *ws, size_t ws_bytes, void *stream);
 
-/* Self-cell interactions of each listed cell (device int32 list): every
+/* (sph_density_self / sph_density_pair treat every particle of a listed cell
+ * as home, whatever the grid's home range.)
+ * Self-cell interactions of each listed cell (device int32 list): every
  * ordered pair i != j in the cell plus the self term of i.  ACCUMULATES
  * with atomics into acc (caller zeroes it first): rho, wcount, rho_dh,
  * wcount_dh and nngb receive their final contributions, div_v and curl_v
@@ -185,9 +198,10 @@ int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t
  * and pair calls). */
 int sph_density_finalize(sph_out *acc, int64_t n, void *stream);
 
-/* The fused hot path: every owned particle gathers from its own cell and
- * the 26 neighbour cells with pseudo-Verlet windows, one writer per
- * particle, no atomics, deterministic; writes FINAL values in input order. */
+/* The fused hot path: every owned HOME particle gathers from its own cell
+ * and the 26 neighbour cells with pseudo-Verlet windows, one writer per
+ * particle, no atomics, deterministic; writes FINAL values in input order
+ * (outputs of non-home particles are left untouched: a level pass). */
 int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, sph_stats *stats, void *ws,
                     size_t ws_bytes, void *stream);
 

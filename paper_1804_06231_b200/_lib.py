@@ -23,12 +23,14 @@ EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cel
 
 class SphGrid(ctypes.Structure):
     _fields_ = [("nc", c_i32 * 3), ("x_lo", c_i32), ("x_hi", c_i32), ("ghost_x", c_i32), ("reserved", c_i32),
-                ("box", c_f64 * 3), ("gamma", c_f32), ("reserved2", c_f32)]
+                ("box", c_f64 * 3), ("gamma", c_f32), ("h_home_min", c_f32), ("h_home_max", c_f32),
+                ("reserved2", c_f32)]
 
 
 class SphCells(ctypes.Structure):
     _fields_ = [("capacity", c_i64), ("n", c_i64), ("cell_start", c_vp), ("xyzh", c_vp), ("vm", c_vp),
-                ("perm", c_vp), ("cell_hmax", c_vp), ("order", c_vp), ("slot_cell", c_vp), ("slot_of", c_vp)]
+                ("perm", c_vp), ("cell_hmax", c_vp), ("order", c_vp), ("slot_cell", c_vp), ("slot_of", c_vp),
+                ("cell_nhome", c_vp)]
 
 
 class SphOut(ctypes.Structure):

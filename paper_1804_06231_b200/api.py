@@ -39,7 +39,8 @@ def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
-def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0) -> SphGrid:
+def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0, h_home=None) -> SphGrid:
+    """h_home = (h_min, h_max): level pass, only particles with h_min < h <= h_max are home."""
     if isinstance(nc, int):
         nc = (nc, nc, nc)
     if isinstance(box, (int, float)):
@@ -52,6 +53,8 @@ def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0) -> SphGrid
     g.x_hi = int(nc[0] if x_hi is None else x_hi)
     g.ghost_x = int(ghost_x)
     g.gamma = float(gamma)
+    if h_home is not None:
+        g.h_home_min, g.h_home_max = float(h_home[0]), float(h_home[1])
     return g
 
 
@@ -81,6 +84,7 @@ class Cells:
     order: torch.Tensor         # (13, capacity) int16 storage of the uint16 sorted lists (include/sph.h)
     slot_cell: torch.Tensor     # (capacity,) int32
     slot_of: torch.Tensor       # (capacity,) int32: slot of each input index
+    cell_nhome: torch.Tensor    # (ncell,) int32: home particles per cell
     n: int = 0
 
     @staticmethod
@@ -94,7 +98,8 @@ class Cells:
                      torch.empty(nce, dtype=torch.float32, device=device),
                      torch.empty((_lib.SPH_NDIR, cap), dtype=torch.int16, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device),
-                     torch.empty(cap, dtype=torch.int32, device=device))
+                     torch.empty(cap, dtype=torch.int32, device=device),
+                     torch.empty(nce, dtype=torch.int32, device=device))
 
     def struct(self) -> SphCells:
         s = SphCells()
@@ -104,6 +109,7 @@ class Cells:
         s.perm, s.cell_hmax, s.order = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.order.data_ptr()
         s.slot_cell = self.slot_cell.data_ptr()
         s.slot_of = self.slot_of.data_ptr()
+        s.cell_nhome = self.cell_nhome.data_ptr()
         return s
 
     def order_np(self):
@@ -237,8 +243,8 @@ class DensityPass:
     build_cells -> sort_cells -> density_all (the hot path)."""
 
     def __init__(self, nc, n_own: int, box=1.0, gamma=GAMMA, capacity: int | None = None, device="cuda",
-                 x_lo=0, x_hi=None, ghost_x=0):
-        self.grid = make_grid(nc, box, gamma, x_lo, x_hi, ghost_x)
+                 x_lo=0, x_hi=None, ghost_x=0, h_home=None):
+        self.grid = make_grid(nc, box, gamma, x_lo, x_hi, ghost_x, h_home)
         self.n_own = int(n_own)
         cap = int(capacity if capacity is not None else n_own)
         self.cells = Cells.alloc(self.grid, cap, device)
@@ -247,14 +253,75 @@ class DensityPass:
         self.device = device
 
     def run(self, xyzh: torch.Tensor, vm: torch.Tensor, n_ghost: int = 0, stats: Stats | None = None,
-            stream=None) -> Out:
+            stream=None, out: Out | None = None) -> Out:
+        out = self.out if out is None else out
         sph_build_cells(self.grid, xyzh, vm, self.cells, self.ws, n_own=self.n_own, n_ghost=n_ghost, stream=stream)
         sph_sort_cells(self.grid, self.cells, self.ws, stream=stream)
-        sph_density_all(self.grid, self.cells, self.out, self.ws, stats=stats, stream=stream)
-        return self.out
+        sph_density_all(self.grid, self.cells, out, self.ws, stats=stats, stream=stream)
+        return out
 
     def check(self, stream=None) -> None:
         check_status(self.ws, stream)
+
+
+def level_grids(h, nc0: int, box=1.0, gamma=GAMMA, max_levels: int = 3):
+    """Level passes for clustered data: cell grids nc0, 2 nc0, 4 nc0, ...
+    Level k is home to the particles whose support fits its cells but not the next finer
+    ones: h_max(k) = the largest fp32 h with gamma h <= box / nc_k, h_min(k) = h_max(k + 1)
+    (0 for the finest).  Levels without particles are dropped.  Returns [(nc, h_min, h_max)]."""
+    import numpy as np
+
+    def hcap(nc):
+        c = float(box) / nc
+        v = np.float32(c / gamma)
+        while float(gamma) * float(v) > c:
+            v = np.nextafter(v, np.float32(0))
+        return float(v)
+
+    h = np.asarray(h, np.float32)
+    ncs = [nc0 * 2 ** k for k in range(max_levels)]
+    caps = [hcap(n) for n in ncs]
+    out = []
+    for k, n in enumerate(ncs):
+        lo = caps[k + 1] if k + 1 < len(ncs) else 0.0
+        if np.any((h > lo) & (h <= caps[k])):
+            out.append((n, lo, caps[k]))
+    return out
+
+
+class LevelPasses:
+    """One density pass per level grid, all writing the same outputs: each
+    particle is home on exactly one level; every level bins all particles as neighbours."""
+
+    def __init__(self, levels, n: int, box=1.0, gamma=GAMMA, device="cuda"):
+        self.levels = list(levels)
+        self.passes = [DensityPass(nc, n, box, gamma, device=device,
+                                   h_home=(lo, hi) if len(self.levels) > 1 else None)
+                       for nc, lo, hi in self.levels]
+        self.out = self.passes[0].out
+
+    def run(self, xyzh: torch.Tensor, vm: torch.Tensor, stats: Stats | None = None, stream=None) -> Out:
+        for dp in self.passes:
+            dp.run(xyzh, vm, stats=stats, stream=stream, out=self.out)
+        return self.out
+
+    def check(self, stream=None) -> None:
+        for dp in self.passes:
+            dp.check(stream)
+
+
+def density_levels(xyzh, vm, levels, box=1.0, gamma=GAMMA, stats: bool = False):
+    """Like density(), through level passes [(nc, h_min, h_max)] (level_grids())."""
+    xyzh = torch.as_tensor(xyzh, dtype=torch.float32).cuda().contiguous()
+    vm = torch.as_tensor(vm, dtype=torch.float32).cuda().contiguous()
+    lp = LevelPasses(levels, xyzh.shape[0], box, gamma)
+    st = Stats() if stats else None
+    out = lp.run(xyzh, vm, stats=st)
+    lp.check()
+    res = out.to_numpy()
+    if stats:
+        res["stats"] = st.read()
+    return res
 
 
 def density(xyzh, vm, nc, box=1.0, gamma=GAMMA, stats: bool = False):

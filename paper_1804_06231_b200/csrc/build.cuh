@@ -36,7 +36,9 @@ __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float
                       isfinite(b.y) && isfinite(b.z) && isfinite(b.w);
         if (!finite) {
             set_status(status, ST_EDOMAIN);
-        } else if (!(a.w > 0.0f) || !(b.w > 0.0f) || (double)g.gamma * (double)a.w > clmin) {
+        } else if (!(a.w > 0.0f) || !(b.w > 0.0f) ||
+                   (is_home(g.h_home_min, g.h_home_max, a.w) && (double)g.gamma * (double)a.w > clmin)) {
+            // (a neighbour-only particle of a level pass may have gamma h > C_l)
             set_status(status, ST_EH_RANGE);
         } else {
             double x[3] = {a.x, a.y, a.z};
@@ -158,7 +160,7 @@ struct alignas(64) ParticleRec {
     int idx, pad[7];
 };
 
-__global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of, int *__restrict__ rank,
+__global__ void k_scatter_rec(DevGrid g, long long n_total, const int *__restrict__ cell_of, int *__restrict__ rank,
                               const int *__restrict__ start, const float4 *__restrict__ xyzh_in,
                               const float4 *__restrict__ vm_in, ParticleRec *__restrict__ rec)
 {
@@ -175,8 +177,10 @@ __global__ void k_scatter_rec(long long n_total, const int *__restrict__ cell_of
             asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(rec + slot), "f"(a.x),
                          "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
                          : "memory");
+            // key of the in-cell order: home particles first, each group in input order
+            const unsigned key = (unsigned)p | (is_home(g.h_home_min, g.h_home_max, a.w) ? 0u : 0x80000000u);
             asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %2, %2, %2, %2, %2, %2};" ::"l"(&rec[slot].idx),
-                         "r"((int)p), "r"(0)
+                         "r"(key), "r"(0)
                          : "memory");
         }
     }
@@ -196,11 +200,11 @@ __device__ __forceinline__ void stable_place(int s0, int e, int r, const Particl
                                              int *__restrict__ fin)
 {
     const float4 qx = rec[s0 + e].xyzh, qv = rec[s0 + e].vm;
-    const int idx = rec[s0 + e].idx;
+    const unsigned key = (unsigned)rec[s0 + e].idx;
     xyzh[s0 + r] = qx;
     vm[s0 + r] = qv;
-    perm[s0 + r] = idx;
-    fin[s0 + e] = s0 + r;                        // scatter slot -> final slot (coalesced)
+    perm[s0 + r] = (int)(key & 0x7fffffffu);
+    fin[s0 + e] = (s0 + r) | (int)(key & 0x80000000u);   // scatter slot -> final slot (coalesced); sign: not home
 }
 
 // slot_of[p] = final slot of input p: fin[scatter slot] (a gathered read instead of a
@@ -211,7 +215,8 @@ __global__ void k_slot_of(long long n_total, const int *__restrict__ scat, const
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
          p += (long long)gridDim.x * blockDim.x) {
         const int t = __ldcs(scat + p);
-        slot_of[p] = t >= 0 ? fin[t] : -1;
+        const int f = t >= 0 ? fin[t] : -1;
+        slot_of[p] = f >= 0 ? f : -1;           // rejected or not home on this grid
     }
 }
 
@@ -219,17 +224,33 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     const ParticleRec *__restrict__ rec,
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
-                                                                    int *__restrict__ fin, int2 *big_items,
-                                                                    int *big_count)
+                                                                    int *__restrict__ fin, int *__restrict__ cell_nhome,
+                                                                    int2 *big_items, int *big_count)
 {
-    __shared__ int sh[STABLE_WARPS][STABLE_SMALL];
+    __shared__ unsigned sh[STABLE_WARPS][STABLE_SMALL];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     constexpr int PER = STABLE_SMALL / 32;
-    for (long long cell = (long long)blockIdx.x * STABLE_WARPS + w; cell < ncell;
-         cell += (long long)gridDim.x * STABLE_WARPS) {
-        const int s0 = start[cell];
-        const int n = start[cell + 1] - s0;
-        for (int e = lane; e < n; e += 32) slot_cell[s0 + e] = (int)cell;
+    // 32 cells per warp step (empty cells cost one lane each: sparse fine grids)
+    for (long long base = ((long long)blockIdx.x * STABLE_WARPS + w) * 32; base < ncell;
+         base += (long long)gridDim.x * STABLE_WARPS * 32) {
+        const long long mycell = base + lane;
+        const int my_s0 = mycell < ncell ? start[mycell] : 0;
+        const int my_n = mycell < ncell ? start[mycell + 1] - my_s0 : 0;
+        if (mycell < ncell && my_n == 0) cell_nhome[mycell] = 0;
+        unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
+      while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const long long cell = base + j;
+        const int s0 = __shfl_sync(0xffffffffu, my_s0, j);
+        const int n = __shfl_sync(0xffffffffu, my_n, j);
+        int nh = 0;
+        for (int e = lane; e < n; e += 32) {
+            slot_cell[s0 + e] = (int)cell;
+            nh += (unsigned)rec[s0 + e].idx < 0x80000000u;
+        }
+        nh = __reduce_add_sync(0xffffffffu, nh);
+        if (lane == 0) cell_nhome[cell] = nh;
         if (n > STABLE_SMALL) {
             if (lane == 0) {
                 int nch = (n + STABLE_BIG_CHUNK - 1) / STABLE_BIG_CHUNK;
@@ -238,11 +259,11 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             }
             continue;
         }
-        int v[PER];
+        unsigned v[PER];
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int e = lane + 32 * k;
-            v[k] = e < n ? rec[s0 + e].idx : 0;
+            v[k] = e < n ? (unsigned)rec[s0 + e].idx : 0u;
             if (e < n) sh[w][e] = v[k];
         }
         __syncwarp();
@@ -256,6 +277,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             }
         }
         __syncwarp();
+      }
     }
 }
 
@@ -265,7 +287,7 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
                                                                   int *__restrict__ perm, int *__restrict__ fin,
                                                                   const int2 *big_items, const int *big_count)
 {
-    __shared__ int tile[STABLE_BIG_TILE];
+    __shared__ unsigned tile[STABLE_BIG_TILE];
     const int nitems = *big_count;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         int2 item = big_items[it];
@@ -273,12 +295,12 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
         int n = start[item.x + 1] - s0;
         int e = item.y * STABLE_BIG_CHUNK + threadIdx.x;
         bool mine = e < n;
-        int v = mine ? rec[s0 + e].idx : 0;
+        unsigned v = mine ? (unsigned)rec[s0 + e].idx : 0u;
         int r = 0;
         for (int t0 = 0; t0 < n; t0 += STABLE_BIG_TILE) {
             int tn = min(STABLE_BIG_TILE, n - t0);
             __syncthreads();
-            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = rec[s0 + t0 + m].idx;
+            for (int m = threadIdx.x; m < tn; m += blockDim.x) tile[m] = (unsigned)rec[s0 + t0 + m].idx;
             __syncthreads();
             if (mine)
                 for (int m = 0; m < tn; ++m) r += tile[m] < v;

@@ -29,6 +29,7 @@ struct DevGrid {
     double cl[3];        // cell edges
     float boxf[3];
     float gamma;
+    float h_home_min, h_home_max;   // level passes: home iff h_home_min < h <= h_home_max (max 0: all)
     float delta;         // window margin SPH_DELTA_FRAC * min(cl)
     float q[SPH_NDIR];   // Q_d = sum_a |d_a| C_a / |d|: projection of the cell offset on axis d
 };
@@ -43,7 +44,15 @@ struct DevCells {
     const uint16_t *ord;    // sorted lists (include/sph.h), [SPH_NDIR][cap]
     const int *slot_cell;
     const int *slot_of;
+    const int *cell_nhome;
 };
+
+// Level passes: is a particle of smoothing length h a HOME particle of
+// grid g (outputs computed here) or a neighbour source only?
+__host__ __device__ __forceinline__ bool is_home(float h_home_min, float h_home_max, float h)
+{
+    return !(h_home_max > 0.0f) || (h > h_home_min && h <= h_home_max);
+}
 
 struct DevOut {
     long long n_out;

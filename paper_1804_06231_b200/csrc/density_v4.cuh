@@ -187,15 +187,16 @@ struct ZCols {
     int slice, c12, c9a, c9b;
 };
 
-__device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__ cs, const long long rb[V4_ROWS],
-                                       bool hasB, int z)
+__device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__ cs, const int *__restrict__ nhome,
+                                       const long long rb[V4_ROWS], bool hasB, int z)
 {
     const int wz = wrap_i(z, g.nz);
     int n[V4_ROWS];
 #pragma unroll
     for (int k = 0; k < V4_ROWS; ++k) n[k] = cs[rb[k] + wz + 1] - cs[rb[k] + wz];
     ZCols c;
-    c.slice = n[5] + (hasB ? n[6] : 0);
+    // home particles of the slice (rows 5, 6 = the tile's two rows); the rest counts all particles
+    c.slice = (z >= 0 && z < g.nz) ? nhome[rb[5] + wz] + (hasB ? nhome[rb[6] + wz] : 0) : 0;
     c.c12 = c.c9a = c.c9b = 0;
 #pragma unroll
     for (int k = 0; k < V4_ROWS; ++k) {
@@ -217,8 +218,8 @@ __device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__
 // {key, z_a | z_b << 16, first particle in slice z_a, count (< 0: global-memory)}.
 // The cut depends only on the row pair's own counts (identical on any GPU count).
 template <bool WRITE>
-__global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, int *__restrict__ off, int4 *tiles,
-                           long long tile_cap, unsigned *status)
+__global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, const int *__restrict__ nhome,
+                           int *__restrict__ off, int4 *tiles, long long tile_cap, unsigned *status)
 {
     const RowPairs r = row_pairs(g);
     for (long long key = blockIdx.x * (long long)blockDim.x + threadIdx.x; key < r.nkeys;
@@ -241,8 +242,8 @@ __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, int *_
                 }
                 ++nt;
             };
-            ZCols cm = zcols(g, cell_start, rb, hasB, -1), c0 = zcols(g, cell_start, rb, hasB, 0),
-                  cp = zcols(g, cell_start, rb, hasB, 1);
+            ZCols cm = zcols(g, cell_start, nhome, rb, hasB, -1), c0 = zcols(g, cell_start, nhome, rb, hasB, 0),
+                  cp = zcols(g, cell_start, nhome, rb, hasB, 1);
             bool open = false;
             int tz = 0, tfirst = 0, home = 0, stg = 0, lst = 0;
             int z = 0, o = 0;                      // next particle: o-th of slice z
@@ -285,7 +286,7 @@ __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, int *_
                     o = 0;
                     cm = c0;
                     c0 = cp;
-                    cp = zcols(g, cell_start, rb, hasB, z + 1);
+                    cp = zcols(g, cell_start, nhome, rb, hasB, z + 1);
                 }
             }
             if (open && home > 0) emit(tz, g.nz - 1, tfirst, home);
@@ -833,7 +834,7 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     const int4 kEnd = make_int4(-1, 0, 0, 0);
 
     // prefetch of a tile's staged-cell counts: thread owns table entries 2 tid, 2 tid + 1
-    int pf_start[2] = {0, 0}, pf_end[2] = {0, 0};
+    int pf_start[2] = {0, 0}, pf_end[2] = {0, 0}, pf_nh[2] = {0, 0};
     auto prefetch = [&](int4 td) {
         if (td.x < 0) return;
         const TileGeom t = tile_geom(g, rp, td);
@@ -846,6 +847,7 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                 const long long cell = staged_cell(g, t, s, fl);
                 pf_start[k] = c.cell_start[cell];
                 pf_end[k] = c.cell_start[cell + 1];
+                pf_nh[k] = c.cell_nhome[cell];
             }
         }
     };
@@ -883,7 +885,7 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                     unsigned fl;
                     staged_cell(g, T, s, fl);
                     cnt2[k] = pf_end[k] - pf_start[k];
-                    ent[k] = make_int4(0, cnt2[k], pf_start[k], (int)fl);
+                    ent[k] = make_int4(0, cnt2[k], pf_start[k], (int)fl | (pf_nh[k] << 8));   // w: flags | home count << 8
                 }
             }
             // counts first; bases and list offsets then come from ONE block scan of packed
@@ -913,10 +915,11 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                 int4 sl = make_int4(0, 0, 0, 0);
                 int ns = 0;
                 if (lane < T.nzh) {
+                    // home particles lead each cell: {A start, A home count, B start}
                     const int4 ea = tab[5 * T.nzs + lane + 1];
                     const int4 eb = tab[6 * T.nzs + lane + 1];
-                    sl = make_int4(ea.z, ea.y, eb.z, 0);
-                    ns = ea.y + (T.hasB ? eb.y : 0);
+                    sl = make_int4(ea.z, ea.w >> 8, eb.z, 0);
+                    ns = (ea.w >> 8) + (T.hasB ? (eb.w >> 8) : 0);
                 }
                 int x = ns;
 #pragma unroll
@@ -1062,9 +1065,9 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                 int qq = T.first + h, z = T.za, slot = 0;
                 for (;; ++z) {
                     const long long ca = rowA + z;
-                    const int a0 = c.cell_start[ca], na = c.cell_start[ca + 1] - a0;
+                    const int a0 = c.cell_start[ca], na = c.cell_nhome[ca];
                     const int b0 = T.hasB ? c.cell_start[ca + g.nz] : 0;
-                    const int nb = T.hasB ? c.cell_start[ca + g.nz + 1] - b0 : 0;
+                    const int nb = T.hasB ? c.cell_nhome[ca + g.nz] : 0;
                     if (qq < na) { slot = a0 + qq; break; }
                     if (qq < na + nb) { slot = b0 + (qq - na); break; }
                     qq -= na + nb;

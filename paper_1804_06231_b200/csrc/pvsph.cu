@@ -59,6 +59,12 @@ int make_grid(const sph_grid *gr, DevGrid &g)
     g.n_owned_cells = (long long)(gr->x_hi - gr->x_lo) * g.ny * g.nz;
     if (g.ncell >= (1LL << 31) - 1) return SPH_EINVAL;
     g.gamma = gr->gamma;
+    if (gr->reserved != 0 || gr->reserved2 != 0.0f) return SPH_EINVAL;
+    if (!(gr->h_home_max >= 0.0f) || !(gr->h_home_min >= 0.0f) || !std::isfinite(gr->h_home_max) ||
+        (gr->h_home_max > 0.0f && !(gr->h_home_min < gr->h_home_max)))
+        return SPH_EINVAL;
+    g.h_home_min = gr->h_home_min;
+    g.h_home_max = gr->h_home_max;
     double clmin = std::fmin(g.cl[0], std::fmin(g.cl[1], g.cl[2]));
     g.delta = (float)(SPH_DELTA_FRAC * clmin);
     for (int d = 0; d < SPH_NDIR; ++d) {
@@ -76,7 +82,7 @@ int make_grid(const sph_grid *gr, DevGrid &g)
 
 bool cells_ok(const sph_cells *c)
 {
-    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell && c->slot_of &&
+    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell && c->slot_of && c->cell_nhome &&
            c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
            ((uintptr_t)c->order % 2 == 0);
@@ -94,6 +100,7 @@ DevCells dev_cells(const sph_cells *c)
     d.ord = c->order;
     d.slot_cell = c->slot_cell;
     d.slot_of = c->slot_of;
+    d.cell_nhome = c->cell_nhome;
     return d;
 }
 
@@ -247,17 +254,19 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     if (n > 0) {
         ParticleRec *rec = at<ParticleRec>(ws, w.rec);
-        k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, cell_of, rank, cells->cell_start, xin, vin,
-                                                                    rec);
+        k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n, cell_of, rank, cells->cell_start, xin,
+                                                                    vin, rec);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
         int *fin = cell_of;                       // cell_of is dead after k_scatter_rec
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, fin, big_items,
+            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, fin, cells->cell_nhome, big_items,
             big_count);
         k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, fin,
                                                           big_items, big_count);
         k_slot_of<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, rank, fin, cells->slot_of);
     }
+    if (n == 0 && (e = cudaMemsetAsync(cells->cell_nhome, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
+        return cuda_fail(e);
     cells->n = n;
     return check_launch();
 }
@@ -376,14 +385,14 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     int4 *tiles = at<int4>(ws, w.tiles);
     int *counter = at<int>(ws, w.counter);
     const DevCells dc = dev_cells(cells);
-    k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, rows, tiles, w.tile_cap,
-                                                                       status);
+    k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
+                                                                       w.tile_cap, status);
     const long long ntiles_scan = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
     k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles_scan, rows, nkeys);
     k_scan_add<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows_sum);
-    k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, rows, tiles, w.tile_cap,
-                                                                      status);
+    k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
+                                                                      w.tile_cap, status);
     cudaError_t e;
     if ((e = cudaMemsetAsync(counter, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     static int blocks_per_sm = 0, sms = 0;

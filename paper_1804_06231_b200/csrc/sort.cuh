@@ -47,11 +47,20 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (long long cell = cbeg + (long long)blockIdx.x * SORT_WARPS + w; cell < cend;
-         cell += (long long)gridDim.x * SORT_WARPS) {
-        const int s0 = c.cell_start[cell];
-        const int n = c.cell_start[cell + 1] - s0;
-        if (n == 0) continue;
+    // 32 cells per warp step: lane l reads cell base + l, then the warp walks the non-empty
+    // ones (sparse fine grids of level passes are mostly empty cells)
+    for (long long base = cbeg + ((long long)blockIdx.x * SORT_WARPS + w) * 32; base < cend;
+         base += (long long)gridDim.x * SORT_WARPS * 32) {
+        const long long mycell = base + lane;
+        const int my_s0 = mycell < cend ? c.cell_start[mycell] : 0;
+        const int my_n = mycell < cend ? c.cell_start[mycell + 1] - my_s0 : 0;
+        unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
+      while (todo) {
+        const int j = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const long long cell = base + j;
+        const int s0 = __shfl_sync(0xffffffffu, my_s0, j);
+        const int n = __shfl_sync(0xffffffffu, my_n, j);
         if (n > SORT_MED && n <= SORT_HUGE_MAX) {
             // medium cells from the front of the list, huge ones from the back (k_sort_bitonic)
             if (lane == 0) {
@@ -114,6 +123,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             for (int d = 0; d < SPH_NDIR; ++d) ord[(long long)d * c.cap + s0 + r[d]] = (uint16_t)lane;
         }
         __syncwarp();
+      }
     }
 }
 

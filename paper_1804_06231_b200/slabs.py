@@ -126,7 +126,9 @@ def exchange_planes(dist, rank: int, world: int, send_lo, send_hi, recv) -> tupl
 class SlabRunner:
     """Device buffers and one density step of one rank."""
 
-    def __init__(self, slab: Slab, dist=None, device="cuda", ghost_capacity: int | None = None):
+    def __init__(self, slab: Slab, dist=None, device="cuda", ghost_capacity: int | None = None, levels=None):
+        """levels: [(nc, h_min, h_max)] level passes (one GPU only); the first
+        level's nc must be the slab's grid."""
         self.slab = slab
         self.dist = dist
         self.world = slab.world
@@ -136,7 +138,12 @@ class SlabRunner:
         self.n_global = slab.n_global
         self.pset = slab.pset
         ghost = self.world > 1
-        self.grid = pv.make_grid(slab.nc, slab.box, slab.gamma, slab.x_lo, slab.x_hi, int(ghost))
+        self.levels = list(levels) if levels else [(slab.nc, 0.0, 0.0)]
+        if len(self.levels) > 1 and ghost:
+            raise ValueError("level passes run on one GPU (x-slabs use one grid)")
+        split = len(self.levels) > 1
+        self.grid = pv.make_grid(slab.nc, slab.box, slab.gamma, slab.x_lo, slab.x_hi, int(ghost),
+                                 self.levels[0][1:] if split else None)
         if ghost:
             per_plane = self.n_own / max(1, slab.x_hi - slab.x_lo)
             gcap = ghost_capacity if ghost_capacity is not None else int(2 * 1.5 * per_plane + 4096)
@@ -151,8 +158,15 @@ class SlabRunner:
         self.n_ghost = 0
         self.plane = self.grid.nc[1] * self.grid.nc[2]   # cells per x plane
         self.nxl = (slab.x_hi - slab.x_lo) + (2 if ghost else 0)
-        self.launches_per_step = BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES + (BUILD_LAUNCHES if ghost else 0)
+        self.launches_per_step = (BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES) * len(self.levels) + \
+            (BUILD_LAUNCHES if ghost else 0)
         self.device = device
+        # finer level grids (one GPU): own cells and workspace each, same outputs
+        self.extra = []
+        for nc, lo, hi in self.levels[1:]:
+            g = pv.make_grid(nc, slab.box, slab.gamma, h_home=(lo, hi))
+            c = pv.Cells.alloc(g, self.cap, device)
+            self.extra.append((g, c, pv.alloc_workspace(g, c.capacity, device)))
 
     # -- data ---------------------------------------------------------------
     def upload(self) -> None:
@@ -187,14 +201,22 @@ class SlabRunner:
         rec(1)
         pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own,
                            n_ghost=self.n_ghost)
+        for g, c, ws in self.extra:
+            pv.sph_build_cells(g, self.xin, self.vin, c, ws, n_own=self.n_own, n_ghost=0)
         rec(2)
         pv.sph_sort_cells(self.grid, self.cells, self.ws)
+        for g, c, ws in self.extra:
+            pv.sph_sort_cells(g, c, ws)
         rec(3)
         pv.sph_density_all(self.grid, self.cells, self.out, self.ws, stats=stats)
+        for g, c, ws in self.extra:
+            pv.sph_density_all(g, c, self.out, ws, stats=stats)
         rec(4)
 
     def check(self) -> None:
         pv.check_status(self.ws)
+        for _, _, ws in self.extra:
+            pv.check_status(ws)
 
     # -- end to end through host buffers -----------------------------------
     def e2e_time(self, steps: int = 3, warmup: int = 1):
