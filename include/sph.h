@@ -172,7 +172,9 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
                     const float *vm_in, sph_cells *cells, void *ws, size_t ws_bytes, void *stream);
 
 /* Sort every cell of [cell_begin, cell_end) along the 13 directions (P:92,
- * P:102): fills cells->order for those cells.  cell_end = -1 means all. */
+ * P:102): fills cells->order for those cells.  cell_end = -1 means all.
+ * With a home range (level pass) only cells within one cell of a home
+ * particle are sorted: the others' lists are never read by sph_density_all. */
 int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end,
                    void *ws, size_t ws_bytes, void *stream);
 

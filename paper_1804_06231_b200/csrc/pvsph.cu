@@ -292,8 +292,14 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMemsetAsync(huge_count, 0, 8, s)) != cudaSuccess) return cuda_fail(e);
     DevCells c = dev_cells(cells);
+    int *need = nullptr;
+    if (g.h_home_max > 0.0f) {                 // level pass: sort only cells next to home particles
+        need = at<int>(ws, w.count);           // (the build's count array, free after the build)
+        if ((e = cudaMemsetAsync(need, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
+        k_mark_needed<<<grid_blocks(g.ncell, 256, 148 * 32), 256, 0, s>>>(g, cells->cell_nhome, need);
+    }
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
-        g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap);
+        g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap, need);
     k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count);
     static bool huge_attr = false;
     if (!huge_attr) {

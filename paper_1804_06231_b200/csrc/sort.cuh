@@ -40,10 +40,33 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
     corner[2] = (double)iz * g.cl[2];
 }
 
+// Level passes: a cell's sorted lists are read only if the cell or one of
+// its 26 neighbours holds home particles of this grid; mark those cells.
+__global__ void k_mark_needed(DevGrid g, const int *__restrict__ cell_nhome, int *__restrict__ need)
+{
+    const long long plane = (long long)g.ny * g.nz;
+    for (long long cell = blockIdx.x * (long long)blockDim.x + threadIdx.x; cell < g.ncell;
+         cell += (long long)gridDim.x * blockDim.x) {
+        if (cell_nhome[cell] == 0) continue;
+        const int ixl = (int)(cell / plane), iy = (int)((cell / g.nz) % g.ny), iz = (int)(cell % g.nz);
+        for (int ox = -1; ox <= 1; ++ox) {
+            int jx = ixl + ox;
+            if (g.ghost_x) {
+                if (jx < 0 || jx >= g.nxl) continue;
+            } else {
+                jx = wrap_i(jx, g.nc[0]);
+            }
+            for (int oy = -1; oy <= 1; ++oy)
+                for (int oz = -1; oz <= 1; ++oz)
+                    need[((long long)jx * g.ny + wrap_i(iy + oy, g.ny)) * g.nz + wrap_i(iz + oz, g.nz)] = 1;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
                                                                     long long cbeg, long long cend, int2 *big_items,
                                                                     int *big_count, int *huge_items, int *huge_count,
-                                                                    int huge_cap)
+                                                                    int huge_cap, const int *__restrict__ need)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -53,7 +76,8 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
          base += (long long)gridDim.x * SORT_WARPS * 32) {
         const long long mycell = base + lane;
         const int my_s0 = mycell < cend ? c.cell_start[mycell] : 0;
-        const int my_n = mycell < cend ? c.cell_start[mycell + 1] - my_s0 : 0;
+        int my_n = mycell < cend ? c.cell_start[mycell + 1] - my_s0 : 0;
+        if (need && my_n > 0 && !need[mycell]) my_n = 0;     // lists never read on this level grid
         unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
       while (todo) {
         const int j = __ffs(todo) - 1;

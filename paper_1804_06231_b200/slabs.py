@@ -159,7 +159,7 @@ class SlabRunner:
         self.plane = self.grid.nc[1] * self.grid.nc[2]   # cells per x plane
         self.nxl = (slab.x_hi - slab.x_lo) + (2 if ghost else 0)
         self.launches_per_step = (BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES) * len(self.levels) + \
-            (BUILD_LAUNCHES if ghost else 0)
+            (BUILD_LAUNCHES if ghost else 0) + (len(self.levels) if split else 0)   # k_mark_needed per level
         self.device = device
         # finer level grids (one GPU): own cells and workspace each, same outputs
         self.extra = []
