@@ -300,7 +300,7 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     }
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
         g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap, need);
-    k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count);
+    k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count, need);
     static bool huge_attr = false;
     if (!huge_attr) {
         cudaFuncSetAttribute(k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true>,
@@ -308,9 +308,9 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
         huge_attr = true;
     }
     k_sort_bitonic<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, SORT_MED_MAX * 8, s>>>(
-        g, c, cells->order, huge_items, huge_count, (int)w.huge_cap);
+        g, c, cells->order, huge_items, huge_count, (int)w.huge_cap, need);
     k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, SORT_HUGE_MAX * 8, s>>>(
-        g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap);
+        g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap, need);
     return check_launch();
 }
 

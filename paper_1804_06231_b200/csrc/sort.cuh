@@ -40,8 +40,9 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
     corner[2] = (double)iz * g.cl[2];
 }
 
-// Level passes: a cell's sorted lists are read only if the cell or one of
-// its 26 neighbours holds home particles of this grid; mark those cells.
+// Level passes: the list of cell j along direction d is read only when the
+// neighbour of j at offset +d or -d holds home particles of this grid; need[j] collects those
+// directions as a 13-bit mask.
 __global__ void k_mark_needed(DevGrid g, const int *__restrict__ cell_nhome, int *__restrict__ need)
 {
     const long long plane = (long long)g.ny * g.nz;
@@ -57,8 +58,13 @@ __global__ void k_mark_needed(DevGrid g, const int *__restrict__ cell_nhome, int
                 jx = wrap_i(jx, g.nc[0]);
             }
             for (int oy = -1; oy <= 1; ++oy)
-                for (int oz = -1; oz <= 1; ++oz)
-                    need[((long long)jx * g.ny + wrap_i(iy + oy, g.ny)) * g.nz + wrap_i(iz + oz, g.nz)] = 1;
+                for (int oz = -1; oz <= 1; ++oz) {
+                    if (!(ox | oy | oz)) continue;
+                    int sg;
+                    const int d = canon_dir(ox, oy, oz, sg);
+                    atomicOr(&need[((long long)jx * g.ny + wrap_i(iy + oy, g.ny)) * g.nz + wrap_i(iz + oz, g.nz)],
+                             1 << d);
+                }
         }
     }
 }
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
 // the items are stored from the back of the list (huge tier).
 template <int MAXN, int T, bool FROM_BACK>
 __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint16_t *ord, const int *items,
-                                                   const int *count, int cap)
+                                                   const int *count, int cap, const int *__restrict__ need)
 {
     extern __shared__ unsigned long long hs[];           // MAXN composites
     const int nitems = *count;
@@ -169,7 +175,9 @@ __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint1
         while (P < n) P <<= 1;
         double corner[3];
         cell_corner(g, cell, corner);
+        const int mask = need ? need[cell] : 0x1fff;
         for (int d = 0; d < SPH_NDIR; ++d) {
+            if (!((mask >> d) & 1)) continue;          // CTA-uniform
             for (int e = threadIdx.x; e < P; e += T) {
                 unsigned long long comp = ~0ull;
                 if (e < n) {
@@ -203,7 +211,8 @@ __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint1
 
 // One CTA per (cell, chunk) item; grid-strides over the queued items.
 __global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells c, uint16_t *ord,
-                                                              const int2 *big_items, const int *big_count)
+                                                              const int2 *big_items, const int *big_count,
+                                                              const int *__restrict__ need)
 {
     __shared__ unsigned long long tile[SORT_BIG_TILE];
     const int nitems = *big_count;
@@ -226,7 +235,9 @@ __global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells
             u2 = (double)p.z - corner[2];
             tie = (unsigned)c.perm[s0 + e];
         }
+        const int mask = need ? need[cell] : 0x1fff;
         for (int d = 0; d < SPH_NDIR; ++d) {
+            if (!((mask >> d) & 1)) continue;          // CTA-uniform
             float key = mine ? pv_key(u0, u1, u2, d) : 0.0f;
             unsigned long long comp = ((unsigned long long)float_order(key) << 32) | tie;
             int r = 0;
