@@ -356,45 +356,6 @@ __global__ void __launch_bounds__(API_WARPS * 32) k_density_self(DevGrid g, DevC
     flush_stats<COUNT>(st, cand, hits);
 }
 
-// One CTA (API_WARPS warps) per cell pair (ci <- cj); warps take i in ci.
-template <bool COUNT>
-__global__ void __launch_bounds__(API_WARPS * 32) k_density_pair(DevGrid g, DevCells c, DevOut o, const int2 *pairs,
-                                                                  long long npairs, sph_stats *st, unsigned *status)
-{
-    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
-    for (long long q = blockIdx.x; q < npairs; q += gridDim.x) {
-        int2 pr = pairs[q];
-        long long ci = pr.x, cj = pr.y;
-        if (!owned_cell(g, ci) || cj < 0 || cj >= g.ncell) {
-            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
-            continue;
-        }
-        HomeCell hc = home_cell(g, ci);
-        long long plane = (long long)g.ny * g.nz;
-        int jxl = (int)(cj / plane), jy = (int)((cj / g.nz) % g.ny), jz = (int)(cj % g.nz);
-        int ox = jxl - hc.ixl, oy = jy - hc.iy, oz = jz - hc.iz;
-        if (!g.ghost_x) ox = ox == g.nc[0] - 1 ? -1 : (ox == 1 - g.nc[0] ? 1 : ox);
-        oy = oy == g.ny - 1 ? -1 : (oy == 1 - g.ny ? 1 : oy);
-        oz = oz == g.nz - 1 ? -1 : (oz == 1 - g.nz ? 1 : oz);
-        if (ox < -1 || ox > 1 || oy < -1 || oy > 1 || oz < -1 || oz > 1 || !(ox | oy | oz)) {
-            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
-            continue;
-        }
-        int cjc, sh[3];
-        neighbour(g, hc, ox, oy, oz, cjc, sh);
-        int k = kind_of(ox, oy, oz);
-        int s0 = c.cell_start[ci], s1 = c.cell_start[ci + 1];
-        for (int i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-            IPart p = load_i(g, c, i, hc.corner);
-            Acc a;
-            acc_zero(a);
-            sweep_pair<COUNT>(g, c, p, cjc, ox, oy, oz, sh, a, cand[k], hits[k]);
-            if (a.nngb > 0) atomic_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
-        }
-    }
-    flush_stats<COUNT>(st, cand, hits);
-}
-
 __global__ void k_finalize(DevOut o, long long n)
 {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {

@@ -1,0 +1,217 @@
+// density_pair.cuh -- sph_density_pair: the paper's pair interaction
+// as one CTA per cell pair (ci <- cj), the literal form of the per-pair sweep
+// (kernel K6).
+//
+//  * Staging: the positions and (v, m) of both cells are bulk-copied into shared memory
+//    (cp.async.bulk + mbarrier); cj's list sorted along the pair's direction d is copied as
+//    staged indices.  cj particles beyond a low box face are pre-shifted by -L, ci's home
+//    coordinate by -L where cj lies beyond a high face (exact differences).
+//  * Warps take tiles of 32 ci particles (lane = i).  A lane's window in cj is exact: the
+//    prefix (cj at +d) or suffix (cj at -d) of the sorted list whose projected separation is
+//    below H_i + delta, found by branch-free bisection.
+//  * In-range candidates are pushed on the lane's stack; when __ballot_sync/__popc show that
+//    most lanes hold two, every lane pops two and evaluates both interactions with
+//    FFMA2 (the left-packing of P:185-187).  Register accumulation; the pair's partial sums
+//    are added to the outputs with red.global.add (other pairs update the same ci).
+//  * Cells above PAIR_MAXN particles take the per-thread global-memory sweep of density.cuh.
+#pragma once
+
+#include "common.cuh"
+#include "density.cuh"
+#include "density_v4.cuh"
+#include "packed.cuh"
+
+namespace pvsph {
+
+constexpr int PAIR_WARPS = 4;
+constexpr int PAIR_MAXN = 1024;          // staged particles per cell
+constexpr int PAIR_Q = 16;               // hit stack depth per lane
+constexpr size_t PAIR_SMEM = (size_t)PAIR_MAXN * 16 * 3 + (size_t)PAIR_MAXN * 2 + (size_t)PAIR_WARPS * PAIR_Q * 32 * 2;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(PAIR_WARPS * 32) k_density_pair_staged(DevGrid g, DevCells c, DevOut o,
+                                                                         const int2 *pairs, long long npairs,
+                                                                         sph_stats *st, unsigned *status)
+{
+    extern __shared__ __align__(16) unsigned char pair_smem[];
+    float4 *Pi = reinterpret_cast<float4 *>(pair_smem);          // ci positions
+    float4 *Pj = Pi + PAIR_MAXN;                                   // cj positions
+    float4 *Vj = Pj + PAIR_MAXN;                                   // cj (v, m)
+    uint16_t *Lj = reinterpret_cast<uint16_t *>(Vj + PAIR_MAXN);   // cj sorted along d (staged indices)
+    uint16_t *stacks = Lj + PAIR_MAXN;
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const unsigned mbar = smem_addr(&s_mbar);
+    unsigned phase = 0;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+
+    for (long long q = blockIdx.x; q < npairs; q += gridDim.x) {
+        const int2 pr = pairs[q];
+        const long long ci = pr.x, cj = pr.y;
+        if (!owned_cell(g, ci) || cj < 0 || cj >= g.ncell) {
+            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+            continue;
+        }
+        const HomeCell hc = home_cell(g, ci);
+        const long long plane = (long long)g.ny * g.nz;
+        const int jxl = (int)(cj / plane), jy = (int)((cj / g.nz) % g.ny), jz = (int)(cj % g.nz);
+        int ox = jxl - hc.ixl, oy = jy - hc.iy, oz = jz - hc.iz;
+        if (!g.ghost_x) ox = ox == g.nc[0] - 1 ? -1 : (ox == 1 - g.nc[0] ? 1 : ox);
+        oy = oy == g.ny - 1 ? -1 : (oy == 1 - g.ny ? 1 : oy);
+        oz = oz == g.nz - 1 ? -1 : (oz == 1 - g.nz ? 1 : oz);
+        if (ox < -1 || ox > 1 || oy < -1 || oy > 1 || oz < -1 || oz > 1 || !(ox | oy | oz)) {
+            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+            continue;
+        }
+        int cjc, sh[3];
+        neighbour(g, hc, ox, oy, oz, cjc, sh);
+        const int kind = kind_of(ox, oy, oz);
+        int sgn;
+        const int d = canon_dir(ox, oy, oz, sgn);
+        const int si = c.cell_start[ci], ni = c.cell_start[ci + 1] - si;
+        const int sj = c.cell_start[cjc], nj = c.cell_start[cjc + 1] - sj;
+        if (ni == 0 || nj == 0) continue;
+        if (ni > PAIR_MAXN || nj > PAIR_MAXN) {
+            // dense cells: the per-thread sweep reading global memory
+            for (int i = si + threadIdx.x; i < si + ni; i += blockDim.x) {
+                IPart p = load_i(g, c, i, hc.corner);
+                Acc a;
+                acc_zero(a);
+                sweep_pair<COUNT>(g, c, p, cjc, ox, oy, oz, sh, a, cand[kind], hits[kind]);
+                if (a.nngb > 0) atomic_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
+            }
+            continue;
+        }
+        // ---- staging: bulk copies of both cells, then cj's sorted list ------------------
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(mbar, (unsigned)(ni + 2 * nj) * 16u);
+            bulk_g2s(smem_addr(Pi), c.xyzh + si, (unsigned)ni * 16u, mbar);
+            bulk_g2s(smem_addr(Pj), c.xyzh + sj, (unsigned)nj * 16u, mbar);
+            bulk_g2s(smem_addr(Vj), c.vm + sj, (unsigned)nj * 16u, mbar);
+        }
+        const uint16_t *src = c.ord + (long long)d * c.cap + sj;
+        for (int k = threadIdx.x; k < nj; k += blockDim.x) Lj[k] = src[k];
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+        const float bx = g.boxf[0], by = g.boxf[1], bz = g.boxf[2];
+        if (sh[0] < 0 || sh[1] < 0 || sh[2] < 0) {
+            // cj beyond a low face: x_j - L, exact (x_j >= L/2)
+            for (int k = threadIdx.x; k < nj; k += blockDim.x) {
+                float4 p = Pj[k];
+                p.x -= sh[0] < 0 ? bx : 0.0f;
+                p.y -= sh[1] < 0 ? by : 0.0f;
+                p.z -= sh[2] < 0 ? bz : 0.0f;
+                Pj[k] = p;
+            }
+        }
+        __syncthreads();
+
+        // ---- warps over tiles of 32 ci particles -------------------------------------------
+        const unsigned sP = smem_addr(Pj), sV = smem_addr(Vj), sL = smem_addr(Lj);
+        const unsigned sQ = smem_addr(stacks + wl * PAIR_Q * 32) + 2u * lane;
+        const float c0 = (float)dir_component(d, 0), c1 = (float)dir_component(d, 1), c2 = (float)dir_component(d, 2);
+        const float rk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
+        for (int t0 = wl * 32; t0 < ni; t0 += PAIR_WARPS * 32) {
+            const int e = t0 + lane;
+            const bool active = e < ni;
+            float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, H2 = -1.f, Hinv = 0.f, Hk = 0.f, m = 0.f;
+            if (active) {
+                const float4 a = Pi[e];
+                const float4 b = c.vm[si + e];
+                // home coordinate shifted by -L where cj lies beyond a high face (exact: x_i >= L/2)
+                x = sh[0] > 0 ? a.x - bx : a.x;
+                y = sh[1] > 0 ? a.y - by : a.y;
+                z = sh[2] > 0 ? a.z - bz : a.z;
+                vx = b.x; vy = b.y; vz = b.z; m = b.w;
+                const double H = (double)g.gamma * (double)a.w;
+                H2 = (float)(H * H);
+                Hinv = (float)(1.0 / H);
+                Hk = ((float)H + g.delta) * rk;
+            }
+            // window: sgn > 0 (cj at +d): prefix of the ascending list with (x_j - x_i) . d < Hk;
+            // sgn < 0 (cj at -d): suffix with (x_i - x_j) . d < Hk
+            int top = 1;
+            while (2 * top <= nj) top <<= 1;
+            int lo = 0;
+            for (int stp = top; stp > 0; stp >>= 1) {
+                const int kk = lo + stp;
+                const bool v = active && kk <= nj;
+                const int pos = sgn > 0 ? kk - 1 : nj - kk;
+                const unsigned id = v ? ldsr_u16(sL + 2u * (unsigned)pos) : 0u;
+                const float4 p = ldsr_f4(sP + 16u * id);
+                const float sep = (float)sgn * fmaf(c0, p.x - x, fmaf(c1, p.y - y, c2 * (p.z - z)));
+                if (v && sep < Hk) lo = kk;
+            }
+            const int len = lo, first = sgn > 0 ? 0 : nj - len;
+            Acc2 A;
+            A.rho = A.wc = A.srt = A.st = A.Dn = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
+            unsigned qp = sQ;
+            int nngb = 0;
+            const f2 Hinv2 = bc2(Hinv);
+            auto drain = [&](bool final) {
+                const unsigned n = (qp - sQ) >> 6;
+                if (n >= 2 || (final && n == 1)) {
+                    const bool two = n >= 2;
+                    const unsigned s0 = lds_u16(qp - 64u), s1 = two ? lds_u16(qp - 128u) : s0;
+                    qp -= two ? 128u : 64u;
+                    nngb += two ? 2 : 1;
+                    const float4 p0 = ldsr_f4(sP + 16u * s0), p1 = ldsr_f4(sP + 16u * s1);
+                    const float4 v0 = ldsr_f4(sV + 16u * s0), v1 = ldsr_f4(sV + 16u * s1);
+                    interact_pair<true>(Hinv2, pk(x - p0.x, x - p1.x), pk(y - p0.y, y - p1.y), pk(z - p0.z, z - p1.z),
+                                        pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx), pk(v0.y - vy, v1.y - vy),
+                                        pk(v0.z - vz, v1.z - vz), pk(1.0f, two ? 1.0f : 0.0f), A);
+                }
+            };
+            const int trip = __reduce_max_sync(0xffffffffu, len);
+            for (int t = 0; t < trip; t += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool ok = t + u < len;
+                    const unsigned id = ok ? ldsr_u16(sL + 2u * (unsigned)(first + t + u)) : 0u;
+                    const float4 p = ldsr_f4(sP + 16u * id);
+                    const float dx = x - p.x, dy = y - p.y, dz = z - p.z;
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (COUNT) cand[kind] += ok ? 1u : 0u;
+                    if (ok && r2 < H2) {
+                        sts_u16(qp, id);
+                        qp += 64u;
+                        if (COUNT) ++hits[kind];
+                    }
+                }
+                // left-packing: drain when most lanes hold two hits, or a stack could overflow
+                for (;;) {
+                    const unsigned n = (qp - sQ) >> 6;
+                    if (!(__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 ||
+                          __any_sync(0xffffffffu, n >= PAIR_Q - 4)))
+                        break;
+                    drain(false);
+                }
+            }
+            while (__any_sync(0xffffffffu, qp != sQ)) drain(true);
+            if (active && nngb > 0) {
+                const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;
+                const float gf = K3 * Hinv;
+                Final f;
+                f.rho = K3 * sum2(A.rho);
+                f.wc = K3 * sum2(A.wc);
+                f.rho_dh = -K3 * g.gamma * Hinv * sum2(A.srt);
+                f.wc_dh = -K3 * g.gamma * Hinv * sum2(A.st);
+                f.div = gf * sum2(A.Dn);                   // rho * div v
+                f.cx = gf * (sum2(A.Px) - sum2(A.Nx));     // rho * curl v
+                f.cy = gf * (sum2(A.Py) - sum2(A.Ny));
+                f.cz = gf * (sum2(A.Pz) - sum2(A.Nz));
+                atomic_out(o, c.perm[si + e], f, nngb);
+            }
+            (void)m;
+        }
+        __syncthreads();                          // shared memory reused by the next pair
+    }
+    flush_stats<COUNT>(st, cand, hits);
+}
+
+}  // namespace pvsph

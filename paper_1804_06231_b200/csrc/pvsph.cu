@@ -12,6 +12,7 @@
 #include "common.cuh"
 #include "density.cuh"
 #include "density_v4.cuh"
+#include "density_pair.cuh"
 #include "sort.cuh"
 
 using namespace pvsph;
@@ -346,14 +347,20 @@ int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t
     if (npairs == 0) return SPH_OK;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned *status = at<unsigned>(ws, 0);
-    int blocks = grid_blocks(npairs, 1, 1 << 30);
     const int2 *pr = reinterpret_cast<const int2 *>(pairs);
+    static bool pair_attr = false;
+    if (!pair_attr) {
+        cudaFuncSetAttribute(k_density_pair_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
+        cudaFuncSetAttribute(k_density_pair_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
+        pair_attr = true;
+    }
+    const int blocks = grid_blocks(npairs, 1, 148 * 8);
     if (stats)
-        k_density_pair<true><<<blocks, API_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(acc), pr, npairs, stats,
-                                                               status);
+        k_density_pair_staged<true><<<blocks, PAIR_WARPS * 32, PAIR_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr,
+                                                                            npairs, stats, status);
     else
-        k_density_pair<false><<<blocks, API_WARPS * 32, 0, s>>>(g, dev_cells(cells), dev_out(acc), pr, npairs,
-                                                                nullptr, status);
+        k_density_pair_staged<false><<<blocks, PAIR_WARPS * 32, PAIR_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr,
+                                                                             npairs, nullptr, status);
     return check_launch();
 }
 

@@ -167,10 +167,35 @@ def test_worked_example(pv):
             assert list(got["nngb"]) == g["expected"]["nngb"]
 
 
-def test_self_plus_pairs_equals_all(pv):
+def _dense_cell_set(occ, seed=5):
+    """nc = 4 with one cell of `occ` particles plus 200 background particles."""
+    rng = np.random.default_rng(seed)
+    nc, Cl, n_bg = 4, 0.25, 200
+    xyzh = np.zeros((n_bg + occ, 4), np.float32)
+    xyzh[:n_bg, :3] = rng.integers(0, 2 ** 24, size=(n_bg, 3)) / 2 ** 24
+    xyzh[n_bg:, :3] = np.floor((1 + rng.random((occ, 3))) * Cl * 2 ** 24) / 2 ** 24
+    xyzh[:, 3] = (0.9 * Cl / synth.GAMMA) * (1 - 0.5 * rng.random(n_bg + occ))
+    vm = np.zeros_like(xyzh)
+    vm[:, :3] = rng.standard_normal((n_bg + occ, 3))
+    vm[:, 3] = 1.0 / (n_bg + occ)
+    return xyzh, vm, nc
+
+
+@pytest.mark.parametrize("case", ["c1", "dense1500"])
+def test_self_plus_pairs_equals_all(pv, case):
     """sph_density_self over every cell + sph_density_pair over all 26 ordered pairs
-    (+ finalize) reproduces sph_density_all within tolerance (P:167 symmetric = 2 one-sided)."""
-    p = synth.make("c1")
+    (+ finalize) reproduces sph_density_all within tolerance (P:167 symmetric = 2 one-sided).
+    dense1500: a cell above the pair kernel's staging capacity (global-memory fallback)."""
+    if case == "c1":
+        p = synth.make("c1")
+        px, pvm, nc = p.xyzh, p.vm, p.nc
+    else:
+        px, pvm, nc = _dense_cell_set(1500)
+
+    class _P:
+        pass
+    p = _P()
+    p.xyzh, p.vm, p.nc, p.n = px, pvm, nc, px.shape[0]
     xyzh = torch.from_numpy(p.xyzh).cuda()
     vm = torch.from_numpy(p.vm).cuda()
     dp = pv.DensityPass(p.nc, p.n)
