@@ -119,7 +119,11 @@ typedef struct sph_grid {
  *                           cell_nhome[c] slots of the cell (written by build)
  *   order[SPH_NDIR * capacity] sorted lists (uint16 in-cell indices):
  *                           direction d, cell c at
- *                           order[d * capacity + cell_start[c] ...]
+ *                           order[d * capacity + cell_start[c] ...];
+ *                           16-byte aligned, readable up to the next 16-byte
+ *                           boundary past its end (the density kernel reads
+ *                           it in aligned 16-byte words; cudaMalloc
+ *                           allocations satisfy this)
  * n is written by sph_build_cells (stored particles).  16-byte alignment
  * is required for xyzh and vm. */
 typedef struct sph_cells {

@@ -976,21 +976,33 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                 PH_ADD(6, tpv0);
                 PH_T0(tl0)
                 // list segments, strided over the threads (balanced): the sorted list reversed,
-                // entries turned into staged indices; 16 independent loads in flight
+                // entries turned into staged indices
                 for (int gseg = threadIdx.x; gseg < nseg; gseg += V4_TP) {
                     const int h = gseg / 26, k = gseg % 26, d = k >> 1, sg = (k & 1) ? -1 : 1;
                     const int r = h / T.nzh, q = h % T.nzh + 1;
                     const int4 e = tab[((sg * dir_component(d, 0) + 1) * 4 + sg * dir_component(d, 1) + r + 1) * T.nzs + q +
                                        sg * dir_component(d, 2)];
-                    const int dst = segoff[gseg];
+                    const int dst = segoff[gseg] + e.y - 1;
+                    // aligned 16-byte words over the segment: an eighth of the L1 wavefronts of
+                    // 2-byte loads (each lane of a warp reads a different segment)
                     const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
-                    for (int k0 = 0; k0 < e.y; k0 += 16) {
-                        unsigned v[16];
+                    const int mis = (int)(((uintptr_t)src >> 1) & 7);
+                    const uint4 *wsrc = reinterpret_cast<const uint4 *>(src - mis);
+                    const int nw = (mis + e.y + 7) >> 3;
+                    for (int w0 = 0; w0 < nw; w0 += 4) {
+                        uint4 v[4];
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) v[u] = k0 + u < e.y ? (unsigned)__ldg(src + k0 + u) : 0u;
+                        for (int u = 0; u < 4; ++u) v[u] = w0 + u < nw ? __ldg(wsrc + w0 + u) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-                        for (int u = 0; u < 16; ++u)
-                            if (k0 + u < e.y) L[dst + e.y - 1 - (k0 + u)] = (uint16_t)(e.x + (int)v[u]);
+                        for (int u = 0; u < 4; ++u) {
+                            const int k = 8 * (w0 + u) - mis;       // list index of the word's first entry
+                            const unsigned wd[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) {
+                                const unsigned q = (t & 1) ? wd[t >> 1] >> 16 : wd[t >> 1] & 0xffffu;
+                                if (k + t >= 0 && k + t < e.y) L[dst - k - t] = (uint16_t)(e.x + (int)q);
+                            }
+                        }
                     }
                 }
                 PH_ADD(7, tl0);
