@@ -627,7 +627,7 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
     // candidates t .. t+3 of two consecutive windows (directions d0, d0 + 1 of a pair):
     // L[lb0 ...] for the first tot0, then L[lb1 ...]
     auto step4pair = [&](int t, unsigned lb0, int tot0, int len00, unsigned fl00, unsigned fl10, int kind0,
-                         unsigned lb1, int tot1, int len01, unsigned fl01, unsigned fl11, int kind1) {
+                         unsigned lb1m, int tot1, int len01, unsigned fl01, unsigned fl11, int kind1) {
         bool ok[4], in0[4];
         unsigned sj[4];
         float4 p[4];
@@ -636,7 +636,8 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
             const int tt = t + u;
             in0[u] = tt < tot0;
             ok[u] = tt < tot0 + tot1;
-            const unsigned e = ldsr_u16(in0[u] ? lb0 + 2u * (unsigned)tt : lb1 + 2u * (unsigned)(tt - tot0));
+            // lb1 - 2 tot0 precomputed: select the base, add 2 tt (2 u folds into the address)
+            const unsigned e = ldsr_u16((in0[u] ? lb0 : lb1m) + 2u * (unsigned)t + 2u * (unsigned)u);
             sj[u] = ok[u] ? e : 0u;
         }
 #pragma unroll
@@ -666,9 +667,14 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
     {
         const int total = active ? eh.y : 0;
         const int trip = __reduce_max_sync(0xffffffffu, total);
-        for (int t = 0; t < trip; t += 8) {
+        int t = 0;
+        for (; t + 4 < trip; t += 8) {
             step4(std::true_type{}, 0u, eh.x, t, total, total, 0u, 0u, 0);
             step4(std::true_type{}, 0u, eh.x, t + 4, total, total, 0u, 0u, 0);
+            drain_check();
+        }
+        if (t < trip) {
+            step4(std::true_type{}, 0u, eh.x, t, total, total, 0u, 0u, 0);
             drain_check();
         }
     }
@@ -736,13 +742,19 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
         // one sweep over both directions' windows (one trip count for the pair)
         const int kind0 = v4_kind(d0), kind1 = nd == 2 ? v4_kind(d0 + 1) : 0;
         const int trip = __reduce_max_sync(0xffffffffu, totv[0] + totv[1]);
-        const unsigned lb0 = S.L + 2u * (unsigned)wbv[0], lb1 = S.L + 2u * (unsigned)wbv[1];
+        const unsigned lb0 = S.L + 2u * (unsigned)wbv[0], lb1m = S.L + 2u * (unsigned)(wbv[1] - totv[0]);
         PH_T0(tw0)
-        for (int t = 0; t < trip; t += 8) {
-            step4pair(t, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1, totv[1], len0v[1], fl0v[1], fl1v[1],
+        int t = 0;
+        for (; t + 4 < trip; t += 8) {
+            step4pair(t, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1m, totv[1], len0v[1], fl0v[1], fl1v[1],
                       kind1);
-            step4pair(t + 4, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1, totv[1], len0v[1], fl0v[1],
+            step4pair(t + 4, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1m, totv[1], len0v[1], fl0v[1],
                       fl1v[1], kind1);
+            drain_check();
+        }
+        if (t < trip) {                                   // a tail of <= 4 candidates
+            step4pair(t, lb0, totv[0], len0v[0], fl0v[0], fl1v[0], kind0, lb1m, totv[1], len0v[1], fl0v[1], fl1v[1],
+                      kind1);
             drain_check();
         }
         PH_ADD(2, tw0);
