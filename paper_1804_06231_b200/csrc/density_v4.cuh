@@ -62,63 +62,48 @@ constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size
 static_assert(V4_ML % 8 == 0 && (V4_WARPS * V4_Q * 32 * 2) % 16 == 0, "16-byte aligned shared arrays");
 
 
-// Results of one particle in slot (cell) order: rho, wcount, rho_dh, wcount_dh, div_v,
-// curl_v (3), nngb (int bits), padding.  48 bytes = two 32-byte sectors, so the final
-// input-order gather (k_unpermute) reads two sectors per particle instead of the nine
-// read-modify-write sectors of scattered 4-byte stores.
-struct alignas(16) OutRec {
-    float4 a, b, c;
+// Results of one particle at its INPUT index: rho, wcount, rho_dh, wcount_dh, div_v, curl_v (3)
+// in the first 32-byte sector, nngb (int bits) in the second.  Each sector is written whole by
+// one 256-bit store (no read-modify-write), scattered while the compute-bound density kernel
+// runs; the input-order transpose (k_unpermute) then reads the records sequentially instead of
+// gathering them at random slots.
+struct alignas(32) OutRec {
+    float4 a, b, c, d;
 };
 
-__device__ __forceinline__ void store_rec(OutRec *orec, int slot, float rho, float wc, float rho_dh, float wc_dh,
+__device__ __forceinline__ void store_rec(OutRec *orec, int idx, float rho, float wc, float rho_dh, float wc_dh,
                                           float div, float cx, float cy, float cz, int nngb)
 {
-    float4 *q = reinterpret_cast<float4 *>(orec + slot);
-    q[0] = make_float4(rho, wc, rho_dh, wc_dh);
-    q[1] = make_float4(div, cx, cy, cz);
-    q[2] = make_float4(__int_as_float(nngb), 0.0f, 0.0f, 0.0f);
+    // evict-first: the scattered records must not push the staged neighbourhoods out of L2
+    asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orec + idx), "f"(rho),
+                 "f"(wc), "f"(rho_dh), "f"(wc_dh), "f"(div), "f"(cx), "f"(cy), "f"(cz)
+                 : "memory");
+    asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %2, %2, %2, %2, %2, %2};" ::"l"(&orec[idx].c), "r"(nngb),
+                 "r"(0)
+                 : "memory");
 }
 
-// out[p] = record of slot_of[p] for the first n_out input indices (coalesced writes,
-// one 48-byte gather per particle; UNPERM_ILP independent gathers in flight per thread).
-constexpr int UNPERM_ILP = 4;
-
+// out[p] = record p for the first n_out input indices that are home on this grid
+// (slot_of[p] >= 0): sequential 64-byte reads, coalesced SoA writes.
 __global__ void __launch_bounds__(256) k_unpermute(DevOut o, const int *__restrict__ slot_of,
                                                     const OutRec *__restrict__ orec)
 {
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long p0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; p0 < o.n_out;
-         p0 += stride * UNPERM_ILP) {
-        float4 a[UNPERM_ILP], b[UNPERM_ILP], c[UNPERM_ILP];
-        int sl[UNPERM_ILP];
-#pragma unroll
-        for (int u = 0; u < UNPERM_ILP; ++u) {
-            const long long p = p0 + u * stride;
-            sl[u] = p < o.n_out ? __ldcs(slot_of + p) : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < UNPERM_ILP; ++u) {
-            if (sl[u] >= 0) {            // < 0: input rejected by sph_build_cells (status word set)
-                const float4 *q = reinterpret_cast<const float4 *>(orec + sl[u]);
-                a[u] = __ldcs(q);
-                b[u] = __ldcs(q + 1);
-                c[u] = __ldcs(q + 2);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < UNPERM_ILP; ++u) {
-            const long long p = p0 + u * stride;
-            if (sl[u] < 0) continue;
-            __stcs(o.rho + p, a[u].x);
-            __stcs(o.wcount + p, a[u].y);
-            __stcs(o.rho_dh + p, a[u].z);
-            __stcs(o.wcount_dh + p, a[u].w);
-            __stcs(o.div_v + p, b[u].x);
-            __stcs(o.curl_v + p, b[u].y);
-            __stcs(o.curl_v + o.n_out + p, b[u].z);
-            __stcs(o.curl_v + 2 * o.n_out + p, b[u].w);
-            __stcs(o.nngb + p, __float_as_int(c[u].x));
-        }
+    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < o.n_out; p += stride) {
+        const int sl = __ldcs(slot_of + p);
+        if (sl < 0) continue;            // rejected input (status word set) or not home on this grid
+        const float4 *q = reinterpret_cast<const float4 *>(orec + p);
+        const float4 a = __ldcs(q), b = __ldcs(q + 1);
+        const int nngb = __ldcs(reinterpret_cast<const int *>(q + 2));
+        __stcs(o.rho + p, a.x);
+        __stcs(o.wcount + p, a.y);
+        __stcs(o.rho_dh + p, a.z);
+        __stcs(o.wcount_dh + p, a.w);
+        __stcs(o.div_v + p, b.x);
+        __stcs(o.curl_v + p, b.y);
+        __stcs(o.curl_v + o.n_out + p, b.z);
+        __stcs(o.curl_v + 2 * o.n_out + p, b.w);
+        __stcs(o.nngb + p, nngb);
     }
 }
 
@@ -342,7 +327,7 @@ __device__ __forceinline__ void v4_particle_global(const DevGrid &g, const DevCe
             }
     Final f = finalise(g, p, a, true);
     const float rinv = 1.0f / f.rho;
-    store_rec(orec, i, f.rho, f.wc, f.rho_dh, f.wc_dh, f.div * rinv, f.cx * rinv, f.cy * rinv, f.cz * rinv, a.nngb);
+    store_rec(orec, c.perm[i], f.rho, f.wc, f.rho_dh, f.wc_dh, f.div * rinv, f.cx * rinv, f.cy * rinv, f.cz * rinv, a.nngb);
 }
 
 // Packed accumulators; D and curl use v_j - v_i (= -v_ij) so the cross products
@@ -773,7 +758,7 @@ __device__ __forceinline__ void v4_particle_staged(const DevGrid &g, const DevCe
         const float wc_dh = dh * (1.5f + sum2(A.st));
         const float gf = K3 * Hinv;
         const float rinv = 1.0f / rho;
-        store_rec(orec, i, rho, wc, rho_dh, wc_dh, gf * sum2(A.Dn) * rinv, gf * (sum2(A.Px) - sum2(A.Nx)) * rinv,
+        store_rec(orec, c.perm[i], rho, wc, rho_dh, wc_dh, gf * sum2(A.Dn) * rinv, gf * (sum2(A.Px) - sum2(A.Nx)) * rinv,
                   gf * (sum2(A.Py) - sum2(A.Ny)) * rinv, gf * (sum2(A.Pz) - sum2(A.Nz)) * rinv, nngb);
     }
 }

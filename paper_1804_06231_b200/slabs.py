@@ -220,36 +220,66 @@ class SlabRunner:
 
     # -- end to end through host buffers -----------------------------------
     def e2e_time(self, steps: int = 3, warmup: int = 1):
-        """ms per step with the H2D copy of the owned inputs (pinned) and the D2H copy of all
-        outputs inside the timed region; returns (ms, h2d_bytes, d2h_bytes)."""
+        """ms per step through host buffers: every step copies its owned inputs from pinned
+        host memory (H2D) and all its outputs back (D2H) inside the timed region.  Steps are
+        pipelined over three streams with double-buffered device inputs and outputs: the H2D
+        of step k+1 and the D2H of step k-1 run on the copy engines while step k computes,
+        as a serving loop would.  Returns (ms, h2d_bytes, d2h_bytes)."""
         n = self.n_own
         hx = torch.from_numpy(self.slab.xyzh).pin_memory()
         hv = torch.from_numpy(self.slab.vm).pin_memory()
-        o = self.out
-        outs = [o.rho, o.rho_dh, o.wcount, o.wcount_dh, o.div_v, o.curl_v, o.nngb]
-        host = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+        names = ["rho", "rho_dh", "wcount", "wcount_dh", "div_v", "curl_v", "nngb"]
+        bufs = [(self.xin, self.vin, self.out),
+                (torch.zeros_like(self.xin), torch.zeros_like(self.vin), pv.Out.alloc(self.n_own, self.device))]
+        host = [[torch.empty(getattr(o, k).shape, dtype=getattr(o, k).dtype, pin_memory=True) for k in names]
+                for _, _, o in bufs]
+        s_c = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = lambda: torch.cuda.Event()                      # noqa: E731
+        in_ready, c_done, out_free = [ev(), ev()], [ev(), ev()], [ev(), ev()]
+        for b in range(2):                                  # both buffer sets free at the start
+            c_done[b].record(s_c)
+            out_free[b].record(s_c)
+        saved = (self.xin, self.vin, self.out)
 
-        def one():
-            self.xin[:n].copy_(hx, non_blocking=True)
-            self.vin[:n].copy_(hv, non_blocking=True)
+        def one(k):
+            b = k % 2
+            xin, vin, out = bufs[b]
+            with torch.cuda.stream(s_in):                   # inputs of step k (buffer free once step k-2 ran)
+                s_in.wait_event(c_done[b])
+                xin[:n].copy_(hx, non_blocking=True)
+                vin[:n].copy_(hv, non_blocking=True)
+                in_ready[b].record(s_in)
+            s_c.wait_event(in_ready[b])
+            s_c.wait_event(out_free[b])                     # outputs of step k-2 copied out
+            self.xin, self.vin, self.out = xin, vin, out
             self.step()
-            for h, t in zip(host, outs):
-                h.copy_(t, non_blocking=True)
+            c_done[b].record(s_c)
+            with torch.cuda.stream(s_out):                  # results of step k
+                s_out.wait_event(c_done[b])
+                for h, key in zip(host[b], names):
+                    h.copy_(getattr(out, key), non_blocking=True)
+                out_free[b].record(s_out)
 
-        for _ in range(warmup):
-            one()
-        torch.cuda.synchronize()
-        if self.dist:
-            self.dist.barrier()
-        s = torch.cuda.current_stream()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for _ in range(steps):
-            one()
-        e1.record(s)
-        torch.cuda.synchronize()
+        try:
+            for k in range(warmup):
+                one(k)
+            torch.cuda.synchronize()
+            if self.dist:
+                self.dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s_c)
+            for k in range(warmup, warmup + steps):
+                one(k)
+            s_c.wait_event(out_free[(warmup + steps - 1) % 2])   # the last results are on the host
+            s_c.wait_event(out_free[(warmup + steps - 2) % 2])
+            e1.record(s_c)
+            torch.cuda.synchronize()
+        finally:
+            self.xin, self.vin, self.out = saved
+        self.e2e_host = dict(zip(names, host[(warmup + steps - 1) % 2]))   # the last step's results
         h2d = 2 * n * 16
-        d2h = sum(t.numel() * t.element_size() for t in outs)
+        d2h = sum(getattr(self.out, k).numel() * getattr(self.out, k).element_size() for k in names)
         return e0.elapsed_time(e1) / steps, h2d, d2h
 
 

@@ -47,3 +47,20 @@ def test_slab_boundary_particles_vs_oracle(pv):
     idx = np.nonzero(np.isin(pl, sorted(edges)))[0]
     idx = idx[:: max(1, idx.size // 50000)]
     compare(got, oracle.celllist(p.xyzh, p.vm, p.nc, targets=idx), idx, "slab boundaries")
+
+
+def test_e2e_pipeline_results(pv):
+    """The pipelined host-buffer path (bench.py's e2e leg: double-buffered inputs/outputs,
+    copies on their own streams) returns exactly the device pass's results."""
+    from paper_1804_06231_b200.slabs import Slab, SlabRunner
+    p = synth.make("c2")
+    single = pv.density(p.xyzh, p.vm, p.nc)
+    r = SlabRunner(Slab.from_set(p, 0, 1))
+    r.upload()
+    ms, h2d, d2h = r.e2e_time(steps=3, warmup=1)
+    assert ms > 0 and h2d == 32 * p.n and d2h == 36 * p.n
+    got = {k: v.numpy() for k, v in r.e2e_host.items()}
+    for f in ("rho", "rho_dh", "wcount", "wcount_dh", "div_v", "nngb"):
+        assert np.array_equal(single[f], got[f]), f
+    for k, ax in enumerate("xyz"):
+        assert np.array_equal(single["curl_" + ax], got["curl_v"][k]), ax
