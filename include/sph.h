@@ -32,6 +32,10 @@
  *     outputs, workspace).  The library allocates nothing and keeps no
  *     global mutable state; calls on different streams with disjoint
  *     outputs and workspaces may run concurrently.
+ *   - The workspace (sph_workspace_bytes) is zero-filled by the caller once
+ *     after allocation; afterwards the calls own its contents (it carries
+ *     the status word and a sph_density_all call counter that tags output
+ *     records, so one workspace serves one grid at a time).
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream).
  *     Calls are asynchronous: argument errors are returned at once,
  *     data-dependent errors set the device status word in the workspace,
@@ -53,7 +57,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 2
+#define SPH_ABI_VERSION 3
 
 #define SPH_OK 0
 #define SPH_EINVAL 1
@@ -111,10 +115,6 @@ typedef struct sph_grid {
  *   perm[capacity]          slot -> input index
  *   cell_hmax[ncell]        max h in each cell
  *   slot_cell[capacity]     local cell of each slot (written by build)
- *   slot_of[capacity]       slot of each input index (written by build; the
- *                           inverse of perm, used to return outputs in input
- *                           order with a coalesced gather); -1 for an input
- *                           that is rejected or not home on this grid
  *   cell_nhome[ncell]       home particles of each cell; they occupy the first
  *                           cell_nhome[c] slots of the cell (written by build)
  *   order[SPH_NDIR * capacity] sorted lists (uint16 in-cell indices):
@@ -136,7 +136,6 @@ typedef struct sph_cells {
     float *cell_hmax;
     uint16_t *order;
     int32_t *slot_cell;
-    int32_t *slot_of;
     int32_t *cell_nhome;
 } sph_cells;
 
@@ -163,7 +162,7 @@ int64_t sph_ncell(const sph_grid *grid);
 size_t sph_workspace_bytes(const sph_grid *grid, int64_t n_total);
 
 /* Bin particles into cells and write the cell-sorted SoA
- * arrays, perm, cell_start, cell_hmax, cell_nhome, slot_of and cells->n =
+ * arrays, perm, cell_start, cell_hmax, cell_nhome and cells->n =
  * n_own + n_ghost.  Within a cell, home particles come first, each group in
  * input order.
  * Inputs xyzh_in/vm_in hold n_own owned particles followed by n_ghost

@@ -29,7 +29,7 @@ class SphGrid(ctypes.Structure):
 
 class SphCells(ctypes.Structure):
     _fields_ = [("capacity", c_i64), ("n", c_i64), ("cell_start", c_vp), ("xyzh", c_vp), ("vm", c_vp),
-                ("perm", c_vp), ("cell_hmax", c_vp), ("order", c_vp), ("slot_cell", c_vp), ("slot_of", c_vp),
+                ("perm", c_vp), ("cell_hmax", c_vp), ("order", c_vp), ("slot_cell", c_vp),
                 ("cell_nhome", c_vp)]
 
 

@@ -83,7 +83,6 @@ class Cells:
     cell_hmax: torch.Tensor
     order: torch.Tensor         # (13, capacity) int16 storage of the uint16 sorted lists (include/sph.h)
     slot_cell: torch.Tensor     # (capacity,) int32
-    slot_of: torch.Tensor       # (capacity,) int32: slot of each input index
     cell_nhome: torch.Tensor    # (ncell,) int32: home particles per cell
     n: int = 0
 
@@ -98,7 +97,6 @@ class Cells:
                      torch.empty(nce, dtype=torch.float32, device=device),
                      torch.empty((_lib.SPH_NDIR, cap), dtype=torch.int16, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device),
-                     torch.empty(cap, dtype=torch.int32, device=device),
                      torch.empty(nce, dtype=torch.int32, device=device))
 
     def struct(self) -> SphCells:
@@ -108,7 +106,6 @@ class Cells:
         s.cell_start, s.xyzh, s.vm = self.cell_start.data_ptr(), self.xyzh.data_ptr(), self.vm.data_ptr()
         s.perm, s.cell_hmax, s.order = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.order.data_ptr()
         s.slot_cell = self.slot_cell.data_ptr()
-        s.slot_of = self.slot_of.data_ptr()
         s.cell_nhome = self.cell_nhome.data_ptr()
         return s
 

@@ -7,15 +7,13 @@
 //                    sectors per particle: no read-modify-write at random slots)
 //   k_stable_*     : per cell, sort the records by input index (the atomic ranks
 //                    arrive in any order) -> xyzh, vm, perm, slot_cell with the
-//                    in-cell order = input order, all reads/writes coalesced;
-//                    fin[scatter slot] = final slot
-//   k_slot_of      : slot_of[input] = fin[scatter slot] (gather, coalesced writes)
+//                    in-cell order = input order, all reads/writes coalesced
 //
 // Stable in-cell order makes everything downstream deterministic and, with
 // slab ghosts received in the sender's cell order, identical across GPU
 // counts.  HBM traffic per particle ~ 32 (read) + 8
 // (cell/rank) + 40 (re-read) + 64 (scattered 64-byte record: two full sectors) +
-// 64 (stable read) + 44 (write) + slot_of gather ~ 300 B (random-access granularity).
+// 64 (stable read) + 40 (write) ~ 250 B (random-access granularity).
 #pragma once
 
 #include "common.cuh"
@@ -160,17 +158,15 @@ struct alignas(64) ParticleRec {
     int idx, pad[7];
 };
 
-__global__ void k_scatter_rec(DevGrid g, long long n_total, const int *__restrict__ cell_of, int *__restrict__ rank,
+__global__ void k_scatter_rec(DevGrid g, long long n_total, const int *__restrict__ cell_of, const int *__restrict__ rank,
                               const int *__restrict__ start, const float4 *__restrict__ xyzh_in,
                               const float4 *__restrict__ vm_in, ParticleRec *__restrict__ rec)
 {
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
          p += (long long)gridDim.x * blockDim.x) {
         const int c = __ldcs(cell_of + p);
-        if (c < 0) rank[p] = -1;                 // rejected input: no slot
-        if (c >= 0) {
-            const int slot = start[c] + rank[p];
-            rank[p] = slot;                      // the scatter slot, for slot_of (k_slot_of)
+        if (c >= 0) {                            // c < 0: rejected input, no slot
+            const int slot = start[c] + __ldcs(rank + p);
             const float4 a = __ldcs(xyzh_in + p), b = __ldcs(vm_in + p);
             // one 256-bit store (STG.256): the whole 32-byte sector at once, no read-modify-write
             // (evict-first: the scattered stream must not push cell_start out of L2)
@@ -196,35 +192,20 @@ constexpr int STABLE_BIG_TILE = 4096;
 // (cell, chunk).  slot_cell is written for every slot.
 __device__ __forceinline__ void stable_place(int s0, int e, int r, const ParticleRec *__restrict__ rec,
                                              float4 *__restrict__ xyzh,
-                                             float4 *__restrict__ vm, int *__restrict__ perm,
-                                             int *__restrict__ fin)
+                                             float4 *__restrict__ vm, int *__restrict__ perm)
 {
     const float4 qx = rec[s0 + e].xyzh, qv = rec[s0 + e].vm;
     const unsigned key = (unsigned)rec[s0 + e].idx;
     xyzh[s0 + r] = qx;
     vm[s0 + r] = qv;
     perm[s0 + r] = (int)(key & 0x7fffffffu);
-    fin[s0 + e] = (s0 + r) | (int)(key & 0x80000000u);   // scatter slot -> final slot (coalesced); sign: not home
-}
-
-// slot_of[p] = final slot of input p: fin[scatter slot] (a gathered read instead of a
-// scattered read-modify-write store per particle).
-__global__ void k_slot_of(long long n_total, const int *__restrict__ scat, const int *__restrict__ fin,
-                          int *__restrict__ slot_of)
-{
-    for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
-         p += (long long)gridDim.x * blockDim.x) {
-        const int t = __ldcs(scat + p);
-        const int f = t >= 0 ? fin[t] : -1;
-        slot_of[p] = f >= 0 ? f : -1;           // rejected or not home on this grid
-    }
 }
 
 __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
                                                                     const ParticleRec *__restrict__ rec,
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
-                                                                    int *__restrict__ fin, int *__restrict__ cell_nhome,
+                                                                    int *__restrict__ cell_nhome,
                                                                     int2 *big_items, int *big_count)
 {
     __shared__ unsigned sh[STABLE_WARPS][STABLE_SMALL];
@@ -273,7 +254,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             if (e < n) {
                 int r = 0;
                 for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
-                stable_place(s0, e, r, rec, xyzh, vm, perm, fin);
+                stable_place(s0, e, r, rec, xyzh, vm, perm);
             }
         }
         __syncwarp();
@@ -284,7 +265,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
 __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__restrict__ start,
                                                                   const ParticleRec *__restrict__ rec,
                                                                   float4 *__restrict__ xyzh, float4 *__restrict__ vm,
-                                                                  int *__restrict__ perm, int *__restrict__ fin,
+                                                                  int *__restrict__ perm,
                                                                   const int2 *big_items, const int *big_count)
 {
     __shared__ unsigned tile[STABLE_BIG_TILE];
@@ -305,7 +286,7 @@ __global__ void __launch_bounds__(STABLE_BIG_CHUNK) k_stable_big(const int *__re
             if (mine)
                 for (int m = 0; m < tn; ++m) r += tile[m] < v;
         }
-        if (mine) stable_place(s0, e, r, rec, xyzh, vm, perm, fin);
+        if (mine) stable_place(s0, e, r, rec, xyzh, vm, perm);
         __syncthreads();
     }
 }

@@ -43,7 +43,6 @@ struct DevCells {
     const float *cell_hmax;
     const uint16_t *ord;    // sorted lists (include/sph.h), [SPH_NDIR][cap]
     const int *slot_cell;
-    const int *slot_of;
     const int *cell_nhome;
 };
 

@@ -63,13 +63,18 @@ static_assert(V4_ML % 8 == 0 && (V4_WARPS * V4_Q * 32 * 2) % 16 == 0, "16-byte a
 
 
 // Results of one particle at its INPUT index: rho, wcount, rho_dh, wcount_dh, div_v, curl_v (3)
-// in the first 32-byte sector, nngb (int bits) in the second.  Each sector is written whole by
-// one 256-bit store (no read-modify-write), scattered while the compute-bound density kernel
-// runs; the input-order transpose (k_unpermute) then reads the records sequentially instead of
-// gathering them at random slots.
+// in the first 32-byte sector; nngb, the input index and the call's generation (tag) in the
+// second.  Each sector is written whole by one 256-bit store (no read-modify-write), scattered
+// while the compute-bound density kernel runs; the input-order transpose (k_unpermute) then
+// reads the records sequentially and keeps those tagged by this call (home particles).
 struct alignas(32) OutRec {
-    float4 a, b, c, d;
+    float4 a, b;
+    int nngb, idx;
+    unsigned gen, pad[5];
 };
+
+// generation of the running sph_density_all call (ws word, bumped by k_v4_tiles<false>)
+__shared__ unsigned s_gen;
 
 __device__ __forceinline__ void store_rec(OutRec *orec, int idx, float rho, float wc, float rho_dh, float wc_dh,
                                           float div, float cx, float cy, float cz, int nngb)
@@ -78,23 +83,23 @@ __device__ __forceinline__ void store_rec(OutRec *orec, int idx, float rho, floa
     asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(orec + idx), "f"(rho),
                  "f"(wc), "f"(rho_dh), "f"(wc_dh), "f"(div), "f"(cx), "f"(cy), "f"(cz)
                  : "memory");
-    asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %2, %2, %2, %2, %2, %2};" ::"l"(&orec[idx].c), "r"(nngb),
-                 "r"(0)
+    asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %4, %4, %4, %4};" ::"l"(&orec[idx].nngb), "r"(nngb),
+                 "r"(idx), "r"(s_gen), "r"(0)
                  : "memory");
 }
 
-// out[p] = record p for the first n_out input indices that are home on this grid
-// (slot_of[p] >= 0): sequential 64-byte reads, coalesced SoA writes.
-__global__ void __launch_bounds__(256) k_unpermute(DevOut o, const int *__restrict__ slot_of,
-                                                    const OutRec *__restrict__ orec)
+// out[p] = record p for the first n_out input indices whose record this call wrote (home on
+// this grid, not rejected): sequential 64-byte reads, coalesced SoA writes.
+__global__ void __launch_bounds__(256) k_unpermute(DevOut o, const OutRec *__restrict__ orec,
+                                                    const unsigned *__restrict__ genp)
 {
+    const unsigned gen = *genp;
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < o.n_out; p += stride) {
-        const int sl = __ldcs(slot_of + p);
-        if (sl < 0) continue;            // rejected input (status word set) or not home on this grid
         const float4 *q = reinterpret_cast<const float4 *>(orec + p);
+        const int4 t = __ldcs(reinterpret_cast<const int4 *>(q + 2));   // nngb, idx, gen, -
+        if (t.y != (int)p || (unsigned)t.z != gen) continue;            // not written by this call
         const float4 a = __ldcs(q), b = __ldcs(q + 1);
-        const int nngb = __ldcs(reinterpret_cast<const int *>(q + 2));
         __stcs(o.rho + p, a.x);
         __stcs(o.wcount + p, a.y);
         __stcs(o.rho_dh + p, a.z);
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(256) k_unpermute(DevOut o, const int *__restri
         __stcs(o.curl_v + p, b.y);
         __stcs(o.curl_v + o.n_out + p, b.z);
         __stcs(o.curl_v + 2 * o.n_out + p, b.w);
-        __stcs(o.nngb + p, nngb);
+        __stcs(o.nngb + p, t.x);
     }
 }
 
@@ -204,8 +209,10 @@ __device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__
 // The cut depends only on the row pair's own counts (identical on any GPU count).
 template <bool WRITE>
 __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, const int *__restrict__ nhome,
-                           int *__restrict__ off, int4 *tiles, long long tile_cap, unsigned *status)
+                           int *__restrict__ off, int4 *tiles, long long tile_cap, unsigned *status, unsigned *gen)
 {
+    // the counting launch opens a new sph_density_all call: its records carry the new tag
+    if (!WRITE && blockIdx.x == 0 && threadIdx.x == 0) *gen += 1u;
     const RowPairs r = row_pairs(g);
     for (long long key = blockIdx.x * (long long)blockDim.x + threadIdx.x; key < r.nkeys;
          key += (long long)gridDim.x * blockDim.x) {
@@ -807,7 +814,8 @@ __device__ __forceinline__ long long staged_cell(const DevGrid &g, const TileGeo
 template <bool COUNT>
 __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCells c, OutRec *orec, sph_stats *st,
                                                          const int4 *__restrict__ tiles,
-                                                         const int *__restrict__ ntiles_p, int *tile_counter)
+                                                         const int *__restrict__ ntiles_p, int *tile_counter,
+                                                         const unsigned *__restrict__ genp)
 {
     extern __shared__ __align__(16) unsigned char v4_smem[];
     float4 *P = reinterpret_cast<float4 *>(v4_smem);
@@ -851,6 +859,7 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
     if (threadIdx.x == 0) {
         const int t0 = atomicAdd(tile_counter, 1);
         s_next = t0 < ntiles ? tiles[t0] : kEnd;
+        s_gen = *genp;
         mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }

@@ -83,7 +83,7 @@ int make_grid(const sph_grid *gr, DevGrid &g)
 
 bool cells_ok(const sph_cells *c)
 {
-    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell && c->slot_of && c->cell_nhome &&
+    return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell && c->cell_nhome &&
            c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
            ((uintptr_t)c->order % 2 == 0);
@@ -100,7 +100,6 @@ DevCells dev_cells(const sph_cells *c)
     d.cell_hmax = c->cell_hmax;
     d.ord = c->order;
     d.slot_cell = c->slot_cell;
-    d.slot_of = c->slot_of;
     d.cell_nhome = c->cell_nhome;
     return d;
 }
@@ -130,7 +129,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
     size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
-        huge_items, rows, rows_sum, tiles, counter, total;
+        huge_items, rows, rows_sum, tiles, counter, gen, total;
     long long tile_cap, huge_cap;
 };
 
@@ -172,6 +171,8 @@ Ws ws_layout(const DevGrid &g, long long n)
     w.tiles = o;
     o = align_up(o + 16 * (size_t)w.tile_cap, 256);
     w.counter = o;
+    o = align_up(o + 4, 256);
+    w.gen = o;                           // sph_density_all call counter: tags the output records
     o = align_up(o + 4, 256);
     w.total = o;
     return w;
@@ -258,13 +259,11 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n, cell_of, rank, cells->cell_start, xin,
                                                                     vin, rec);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
-        int *fin = cell_of;                       // cell_of is dead after k_scatter_rec
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, fin, cells->cell_nhome, big_items,
+            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, big_items,
             big_count);
-        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, fin,
-                                                          big_items, big_count);
-        k_slot_of<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(n, rank, fin, cells->slot_of);
+        k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, big_items,
+                                                          big_count);
     }
     if (n == 0 && (e = cudaMemsetAsync(cells->cell_nhome, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
         return cuda_fail(e);
@@ -398,14 +397,15 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     int4 *tiles = at<int4>(ws, w.tiles);
     int *counter = at<int>(ws, w.counter);
     const DevCells dc = dev_cells(cells);
+    unsigned *gen = at<unsigned>(ws, w.gen);
     k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
-                                                                       w.tile_cap, status);
+                                                                       w.tile_cap, status, gen);
     const long long ntiles_scan = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
     k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles_scan, rows, nkeys);
     k_scan_add<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows_sum);
     k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
-                                                                      w.tile_cap, status);
+                                                                      w.tile_cap, status, gen);
     cudaError_t e;
     if ((e = cudaMemsetAsync(counter, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     static int blocks_per_sm = 0, sms = 0;
@@ -421,11 +421,11 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     const int blocks = sms * blocks_per_sm;
     OutRec *orec = at<OutRec>(ws, w.orec);
     if (stats)
-        k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter);
+        k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter, gen);
     else
-        k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter);
+        k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter, gen);
     if (out->n_out > 0)
-        k_unpermute<<<grid_blocks(out->n_out, 256, 148 * 16), 256, 0, s>>>(dev_out(out), dc.slot_of, orec);
+        k_unpermute<<<grid_blocks(out->n_out, 256, 148 * 16), 256, 0, s>>>(dev_out(out), orec, gen);
     return check_launch();
 }
 
