@@ -9,7 +9,9 @@
 //
 // Small cells (n <= SORT_SMALL = 32): one warp per cell, one particle per lane,
 // 32-bit composites (quantised fp32 key, in-cell index) ranked by counting.
-// Larger cells are queued as (cell, chunk) items and ranked by k_sort_big, one
+// Cells of up to SORT_MED = 128: k_sort_mid, one warp per cell, same composites.
+// Medium/huge cells: bitonic sorts in shared memory (k_sort_bitonic).  Cells above
+// SORT_HUGE_MAX are queued as (cell, chunk) items and ranked by k_sort_big, one
 // CTA per chunk of SORT_BIG_CHUNK elements, streaming the cell's 64-bit
 // composites (orderable fp32 key << 32 | input index) through shared memory.
 #pragma once
@@ -72,7 +74,8 @@ __global__ void k_mark_needed(DevGrid g, const int *__restrict__ cell_nhome, int
 __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, DevCells c, uint16_t *ord,
                                                                     long long cbeg, long long cend, int2 *big_items,
                                                                     int *big_count, int *huge_items, int *huge_count,
-                                                                    int huge_cap, const int *__restrict__ need)
+                                                                    int huge_cap, int *mid_items, int *mid_count,
+                                                                    const int *__restrict__ need)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -97,6 +100,10 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
                 if (n <= SORT_MED_MAX) huge_items[atomicAdd(&huge_count[0], 1)] = (int)cell;
                 else huge_items[huge_cap - 1 - atomicAdd(&huge_count[1], 1)] = (int)cell;
             }
+            continue;
+        }
+        if (n > SORT_SMALL && n <= SORT_MED) {             // k_sort_mid: one warp per cell
+            if (lane == 0) mid_items[atomicAdd(mid_count, 1)] = (int)cell;
             continue;
         }
         if (n > SORT_SMALL) {
@@ -205,6 +212,72 @@ __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint1
             }
             for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
             __syncthreads();
+        }
+    }
+}
+
+// Cells of SORT_SMALL < n <= SORT_MED particles: one warp per cell, up to four particles per
+// lane, the 32-bit composites of k_sort_small (quantised key << 7 | in-cell index, n <= 128)
+// of one direction at a time in shared memory, ranked by counting.
+constexpr int SORT_MID_PER = SORT_MED / 32;
+
+__global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCells c, uint16_t *ord,
+                                                               const int *__restrict__ mid_items,
+                                                               const int *__restrict__ mid_count,
+                                                               const int *__restrict__ need)
+{
+    __shared__ unsigned sh[SORT_WARPS][SORT_MED];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned *S = sh[w];
+    const int nitems = *mid_count;
+    const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
+    const float scale = 33554432.0f / (2.0f * cmax);
+    for (int it = blockIdx.x * SORT_WARPS + w; it < nitems; it += gridDim.x * SORT_WARPS) {
+        const long long cell = mid_items[it];
+        const int s0 = c.cell_start[cell];
+        const int n = c.cell_start[cell + 1] - s0;
+        const int mask = need ? need[cell] : 0x1fff;
+        double corner[3];
+        cell_corner(g, cell, corner);
+        float u[SORT_MID_PER][3];
+#pragma unroll
+        for (int k = 0; k < SORT_MID_PER; ++k) {
+            const int e = lane + 32 * k;
+            const float4 p = e < n ? c.xyzh[s0 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+            // as k_sort_small: x - fp32(corner) in fp32
+            u[k][0] = p.x - (float)corner[0];
+            u[k][1] = p.y - (float)corner[1];
+            u[k][2] = p.z - (float)corner[2];
+        }
+#pragma unroll 1
+        for (int d = 0; d < SPH_NDIR; ++d) {
+            if (!((mask >> d) & 1)) continue;              // warp-uniform
+            const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+            const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
+            const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
+            unsigned comp[SORT_MID_PER];
+#pragma unroll
+            for (int k = 0; k < SORT_MID_PER; ++k) {
+                const int e = lane + 32 * k;
+                const float key = ((float)a0 * u[k][0] + (float)a1 * u[k][1] + (float)a2 * u[k][2]) * inv;
+                float qk = floorf((key + cmax) * scale);
+                qk = fminf(fmaxf(qk, 0.0f), 33554431.0f);
+                comp[k] = ((unsigned)qk << 7) | (unsigned)e;
+                if (e < n) S[e] = comp[k];
+            }
+            __syncwarp();
+            int r[SORT_MID_PER] = {0, 0, 0, 0};
+            for (int m = 0; m < n; ++m) {
+                const unsigned v = S[m];
+#pragma unroll
+                for (int k = 0; k < SORT_MID_PER; ++k) r[k] += v < comp[k];
+            }
+#pragma unroll
+            for (int k = 0; k < SORT_MID_PER; ++k) {
+                const int e = lane + 32 * k;
+                if (e < n) ord[(long long)d * c.cap + s0 + r[k]] = (uint16_t)e;
+            }
+            __syncwarp();
         }
     }
 }
