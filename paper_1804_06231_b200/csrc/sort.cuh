@@ -30,6 +30,13 @@ constexpr int SORT_WARPS = 8;
 constexpr int SORT_BIG_CHUNK = 256;
 constexpr int SORT_BIG_TILE = 2048;
 
+// r += (a < b) as a compare and a predicated add (the compiler's select form costs three
+// instructions per comparison in the rank loops below)
+__device__ __forceinline__ void count_lt(unsigned &r, unsigned a, unsigned b)
+{
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(r) : "r"(a), "r"(b));
+}
+
 __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, double corner[3])
 {
     long long plane = (long long)g.ny * g.nz;
@@ -150,10 +157,13 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             const uint4 c1 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 4]);
             const uint4 c2 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 8]);
             const unsigned c12 = S[m * 16 + 12];
-            r[0] += c0.x < comp[0]; r[1] += c0.y < comp[1]; r[2] += c0.z < comp[2]; r[3] += c0.w < comp[3];
-            r[4] += c1.x < comp[4]; r[5] += c1.y < comp[5]; r[6] += c1.z < comp[6]; r[7] += c1.w < comp[7];
-            r[8] += c2.x < comp[8]; r[9] += c2.y < comp[9]; r[10] += c2.z < comp[10]; r[11] += c2.w < comp[11];
-            r[12] += c12 < comp[12];
+            count_lt(r[0], c0.x, comp[0]); count_lt(r[1], c0.y, comp[1]);
+            count_lt(r[2], c0.z, comp[2]); count_lt(r[3], c0.w, comp[3]);
+            count_lt(r[4], c1.x, comp[4]); count_lt(r[5], c1.y, comp[5]);
+            count_lt(r[6], c1.z, comp[6]); count_lt(r[7], c1.w, comp[7]);
+            count_lt(r[8], c2.x, comp[8]); count_lt(r[9], c2.y, comp[9]);
+            count_lt(r[10], c2.z, comp[10]); count_lt(r[11], c2.w, comp[11]);
+            count_lt(r[12], c12, comp[12]);
         }
         if (mine) {
 #pragma unroll
@@ -266,11 +276,11 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
                 if (e < n) S[e] = comp[k];
             }
             __syncwarp();
-            int r[SORT_MID_PER] = {0, 0, 0, 0};
+            unsigned r[SORT_MID_PER] = {0, 0, 0, 0};
             for (int m = 0; m < n; ++m) {
                 const unsigned v = S[m];
 #pragma unroll
-                for (int k = 0; k < SORT_MID_PER; ++k) r[k] += v < comp[k];
+                for (int k = 0; k < SORT_MID_PER; ++k) count_lt(r[k], v, comp[k]);
             }
 #pragma unroll
             for (int k = 0; k < SORT_MID_PER; ++k) {
