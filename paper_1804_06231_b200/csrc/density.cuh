@@ -93,21 +93,32 @@ __device__ __forceinline__ IPart load_i(const DevGrid &g, const DevCells &c, int
     return p;
 }
 
-// Self cell: all j != i of the home cell, in the order of its d = 0 list.
+// Self cell: all j != i of the home cell, in the order of its d = 0 list.  Batches of four
+// candidates keep their global loads in flight together (the loop is latency-bound).
 template <bool COUNT>
 __device__ __forceinline__ void sweep_self(const DevCells &c, const IPart &p, int s0, int s1, Acc &a,
                                            unsigned &cand, unsigned &hits)
 {
-    for (int q = s0; q < s1; ++q) {
-        const int j = s0 + c.ord[q];
-        if (j == p.slot) continue;
-        const float4 e = c.xyzh[j];
-        float dx = p.x - e.x, dy = p.y - e.y, dz = p.z - e.z;
-        float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        if (COUNT) ++cand;
-        if (r2 < p.H2) {
-            interact(p, dx, dy, dz, r2, c.vm[j], a);
-            if (COUNT) ++hits;
+    for (int q0 = s0; q0 < s1; q0 += 4) {
+        int j[4];
+        float4 e[4], v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) j[u] = q0 + u < s1 ? s0 + c.ord[q0 + u] : p.slot;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            e[u] = c.xyzh[j[u]];
+            v[u] = c.vm[j[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (j[u] == p.slot) continue;                  // i itself, or past the cell
+            float dx = p.x - e[u].x, dy = p.y - e[u].y, dz = p.z - e[u].z;
+            float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (COUNT) ++cand;
+            if (r2 < p.H2) {
+                interact(p, dx, dy, dz, r2, v[u], a);
+                if (COUNT) ++hits;
+            }
         }
     }
 }
@@ -148,19 +159,39 @@ __device__ __forceinline__ void sweep_pair(const DevGrid &g, const DevCells &c, 
     float sjz = sh[2] < 0 ? g.boxf[2] : 0.0f;
     const uint16_t *L = c.ord + (long long)d * c.cap;
     int s0 = c.cell_start[cj], s1 = c.cell_start[cj + 1];
-    int q = s > 0 ? s0 : s1 - 1;
-    const int qend = s > 0 ? s1 : s0 - 1;
-    for (; q != qend; q += s) {
-        const int j = s0 + L[q];
-        const float4 e = c.xyzh[j];
-        float dx = xi - (e.x - sjx), dy = yi - (e.y - sjy), dz = zi - (e.z - sjz);
-        if (!(fmaf(dx, sx, fmaf(dy, sy, dz * sz)) < p.Hd)) break;   // sorted early exit
-        float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        if (COUNT) ++cand;
-        if (r2 < p.H2) {
-            interact(p, dx, dy, dz, r2, c.vm[j], a);
-            if (COUNT) ++hits;
+    const int n = s1 - s0;
+    // batches of four in sweep order (loads in flight together); the sweep stops at the first
+    // candidate whose projected separation reaches H_i + delta
+    for (int k0 = 0; k0 < n; k0 += 4) {
+        int j[4];
+        float4 e[4], v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = min(k0 + u, n - 1);
+            j[u] = s0 + L[s > 0 ? s0 + k : s1 - 1 - k];
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            e[u] = c.xyzh[j[u]];
+            v[u] = c.vm[j[u]];
+        }
+        bool stop = false;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (stop || k0 + u >= n) break;
+            float dx = xi - (e[u].x - sjx), dy = yi - (e[u].y - sjy), dz = zi - (e[u].z - sjz);
+            if (!(fmaf(dx, sx, fmaf(dy, sy, dz * sz)) < p.Hd)) {   // sorted early exit
+                stop = true;
+                break;
+            }
+            float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (COUNT) ++cand;
+            if (r2 < p.H2) {
+                interact(p, dx, dy, dz, r2, v[u], a);
+                if (COUNT) ++hits;
+            }
+        }
+        if (stop) break;
     }
 }
 

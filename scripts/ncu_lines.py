@@ -50,7 +50,7 @@ for r in rows:
     elif blocks and blocks[-1][1] is not None and r:
         blocks[-1][2].append(r)
 blk = [b for b in blocks if kname in b[0].replace("(bool)0", "ILb0").replace("(bool)1", "ILb1") or kname in b[0]]
-name, h, data = blk[0] if blk else blocks[0]
+name, h, data = (blk or blocks)[int(os.environ.get("NCU_BLOCK", "0"))]
 ci, cs = h.index("Instructions Executed"), h.index("Warp Stall Sampling (All Samples)")
 byline = collections.defaultdict(lambda: [0, 0])
 tot_i = tot_s = 0
