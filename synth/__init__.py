@@ -7,7 +7,8 @@ sums.  Both `oracle/` and the CUDA path read what it produces; neither is
 imported here.
 """
 from .gen import (CONFIGS, GAMMA, ETA, ParticleSet, make, make_config,
-                  uniform_set, lattice_set, clustered_set, tiny_random_set)
+                  uniform_set, lattice_set, clustered_set, tiny_random_set, test27cells_set)
 
 __all__ = ["CONFIGS", "GAMMA", "ETA", "ParticleSet", "make", "make_config",
-           "uniform_set", "lattice_set", "clustered_set", "tiny_random_set"]
+           "uniform_set", "lattice_set", "clustered_set", "tiny_random_set",
+           "test27cells_set"]

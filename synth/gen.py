@@ -260,6 +260,33 @@ def tiny_random_set(seed: int, n: int, nc: int, h_frac: float = 0.8, h_jitter: f
     return ParticleSet(f"tiny-{seed}-{n}", seed, xyzh, vm, nc)
 
 
+def test27cells_set(seed: int, nc: int, per_cell: int = 216, eta: float = ETA, v_sigma: float = 1.0) -> ParticleSet:
+    """Batched test27cells instances: a periodic nc^3 grid whose
+    every cell holds exactly `per_cell` particles placed uniformly at random inside it (on the
+    2^-24 position grid, so fp64 binning puts each in its own cell); every cell is the centre
+    of one 27-cell instance.  h = eta * C_l / per_cell^(1/3) for all particles (the mean
+    inter-particle spacing times eta), masses 1/N, velocities N(0, v_sigma).  Particles are
+    written cell by cell in x-major cell order."""
+    ncell = nc ** 3
+    n = ncell * per_cell
+    g = _rng(seed, 0x2727)
+    # grid-unit bounds of cell c along an axis: [ceil(c G / nc), ceil((c + 1) G / nc))
+    lo = -((-np.arange(nc + 1, dtype=np.int64) * GRID) // nc)
+    cell = np.repeat(np.arange(ncell, dtype=np.int64), per_cell)
+    ix, iy, iz = cell // (nc * nc), (cell // nc) % nc, cell % nc
+    xyzh = np.empty((n, 4), np.float32)
+    for a, ia in enumerate((ix, iy, iz)):
+        k = lo[ia] + (g.random(n) * (lo[ia + 1] - lo[ia])).astype(np.int64)
+        xyzh[:, a] = (k.astype(np.float64) / GRID).astype(np.float32)
+    h = eta * (1.0 / nc) / per_cell ** (1.0 / 3.0)
+    xyzh[:, 3] = np.float32(h)
+    vm = np.empty((n, 4), np.float32)
+    vm[:, 0:3] = (v_sigma * g.standard_normal((n, 3))).astype(np.float32)
+    vm[:, 3] = np.float32(1.0 / n)
+    return ParticleSet(f"test27cells-{nc}-{per_cell}", seed, xyzh, vm, nc,
+                       meta={"per_cell": per_cell, "eta": eta})
+
+
 # ---------------------------------------------------------------------------
 # The five BASELINE.json configurations (DESIGN.md §3 gives the readings).
 # ---------------------------------------------------------------------------
