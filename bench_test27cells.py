@@ -11,7 +11,8 @@ CUDA events (median of --reps after --warmup).  The whole-pass engine (`sph_dens
 runs on the same set for comparison.
 
 Reported per orientation (the paper's Table 3 layout): GPU time per SYMMETRIC cell pair
-(= two one-sided gathers, the work of the paper's pair function: both cells updated),
+(= two one-sided gathers, the work of the paper's pair function: both cells updated; and
+the symmetric kernel `sph_density_pair_sym`, one evaluation per distance),
 in-range interactions and pseudo-Verlet candidates per pair, interactions/s; and the
 weighted total of one instance, 8 corner + 12 edge + 6 face pairs.  The paper's
 single-core AVX times are printed as context only (other hardware; Table 3).  The
@@ -48,6 +49,17 @@ def pairs_of(nc: int, nonzero: int, torch):
         cj = (((ix + a) % nc) * nc + (iy + b) % nc) * nc + (iz + c) % nc
         out.append(torch.stack([cell, cj], dim=1))
     return torch.cat(out).to(torch.int32).contiguous(), len(offs)
+
+
+def half_pairs_of(nc: int, nonzero: int, torch):
+    """(ci, cj) for every cell and the lexicographically positive offsets of one class: each
+    unordered neighbour pair once (the symmetric kernel's input)."""
+    offs = [(a, b, c) for a in (-1, 0, 1) for b in (-1, 0, 1) for c in (-1, 0, 1)
+            if (a != 0) + (b != 0) + (c != 0) == nonzero and (a, b, c) > (0, 0, 0)]
+    cell = torch.arange(nc ** 3, dtype=torch.int64)
+    ix, iy, iz = cell // (nc * nc), (cell // nc) % nc, cell % nc
+    out = [torch.stack([cell, (((ix + a) % nc) * nc + (iy + b) % nc) * nc + (iz + c) % nc], dim=1) for a, b, c in offs]
+    return torch.cat(out).to(torch.int32).contiguous()
 
 
 def main():
@@ -107,7 +119,17 @@ def main():
         ki = KIND_INDEX[name]
         ms = timed(lambda: pv.sph_density_pair(dp.grid, dp.cells, pr, acc, dp.ws))
         nsym = ncell * k / 2                              # symmetric pairs = one-sided pairs / 2
+        # the symmetric kernel: each unordered pair once, both cells updated
+        hp = half_pairs_of(args.nc, nz, torch).cuda()
+        st2 = pv.Stats()
+        pv.sph_density_pair_sym(dp.grid, dp.cells, hp, acc, dp.ws, stats=st2)
+        torch.cuda.synchronize()
+        cnt2 = st2.read()
+        ms_sym = timed(lambda: pv.sph_density_pair_sym(dp.grid, dp.cells, hp, acc, dp.ws))
         res[name] = {"one_sided_pairs": int(pr.shape[0]), "ms_all_pairs": ms,
+                     "sym_kernel_us_per_symmetric_pair": 1e3 * ms_sym / hp.shape[0],
+                     "sym_kernel_candidates_per_pair": cnt2["cand"][ki] / hp.shape[0],
+                     "sym_kernel_interactions_per_pair": cnt2["hits"][ki] / hp.shape[0],
                      "us_per_symmetric_pair": 1e3 * ms / nsym,
                      "interactions_per_symmetric_pair": cnt["hits"][ki] / nsym,
                      "candidates_per_symmetric_pair": cnt["cand"][ki] / nsym,
@@ -115,6 +137,8 @@ def main():
                      "paper_avx_us_per_pair": 1e3 * PAPER_AVX_MS[name]}
     total_us = 8 * res["corner"]["us_per_symmetric_pair"] + 12 * res["edge"]["us_per_symmetric_pair"] + \
         6 * res["face"]["us_per_symmetric_pair"]
+    total_sym_us = 8 * res["corner"]["sym_kernel_us_per_symmetric_pair"] + \
+        12 * res["edge"]["sym_kernel_us_per_symmetric_pair"] + 6 * res["face"]["sym_kernel_us_per_symmetric_pair"]
     # the whole-pass engine on the same set: self + 26 one-sided gathers of every cell
     out = pv.Out.alloc(p.n)
     ms_all = timed(lambda: pv.sph_density_all(dp.grid, dp.cells, out, dp.ws))
@@ -123,6 +147,7 @@ def main():
             "dtype": "f32", "data": "synthetic", "reps": args.reps, "warmup": args.warmup,
             "orientations": res,
             "weighted_total_us_per_instance": total_us,
+            "weighted_total_us_per_instance_sym_kernel": total_sym_us,
             "weighted_total_definition": "8 corner + 12 edge + 6 face symmetric pairs (P:250)",
             "paper_avx_weighted_total_us": 1e3 * PAPER_AVX_MS["total"],
             "density_all_ms": ms_all, "density_all_us_per_cell": 1e3 * ms_all / ncell}

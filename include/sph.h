@@ -199,6 +199,17 @@ int sph_density_self(const sph_grid *grid, const sph_cells *cells, const int32_t
 int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t *pairs, int64_t npairs,
                      sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream);
 
+/* Symmetric pair sweeps: for each device pair
+ * (ci, cj) of `pairs` ([npairs][2] int32, cj one of the 26 neighbours of
+ * ci, each unordered pair listed once), every candidate distance of the
+ * pair is evaluated once and BOTH particles accumulate: i when r < H_i, j
+ * when r < H_j (the window in cj's list uses max(H_i, gamma * hmax(cj)) +
+ * delta).  Equals sph_density_pair on (ci, cj) plus (cj, ci) within fp32
+ * summation order; accumulates like sph_density_self (atomics; finalize
+ * with sph_density_finalize).  j in a ghost cell (slabs) is not updated. */
+int sph_density_pair_sym(const sph_grid *grid, const sph_cells *cells, const int32_t *pairs, int64_t npairs,
+                         sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream);
+
 /* div_v /= rho and curl_v /= rho for the first n elements (after the self
  * and pair calls). */
 int sph_density_finalize(sph_out *acc, int64_t n, void *stream);

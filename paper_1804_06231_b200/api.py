@@ -208,6 +208,16 @@ def sph_density_pair(grid: SphGrid, cells: Cells, pairs: torch.Tensor, acc: Out,
                                         _stream(stream)), "sph_density_pair")
 
 
+def sph_density_pair_sym(grid: SphGrid, cells: Cells, pairs: torch.Tensor, acc: Out, ws: torch.Tensor,
+                         stats: Stats | None = None, stream=None) -> None:
+    """Symmetric pairs (include/sph.h): each unordered (ci, cj) listed once, both sides updated."""
+    assert pairs.dtype == torch.int32 and pairs.is_contiguous() and (pairs.numel() == 0 or pairs.shape[-1] == 2)
+    s, o = cells.struct(), acc.struct()
+    _check(_lib.load().sph_density_pair_sym(ctypes.byref(grid), ctypes.byref(s), _ptr(pairs), pairs.numel() // 2,
+                                            ctypes.byref(o), stats.ptr() if stats else None, _ptr(ws), ws.numel(),
+                                            _stream(stream)), "sph_density_pair_sym")
+
+
 def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
     o = acc.struct()
     _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),

@@ -214,4 +214,270 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) k_density_pair_staged(DevGrid
     flush_stats<COUNT>(st, cand, hits);
 }
 
+// ---- symmetric pair kernel -------------------------------------
+// One CTA per UNORDERED neighbour pair (ci, cj): every distance of the pair is evaluated once
+// and both particles take their share.  Lane = i in ci, as in k_density_pair_staged; the
+// window in cj's sorted list uses max(H_i, gamma hmax(cj)) + delta, so every j that reaches i
+// (r < H_j) is a candidate too.  A hit is pushed with two flags (r < H_i: i's sum, r < H_j:
+// j's sum).  i's sums stay in registers; j's are the same M4 terms with H_j and m_i (x_ji =
+// -x_ij, v_ji = -v_ij leave every product unchanged) and go to per-j accumulators in shared
+// memory (red.shared.add).  Both sides reach the outputs with red.global.add, as in the
+// one-sided kernel; j in a ghost cell (slabs) is skipped.
+constexpr int SYM_WARPS = 4;
+constexpr int SYM_MAXN = 512;            // staged particles per cell (3 CTAs per SM)
+constexpr int SYM_Q = 16;
+constexpr int SYM_NACC = 12;             // per-j sums: rho wc srt st Dn Px Nx Py Ny Pz Nz, nngb
+constexpr size_t SYM_SMEM = (size_t)SYM_MAXN * 16 * 4 + (size_t)SYM_MAXN * 4 * SYM_NACC + (size_t)SYM_MAXN * 4 +
+                            (size_t)SYM_MAXN * 2 + (size_t)SYM_WARPS * SYM_Q * 32 * 2;
+
+__device__ __forceinline__ void red_shared_f32(float *a, float v) { atomicAdd(a, v); }
+
+template <bool COUNT>
+__global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, DevCells c, DevOut o,
+                                                                     const int2 *pairs, long long npairs,
+                                                                     sph_stats *st, unsigned *status)
+{
+    extern __shared__ __align__(16) unsigned char sym_smem[];
+    float4 *Pi = reinterpret_cast<float4 *>(sym_smem);             // ci positions
+    float4 *Vi = Pi + SYM_MAXN;                                      // ci (v, m)
+    float4 *Pj = Vi + SYM_MAXN;                                      // cj positions, w = H_j^2
+    float4 *Vj = Pj + SYM_MAXN;                                      // cj (v, m)
+    float *Aj = reinterpret_cast<float *>(Vj + SYM_MAXN);            // [SYM_NACC][SYM_MAXN]
+    float *HinvJ = Aj + SYM_NACC * SYM_MAXN;                         // 1 / H_j
+    uint16_t *Lj = reinterpret_cast<uint16_t *>(HinvJ + SYM_MAXN);   // cj sorted along d
+    uint16_t *stacks = Lj + SYM_MAXN;
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const unsigned mbar = smem_addr(&s_mbar);
+    unsigned phase = 0;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+
+    for (long long q = blockIdx.x; q < npairs; q += gridDim.x) {
+        const int2 pr = pairs[q];
+        const long long ci = pr.x, cj = pr.y;
+        if (!owned_cell(g, ci) || cj < 0 || cj >= g.ncell) {
+            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+            continue;
+        }
+        const HomeCell hc = home_cell(g, ci);
+        const long long plane = (long long)g.ny * g.nz;
+        const int jxl = (int)(cj / plane), jy = (int)((cj / g.nz) % g.ny), jz = (int)(cj % g.nz);
+        int ox = jxl - hc.ixl, oy = jy - hc.iy, oz = jz - hc.iz;
+        if (!g.ghost_x) ox = ox == g.nc[0] - 1 ? -1 : (ox == 1 - g.nc[0] ? 1 : ox);
+        oy = oy == g.ny - 1 ? -1 : (oy == 1 - g.ny ? 1 : oy);
+        oz = oz == g.nz - 1 ? -1 : (oz == 1 - g.nz ? 1 : oz);
+        if (ox < -1 || ox > 1 || oy < -1 || oy > 1 || oz < -1 || oz > 1 || !(ox | oy | oz)) {
+            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+            continue;
+        }
+        int cjc, sh[3];
+        neighbour(g, hc, ox, oy, oz, cjc, sh);
+        const int kind = kind_of(ox, oy, oz);
+        int sgn;
+        const int d = canon_dir(ox, oy, oz, sgn);
+        const int si = c.cell_start[ci], ni = c.cell_start[ci + 1] - si;
+        const int sj = c.cell_start[cjc], nj = c.cell_start[cjc + 1] - sj;
+        if (ni == 0 || nj == 0) continue;
+        const bool j_owned = owned_cell(g, cjc);
+        if (ni > SYM_MAXN || nj > SYM_MAXN) {
+            // dense cells: the two one-sided per-thread sweeps reading global memory
+            for (int i = si + threadIdx.x; i < si + ni; i += blockDim.x) {
+                IPart p = load_i(g, c, i, hc.corner);
+                Acc a;
+                acc_zero(a);
+                sweep_pair<COUNT>(g, c, p, cjc, ox, oy, oz, sh, a, cand[kind], hits[kind]);
+                if (a.nngb > 0) atomic_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
+            }
+            if (j_owned) {
+                const HomeCell hj = home_cell(g, cjc);
+                int cic, sh2[3];
+                neighbour(g, hj, -ox, -oy, -oz, cic, sh2);
+                for (int j = sj + threadIdx.x; j < sj + nj; j += blockDim.x) {
+                    IPart p = load_i(g, c, j, hj.corner);
+                    Acc a;
+                    acc_zero(a);
+                    unsigned dummy = 0;
+                    sweep_pair<COUNT>(g, c, p, cic, -ox, -oy, -oz, sh2, a, dummy, hits[kind]);
+                    if (a.nngb > 0) atomic_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
+                }
+            }
+            continue;
+        }
+        // ---- staging: both cells (positions and v, m), cj's sorted list, zeroed j sums --------
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(mbar, (unsigned)(2 * ni + 2 * nj) * 16u);
+            bulk_g2s(smem_addr(Pi), c.xyzh + si, (unsigned)ni * 16u, mbar);
+            bulk_g2s(smem_addr(Vi), c.vm + si, (unsigned)ni * 16u, mbar);
+            bulk_g2s(smem_addr(Pj), c.xyzh + sj, (unsigned)nj * 16u, mbar);
+            bulk_g2s(smem_addr(Vj), c.vm + sj, (unsigned)nj * 16u, mbar);
+        }
+        const uint16_t *src = c.ord + (long long)d * c.cap + sj;
+        for (int k = threadIdx.x; k < nj; k += blockDim.x) Lj[k] = src[k];
+        for (int k = threadIdx.x; k < SYM_NACC * nj; k += blockDim.x) Aj[(k / nj) * SYM_MAXN + k % nj] = 0.0f;
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+        const float bx = g.boxf[0], by = g.boxf[1], bz = g.boxf[2];
+        for (int k = threadIdx.x; k < nj; k += blockDim.x) {
+            float4 p = Pj[k];
+            // cj beyond a low face: x_j - L, exact (x_j >= L/2); w <- H_j^2 as the gather rounds it
+            p.x -= sh[0] < 0 ? bx : 0.0f;
+            p.y -= sh[1] < 0 ? by : 0.0f;
+            p.z -= sh[2] < 0 ? bz : 0.0f;
+            const double H = (double)g.gamma * (double)p.w;
+            p.w = (float)(H * H);
+            HinvJ[k] = (float)(1.0 / H);
+            Pj[k] = p;
+        }
+        const float Hjmax = (float)((double)g.gamma * (double)c.cell_hmax[cjc]);
+        __syncthreads();
+
+        const unsigned sP = smem_addr(Pj), sV = smem_addr(Vj), sL = smem_addr(Lj);
+        const unsigned sQ = smem_addr(stacks + wl * SYM_Q * 32) + 2u * lane;
+        const float c0 = (float)dir_component(d, 0), c1 = (float)dir_component(d, 1), c2 = (float)dir_component(d, 2);
+        const float rk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
+        for (int t0 = wl * 32; t0 < ni; t0 += SYM_WARPS * 32) {
+            const int e = t0 + lane;
+            const bool active = e < ni;
+            float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, H2 = -1.f, Hinv = 0.f, Hk = 0.f, m = 0.f;
+            if (active) {
+                const float4 a = Pi[e];
+                const float4 b = Vi[e];
+                x = sh[0] > 0 ? a.x - bx : a.x;
+                y = sh[1] > 0 ? a.y - by : a.y;
+                z = sh[2] > 0 ? a.z - bz : a.z;
+                vx = b.x; vy = b.y; vz = b.z; m = b.w;
+                const double H = (double)g.gamma * (double)a.w;
+                H2 = (float)(H * H);
+                Hinv = (float)(1.0 / H);
+                Hk = (fmaxf((float)H, Hjmax) + g.delta) * rk;
+            }
+            int top = 1;
+            while (2 * top <= nj) top <<= 1;
+            int lo = 0;
+            for (int stp = top; stp > 0; stp >>= 1) {
+                const int kk = lo + stp;
+                const bool v = active && kk <= nj;
+                const int pos = sgn > 0 ? kk - 1 : nj - kk;
+                const unsigned id = v ? ldsr_u16(sL + 2u * (unsigned)pos) : 0u;
+                const float4 p = ldsr_f4(sP + 16u * id);
+                const float sep = (float)sgn * fmaf(c0, p.x - x, fmaf(c1, p.y - y, c2 * (p.z - z)));
+                if (v && sep < Hk) lo = kk;
+            }
+            const int len = lo, first = sgn > 0 ? 0 : nj - len;
+            Acc2 A;
+            A.rho = A.wc = A.srt = A.st = A.Dn = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
+            unsigned qp = sQ;
+            int nngb = 0;
+            const f2 Hinv2 = bc2(Hinv);
+            auto drain = [&](bool final) {
+                const unsigned n = (qp - sQ) >> 6;
+                if (n >= 2 || (final && n == 1)) {
+                    const bool two = n >= 2;
+                    const unsigned e0 = lds_u16(qp - 64u), e1 = two ? lds_u16(qp - 128u) : (e0 & 0x3fffu);
+                    qp -= two ? 128u : 64u;
+                    const unsigned s0 = e0 & 0x3fffu, s1 = e1 & 0x3fffu;
+                    const bool i0 = (e0 >> 14) & 1u, i1 = two && ((e1 >> 14) & 1u);
+                    const bool j0 = (e0 >> 15) & 1u, j1 = two && ((e1 >> 15) & 1u);
+                    nngb += (int)i0 + (int)i1;
+                    const float4 p0 = ldsr_f4(sP + 16u * s0), p1 = ldsr_f4(sP + 16u * s1);
+                    const float4 v0 = ldsr_f4(sV + 16u * s0), v1 = ldsr_f4(sV + 16u * s1);
+                    const f2 dx = pk(x - p0.x, x - p1.x), dy = pk(y - p0.y, y - p1.y), dz = pk(z - p0.z, z - p1.z);
+                    const f2 nvx = pk(v0.x - vx, v1.x - vx), nvy = pk(v0.y - vy, v1.y - vy),
+                             nvz = pk(v0.z - vz, v1.z - vz);
+                    interact_pair<true>(Hinv2, dx, dy, dz, pk(v0.w, v1.w), nvx, nvy, nvz,
+                                        pk(i0 ? 1.0f : 0.0f, i1 ? 1.0f : 0.0f), A);
+                    if (j0 || j1) {
+                        // j's share: the same terms with H_j and m_i
+                        Acc2 B;
+                        B.rho = B.wc = B.srt = B.st = B.Dn = B.Px = B.Nx = B.Py = B.Ny = B.Pz = B.Nz = zero2();
+                        const f2 hj = pk(HinvJ[s0], HinvJ[s1]);
+                        interact_pair<true>(hj, dx, dy, dz, bc2(m), nvx, nvy, nvz,
+                                            pk(j0 ? 1.0f : 0.0f, j1 ? 1.0f : 0.0f), B);
+                        const f2 bs[11] = {B.rho, B.wc, B.srt, B.st, B.Dn, B.Px, B.Nx, B.Py, B.Ny, B.Pz, B.Nz};
+#pragma unroll
+                        for (int k = 0; k < 11; ++k) {
+                            float a0, a1;
+                            upk(bs[k], a0, a1);
+                            if (j0) red_shared_f32(&Aj[k * SYM_MAXN + s0], a0);
+                            if (j1) red_shared_f32(&Aj[k * SYM_MAXN + s1], a1);
+                        }
+                        if (j0) atomicAdd(reinterpret_cast<int *>(&Aj[11 * SYM_MAXN + s0]), 1);
+                        if (j1) atomicAdd(reinterpret_cast<int *>(&Aj[11 * SYM_MAXN + s1]), 1);
+                    }
+                }
+            };
+            const int trip = __reduce_max_sync(0xffffffffu, len);
+            for (int t = 0; t < trip; t += 4) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool ok = t + u < len;
+                    const unsigned id = ok ? ldsr_u16(sL + 2u * (unsigned)(first + t + u)) : 0u;
+                    const float4 p = ldsr_f4(sP + 16u * id);
+                    const float dx = x - p.x, dy = y - p.y, dz = z - p.z;
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    const bool hi = ok && r2 < H2, hj = ok && j_owned && r2 < p.w;
+                    if (COUNT) {
+                        cand[kind] += ok ? 1u : 0u;
+                        hits[kind] += (hi ? 1u : 0u) + (ok && r2 < p.w ? 1u : 0u);
+                    }
+                    if (hi || hj) {
+                        sts_u16(qp, id | (hi ? 0x4000u : 0u) | (hj ? 0x8000u : 0u));
+                        qp += 64u;
+                    }
+                }
+                for (;;) {
+                    const unsigned n = (qp - sQ) >> 6;
+                    if (!(__popc(__ballot_sync(0xffffffffu, n >= 2)) >= 24 ||
+                          __any_sync(0xffffffffu, n >= SYM_Q - 4)))
+                        break;
+                    drain(false);
+                }
+            }
+            while (__any_sync(0xffffffffu, qp != sQ)) drain(true);
+            if (active && nngb > 0) {
+                const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;
+                const float gf = K3 * Hinv;
+                Final f;
+                f.rho = K3 * sum2(A.rho);
+                f.wc = K3 * sum2(A.wc);
+                f.rho_dh = -K3 * g.gamma * Hinv * sum2(A.srt);
+                f.wc_dh = -K3 * g.gamma * Hinv * sum2(A.st);
+                f.div = gf * sum2(A.Dn);
+                f.cx = gf * (sum2(A.Px) - sum2(A.Nx));
+                f.cy = gf * (sum2(A.Py) - sum2(A.Ny));
+                f.cz = gf * (sum2(A.Pz) - sum2(A.Nz));
+                atomic_out(o, c.perm[si + e], f, nngb);
+            }
+        }
+        __syncthreads();
+        // j's sums to the outputs
+        if (j_owned) {
+            for (int k = threadIdx.x; k < nj; k += blockDim.x) {
+                const int nn = reinterpret_cast<const int *>(Aj)[11 * SYM_MAXN + k];
+                if (nn == 0) continue;
+                const float hinv = HinvJ[k];
+                const float K3 = (16.0f / kPi) * hinv * hinv * hinv, gf = K3 * hinv;
+                const float *a = Aj + k;
+                Final f;
+                f.rho = K3 * a[0 * SYM_MAXN];
+                f.wc = K3 * a[1 * SYM_MAXN];
+                f.rho_dh = -K3 * g.gamma * hinv * a[2 * SYM_MAXN];
+                f.wc_dh = -K3 * g.gamma * hinv * a[3 * SYM_MAXN];
+                f.div = gf * a[4 * SYM_MAXN];
+                f.cx = gf * (a[5 * SYM_MAXN] - a[6 * SYM_MAXN]);
+                f.cy = gf * (a[7 * SYM_MAXN] - a[8 * SYM_MAXN]);
+                f.cz = gf * (a[9 * SYM_MAXN] - a[10 * SYM_MAXN]);
+                atomic_out(o, c.perm[sj + k], f, nn);
+            }
+        }
+        __syncthreads();                          // shared memory reused by the next pair
+    }
+    flush_stats<COUNT>(st, cand, hits);
+}
+
 }  // namespace pvsph

@@ -368,6 +368,34 @@ int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t
     return check_launch();
 }
 
+int sph_density_pair_sym(const sph_grid *grid, const sph_cells *cells, const int32_t *pairs, int64_t npairs,
+                         sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !out_ok(acc) || !ws || npairs < 0 || (npairs > 0 && !pairs)) return SPH_EINVAL;
+    if (((uintptr_t)pairs % 8) || ws_bytes < 4) return SPH_EINVAL;
+    if (npairs == 0) return SPH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned *status = at<unsigned>(ws, 0);
+    const int2 *pr = reinterpret_cast<const int2 *>(pairs);
+    static bool sym_attr = false;
+    if (!sym_attr) {
+        cudaFuncSetAttribute(k_density_pair_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
+        sym_attr = true;
+    }
+    const int blocks = grid_blocks(npairs, 1, 148 * 12);
+    if (stats)
+        k_density_pair_sym<true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr, npairs,
+                                                                        stats, status);
+    else
+        k_density_pair_sym<false><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr,
+                                                                         npairs, nullptr, status);
+    return check_launch();
+}
+
 int sph_density_finalize(sph_out *acc, int64_t n, void *stream)
 {
     if (!out_ok(acc) || n < 0 || n > acc->n_out) return SPH_EINVAL;

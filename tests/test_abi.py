@@ -79,6 +79,7 @@ def test_host_argument_errors_return_einval(lib):
     assert lib.sph_density_all(ctypes.byref(g), ctypes.byref(cells), ctypes.byref(out), None, None, 0, None) == 1
     assert lib.sph_density_self(None, ctypes.byref(cells), None, 0, ctypes.byref(out), None, None, 0, None) == 1
     assert lib.sph_density_pair(ctypes.byref(g), None, None, 0, ctypes.byref(out), None, None, 0, None) == 1
+    assert lib.sph_density_pair_sym(ctypes.byref(g), None, None, 0, ctypes.byref(out), None, None, 0, None) == 1
     assert lib.sph_density_finalize(ctypes.byref(out), 5, None) == 1
     assert lib.sph_status(None, None) == 1
 

@@ -62,3 +62,48 @@ def test_pairs_by_orientation_vs_oracle(pv, t27):
     alln = out.to_numpy()
     assert np.array_equal(alln["nngb"], got["nngb"])
     compare(alln, ref, None, "test27cells density_all")
+
+
+def _half_offsets_pairs(nc, nonzero=None):
+    """(ci, cj) for every cell and one offset of each +-pair (13 per cell; or one class)."""
+    cells = np.arange(nc ** 3, dtype=np.int64)
+    ix, iy, iz = cells // (nc * nc), (cells // nc) % nc, cells % nc
+    out = []
+    for a in (-1, 0, 1):
+        for b in (-1, 0, 1):
+            for c in (-1, 0, 1):
+                if (a, b, c) <= (0, 0, 0):                # lexicographically positive offsets only
+                    continue
+                if nonzero is not None and (a != 0) + (b != 0) + (c != 0) != nonzero:
+                    continue
+                cj = (((ix + a) % nc) * nc + (iy + b) % nc) * nc + (iz + c) % nc
+                out.append(np.stack([cells, cj], 1))
+    return torch.from_numpy(np.concatenate(out).astype(np.int32)).cuda().contiguous()
+
+
+@pytest.mark.parametrize("case", ["c1", "test27cells"])
+def test_symmetric_pairs_vs_oracle(pv, t27, case):
+    """sph_density_pair_sym over the 13 positive offsets of every cell (each unordered pair once)
+    + sph_density_self + finalize == the oracle (P:167: one distance evaluation, both sides);
+    in-range pairs per kind == Code 2 hits (both sides counted)."""
+    p = synth.make("c1") if case == "c1" else t27
+    x, v = torch.from_numpy(p.xyzh).cuda(), torch.from_numpy(p.vm).cuda()
+    dp = pv.DensityPass(p.nc, p.n)
+    pv.sph_build_cells(dp.grid, x, v, dp.cells, dp.ws)
+    pv.sph_sort_cells(dp.grid, dp.cells, dp.ws)
+    acc = pv.Out.alloc(p.n, zero=True)
+    st = pv.Stats()
+    pv.sph_density_self(dp.grid, dp.cells, torch.arange(p.nc ** 3, dtype=torch.int32, device="cuda"), acc, dp.ws,
+                        stats=st)
+    pv.sph_density_pair_sym(dp.grid, dp.cells, _half_offsets_pairs(p.nc), acc, dp.ws, stats=st)
+    pv.sph_density_finalize(acc)
+    dp.check()
+    got = acc.to_numpy()
+    ref = oracle.celllist(p.xyzh, p.vm, p.nc)
+    compare(got, ref, None, f"{case} symmetric pairs")
+    c, unsafe = oracle.pv_counts(p.xyzh, p.nc)
+    tot = c.sum(axis=0)
+    band = int(ref["band"].sum())
+    cnt = st.read()
+    for k in range(4):
+        assert abs(cnt["hits"][k] - tot[k, 2]) <= band, k
