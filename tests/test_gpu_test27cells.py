@@ -107,3 +107,20 @@ def test_symmetric_pairs_vs_oracle(pv, t27, case):
     cnt = st.read()
     for k in range(4):
         assert abs(cnt["hits"][k] - tot[k, 2]) <= band, k
+
+
+def test_symmetric_pairs_dense_fallback(pv):
+    """A cell above the symmetric kernel's staging capacity (SYM_MAXN = 512) takes the two
+    one-sided global-memory sweeps; the result still equals the oracle."""
+    from tests.test_gpu_parity import _dense_cell_set
+    xyzh, vm, nc = _dense_cell_set(700)
+    x, v = torch.from_numpy(xyzh).cuda(), torch.from_numpy(vm).cuda()
+    dp = pv.DensityPass(nc, xyzh.shape[0])
+    pv.sph_build_cells(dp.grid, x, v, dp.cells, dp.ws)
+    pv.sph_sort_cells(dp.grid, dp.cells, dp.ws)
+    acc = pv.Out.alloc(xyzh.shape[0], zero=True)
+    pv.sph_density_self(dp.grid, dp.cells, torch.arange(nc ** 3, dtype=torch.int32, device="cuda"), acc, dp.ws)
+    pv.sph_density_pair_sym(dp.grid, dp.cells, _half_offsets_pairs(nc), acc, dp.ws)
+    pv.sph_density_finalize(acc)
+    dp.check()
+    compare(acc.to_numpy(), oracle.bruteforce(xyzh, vm), None, "symmetric dense fallback")
