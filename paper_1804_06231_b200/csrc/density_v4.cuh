@@ -209,7 +209,8 @@ __device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__
 // The cut depends only on the row pair's own counts (identical on any GPU count).
 template <bool WRITE>
 __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, const int *__restrict__ nhome,
-                           int *__restrict__ off, int4 *tiles, long long tile_cap, unsigned *status, unsigned *gen)
+                           int *__restrict__ off, int4 *tiles, long long tile_cap, unsigned *status, unsigned *gen,
+                           int *gtiles, int *gcount)
 {
     // the counting launch opens a new sph_density_all call: its records carry the new tag
     if (!WRITE && blockIdx.x == 0 && threadIdx.x == 0) *gen += 1u;
@@ -228,8 +229,12 @@ __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, const 
             int pos = WRITE ? off[key] : 0;
             auto emit = [&](int za, int zb, int first, int cnt) {
                 if (WRITE) {
-                    if (pos < tile_cap) tiles[pos] = make_int4((int)key, za | (zb << 16), first, cnt);
-                    else set_status(status, ST_ECAPACITY);
+                    if (pos < tile_cap) {
+                        tiles[pos] = make_int4((int)key, za | (zb << 16), first, cnt);
+                        if (cnt < 0) gtiles[atomicAdd(gcount, 1)] = pos;   // k_density_dense's work list
+                    } else {
+                        set_status(status, ST_ECAPACITY);
+                    }
                     ++pos;
                 }
                 ++nt;
@@ -1074,8 +1079,9 @@ __global__ void __launch_bounds__(V4_TP, V4_CTAS) k_density_v4(DevGrid g, DevCel
                 else
                     v4_particle_staged<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
             }
-        } else {
-            // global-memory sweep: a slice that cannot be staged, or a tile whose check failed
+        } else if (T.cnt > 0) {
+            // global-memory sweep: a tile whose staging check failed (the slices the builder
+            // could not stage, cnt < 0, go to k_density_dense)
             const long long rowA = ((long long)(T.xo + g.ghost_x) * g.ny + T.y0) * g.nz;
             const int ntot = T.cnt > 0 ? T.cnt : -T.cnt;
             for (int h = threadIdx.x; h < ntot; h += V4_TP) {

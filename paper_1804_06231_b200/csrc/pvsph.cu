@@ -13,6 +13,7 @@
 #include "density.cuh"
 #include "density_v4.cuh"
 #include "density_pair.cuh"
+#include "density_dense.cuh"
 #include "sort.cuh"
 
 using namespace pvsph;
@@ -129,7 +130,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
     size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
-        huge_items, mid_items, rows, rows_sum, tiles, counter, gen, total;
+        huge_items, mid_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, total;
     long long tile_cap, huge_cap;
 };
 
@@ -176,6 +177,10 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4, 256);
     w.gen = o;                           // sph_density_all call counter: tags the output records
     o = align_up(o + 4, 256);
+    w.gtiles = o;                        // tiles k_v4_tiles could not stage (k_density_dense)
+    o = align_up(o + 4 * (size_t)w.tile_cap, 256);
+    w.gcount = o;                        // [listed, claimed]
+    o = align_up(o + 8, 256);
     w.total = o;
     return w;
 }
@@ -431,15 +436,17 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     int *counter = at<int>(ws, w.counter);
     const DevCells dc = dev_cells(cells);
     unsigned *gen = at<unsigned>(ws, w.gen);
+    int *gtiles = at<int>(ws, w.gtiles), *gcount = at<int>(ws, w.gcount);
     k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
-                                                                       w.tile_cap, status, gen);
+                                                                       w.tile_cap, status, gen, gtiles, gcount);
     const long long ntiles_scan = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
     k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles_scan, rows, nkeys);
     k_scan_add<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows_sum);
-    k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
-                                                                      w.tile_cap, status, gen);
     cudaError_t e;
+    if ((e = cudaMemsetAsync(gcount, 0, 8, s)) != cudaSuccess) return cuda_fail(e);
+    k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
+                                                                      w.tile_cap, status, gen, gtiles, gcount);
     if ((e = cudaMemsetAsync(counter, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     static int blocks_per_sm = 0, sms = 0;
     if (!blocks_per_sm) {
@@ -448,6 +455,8 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_density_v4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
         cudaFuncSetAttribute(k_density_v4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
+        cudaFuncSetAttribute(k_density_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
+        cudaFuncSetAttribute(k_density_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_density_v4<false>, V4_TP, V4_SMEM);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
@@ -457,6 +466,13 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
         k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter, gen);
     else
         k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter, gen);
+    // the slices k_v4_tiles could not stage (dense clustered cells): warp-level engine
+    if (stats)
+        k_density_dense<true><<<sms * 2, DENSE_WARPS * 32, DENSE_SMEM, s>>>(g, dc, orec, stats, tiles, gtiles, gcount,
+                                                                         gcount + 1, gen);
+    else
+        k_density_dense<false><<<sms * 2, DENSE_WARPS * 32, DENSE_SMEM, s>>>(g, dc, orec, nullptr, tiles, gtiles,
+                                                                          gcount, gcount + 1, gen);
     if (out->n_out > 0)
         k_unpermute<<<grid_blocks(out->n_out, 256, 148 * 16), 256, 0, s>>>(dev_out(out), orec, gen);
     return check_launch();

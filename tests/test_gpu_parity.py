@@ -457,3 +457,21 @@ def test_max_cell_occupancy(pv, occ, code):
         got = dp.out.to_numpy()
         idx = np.arange(0, occ, 997)
         compare(got, oracle.bruteforce(xyzh, vm, targets=idx), idx, "maxocc")
+
+
+@pytest.mark.parametrize("occ", [1500, 3000])
+def test_dense_cells_density_all_vs_oracle(pv, occ):
+    """A cell far above the tile staging capacity: its slices go to k_density_dense (warp-level,
+    chunked staging of the sorted lists).  sph_density_all == the oracle; hits per kind == the
+    oracle's in-range counts; candidates == Code 2 counts (exact windows)."""
+    xyzh, vm, nc = _dense_cell_set(occ)
+    got = run(pv, xyzh, vm, nc, stats=True)
+    ref = oracle.bruteforce(xyzh, vm)
+    compare(got, ref, None, f"dense {occ}")
+    c, unsafe = oracle.pv_counts(xyzh, nc)
+    assert unsafe == 0
+    tot = c.sum(0)
+    band = int(ref["band"].sum())
+    for k in range(4):
+        assert abs(got["stats"]["hits"][k] - tot[k, 2]) <= band
+        assert abs(got["stats"]["cand"][k] - tot[k, 1]) <= max(2, 1e-5 * tot[k, 1])
