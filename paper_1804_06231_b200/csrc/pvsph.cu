@@ -130,7 +130,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
     size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
-        huge_items, mid_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, total;
+        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, total;
     long long tile_cap, huge_cap;
 };
 
@@ -158,13 +158,15 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4, 256);
     w.big_items = o;                     // (cell, chunk) items: cells of > 32 particles, chunks of 256
     o = align_up(o + 8 * (size_t)(n / 32 + 64), 256);
-    w.huge_count = o;                    // [medium, huge, mid (k_sort_mid), -]
+    w.huge_count = o;                    // [medium, huge, mid (k_sort_mid), w256 (k_sort_warp256)]
     o = align_up(o + 16, 256);
     w.huge_items = o;                    // cells of > SORT_MED particles (medium from the front, huge from the back)
     w.huge_cap = n / SORT_MED + 64;
     o = align_up(o + 4 * (size_t)w.huge_cap, 256);
     w.mid_items = o;                     // cells of SORT_SMALL < n <= SORT_MED particles
     o = align_up(o + 4 * (size_t)(n / (SORT_SMALL + 1) + 64), 256);
+    w.w256_items = o;                    // cells of SORT_MED < n <= SORT_W256 particles
+    o = align_up(o + 4 * (size_t)(n / (SORT_MED + 1) + 64), 256);
     const long long nkeys = row_pairs(g).nkeys;
     w.rows = o;
     o = align_up(o + 4 * (size_t)(nkeys + 1), 256);
@@ -298,7 +300,7 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     int *huge_items = at<int>(ws, w.huge_items);
     if ((e = cudaMemsetAsync(big_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMemsetAsync(huge_count, 0, 16, s)) != cudaSuccess) return cuda_fail(e);
-    int *mid_items = at<int>(ws, w.mid_items);
+    int *mid_items = at<int>(ws, w.mid_items), *w256_items = at<int>(ws, w.w256_items);
     DevCells c = dev_cells(cells);
     int *need = nullptr;
     if (g.h_home_max > 0.0f) {                 // level pass: sort only cells next to home particles
@@ -308,8 +310,9 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     }
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
         g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap,
-        mid_items, huge_count + 2, need);
+        mid_items, huge_count + 2, w256_items, huge_count + 3, need);
     k_sort_mid<<<148 * 8, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, mid_items, huge_count + 2, need);
+    k_sort_warp256<<<148 * 4, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, w256_items, huge_count + 3, need);
     k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count, need);
     static bool huge_attr = false;
     if (!huge_attr) {

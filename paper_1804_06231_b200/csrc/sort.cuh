@@ -10,6 +10,7 @@
 // Small cells (n <= SORT_SMALL = 32): one warp per cell, one particle per lane,
 // 32-bit composites (quantised fp32 key, in-cell index) ranked by counting.
 // Cells of up to SORT_MED = 128: k_sort_mid, one warp per cell, same composites.
+// Cells of up to SORT_W256 = 256: k_sort_warp256, a register bitonic sort per warp.
 // Medium/huge cells: bitonic sorts in shared memory (k_sort_bitonic).  Cells above
 // SORT_HUGE_MAX are queued as (cell, chunk) items and ranked by k_sort_big, one
 // CTA per chunk of SORT_BIG_CHUNK elements, streaming the cell's 64-bit
@@ -21,11 +22,12 @@
 namespace pvsph {
 
 constexpr int SORT_SMALL = 32;
-constexpr int SORT_MED = 128;           // cells above: one CTA sorts each direction (bitonic, shared memory)
+constexpr int SORT_MED = 128;           // cells above: bitonic sorts (k_sort_warp256, k_sort_bitonic)
+constexpr int SORT_W256 = 256;          //   up to here: one warp per cell, in registers (k_sort_warp256)
 constexpr int SORT_MED_MAX = 2048;      //   medium tier: 256 threads, 16 KB shared memory
 constexpr int SORT_MED_T = 256;
 constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 1024 threads, 128 KB; above it chunked ranking again
-constexpr int SORT_HUGE_T = 1024;
+constexpr int SORT_HUGE_T = 512;
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_BIG_CHUNK = 256;
 constexpr int SORT_BIG_TILE = 2048;
@@ -82,6 +84,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
                                                                     long long cbeg, long long cend, int2 *big_items,
                                                                     int *big_count, int *huge_items, int *huge_count,
                                                                     int huge_cap, int *mid_items, int *mid_count,
+                                                                    int *w256_items, int *w256_count,
                                                                     const int *__restrict__ need)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
@@ -101,6 +104,10 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const long long cell = base + j;
         const int s0 = __shfl_sync(0xffffffffu, my_s0, j);
         const int n = __shfl_sync(0xffffffffu, my_n, j);
+        if (n > SORT_MED && n <= SORT_W256) {              // k_sort_warp256
+            if (lane == 0) w256_items[atomicAdd(w256_count, 1)] = (int)cell;
+            continue;
+        }
         if (n > SORT_MED && n <= SORT_HUGE_MAX) {
             // medium cells from the front of the list, huge ones from the back (k_sort_bitonic)
             if (lane == 0) {
@@ -174,54 +181,188 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
     }
 }
 
-// One CTA per cell of SORT_MED < n <= MAXN particles (clustered data): for each direction the
+// One CTA per cell of SORT_W256 < n <= MAXN particles (clustered data): for each direction the
 // 64-bit composites (orderable fp32 key << 32 | in-cell index; in-cell order is the input
-// order) are bitonic-sorted in shared memory, O(n log^2 n) instead of O(n^2).  FROM_BACK:
-// the items are stored from the back of the list (huge tier).
+// order) are bitonic-sorted over P = next power of two >= n in shared memory, with every
+// exchange at distance j < 256 done in registers: a warp holds a 256-element chunk (8 per
+// lane; j < 8 inside the lane, 8 <= j < 256 by shuffles).  Each chunk is first sorted whole in
+// registers; then for every merge size k >= 512 the distances j >= 256 take one shared-memory
+// stage and a barrier each, the last eight distances one register pass.  FROM_BACK: the items
+// are stored from the back of the list (huge tier).
+constexpr int BT_CHUNK = 256;
+constexpr int BT_E = BT_CHUNK / 32;
+
+// Bitonic stages j = J0, J0/2, ..., 1 of merge size k on the warp's chunk in registers
+// (element index i = base + 8 lane + q).
+template <int J0>
+__device__ __forceinline__ void bt_reg_stages(unsigned long long (&v)[BT_E], int base, int lane, int k)
+{
+#pragma unroll
+    for (int j = J0; j > 0; j >>= 1) {
+        if (j >= BT_E) {
+#pragma unroll
+            for (int q = 0; q < BT_E; ++q) {
+                const int i = base + lane * BT_E + q, l = i ^ j;
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[q], j / BT_E);
+                const bool lo = ((i & k) == 0) == (i < l);
+                v[q] = lo ? (o < v[q] ? o : v[q]) : (o > v[q] ? o : v[q]);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < BT_E; ++q) {
+                if (q & j) continue;
+                const int i = base + lane * BT_E + q;
+                const unsigned long long a = v[q], b = v[q + j];
+                const bool sw = ((i & k) == 0) ? (a > b) : (a < b);
+                v[q] = sw ? b : a;
+                v[q + j] = sw ? a : b;
+            }
+        }
+    }
+}
+
 template <int MAXN, int T, bool FROM_BACK>
 __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint16_t *ord, const int *items,
                                                    const int *count, int cap, const int *__restrict__ need)
 {
     extern __shared__ unsigned long long hs[];           // MAXN composites
+    constexpr int NW = T / 32;
     const int nitems = *count;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         const long long cell = items[FROM_BACK ? cap - 1 - it : it];
         const int s0 = c.cell_start[cell];
         const int n = c.cell_start[cell + 1] - s0;
-        int P = 1;
+        int P = BT_CHUNK;
         while (P < n) P <<= 1;
         double corner[3];
         cell_corner(g, cell, corner);
         const int mask = need ? need[cell] : 0x1fff;
         for (int d = 0; d < SPH_NDIR; ++d) {
             if (!((mask >> d) & 1)) continue;          // CTA-uniform
-            for (int e = threadIdx.x; e < P; e += T) {
-                unsigned long long comp = ~0ull;
-                if (e < n) {
-                    const float4 p = c.xyzh[s0 + e];
-                    const float key = pv_key((double)p.x - corner[0], (double)p.y - corner[1], (double)p.z - corner[2], d);
-                    comp = ((unsigned long long)float_order(key) << 32) | (unsigned)e;
+            // chunks: composites straight into registers, sorted whole (k = 2 .. 256)
+            for (int ch = w; ch < P / BT_CHUNK; ch += NW) {
+                const int base = ch * BT_CHUNK;
+                unsigned long long v[BT_E];
+#pragma unroll
+                for (int q = 0; q < BT_E; ++q) {
+                    const int e = base + lane * BT_E + q;
+                    v[q] = ~0ull;
+                    if (e < n) {
+                        const float4 p = c.xyzh[s0 + e];
+                        const float key = pv_key((double)p.x - corner[0], (double)p.y - corner[1],
+                                                 (double)p.z - corner[2], d);
+                        v[q] = ((unsigned long long)float_order(key) << 32) | (unsigned)e;
+                    }
                 }
-                hs[e] = comp;
+                bt_reg_stages<1>(v, base, lane, 2);
+                bt_reg_stages<2>(v, base, lane, 4);
+                bt_reg_stages<4>(v, base, lane, 8);
+                bt_reg_stages<8>(v, base, lane, 16);
+                bt_reg_stages<16>(v, base, lane, 32);
+                bt_reg_stages<32>(v, base, lane, 64);
+                bt_reg_stages<64>(v, base, lane, 128);
+                bt_reg_stages<128>(v, base, lane, 256);
+#pragma unroll
+                for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
             }
-            __syncthreads();
-            for (int k = 2; k <= P; k <<= 1) {
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    for (int i = threadIdx.x; i < P; i += T) {
-                        const int ixj = i ^ j;
-                        if (ixj > i) {
-                            const unsigned long long a = hs[i], b = hs[ixj];
-                            if ((a > b) == ((i & k) == 0)) {
-                                hs[i] = b;
-                                hs[ixj] = a;
-                            }
+            for (int k = 2 * BT_CHUNK; k <= P; k <<= 1) {
+                for (int j = k >> 1; j >= BT_CHUNK; j >>= 1) {
+                    __syncthreads();
+                    for (int pi = threadIdx.x; pi < P / 2; pi += T) {
+                        const int i = (pi / j) * 2 * j + (pi % j), l = i + j;
+                        const unsigned long long a = hs[i], b = hs[l];
+                        const bool sw = ((i & k) == 0) ? (a > b) : (a < b);
+                        if (sw) {
+                            hs[i] = b;
+                            hs[l] = a;
                         }
                     }
-                    __syncthreads();
+                }
+                __syncthreads();
+                for (int ch = w; ch < P / BT_CHUNK; ch += NW) {
+                    const int base = ch * BT_CHUNK;
+                    unsigned long long v[BT_E];
+#pragma unroll
+                    for (int q = 0; q < BT_E; ++q) v[q] = hs[base + lane * BT_E + q];
+                    bt_reg_stages<128>(v, base, lane, k);
+#pragma unroll
+                    for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
                 }
             }
+            __syncthreads();
             for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
             __syncthreads();
+        }
+    }
+}
+
+// Cells of SORT_MED < n <= SORT_W256 particles: one warp per cell, bitonic sort of the 64-bit
+// composites of k_sort_bitonic over P = 256 elements held in registers (lane l holds elements
+// 8 l .. 8 l + 7): exchanges at distance j < 8 inside the lane, j >= 8 by warp shuffles; no
+// shared memory, no barrier, eight cells per CTA at a time.
+__global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_warp256(DevGrid g, DevCells c, uint16_t *ord,
+                                                                   const int *__restrict__ items,
+                                                                   const int *__restrict__ count,
+                                                                   const int *__restrict__ need)
+{
+    constexpr int E = SORT_W256 / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nitems = *count;
+    for (int it = blockIdx.x * SORT_WARPS + w; it < nitems; it += gridDim.x * SORT_WARPS) {
+        const long long cell = items[it];
+        const int s0 = c.cell_start[cell];
+        const int n = c.cell_start[cell + 1] - s0;
+        double corner[3];
+        cell_corner(g, cell, corner);
+        const int mask = need ? need[cell] : 0x1fff;
+        float4 p[E];
+#pragma unroll
+        for (int q = 0; q < E; ++q) {
+            const int e = lane * E + q;
+            p[q] = e < n ? c.xyzh[s0 + e] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll 1
+        for (int d = 0; d < SPH_NDIR; ++d) {
+            if (!((mask >> d) & 1)) continue;              // warp-uniform
+            unsigned long long v[E];
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int e = lane * E + q;
+                const float key = pv_key((double)p[q].x - corner[0], (double)p[q].y - corner[1],
+                                         (double)p[q].z - corner[2], d);
+                v[q] = e < n ? ((unsigned long long)float_order(key) << 32) | (unsigned)e : ~0ull;
+            }
+#pragma unroll
+            for (int k = 2; k <= SORT_W256; k <<= 1) {
+#pragma unroll
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    if (j >= E) {
+#pragma unroll
+                        for (int q = 0; q < E; ++q) {
+                            const int i = lane * E + q, l = i ^ j;
+                            const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[q], j / E);
+                            const bool lo = ((i & k) == 0) == (i < l);
+                            v[q] = lo ? (o < v[q] ? o : v[q]) : (o > v[q] ? o : v[q]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < E; ++q) {
+                            if (q & j) continue;
+                            const int i = lane * E + q;
+                            const unsigned long long a = v[q], b = v[q + j];
+                            const bool sw = ((i & k) == 0) ? (a > b) : (a < b);
+                            v[q] = sw ? b : a;
+                            v[q + j] = sw ? a : b;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                const int e = lane * E + q;
+                if (e < n) ord[(long long)d * c.cap + s0 + e] = (uint16_t)(v[q] & 0xffffffffull);
+            }
         }
     }
 }
