@@ -16,6 +16,7 @@
 // 64 (stable read) + 40 (write) ~ 250 B (random-access granularity).
 #pragma once
 
+#include "bitonic.cuh"
 #include "common.cuh"
 
 namespace pvsph {
@@ -186,6 +187,8 @@ constexpr int STABLE_SMALL = 128;
 constexpr int STABLE_WARPS = 8;
 constexpr int STABLE_BIG_CHUNK = 256;
 constexpr int STABLE_BIG_TILE = 4096;
+constexpr int STABLE_BT_MAX = 16384;     // cells of STABLE_SMALL < n <= this: k_stable_bitonic
+constexpr int STABLE_BT_T = 512;
 
 // One warp per cell of <= STABLE_SMALL particles: rank each input index among the
 // cell's (all distinct) and move its record there.  Larger cells are queued as
@@ -206,7 +209,8 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
                                                                     int *__restrict__ cell_nhome,
-                                                                    int2 *big_items, int *big_count)
+                                                                    int2 *big_items, int *big_count, int *bt_items,
+                                                                    int *bt_count)
 {
     __shared__ unsigned sh[STABLE_WARPS][STABLE_SMALL];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -232,6 +236,10 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         }
         nh = __reduce_add_sync(0xffffffffu, nh);
         if (lane == 0) cell_nhome[cell] = nh;
+        if (n > STABLE_SMALL && n <= STABLE_BT_MAX) {      // k_stable_bitonic
+            if (lane == 0) bt_items[atomicAdd(bt_count, 1)] = (int)cell;
+            continue;
+        }
         if (n > STABLE_SMALL) {
             if (lane == 0) {
                 int nch = (n + STABLE_BIG_CHUNK - 1) / STABLE_BIG_CHUNK;
@@ -259,6 +267,44 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         }
         __syncwarp();
       }
+    }
+}
+
+// One CTA per cell of STABLE_SMALL < n <= STABLE_BT_MAX particles: the records' keys (input
+// index | not-home bit << 31) with their in-cell position as 64-bit composites, bitonic-sorted
+// (bitonic.cuh: 256-element chunks in registers, distances >= 256 through shared memory), then
+// every record moved to its rank.  Keys are distinct, so the order is the stable one.
+__global__ void __launch_bounds__(STABLE_BT_T) k_stable_bitonic(const int *__restrict__ start,
+                                                                const ParticleRec *__restrict__ rec,
+                                                                float4 *__restrict__ xyzh, float4 *__restrict__ vm,
+                                                                int *__restrict__ perm, const int *__restrict__ items,
+                                                                const int *__restrict__ count)
+{
+    extern __shared__ unsigned long long hs[];            // STABLE_BT_MAX composites
+    constexpr int NW = STABLE_BT_T / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nitems = *count;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const long long cell = items[it];
+        const int s0 = start[cell], n = start[cell + 1] - s0;
+        int P = BT_CHUNK;
+        while (P < n) P <<= 1;
+        for (int ch = w; ch < P / BT_CHUNK; ch += NW) {
+            const int base = ch * BT_CHUNK;
+            unsigned long long v[BT_E];
+#pragma unroll
+            for (int q = 0; q < BT_E; ++q) {
+                const int e = base + lane * BT_E + q;
+                v[q] = e < n ? ((unsigned long long)(unsigned)rec[s0 + e].idx << 32) | (unsigned)e : ~0ull;
+            }
+            bt_sort_chunk(v, base, lane);
+#pragma unroll
+            for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
+        }
+        bt_cta_merge<STABLE_BT_T>(hs, P, lane, w);
+        for (int r = threadIdx.x; r < n; r += STABLE_BT_T)
+            stable_place(s0, (int)(hs[r] & 0xffffffffull), r, rec, xyzh, vm, perm);
+        __syncthreads();
     }
 }
 

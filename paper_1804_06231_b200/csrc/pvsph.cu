@@ -268,9 +268,18 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         k_scatter_rec<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n, cell_of, rank, cells->cell_start, xin,
                                                                     vin, rec);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
+        int *bt_items = at<int>(ws, w.huge_items), *bt_count = at<int>(ws, w.huge_count);
+        if ((e = cudaMemsetAsync(bt_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
             g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, big_items,
-            big_count);
+            big_count, bt_items, bt_count);
+        static bool bt_attr = false;
+        if (!bt_attr) {
+            cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
+            bt_attr = true;
+        }
+        k_stable_bitonic<<<148, STABLE_BT_T, STABLE_BT_MAX * 8, s>>>(cells->cell_start, rec, xs, vs, cells->perm,
+                                                                    bt_items, bt_count);
         k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, big_items,
                                                           big_count);
     }

@@ -17,6 +17,7 @@
 // composites (orderable fp32 key << 32 | input index) through shared memory.
 #pragma once
 
+#include "bitonic.cuh"
 #include "common.cuh"
 
 namespace pvsph {
@@ -189,38 +190,6 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
 // registers; then for every merge size k >= 512 the distances j >= 256 take one shared-memory
 // stage and a barrier each, the last eight distances one register pass.  FROM_BACK: the items
 // are stored from the back of the list (huge tier).
-constexpr int BT_CHUNK = 256;
-constexpr int BT_E = BT_CHUNK / 32;
-
-// Bitonic stages j = J0, J0/2, ..., 1 of merge size k on the warp's chunk in registers
-// (element index i = base + 8 lane + q).
-template <int J0>
-__device__ __forceinline__ void bt_reg_stages(unsigned long long (&v)[BT_E], int base, int lane, int k)
-{
-#pragma unroll
-    for (int j = J0; j > 0; j >>= 1) {
-        if (j >= BT_E) {
-#pragma unroll
-            for (int q = 0; q < BT_E; ++q) {
-                const int i = base + lane * BT_E + q, l = i ^ j;
-                const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[q], j / BT_E);
-                const bool lo = ((i & k) == 0) == (i < l);
-                v[q] = lo ? (o < v[q] ? o : v[q]) : (o > v[q] ? o : v[q]);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < BT_E; ++q) {
-                if (q & j) continue;
-                const int i = base + lane * BT_E + q;
-                const unsigned long long a = v[q], b = v[q + j];
-                const bool sw = ((i & k) == 0) ? (a > b) : (a < b);
-                v[q] = sw ? b : a;
-                v[q + j] = sw ? a : b;
-            }
-        }
-    }
-}
-
 template <int MAXN, int T, bool FROM_BACK>
 __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint16_t *ord, const int *items,
                                                    const int *count, int cap, const int *__restrict__ need)
@@ -255,42 +224,11 @@ __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint1
                         v[q] = ((unsigned long long)float_order(key) << 32) | (unsigned)e;
                     }
                 }
-                bt_reg_stages<1>(v, base, lane, 2);
-                bt_reg_stages<2>(v, base, lane, 4);
-                bt_reg_stages<4>(v, base, lane, 8);
-                bt_reg_stages<8>(v, base, lane, 16);
-                bt_reg_stages<16>(v, base, lane, 32);
-                bt_reg_stages<32>(v, base, lane, 64);
-                bt_reg_stages<64>(v, base, lane, 128);
-                bt_reg_stages<128>(v, base, lane, 256);
+                bt_sort_chunk(v, base, lane);
 #pragma unroll
                 for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
             }
-            for (int k = 2 * BT_CHUNK; k <= P; k <<= 1) {
-                for (int j = k >> 1; j >= BT_CHUNK; j >>= 1) {
-                    __syncthreads();
-                    for (int pi = threadIdx.x; pi < P / 2; pi += T) {
-                        const int i = (pi / j) * 2 * j + (pi % j), l = i + j;
-                        const unsigned long long a = hs[i], b = hs[l];
-                        const bool sw = ((i & k) == 0) ? (a > b) : (a < b);
-                        if (sw) {
-                            hs[i] = b;
-                            hs[l] = a;
-                        }
-                    }
-                }
-                __syncthreads();
-                for (int ch = w; ch < P / BT_CHUNK; ch += NW) {
-                    const int base = ch * BT_CHUNK;
-                    unsigned long long v[BT_E];
-#pragma unroll
-                    for (int q = 0; q < BT_E; ++q) v[q] = hs[base + lane * BT_E + q];
-                    bt_reg_stages<128>(v, base, lane, k);
-#pragma unroll
-                    for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
-                }
-            }
-            __syncthreads();
+            bt_cta_merge<T>(hs, P, lane, w);
             for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
             __syncthreads();
         }

@@ -29,7 +29,7 @@ import torch
 
 from . import api as pv
 
-BUILD_LAUNCHES = 7      # k_bin, 3 scan kernels, k_scatter_rec, k_stable_small/big
+BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_rec, k_stable_small/bitonic/big
 SORT_LAUNCHES = 6       # k_sort_small, k_sort_mid, k_sort_warp256, k_sort_big, k_sort_bitonic (medium, huge)
 DENSITY_LAUNCHES = 8    # k_v4_tiles (count), 3 scan kernels, k_v4_tiles (write), k_density_v4, k_density_dense,
                         # k_unpermute
