@@ -64,3 +64,43 @@ def test_e2e_pipeline_results(pv):
         assert np.array_equal(single[f], got[f]), f
     for k, ax in enumerate("xyz"):
         assert np.array_equal(single["curl_" + ax], got["curl_v"][k]), ax
+
+
+def test_symmetric_pairs_on_slabs(pv):
+    """sph_density_pair_sym on x-slabs: j in a ghost cell is never updated.  Each rank lists,
+    for every owned cell, the 13 positive offsets (an owned or ghost neighbour) plus the
+    negative offsets that land in a ghost plane; + self over owned cells + finalize, gathered
+    over ranks == the oracle."""
+    import torch
+    from paper_1804_06231_b200.slabs import FakeRanks
+    p = synth.make("c2")
+    fr = FakeRanks(p, 2)
+    fr.step()                                    # builds cells with ghosts on every rank
+    res = {}
+    for r in fr.runners:
+        ny = nz = p.nc
+        nxl = r.nxl
+        cells = np.arange(nxl * ny * nz)
+        jx, iy, iz = cells // (ny * nz), (cells // nz) % ny, cells % nz
+        own = (jx >= 1) & (jx < nxl - 1)
+        pairs = []
+        for a in (-1, 0, 1):
+            for b in (-1, 0, 1):
+                for c in (-1, 0, 1):
+                    if (a, b, c) == (0, 0, 0):
+                        continue
+                    kx = jx + a
+                    cj = (kx * ny + (iy + b) % ny) * nz + (iz + c) % nz
+                    ghost_j = (kx == 0) | (kx == nxl - 1)
+                    sel = own & (kx >= 0) & (kx < nxl) & (((a, b, c) > (0, 0, 0)) | ghost_j)
+                    pairs.append(np.stack([cells[sel], cj[sel]], 1))
+        pr = torch.from_numpy(np.concatenate(pairs).astype(np.int32)).cuda().contiguous()
+        acc = pv.Out.alloc(r.n_own, zero=True)
+        owned = torch.from_numpy(cells[own].astype(np.int32)).cuda()
+        pv.sph_density_self(r.grid, r.cells, owned, acc, r.ws)
+        pv.sph_density_pair_sym(r.grid, r.cells, pr, acc, r.ws)
+        pv.sph_density_finalize(acc)
+        r.check()
+        for k, v in acc.to_numpy().items():
+            res.setdefault(k, np.zeros(p.n, v.dtype))[r.slab.gid] = v
+    compare(res, oracle.celllist(p.xyzh, p.vm, p.nc), None, "symmetric pairs on slabs")
