@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--levels", type=int, default=0,
                     help="level passes (DESIGN.md §4.5); 0 = auto: 3 for the clustered c4, else 1")
+    ap.add_argument("--balance", type=int, default=-1,
+                    help="N > 1: x-slab cuts by estimated work (1) or equal planes (0); -1 = auto: on for c4")
     return ap.parse_args()
 
 
@@ -265,7 +267,8 @@ def run_ours(args):
         p = synth.make(args.config)
         part = slabs.Slab.single(p)
     else:
-        part = slabs.Slab.from_config(args.config, rank, world)
+        balance = args.balance if args.balance >= 0 else int(args.config == "c4")
+        part = slabs.Slab.from_config(args.config, rank, world, balance=bool(balance))
     t_gen = time.perf_counter() - t_gen
 
     nlev = args.levels or (3 if args.config == "c4" and world == 1 else 1)
@@ -357,6 +360,7 @@ def run_ours(args):
                 "config": {"workload": f"{args.config} (BASELINE.json configs, DESIGN.md §3)",
                            "n_particles": part.n_global, "cells": f"{part.nc}^3",
                            "parallelism": f"x-slab{world}" if world > 1 else "single",
+                           "slab_planes": [part.x_lo, part.x_hi] if world > 1 else None,
                            "level_grids": [lv[0] for lv in runner.levels],
                            "l2": "inputs (>= 4 GB at c5) larger than L2; no flush",
                            "step": "ghost exchange + build_cells + sort_cells + density_all"},

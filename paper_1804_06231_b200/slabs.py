@@ -39,6 +39,47 @@ def slab_bounds(nc: int, world: int, rank: int) -> tuple[int, int]:
     return rank * nc // world, (rank + 1) * nc // world
 
 
+def plane_costs(xyzh: np.ndarray, nc: int, box: float = 1.0) -> np.ndarray:
+    """Estimated density work per x-plane: sum over its cells of n_c x (particles in the 27
+    cells around c), the naive candidate count of the cell (SURVEY.md §8(f) #2 "slab cuts by
+    estimated work"; periodic neighbours)."""
+    x = xyzh[:, :3].astype(np.float64) * nc / box
+    ijk = np.clip(np.floor(x), 0, nc - 1).astype(np.int64)
+    cnt = np.bincount((ijk[:, 0] * nc + ijk[:, 1]) * nc + ijk[:, 2], minlength=nc ** 3).reshape(nc, nc, nc)
+    nb = np.zeros_like(cnt)
+    for a in (-1, 0, 1):
+        for b in (-1, 0, 1):
+            for c in (-1, 0, 1):
+                nb += np.roll(cnt, (a, b, c), axis=(0, 1, 2))
+    return (cnt * nb).sum(axis=(1, 2)).astype(np.float64)
+
+
+def balanced_bounds(costs: np.ndarray, world: int, min_planes: int = 2) -> list[tuple[int, int]]:
+    """x-slab cuts minimising the largest per-rank estimated cost (contiguous partition of the
+    planes, each slab >= `min_planes` planes: the ghost exchange needs two); dynamic programming
+    over (rank, cut plane).  Equal cuts are one feasible partition, so the result is never worse."""
+    nc = len(costs)
+    if nc < world * min_planes:
+        raise ValueError("each slab needs >= 2 cell planes")
+    cum = np.concatenate([[0.0], np.cumsum(np.asarray(costs, np.float64))])
+    inf = float("inf")
+    best = np.full((world + 1, nc + 1), inf)       # best[r][i]: planes [0, i) on r ranks
+    arg = np.zeros((world + 1, nc + 1), np.int64)
+    best[0][0] = 0.0
+    for r in range(1, world + 1):
+        for i in range(r * min_planes, nc - (world - r) * min_planes + 1):
+            for j in range((r - 1) * min_planes, i - min_planes + 1):
+                v = max(best[r - 1][j], cum[i] - cum[j])
+                if v < best[r][i]:
+                    best[r][i], arg[r][i] = v, j
+    bounds, i = [], nc
+    for r in range(world, 0, -1):
+        j = int(arg[r][i])
+        bounds.append((j, i))
+        i = j
+    return bounds[::-1]
+
+
 def planes_of(xyzh: np.ndarray, nc: int, box: float = 1.0) -> np.ndarray:
     """Cell x-plane of every particle: floor(x nc / box) in fp64, clamped (same rule as sph_build_cells)."""
     return np.clip(np.floor(xyzh[:, 0].astype(np.float64) * nc / box), 0, nc - 1).astype(np.int64)
@@ -64,21 +105,25 @@ class Slab:
         return Slab(p.nc, p.box, p.gamma, 0, 1, 0, p.nc, p.xyzh, p.vm, np.arange(p.n), p.n, p)
 
     @staticmethod
-    def from_set(p, rank: int, world: int) -> "Slab":
+    def from_set(p, rank: int, world: int, bounds: list | None = None) -> "Slab":
+        """bounds: [(x_lo, x_hi)] per rank (balanced_bounds), else equal plane counts."""
         if world == 1:
             return Slab.single(p)
-        if p.nc // world < 2:
+        if bounds is None and p.nc // world < 2:
             raise ValueError("each slab needs >= 2 cell planes")
-        lo, hi = slab_bounds(p.nc, world, rank)
+        lo, hi = bounds[rank] if bounds is not None else slab_bounds(p.nc, world, rank)
         pl = planes_of(p.xyzh, p.nc, p.box)
         gid = np.nonzero((pl >= lo) & (pl < hi))[0]
         return Slab(p.nc, p.box, p.gamma, rank, world, lo, hi, np.ascontiguousarray(p.xyzh[gid]),
                     np.ascontiguousarray(p.vm[gid]), gid, p.n)
 
     @staticmethod
-    def from_config(cfg: str, rank: int, world: int) -> "Slab":
+    def from_config(cfg: str, rank: int, world: int, balance: bool = False) -> "Slab":
+        """balance: cut the slabs by estimated work (plane_costs) instead of equal planes."""
         import synth
-        return Slab.from_set(synth.make(cfg), rank, world)
+        p = synth.make(cfg)
+        bounds = balanced_bounds(plane_costs(p.xyzh, p.nc, p.box), world) if balance and world > 1 else None
+        return Slab.from_set(p, rank, world, bounds)
 
     @property
     def n_own(self) -> int:
@@ -289,9 +334,12 @@ class FakeRanks:
     device copies instead of NCCL (a test harness for the slab logic; nothing waits
     on another rank, every launch is ordered on one stream)."""
 
-    def __init__(self, p, world: int, device="cuda"):
+    def __init__(self, p, world: int, device="cuda", balance: bool = False):
         self.world = world
-        self.runners = [SlabRunner(Slab.from_set(p, r, world), dist=None, device=device) for r in range(world)]
+        bounds = balanced_bounds(plane_costs(p.xyzh, p.nc, p.box), world) if balance else None
+        self.bounds = bounds
+        self.runners = [SlabRunner(Slab.from_set(p, r, world, bounds), dist=None, device=device)
+                        for r in range(world)]
         for r in self.runners:
             r.upload()
         self.n_global = p.n

@@ -104,3 +104,19 @@ def test_symmetric_pairs_on_slabs(pv):
         for k, v in acc.to_numpy().items():
             res.setdefault(k, np.zeros(p.n, v.dtype))[r.slab.gid] = v
     compare(res, oracle.celllist(p.xyzh, p.vm, p.nc), None, "symmetric pairs on slabs")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_balanced_slabs_bitwise_equal_single(pv, world):
+    """Cost-balanced (uneven) x-slab cuts on clustered data: outputs bitwise identical to the
+    single-GPU pass on the same grid (the tile cut and every particle's summation order do
+    not depend on where the slabs are cut)."""
+    from paper_1804_06231_b200.slabs import FakeRanks, slab_bounds
+    p = synth.clustered_set("cl64k", seed=7, n=65536, nc=13, n_spheres=16)
+    single = pv.density(p.xyzh, p.vm, p.nc)
+    fr = FakeRanks(p, world, balance=True)
+    assert fr.bounds != [slab_bounds(p.nc, world, r) for r in range(world)]   # really uneven
+    fr.step()
+    got = fr.gather()
+    for f in single:
+        assert np.array_equal(single[f], got[f]), (world, f)

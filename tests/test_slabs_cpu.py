@@ -79,3 +79,34 @@ def test_ghost_exchange_gloo(world, sizes):
     for p in procs:
         p.join(timeout=60)
     assert all(res[r] for r in range(world)), res
+
+
+def test_balanced_bounds_cover_and_balance():
+    """Cost-balanced x-slab cuts: contiguous cover of all planes, >= 2
+    planes per slab, and on clustered data a smaller max/mean cost than equal cuts."""
+    import numpy as np
+    import synth
+    from paper_1804_06231_b200.slabs import balanced_bounds, plane_costs, slab_bounds
+    p = synth.clustered_set("cl64k", seed=7, n=65536, nc=13, n_spheres=16)
+    costs = plane_costs(p.xyzh, p.nc)
+    assert costs.shape == (13,) and np.all(costs >= 0)
+    for world in (2, 3, 4, 6):
+        b = balanced_bounds(costs, world)
+        assert b[0][0] == 0 and b[-1][1] == 13 and all(b[k][1] == b[k + 1][0] for k in range(world - 1))
+        assert all(hi - lo >= 2 for lo, hi in b)
+        imb = max(costs[lo:hi].sum() for lo, hi in b) / (costs.sum() / world)
+        eq = [slab_bounds(13, world, r) for r in range(world)]
+        imb_eq = max(costs[lo:hi].sum() for lo, hi in eq) / (costs.sum() / world)
+        assert imb <= imb_eq + 1e-9, (world, imb, imb_eq)
+
+
+def test_plane_costs_uniform_lattice():
+    """Closed form: one particle per cell of an nc^3 lattice -> every cell costs 1 x 27."""
+    import numpy as np
+    from paper_1804_06231_b200.slabs import plane_costs
+    nc = 5
+    g = (np.arange(nc) + 0.5) / nc
+    x, y, z = np.meshgrid(g, g, g, indexing="ij")
+    xyzh = np.zeros((nc ** 3, 4), np.float32)
+    xyzh[:, 0], xyzh[:, 1], xyzh[:, 2] = x.ravel(), y.ravel(), z.ravel()
+    assert np.array_equal(plane_costs(xyzh, nc), np.full(nc, 27.0 * nc * nc))
