@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 3
+#define SPH_ABI_VERSION 4
 
 #define SPH_OK 0
 #define SPH_EINVAL 1
@@ -93,7 +93,13 @@ typedef struct sph_grid {
                         /*   are HOME (outputs computed) on this grid; the  */
                         /*   others are binned as neighbour sources only    */
                         /*   and may have gamma*h > C_l.  0, 0: all home.   */
-    float reserved2;    /* must be 0                                        */
+    float skin;         /* list reuse: the      */
+                        /*   largest displacement any particle may have had */
+                        /*   since the cells and lists were built (moved by */
+                        /*   sph_drift); 0 = none.  The build then requires */
+                        /*   gamma*h + 2*skin <= C_l for home particles and */
+                        /*   the density calls widen every window by 4*skin */
+                        /*   (DESIGN.md §4.6).                              */
 } sph_grid;
 
 /* Per-direction sorted lists ("index" of P:92).  For cell c and direction
@@ -231,6 +237,16 @@ int sph_status_reset(void *ws, void *stream);
 /* Static description of an error code (the last CUDA error text for
  * SPH_ECUDA). */
 const char *sph_strerror(int code);
+
+/* List reuse ("max_dx"): move every stored
+ * particle of `cells` by its velocity, x <- fp32(x + fp32(v * dt)) per
+ * component (two roundings), keeping cells, order and lists as they are.
+ * Positions may leave [0, box) by up to the skin.  If max_disp (device
+ * float, caller-initialised) is not NULL it receives the largest |v| dt
+ * (atomic max).  The caller keeps the accumulated displacement below the
+ * grid's skin and rebuilds (sph_build_cells + sph_sort_cells) before it
+ * would exceed it; the density calls on the same grid are then exact. */
+int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp, void *stream);
 
 /* SPH_ABI_VERSION of the loaded library. */
 int sph_abi_version(void);

@@ -39,8 +39,9 @@ def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
     return ctypes.c_void_p(0 if t is None else t.data_ptr())
 
 
-def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0, h_home=None) -> SphGrid:
-    """h_home = (h_min, h_max): level pass, only particles with h_min < h <= h_max are home."""
+def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0, h_home=None, skin=0.0) -> SphGrid:
+    """h_home = (h_min, h_max): level pass, only particles with h_min < h <= h_max are home.
+    skin: list reuse, the largest displacement allowed between rebuilds (include/sph.h)."""
     if isinstance(nc, int):
         nc = (nc, nc, nc)
     if isinstance(box, (int, float)):
@@ -55,6 +56,7 @@ def make_grid(nc, box=1.0, gamma=GAMMA, x_lo=0, x_hi=None, ghost_x=0, h_home=Non
     g.gamma = float(gamma)
     if h_home is not None:
         g.h_home_min, g.h_home_max = float(h_home[0]), float(h_home[1])
+    g.skin = float(skin)
     return g
 
 
@@ -218,6 +220,14 @@ def sph_density_pair_sym(grid: SphGrid, cells: Cells, pairs: torch.Tensor, acc: 
                                             _stream(stream)), "sph_density_pair_sym")
 
 
+def sph_drift(grid: SphGrid, cells: Cells, dt: float, max_disp: torch.Tensor | None = None, stream=None) -> None:
+    """List reuse: x <- x + v dt for the stored particles (include/sph.h); max_disp: a (1,)
+    float32 device tensor receiving the largest |v| dt (atomic max)."""
+    s = cells.struct()
+    _check(_lib.load().sph_drift(ctypes.byref(grid), ctypes.byref(s), float(dt),
+                                 _ptr(max_disp) if max_disp is not None else None, _stream(stream)), "sph_drift")
+
+
 def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
     o = acc.struct()
     _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),
@@ -250,8 +260,8 @@ class DensityPass:
     build_cells -> sort_cells -> density_all (the hot path)."""
 
     def __init__(self, nc, n_own: int, box=1.0, gamma=GAMMA, capacity: int | None = None, device="cuda",
-                 x_lo=0, x_hi=None, ghost_x=0, h_home=None):
-        self.grid = make_grid(nc, box, gamma, x_lo, x_hi, ghost_x, h_home)
+                 x_lo=0, x_hi=None, ghost_x=0, h_home=None, skin=0.0):
+        self.grid = make_grid(nc, box, gamma, x_lo, x_hi, ghost_x, h_home, skin)
         self.n_own = int(n_own)
         cap = int(capacity if capacity is not None else n_own)
         self.cells = Cells.alloc(self.grid, cap, device)

@@ -36,7 +36,8 @@ __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float
         if (!finite) {
             set_status(status, ST_EDOMAIN);
         } else if (!(a.w > 0.0f) || !(b.w > 0.0f) ||
-                   (is_home(g.h_home_min, g.h_home_max, a.w) && (double)g.gamma * (double)a.w > clmin)) {
+                   (is_home(g.h_home_min, g.h_home_max, a.w) &&
+                    (double)g.gamma * (double)a.w + 2.0 * (double)g.skin > clmin)) {
             // (a neighbour-only particle of a level pass may have gamma h > C_l)
             set_status(status, ST_EH_RANGE);
         } else {
@@ -180,6 +181,33 @@ __global__ void k_scatter_rec(DevGrid g, long long n_total, const int *__restric
                          "r"(key), "r"(0)
                          : "memory");
         }
+    }
+}
+
+// sph_drift: x <- fp32(x + fp32(v dt)) per component for every stored particle (list reuse,
+// DESIGN.md §4.6); the largest |v| dt to *max_disp (non-negative floats order like their bits).
+__global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm, long long n, float dt,
+                        float *max_disp)
+{
+    float mx = 0.0f;
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n;
+         s += (long long)gridDim.x * blockDim.x) {
+        float4 p = xyzh[s];
+        const float4 v = vm[s];
+        const float dx = __fmul_rn(v.x, dt), dy = __fmul_rn(v.y, dt), dz = __fmul_rn(v.z, dt);
+        p.x = __fadd_rn(p.x, dx);
+        p.y = __fadd_rn(p.y, dy);
+        p.z = __fadd_rn(p.z, dz);
+        xyzh[s] = p;
+        mx = fmaxf(mx, sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+    }
+    if (max_disp) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(max_disp), __float_as_int(mx));
     }
 }
 

@@ -30,7 +30,8 @@ struct DevGrid {
     float boxf[3];
     float gamma;
     float h_home_min, h_home_max;   // level passes: home iff h_home_min < h <= h_home_max (max 0: all)
-    float delta;         // window margin SPH_DELTA_FRAC * min(cl)
+    float delta;         // window margin SPH_DELTA_FRAC * min(cl) + 4 skin
+    float skin;          // list reuse: largest displacement since the build (sph_grid.skin)
     float q[SPH_NDIR];   // Q_d = sum_a |d_a| C_a / |d|: projection of the cell offset on axis d
 };
 

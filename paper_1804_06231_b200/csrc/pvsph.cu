@@ -61,14 +61,17 @@ int make_grid(const sph_grid *gr, DevGrid &g)
     g.n_owned_cells = (long long)(gr->x_hi - gr->x_lo) * g.ny * g.nz;
     if (g.ncell >= (1LL << 31) - 1) return SPH_EINVAL;
     g.gamma = gr->gamma;
-    if (gr->reserved != 0 || gr->reserved2 != 0.0f) return SPH_EINVAL;
+    if (gr->reserved != 0 || !(gr->skin >= 0.0f) || !std::isfinite(gr->skin)) return SPH_EINVAL;
     if (!(gr->h_home_max >= 0.0f) || !(gr->h_home_min >= 0.0f) || !std::isfinite(gr->h_home_max) ||
         (gr->h_home_max > 0.0f && !(gr->h_home_min < gr->h_home_max)))
         return SPH_EINVAL;
     g.h_home_min = gr->h_home_min;
     g.h_home_max = gr->h_home_max;
     double clmin = std::fmin(g.cl[0], std::fmin(g.cl[1], g.cl[2]));
-    g.delta = (float)(SPH_DELTA_FRAC * clmin);
+    g.skin = gr->skin;
+    // window margin: the fp32 margin of §4.2 plus 4 skin (stale sort order after drifts, §4.6)
+    g.delta = (float)(SPH_DELTA_FRAC * clmin + 4.0 * (double)gr->skin);
+    if (gr->skin > 0.0f && !(2.0 * (double)gr->skin < clmin)) return SPH_EINVAL;
     for (int d = 0; d < SPH_NDIR; ++d) {
         int nz = 0;
         double q = 0.0;
@@ -410,6 +413,18 @@ int sph_density_pair_sym(const sph_grid *grid, const sph_cells *cells, const int
     else
         k_density_pair_sym<false><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr,
                                                                          npairs, nullptr, status);
+    return check_launch();
+}
+
+int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !std::isfinite(dt)) return SPH_EINVAL;
+    if (cells->n <= 0) return SPH_OK;
+    k_drift<<<grid_blocks(cells->n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<float4 *>(cells->xyzh), reinterpret_cast<const float4 *>(cells->vm), cells->n, dt, max_disp);
     return check_launch();
 }
 

@@ -47,14 +47,14 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.sph_abi_version() == 3
+    assert lib.sph_abi_version() == 4
     for code in range(6):
         assert len(lib.sph_strerror(code)) > 0
 
 
-def _grid(nc=(4, 4, 4), box=1.0, x_lo=0, x_hi=None, ghost=0, gamma=1.825742):
+def _grid(nc=(4, 4, 4), box=1.0, x_lo=0, x_hi=None, ghost=0, gamma=1.825742, skin=0.0):
     from paper_1804_06231_b200.api import make_grid
-    return make_grid(nc, box, gamma, x_lo, x_hi, ghost)
+    return make_grid(nc, box, gamma, x_lo, x_hi, ghost, skin=skin)
 
 
 def test_grid_validation(lib):
@@ -65,6 +65,9 @@ def test_grid_validation(lib):
     assert lib.sph_ncell(ctypes.byref(_grid(x_lo=1, x_hi=3, ghost=1))) == 4 * 16
     assert lib.sph_ncell(ctypes.byref(_grid(nc=(8, 4, 4), x_lo=0, x_hi=7, ghost=1))) < 0   # ghost planes coincide
     assert lib.sph_ncell(ctypes.byref(_grid(gamma=0.0))) < 0
+    assert lib.sph_ncell(ctypes.byref(_grid(skin=0.01))) == 64                 # list reuse margin
+    assert lib.sph_ncell(ctypes.byref(_grid(skin=-0.01))) < 0
+    assert lib.sph_ncell(ctypes.byref(_grid(skin=0.125))) < 0                  # 2 skin >= C_l
     assert lib.sph_workspace_bytes(ctypes.byref(g), 1000) > 8000
     assert lib.sph_workspace_bytes(ctypes.byref(_grid(nc=(1, 4, 4))), 10) == 0
 
