@@ -1,6 +1,6 @@
 // build.cuh -- sph_build_cells: cell binning as a counting sort.
 //
-//   k_bin          : validate, fp64 bin, atomic slot rank within the cell, cell_hmax
+//   k_bin          : validate, fp64 bin, atomic slot rank within the cell
 //   k_scan_*       : exclusive scan of the per-cell counts -> cell_start
 //   k_scatter_rec  : the particle's 64-byte record (x, y, z, h, vx, vy, vz, m,
 //                    input index) to slot cell_start[cell] + rank (two full
@@ -23,7 +23,7 @@ namespace pvsph {
 
 __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float4 *__restrict__ xyzh_in,
                       const float4 *__restrict__ vm_in, int *__restrict__ cell_of, int *__restrict__ rank,
-                      int *__restrict__ count, float *__restrict__ cell_hmax, unsigned *status)
+                      int *__restrict__ count, unsigned *status)
 {
     double clmin = fmin(g.cl[0], fmin(g.cl[1], g.cl[2]));
     for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n_total;
@@ -63,7 +63,6 @@ __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float
             } else {
                 cell = (ixl * g.ny + ic[1]) * g.nz + ic[2];
                 rank[p] = atomicAdd(&count[cell], 1);
-                atomicMax(reinterpret_cast<int *>(&cell_hmax[cell]), __float_as_int(a.w));  // h > 0
             }
         }
         cell_of[p] = cell;
@@ -237,6 +236,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
                                                                     int *__restrict__ cell_nhome,
+                                                                    float *__restrict__ cell_hmax,
                                                                     int2 *big_items, int *big_count, int *bt_items,
                                                                     int *bt_count)
 {
@@ -249,7 +249,10 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         const long long mycell = base + lane;
         const int my_s0 = mycell < ncell ? start[mycell] : 0;
         const int my_n = mycell < ncell ? start[mycell + 1] - my_s0 : 0;
-        if (mycell < ncell && my_n == 0) cell_nhome[mycell] = 0;
+        if (mycell < ncell && my_n == 0) {
+            cell_nhome[mycell] = 0;
+            cell_hmax[mycell] = 0.0f;
+        }
         unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
       while (todo) {
         const int j = __ffs(todo) - 1;
@@ -258,12 +261,18 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         const int s0 = __shfl_sync(0xffffffffu, my_s0, j);
         const int n = __shfl_sync(0xffffffffu, my_n, j);
         int nh = 0;
+        float hm = 0.0f;
         for (int e = lane; e < n; e += 32) {
             slot_cell[s0 + e] = (int)cell;
             nh += (unsigned)rec[s0 + e].idx < 0x80000000u;
+            hm = fmaxf(hm, rec[s0 + e].xyzh.w);
         }
         nh = __reduce_add_sync(0xffffffffu, nh);
-        if (lane == 0) cell_nhome[cell] = nh;
+        hm = __int_as_float(__reduce_max_sync(0xffffffffu, (unsigned)__float_as_int(hm)));   // h > 0
+        if (lane == 0) {
+            cell_nhome[cell] = nh;
+            cell_hmax[cell] = hm;
+        }
         if (n > STABLE_SMALL && n <= STABLE_BT_MAX) {      // k_stable_bitonic
             if (lane == 0) bt_items[atomicAdd(bt_count, 1)] = (int)cell;
             continue;

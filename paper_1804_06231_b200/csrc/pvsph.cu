@@ -249,7 +249,6 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     cudaError_t e;
     if ((e = cudaMemsetAsync(at<unsigned>(ws, w.status), 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     if ((e = cudaMemsetAsync(at<int>(ws, w.count), 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
-    if ((e = cudaMemsetAsync(cells->cell_hmax, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
     unsigned *status = at<unsigned>(ws, w.status);
     int *cell_of = at<int>(ws, w.cell_of), *rank = at<int>(ws, w.rank), *count = at<int>(ws, w.count);
     int *tile_sum = at<int>(ws, w.tile_sum);
@@ -257,7 +256,7 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     const float4 *vin = reinterpret_cast<const float4 *>(vm_in);
     if (n > 0) {
         k_bin<<<grid_blocks(n, 256, 148 * 32), 256, 0, s>>>(g, n_own, n, xin, vin, cell_of, rank, count,
-                                                            cells->cell_hmax, status);
+                                                            status);
     }
     long long ntiles = (g.ncell + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles, SCAN_T, 0, s>>>(count, g.ncell, cells->cell_start, tile_sum, status);
@@ -274,8 +273,8 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         int *bt_items = at<int>(ws, w.huge_items), *bt_count = at<int>(ws, w.huge_count);
         if ((e = cudaMemsetAsync(bt_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, big_items,
-            big_count, bt_items, bt_count);
+            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, cells->cell_hmax,
+            big_items, big_count, bt_items, bt_count);
         static bool bt_attr = false;
         if (!bt_attr) {
             cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
@@ -287,6 +286,8 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
                                                           big_count);
     }
     if (n == 0 && (e = cudaMemsetAsync(cells->cell_nhome, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
+        return cuda_fail(e);
+    if (n == 0 && (e = cudaMemsetAsync(cells->cell_hmax, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
         return cuda_fail(e);
     cells->n = n;
     return check_launch();
