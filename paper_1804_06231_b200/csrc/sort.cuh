@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const float u0 = p.x - (float)corner[0], u1 = p.y - (float)corner[1], u2 = p.z - (float)corner[2];
         const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
         const float scale = 33554432.0f / (2.0f * cmax);     // 2^25 over the key range
+        const float cmax_s = cmax * scale;
         unsigned comp[SPH_NDIR];
 #pragma unroll
         for (int d = 0; d < SPH_NDIR; ++d) {
@@ -151,8 +152,8 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
             const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
             const float key = ((float)a0 * u0 + (float)a1 * u1 + (float)a2 * u2) * inv;
-            float qk = floorf((key + cmax) * scale);
-            qk = fminf(fmaxf(qk, 0.0f), 33554431.0f);
+            // quantised key: floor((key + cmax) scale) as one FFMA and a rounding conversion
+            const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
             comp[d] = ((unsigned)qk << 7) | (unsigned)lane;
             if (mine) S[lane * 16 + d] = comp[d];
         }
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
     const int nitems = *mid_count;
     const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
     const float scale = 33554432.0f / (2.0f * cmax);
+    const float cmax_s = cmax * scale;
     for (int it = blockIdx.x * SORT_WARPS + w; it < nitems; it += gridDim.x * SORT_WARPS) {
         const long long cell = mid_items[it];
         const int s0 = c.cell_start[cell];
@@ -349,8 +351,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
             for (int k = 0; k < SORT_MID_PER; ++k) {
                 const int e = lane + 32 * k;
                 const float key = ((float)a0 * u[k][0] + (float)a1 * u[k][1] + (float)a2 * u[k][2]) * inv;
-                float qk = floorf((key + cmax) * scale);
-                qk = fminf(fmaxf(qk, 0.0f), 33554431.0f);
+                const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
                 comp[k] = ((unsigned)qk << 7) | (unsigned)e;
                 if (e < n) S[e] = comp[k];
             }
