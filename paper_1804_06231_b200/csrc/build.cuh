@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     int *__restrict__ perm, int *__restrict__ slot_cell,
                                                                     int *__restrict__ cell_nhome,
                                                                     float *__restrict__ cell_hmax,
+                                                                    int *__restrict__ row_home, int nz,
                                                                     int2 *big_items, int *big_count, int *bt_items,
                                                                     int *bt_count)
 {
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         if (lane == 0) {
             cell_nhome[cell] = nh;
             cell_hmax[cell] = hm;
+            if (nh > 0) row_home[cell / nz] = 1;         // k_v4_tiles skips rows without home particles
         }
         if (n > STABLE_SMALL && n <= STABLE_BT_MAX) {      // k_stable_bitonic
             if (lane == 0) bt_items[atomicAdd(bt_count, 1)] = (int)cell;

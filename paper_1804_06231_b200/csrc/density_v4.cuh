@@ -210,7 +210,7 @@ __device__ __forceinline__ ZCols zcols(const DevGrid &g, const int *__restrict__
 template <bool WRITE>
 __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, const int *__restrict__ nhome,
                            int *__restrict__ off, int4 *tiles, long long tile_cap, unsigned *status, unsigned *gen,
-                           int *gtiles, int *gcount)
+                           int *gtiles, int *gcount, const int *__restrict__ row_home)
 {
     // the counting launch opens a new sph_density_all call: its records carry the new tag
     if (!WRITE && blockIdx.x == 0 && threadIdx.x == 0) *gen += 1u;
@@ -220,7 +220,10 @@ __global__ void k_v4_tiles(DevGrid g, const int *__restrict__ cell_start, const 
         int xo, yp;
         key_rowpair(r, key, xo, yp);
         int nt = 0;
-        if (xo < r.nxo && yp < r.nyp) {
+        // row pairs without a home particle (most rows of a fine level grid) emit nothing
+        const long long ra = (long long)(xo + g.ghost_x) * g.ny + 2 * yp;
+        const bool any_home = xo < r.nxo && yp < r.nyp && (row_home[ra] || (2 * yp + 1 < g.ny && row_home[ra + 1]));
+        if (any_home) {
             const int y0 = 2 * yp;
             const bool hasB = y0 + 1 < g.ny;
             long long rb[V4_ROWS];

@@ -133,7 +133,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
     size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
-        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, total;
+        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, row_home, total;
     long long tile_cap, huge_cap;
 };
 
@@ -186,6 +186,8 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 4 * (size_t)w.tile_cap, 256);
     w.gcount = o;                        // [listed, claimed]
     o = align_up(o + 8, 256);
+    w.row_home = o;                      // per local (x, y) row: any home particle (build -> k_v4_tiles)
+    o = align_up(o + 4 * (size_t)g.nxl * g.ny, 256);
     w.total = o;
     return w;
 }
@@ -271,10 +273,12 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
                                                                     vin, rec);
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
         int *bt_items = at<int>(ws, w.huge_items), *bt_count = at<int>(ws, w.huge_count);
+        int *row_home = at<int>(ws, w.row_home);
         if ((e = cudaMemsetAsync(bt_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaMemsetAsync(row_home, 0, 4 * (size_t)g.nxl * g.ny, s)) != cudaSuccess) return cuda_fail(e);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
             g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, cells->cell_hmax,
-            big_items, big_count, bt_items, bt_count);
+            row_home, g.nz, big_items, big_count, bt_items, bt_count);
         static bool bt_attr = false;
         if (!bt_attr) {
             cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
@@ -466,7 +470,8 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     unsigned *gen = at<unsigned>(ws, w.gen);
     int *gtiles = at<int>(ws, w.gtiles), *gcount = at<int>(ws, w.gcount);
     k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
-                                                                       w.tile_cap, status, gen, gtiles, gcount);
+                                                                       w.tile_cap, status, gen, gtiles, gcount,
+                                                                       at<int>(ws, w.row_home));
     const long long ntiles_scan = (nkeys + SCAN_TILE - 1) / SCAN_TILE;
     k_scan_tiles<<<(int)ntiles_scan, SCAN_T, 0, s>>>(rows, nkeys, rows, rows_sum, status, 0x7fffffff);
     k_scan_sums<<<1, SCAN_T, 0, s>>>(rows_sum, ntiles_scan, rows, nkeys);
@@ -474,7 +479,8 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     cudaError_t e;
     if ((e = cudaMemsetAsync(gcount, 0, 8, s)) != cudaSuccess) return cuda_fail(e);
     k_v4_tiles<true><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
-                                                                      w.tile_cap, status, gen, gtiles, gcount);
+                                                                      w.tile_cap, status, gen, gtiles, gcount,
+                                                                      at<int>(ws, w.row_home));
     if ((e = cudaMemsetAsync(counter, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     static int blocks_per_sm = 0, sms = 0;
     if (!blocks_per_sm) {
