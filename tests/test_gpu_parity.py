@@ -475,3 +475,20 @@ def test_dense_cells_density_all_vs_oracle(pv, occ):
     for k in range(4):
         assert abs(got["stats"]["hits"][k] - tot[k, 2]) <= band
         assert abs(got["stats"]["cand"][k] - tot[k, 1]) <= max(2, 1e-5 * tot[k, 1])
+
+
+def test_noncubic_cell_grid_vs_oracle(pv):
+    """Cells of different edge per axis (nc = 5 x 7 x 6 in the unit box): windows are projected
+    separations along unit axes, valid for any cell shape; == the brute-force oracle."""
+    p = synth.tiny_random_set(seed=21, n=6000, nc=7, h_frac=0.9)      # gamma h <= 0.9 min C_l
+    got = pv.density(p.xyzh, p.vm, (5, 7, 6))
+    compare(got, oracle.bruteforce(p.xyzh, p.vm), None, "nc 5x7x6")
+
+
+def test_box_length_two_vs_oracle(pv):
+    """A periodic box of side 2 (positions and h scaled): == the oracle with box = 2."""
+    p = synth.tiny_random_set(seed=22, n=6000, nc=6, h_frac=0.9)
+    x = p.xyzh.copy()
+    x[:, :4] *= 2.0                                                    # exact scaling by 2
+    got = pv.density(x, p.vm, 6, box=2.0)
+    compare(got, oracle.bruteforce(x, p.vm, box=2.0), None, "box 2")
