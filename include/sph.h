@@ -41,7 +41,8 @@
  *     data-dependent errors set the device status word in the workspace,
  *     read by sph_status() (one stream synchronisation).
  *   - Return codes: SPH_OK, SPH_EINVAL (null pointer, bad size or grid,
- *     workspace too small), SPH_EH_RANGE (h <= 0, m <= 0 or gamma*h > C_l),
+ *     workspace too small), SPH_EH_RANGE (h <= 0, m <= 0, or gamma*h +
+ *     2*skin > C_l for a home particle),
  *     SPH_ECAPACITY (a cell holds more than SPH_MAX_CELL particles, or the
  *     particle arrays are too small), SPH_EDOMAIN (non-finite value, or a
  *     position outside [0, box) / outside the rank's slab), SPH_ECUDA (a
@@ -71,7 +72,8 @@ extern "C" {
 
 /* Number of sort directions and the window margin: a candidate is
  * swept when its projected separation is below H_i + SPH_DELTA_FRAC * C_l
- * (reading R5: covers fp32 rounding of the keys). */
+ * + 4 * skin (reading R5: covers fp32 rounding of the keys; the
+ * skin term covers drifts since the lists were built, §4.6). */
 #define SPH_NDIR 13
 #define SPH_DELTA_FRAC (1.0 / 65536.0)
 
