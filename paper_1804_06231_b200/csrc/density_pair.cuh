@@ -216,21 +216,36 @@ __global__ void __launch_bounds__(PAIR_WARPS * 32) k_density_pair_staged(DevGrid
 
 // ---- symmetric pair kernel -------------------------------------
 // One CTA per UNORDERED neighbour pair (ci, cj): every distance of the pair is evaluated once
-// and both particles take their share.  Lane = i in ci, as in k_density_pair_staged; the
-// window in cj's sorted list uses max(H_i, gamma hmax(cj)) + delta, so every j that reaches i
-// (r < H_j) is a candidate too.  A hit is pushed with two flags (r < H_i: i's sum, r < H_j:
-// j's sum).  i's sums stay in registers; j's are the same M4 terms with H_j and m_i (x_ji =
-// -x_ij, v_ji = -v_ij leave every product unchanged) and go to per-j accumulators in shared
-// memory (red.shared.add).  Both sides reach the outputs with red.global.add, as in the
-// one-sided kernel; j in a ghost cell (slabs) is skipped.
+// and both particles take their share.  Phase 1, lane = i in ci (as k_density_pair_staged):
+// the window in cj's sorted list uses max(H_i, gamma hmax(cj)) + delta, so every j that
+// reaches i (r < H_j) is a candidate too; r < H_i goes to the lane's stack (FFMA2 drains,
+// register sums), r < H_j records i in j's bucket in shared memory (one shared atomic for
+// the slot).  Phase 2, lane = j in cj: the bucket's interactions with H_j and m_i (x_ji =
+// -x_ij, v_ji = -v_ij leave every product unchanged), two per step with FFMA2, register
+// sums.  Both sides reach the outputs with red.global.add, as in the one-sided kernel; j in
+// a ghost cell (slabs) is skipped.  A bucket that overflows adds that hit's share directly.
 constexpr int SYM_WARPS = 4;
 constexpr int SYM_MAXN = 512;            // staged particles per cell (3 CTAs per SM)
 constexpr int SYM_Q = 16;
-constexpr int SYM_NACC = 12;             // per-j sums: rho wc srt st Dn Px Nx Py Ny Pz Nz, nngb
-constexpr size_t SYM_SMEM = (size_t)SYM_MAXN * 16 * 4 + (size_t)SYM_MAXN * 4 * SYM_NACC + (size_t)SYM_MAXN * 4 +
-                            (size_t)SYM_MAXN * 2 + (size_t)SYM_WARPS * SYM_Q * 32 * 2;
+constexpr int SYM_JCAP = 32;             // bucket entries per j
+constexpr size_t SYM_SMEM = (size_t)SYM_MAXN * 16 * 4 + (size_t)SYM_MAXN * 4 * 2 + (size_t)SYM_MAXN * 2 +
+                            (size_t)SYM_WARPS * SYM_Q * 32 * 2 + (size_t)SYM_MAXN * SYM_JCAP * 2;
 
-__device__ __forceinline__ void red_shared_f32(float *a, float v) { atomicAdd(a, v); }
+__device__ __forceinline__ void sym_flush(const DevGrid &g, const DevOut &o, int out, float Hinv, const Acc2 &B,
+                                          int nn)
+{
+    const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv, gf = K3 * Hinv;
+    Final f;
+    f.rho = K3 * sum2(B.rho);
+    f.wc = K3 * sum2(B.wc);
+    f.rho_dh = -K3 * g.gamma * Hinv * sum2(B.srt);
+    f.wc_dh = -K3 * g.gamma * Hinv * sum2(B.st);
+    f.div = gf * sum2(B.Dn);                       // rho * div v
+    f.cx = gf * (sum2(B.Px) - sum2(B.Nx));         // rho * curl v
+    f.cy = gf * (sum2(B.Py) - sum2(B.Ny));
+    f.cz = gf * (sum2(B.Pz) - sum2(B.Nz));
+    atomic_out(o, out, f, nn);
+}
 
 template <bool COUNT>
 __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, DevCells c, DevOut o,
@@ -238,14 +253,15 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                                                                      sph_stats *st, unsigned *status)
 {
     extern __shared__ __align__(16) unsigned char sym_smem[];
-    float4 *Pi = reinterpret_cast<float4 *>(sym_smem);             // ci positions
+    float4 *Pi = reinterpret_cast<float4 *>(sym_smem);             // ci positions (home shift applied)
     float4 *Vi = Pi + SYM_MAXN;                                      // ci (v, m)
-    float4 *Pj = Vi + SYM_MAXN;                                      // cj positions, w = H_j^2
+    float4 *Pj = Vi + SYM_MAXN;                                      // cj positions (pre-shifted), w = H_j^2
     float4 *Vj = Pj + SYM_MAXN;                                      // cj (v, m)
-    float *Aj = reinterpret_cast<float *>(Vj + SYM_MAXN);            // [SYM_NACC][SYM_MAXN]
-    float *HinvJ = Aj + SYM_NACC * SYM_MAXN;                         // 1 / H_j
-    uint16_t *Lj = reinterpret_cast<uint16_t *>(HinvJ + SYM_MAXN);   // cj sorted along d
+    float *HinvJ = reinterpret_cast<float *>(Vj + SYM_MAXN);         // 1 / H_j
+    int *JC = reinterpret_cast<int *>(HinvJ + SYM_MAXN);             // bucket fill of each j
+    uint16_t *Lj = reinterpret_cast<uint16_t *>(JC + SYM_MAXN);      // cj sorted along d
     uint16_t *stacks = Lj + SYM_MAXN;
+    uint16_t *JB = stacks + SYM_WARPS * SYM_Q * 32;                  // [SYM_MAXN][SYM_JCAP] i of j's hits
     __shared__ __align__(8) unsigned long long s_mbar;
     const unsigned mbar = smem_addr(&s_mbar);
     unsigned phase = 0;
@@ -308,7 +324,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             }
             continue;
         }
-        // ---- staging: both cells (positions and v, m), cj's sorted list, zeroed j sums --------
+        // ---- staging: both cells (positions and v, m), cj's sorted list, empty buckets ----------
         if (threadIdx.x == 0) {
             mbar_expect_tx(mbar, (unsigned)(2 * ni + 2 * nj) * 16u);
             bulk_g2s(smem_addr(Pi), c.xyzh + si, (unsigned)ni * 16u, mbar);
@@ -317,8 +333,10 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             bulk_g2s(smem_addr(Vj), c.vm + sj, (unsigned)nj * 16u, mbar);
         }
         const uint16_t *src = c.ord + (long long)d * c.cap + sj;
-        for (int k = threadIdx.x; k < nj; k += blockDim.x) Lj[k] = src[k];
-        for (int k = threadIdx.x; k < SYM_NACC * nj; k += blockDim.x) Aj[(k / nj) * SYM_MAXN + k % nj] = 0.0f;
+        for (int k = threadIdx.x; k < nj; k += blockDim.x) {
+            Lj[k] = src[k];
+            JC[k] = 0;
+        }
         mbar_wait(mbar, phase);
         phase ^= 1u;
         const float bx = g.boxf[0], by = g.boxf[1], bz = g.boxf[2];
@@ -333,6 +351,14 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             HinvJ[k] = (float)(1.0 / H);
             Pj[k] = p;
         }
+        for (int k = threadIdx.x; k < ni; k += blockDim.x) {
+            // ci's home coordinate shifted by -L where cj lies beyond a high face (exact: x_i >= L/2)
+            float4 p = Pi[k];
+            p.x -= sh[0] > 0 ? bx : 0.0f;
+            p.y -= sh[1] > 0 ? by : 0.0f;
+            p.z -= sh[2] > 0 ? bz : 0.0f;
+            Pi[k] = p;
+        }
         const float Hjmax = (float)((double)g.gamma * (double)c.cell_hmax[cjc]);
         __syncthreads();
 
@@ -340,6 +366,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
         const unsigned sQ = smem_addr(stacks + wl * SYM_Q * 32) + 2u * lane;
         const float c0 = (float)dir_component(d, 0), c1 = (float)dir_component(d, 1), c2 = (float)dir_component(d, 2);
         const float rk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
+        // ---- phase 1: lane = i ------------------------------------------------------------------
         for (int t0 = wl * 32; t0 < ni; t0 += SYM_WARPS * 32) {
             const int e = t0 + lane;
             const bool active = e < ni;
@@ -347,11 +374,9 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             if (active) {
                 const float4 a = Pi[e];
                 const float4 b = Vi[e];
-                x = sh[0] > 0 ? a.x - bx : a.x;
-                y = sh[1] > 0 ? a.y - by : a.y;
-                z = sh[2] > 0 ? a.z - bz : a.z;
+                x = a.x; y = a.y; z = a.z;
                 vx = b.x; vy = b.y; vz = b.z; m = b.w;
-                const double H = (double)g.gamma * (double)a.w;
+                const double H = (double)g.gamma * (double)a.w;   // w is h (only x, y, z were shifted)
                 H2 = (float)(H * H);
                 Hinv = (float)(1.0 / H);
                 Hk = (fmaxf((float)H, Hjmax) + g.delta) * rk;
@@ -378,37 +403,14 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                 const unsigned n = (qp - sQ) >> 6;
                 if (n >= 2 || (final && n == 1)) {
                     const bool two = n >= 2;
-                    const unsigned e0 = lds_u16(qp - 64u), e1 = two ? lds_u16(qp - 128u) : (e0 & 0x3fffu);
+                    const unsigned s0 = lds_u16(qp - 64u), s1 = two ? lds_u16(qp - 128u) : s0;
                     qp -= two ? 128u : 64u;
-                    const unsigned s0 = e0 & 0x3fffu, s1 = e1 & 0x3fffu;
-                    const bool i0 = (e0 >> 14) & 1u, i1 = two && ((e1 >> 14) & 1u);
-                    const bool j0 = (e0 >> 15) & 1u, j1 = two && ((e1 >> 15) & 1u);
-                    nngb += (int)i0 + (int)i1;
+                    nngb += two ? 2 : 1;
                     const float4 p0 = ldsr_f4(sP + 16u * s0), p1 = ldsr_f4(sP + 16u * s1);
                     const float4 v0 = ldsr_f4(sV + 16u * s0), v1 = ldsr_f4(sV + 16u * s1);
-                    const f2 dx = pk(x - p0.x, x - p1.x), dy = pk(y - p0.y, y - p1.y), dz = pk(z - p0.z, z - p1.z);
-                    const f2 nvx = pk(v0.x - vx, v1.x - vx), nvy = pk(v0.y - vy, v1.y - vy),
-                             nvz = pk(v0.z - vz, v1.z - vz);
-                    interact_pair<true>(Hinv2, dx, dy, dz, pk(v0.w, v1.w), nvx, nvy, nvz,
-                                        pk(i0 ? 1.0f : 0.0f, i1 ? 1.0f : 0.0f), A);
-                    if (j0 || j1) {
-                        // j's share: the same terms with H_j and m_i
-                        Acc2 B;
-                        B.rho = B.wc = B.srt = B.st = B.Dn = B.Px = B.Nx = B.Py = B.Ny = B.Pz = B.Nz = zero2();
-                        const f2 hj = pk(HinvJ[s0], HinvJ[s1]);
-                        interact_pair<true>(hj, dx, dy, dz, bc2(m), nvx, nvy, nvz,
-                                            pk(j0 ? 1.0f : 0.0f, j1 ? 1.0f : 0.0f), B);
-                        const f2 bs[11] = {B.rho, B.wc, B.srt, B.st, B.Dn, B.Px, B.Nx, B.Py, B.Ny, B.Pz, B.Nz};
-#pragma unroll
-                        for (int k = 0; k < 11; ++k) {
-                            float a0, a1;
-                            upk(bs[k], a0, a1);
-                            if (j0) red_shared_f32(&Aj[k * SYM_MAXN + s0], a0);
-                            if (j1) red_shared_f32(&Aj[k * SYM_MAXN + s1], a1);
-                        }
-                        if (j0) atomicAdd(reinterpret_cast<int *>(&Aj[11 * SYM_MAXN + s0]), 1);
-                        if (j1) atomicAdd(reinterpret_cast<int *>(&Aj[11 * SYM_MAXN + s1]), 1);
-                    }
+                    interact_pair<true>(Hinv2, pk(x - p0.x, x - p1.x), pk(y - p0.y, y - p1.y), pk(z - p0.z, z - p1.z),
+                                        pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx), pk(v0.y - vy, v1.y - vy),
+                                        pk(v0.z - vz, v1.z - vz), pk(1.0f, two ? 1.0f : 0.0f), A);
                 }
             };
             const int trip = __reduce_max_sync(0xffffffffu, len);
@@ -420,14 +422,29 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                     const float4 p = ldsr_f4(sP + 16u * id);
                     const float dx = x - p.x, dy = y - p.y, dz = z - p.z;
                     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    const bool hi = ok && r2 < H2, hj = ok && j_owned && r2 < p.w;
+                    const bool hi = ok && r2 < H2, hj = ok && r2 < p.w;
                     if (COUNT) {
                         cand[kind] += ok ? 1u : 0u;
-                        hits[kind] += (hi ? 1u : 0u) + (ok && r2 < p.w ? 1u : 0u);
+                        hits[kind] += (hi ? 1u : 0u) + (hj ? 1u : 0u);
                     }
-                    if (hi || hj) {
-                        sts_u16(qp, id | (hi ? 0x4000u : 0u) | (hj ? 0x8000u : 0u));
+                    if (hi) {
+                        sts_u16(qp, id);
                         qp += 64u;
+                    }
+                    if (hj && j_owned) {
+                        const int slot = atomicAdd(&JC[id], 1);
+                        if (slot < SYM_JCAP) {
+                            JB[id * SYM_JCAP + slot] = (uint16_t)e;
+                        } else {
+                            // bucket full: this hit's share of j goes to the outputs directly
+                            Acc2 B;
+                            B.rho = B.wc = B.srt = B.st = B.Dn = B.Px = B.Nx = B.Py = B.Ny = B.Pz = B.Nz = zero2();
+                            const float4 vj = Vj[id];
+                            interact_pair<true>(bc2(HinvJ[id]), pk(dx, 0.f), pk(dy, 0.f), pk(dz, 0.f), pk(m, 0.f),
+                                                pk(vj.x - vx, 0.f), pk(vj.y - vy, 0.f), pk(vj.z - vz, 0.f),
+                                                pk(1.0f, 0.0f), B);
+                            sym_flush(g, o, c.perm[sj + id], HinvJ[id], B, 1);
+                        }
                     }
                 }
                 for (;;) {
@@ -439,40 +456,34 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                 }
             }
             while (__any_sync(0xffffffffu, qp != sQ)) drain(true);
-            if (active && nngb > 0) {
-                const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;
-                const float gf = K3 * Hinv;
-                Final f;
-                f.rho = K3 * sum2(A.rho);
-                f.wc = K3 * sum2(A.wc);
-                f.rho_dh = -K3 * g.gamma * Hinv * sum2(A.srt);
-                f.wc_dh = -K3 * g.gamma * Hinv * sum2(A.st);
-                f.div = gf * sum2(A.Dn);
-                f.cx = gf * (sum2(A.Px) - sum2(A.Nx));
-                f.cy = gf * (sum2(A.Py) - sum2(A.Ny));
-                f.cz = gf * (sum2(A.Pz) - sum2(A.Nz));
-                atomic_out(o, c.perm[si + e], f, nngb);
-            }
+            if (active && nngb > 0) sym_flush(g, o, c.perm[si + e], Hinv, A, nngb);
         }
-        __syncthreads();
-        // j's sums to the outputs
+        __syncthreads();                          // buckets complete
+        // ---- phase 2: lane = j, its bucket of i ---------------------------------------------------
         if (j_owned) {
-            for (int k = threadIdx.x; k < nj; k += blockDim.x) {
-                const int nn = reinterpret_cast<const int *>(Aj)[11 * SYM_MAXN + k];
-                if (nn == 0) continue;
-                const float hinv = HinvJ[k];
-                const float K3 = (16.0f / kPi) * hinv * hinv * hinv, gf = K3 * hinv;
-                const float *a = Aj + k;
-                Final f;
-                f.rho = K3 * a[0 * SYM_MAXN];
-                f.wc = K3 * a[1 * SYM_MAXN];
-                f.rho_dh = -K3 * g.gamma * hinv * a[2 * SYM_MAXN];
-                f.wc_dh = -K3 * g.gamma * hinv * a[3 * SYM_MAXN];
-                f.div = gf * a[4 * SYM_MAXN];
-                f.cx = gf * (a[5 * SYM_MAXN] - a[6 * SYM_MAXN]);
-                f.cy = gf * (a[7 * SYM_MAXN] - a[8 * SYM_MAXN]);
-                f.cz = gf * (a[9 * SYM_MAXN] - a[10 * SYM_MAXN]);
-                atomic_out(o, c.perm[sj + k], f, nn);
+            for (int t0 = wl * 32; t0 < nj; t0 += SYM_WARPS * 32) {
+                const int k = t0 + lane;
+                const bool active = k < nj;
+                const int nb = active ? min(JC[k], SYM_JCAP) : 0;
+                const float4 pj = active ? Pj[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 vj = active ? Vj[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float hinv = active ? HinvJ[k] : 0.0f;
+                Acc2 B;
+                B.rho = B.wc = B.srt = B.st = B.Dn = B.Px = B.Nx = B.Py = B.Ny = B.Pz = B.Nz = zero2();
+                const f2 hj2 = bc2(hinv);
+                const int trip = __reduce_max_sync(0xffffffffu, nb);
+                for (int t = 0; t < trip; t += 2) {
+                    const bool a0 = t < nb, a1 = t + 1 < nb;
+                    const int i0 = a0 ? JB[k * SYM_JCAP + t] : 0, i1 = a1 ? JB[k * SYM_JCAP + t + 1] : i0;
+                    const float4 p0 = Pi[i0], p1 = Pi[i1];
+                    const float4 w0 = Vi[i0], w1 = Vi[i1];
+                    // x_ij = x_i - x_j and v_j - v_i, as in phase 1; m_i; H_j
+                    interact_pair<true>(hj2, pk(p0.x - pj.x, p1.x - pj.x), pk(p0.y - pj.y, p1.y - pj.y),
+                                        pk(p0.z - pj.z, p1.z - pj.z), pk(w0.w, w1.w), pk(vj.x - w0.x, vj.x - w1.x),
+                                        pk(vj.y - w0.y, vj.y - w1.y), pk(vj.z - w0.z, vj.z - w1.z),
+                                        pk(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f), B);
+                }
+                if (nb > 0) sym_flush(g, o, c.perm[sj + k], hinv, B, nb);
             }
         }
         __syncthreads();                          // shared memory reused by the next pair
