@@ -99,6 +99,7 @@ class Slab:
     gid: np.ndarray           # their global indices
     n_global: int
     pset: object = None       # the full ParticleSet (single-GPU only)
+    ghost_n: int = -1         # particles in the two ghost planes (known when cut from a full set)
 
     @staticmethod
     def single(p) -> "Slab":
@@ -114,8 +115,10 @@ class Slab:
         lo, hi = bounds[rank] if bounds is not None else slab_bounds(p.nc, world, rank)
         pl = planes_of(p.xyzh, p.nc, p.box)
         gid = np.nonzero((pl >= lo) & (pl < hi))[0]
+        per_plane = np.bincount(pl, minlength=p.nc)
+        ghost_n = int(per_plane[(lo - 1) % p.nc] + per_plane[hi % p.nc])
         return Slab(p.nc, p.box, p.gamma, rank, world, lo, hi, np.ascontiguousarray(p.xyzh[gid]),
-                    np.ascontiguousarray(p.vm[gid]), gid, p.n)
+                    np.ascontiguousarray(p.vm[gid]), gid, p.n, ghost_n=ghost_n)
 
     @staticmethod
     def from_config(cfg: str, rank: int, world: int, balance: bool = False) -> "Slab":
@@ -192,7 +195,12 @@ class SlabRunner:
                                  self.levels[0][1:] if split else None)
         if ghost:
             per_plane = self.n_own / max(1, slab.x_hi - slab.x_lo)
-            gcap = ghost_capacity if ghost_capacity is not None else int(2 * 1.5 * per_plane + 4096)
+            if ghost_capacity is not None:
+                gcap = ghost_capacity
+            elif slab.ghost_n >= 0:              # exact (cut from the full set) + headroom for drift
+                gcap = int(1.05 * slab.ghost_n) + 4096
+            else:
+                gcap = int(2 * 1.5 * per_plane + 4096)
         else:
             gcap = 0
         self.cap = self.n_own + gcap

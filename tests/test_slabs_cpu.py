@@ -110,3 +110,19 @@ def test_plane_costs_uniform_lattice():
     xyzh = np.zeros((nc ** 3, 4), np.float32)
     xyzh[:, 0], xyzh[:, 1], xyzh[:, 2] = x.ravel(), y.ravel(), z.ravel()
     assert np.array_equal(plane_costs(xyzh, nc), np.full(nc, 27.0 * nc * nc))
+
+
+def test_slab_ghost_counts_exact():
+    """A slab cut from the full set records how many particles its two ghost planes hold (the
+    ghost buffer is sized from it: uneven, cost-balanced cuts can land on dense planes)."""
+    import numpy as np
+    import synth
+    from paper_1804_06231_b200.slabs import Slab, balanced_bounds, plane_costs, planes_of
+    p = synth.clustered_set("cl64k", seed=7, n=65536, nc=13, n_spheres=16)
+    b = balanced_bounds(plane_costs(p.xyzh, p.nc), 3)
+    pl = planes_of(p.xyzh, p.nc)
+    for r in range(3):
+        s = Slab.from_set(p, r, 3, b)
+        lo, hi = b[r]
+        assert s.ghost_n == int(((pl == (lo - 1) % 13) | (pl == hi % 13)).sum())
+        assert s.n_own == int(((pl >= lo) & (pl < hi)).sum())
