@@ -263,16 +263,17 @@ def run_ours(args):
     pv.load()
 
     t_gen = time.perf_counter()
+    p = synth.make(args.config)                         # every rank: the same seeded set
+    nlev = args.levels or (3 if args.config == "c4" else 1)
+    levels = pv.level_grids(p.xyzh[:, 3], p.nc, max_levels=nlev) if nlev > 1 else None
     if world == 1:
-        p = synth.make(args.config)
         part = slabs.Slab.single(p)
     else:
         balance = args.balance if args.balance >= 0 else int(args.config == "c4")
-        part = slabs.Slab.from_config(args.config, rank, world, balance=bool(balance))
+        bounds = slabs.balanced_bounds(slabs.plane_costs(p.xyzh, p.nc, p.box), world) if balance else None
+        part = slabs.Slab.from_set(p, rank, world, bounds)
+        del p
     t_gen = time.perf_counter() - t_gen
-
-    nlev = args.levels or (3 if args.config == "c4" and world == 1 else 1)
-    levels = pv.level_grids(part.pset.xyzh[:, 3], part.nc, max_levels=nlev) if nlev > 1 else None
     runner = slabs.SlabRunner(part, dist=dist, levels=levels)
     runner.upload()
     stream = torch.cuda.current_stream()

@@ -175,8 +175,10 @@ size_t sph_workspace_bytes(const sph_grid *grid, int64_t n_total);
  * input order.
  * Inputs xyzh_in/vm_in hold n_own owned particles followed by n_ghost
  * ghost particles (float4 each, device).  Owned particles must lie in the
- * rank's owned planes, ghosts in its ghost planes (n_ghost > 0 needs
- * ghost_x = 1).  Resets the status word, then reports SPH_EDOMAIN /
+ * rank's owned planes (n_ghost > 0 needs ghost_x = 1); ghosts outside the
+ * ghost planes are dropped (not stored: a finer level grid keeps only its
+ * own ghost planes of the coarse ghosts), so cells->n is an upper bound and
+ * cell_start[ncell] the stored count.  Resets the status word, then reports SPH_EDOMAIN /
  * SPH_EH_RANGE / SPH_ECAPACITY through it.  Cell bins use fp64:
  * ix = floor(x * nc / box), clamped to [0, nc-1]. */
 int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in,

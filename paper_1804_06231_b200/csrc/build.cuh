@@ -59,7 +59,9 @@ __global__ void k_bin(DevGrid g, long long n_own, long long n_total, const float
                 }
             }
             if (ixl < 0) {
-                set_status(status, ST_EDOMAIN);
+                // a ghost outside the ghost planes is not needed on this grid (a finer level
+                // grid keeps only its own thinner ghost planes): dropped; anything else is an error
+                if (!(inside && p >= n_own && g.ghost_x)) set_status(status, ST_EDOMAIN);
             } else {
                 cell = (ixl * g.ny + ic[1]) * g.nz + ic[2];
                 rank[p] = atomicAdd(&count[cell], 1);

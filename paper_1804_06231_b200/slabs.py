@@ -176,8 +176,9 @@ class SlabRunner:
     """Device buffers and one density step of one rank."""
 
     def __init__(self, slab: Slab, dist=None, device="cuda", ghost_capacity: int | None = None, levels=None):
-        """levels: [(nc, h_min, h_max)] level passes (one GPU only); the first
-        level's nc must be the slab's grid."""
+        """levels: [(nc, h_min, h_max)] level passes; the first level's nc
+        must be the slab's grid, the others multiples of it (on x-slabs each level owns the
+        same x range)."""
         self.slab = slab
         self.dist = dist
         self.world = slab.world
@@ -188,8 +189,6 @@ class SlabRunner:
         self.pset = slab.pset
         ghost = self.world > 1
         self.levels = list(levels) if levels else [(slab.nc, 0.0, 0.0)]
-        if len(self.levels) > 1 and ghost:
-            raise ValueError("level passes run on one GPU (x-slabs use one grid)")
         split = len(self.levels) > 1
         self.grid = pv.make_grid(slab.nc, slab.box, slab.gamma, slab.x_lo, slab.x_hi, int(ghost),
                                  self.levels[0][1:] if split else None)
@@ -218,7 +217,10 @@ class SlabRunner:
         # finer level grids (one GPU): own cells and workspace each, same outputs
         self.extra = []
         for nc, lo, hi in self.levels[1:]:
-            g = pv.make_grid(nc, slab.box, slab.gamma, h_home=(lo, hi))
+            # level k on x-slabs: planes [x_lo f, x_hi f) of the f-times finer grid, its thinner
+            # ghost planes taken from the coarse ghosts (the build drops the others)
+            f = nc // slab.nc
+            g = pv.make_grid(nc, slab.box, slab.gamma, slab.x_lo * f, slab.x_hi * f, int(ghost), h_home=(lo, hi))
             c = pv.Cells.alloc(g, self.cap, device)
             self.extra.append((g, c, pv.alloc_workspace(g, c.capacity, device)))
 
@@ -253,10 +255,16 @@ class SlabRunner:
         if self.world > 1:
             self.exchange()
         rec(1)
+        self.compute(stats=stats, rec=rec)
+
+    def compute(self, stats=None, rec=None) -> None:
+        """Build, sort and density of every level grid on the current inputs (owned particles
+        and the n_ghost ghosts behind them)."""
+        rec = rec or (lambda k: None)
         pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own,
                            n_ghost=self.n_ghost)
         for g, c, ws in self.extra:
-            pv.sph_build_cells(g, self.xin, self.vin, c, ws, n_own=self.n_own, n_ghost=0)
+            pv.sph_build_cells(g, self.xin, self.vin, c, ws, n_own=self.n_own, n_ghost=self.n_ghost)
         rec(2)
         pv.sph_sort_cells(self.grid, self.cells, self.ws)
         for g, c, ws in self.extra:
@@ -342,11 +350,11 @@ class FakeRanks:
     device copies instead of NCCL (a test harness for the slab logic; nothing waits
     on another rank, every launch is ordered on one stream)."""
 
-    def __init__(self, p, world: int, device="cuda", balance: bool = False):
+    def __init__(self, p, world: int, device="cuda", balance: bool = False, levels=None):
         self.world = world
         bounds = balanced_bounds(plane_costs(p.xyzh, p.nc, p.box), world) if balance else None
         self.bounds = bounds
-        self.runners = [SlabRunner(Slab.from_set(p, r, world, bounds), dist=None, device=device)
+        self.runners = [SlabRunner(Slab.from_set(p, r, world, bounds), dist=None, device=device, levels=levels)
                         for r in range(world)]
         for r in self.runners:
             r.upload()
@@ -370,9 +378,7 @@ class FakeRanks:
             r.vin[b:c].copy_(gv_hi)
             r.n_ghost = c - r.n_own
         for r in self.runners:
-            pv.sph_build_cells(r.grid, r.xin, r.vin, r.cells, r.ws, n_own=r.n_own, n_ghost=r.n_ghost)
-            pv.sph_sort_cells(r.grid, r.cells, r.ws)
-            pv.sph_density_all(r.grid, r.cells, r.out, r.ws)
+            r.compute()
         for r in self.runners:
             r.check()
 

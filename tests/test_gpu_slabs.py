@@ -120,3 +120,22 @@ def test_balanced_slabs_bitwise_equal_single(pv, world):
     got = fr.gather()
     for f in single:
         assert np.array_equal(single[f], got[f]), (world, f)
+
+
+@pytest.mark.parametrize("world,balance", [(2, False), (3, True)])
+def test_levels_on_slabs_bitwise_equal_single(pv, world, balance):
+    """Level passes on x-slabs: every level grid cut at the same x, its
+    thinner ghost planes taken from the coarse ghosts -- outputs bitwise identical to the
+    level passes on one GPU."""
+    from paper_1804_06231_b200.slabs import FakeRanks
+    p = synth.clustered_set("cl64k", seed=7, n=65536, nc=13, n_spheres=16)
+    lv = pv.level_grids(p.xyzh[:, 3], p.nc, max_levels=3)
+    assert len(lv) == 3
+    single = pv.density_levels(p.xyzh, p.vm, lv)
+    fr = FakeRanks(p, world, balance=balance, levels=lv)
+    fr.step()
+    got = fr.gather()
+    for f in single:
+        if f == "stats":
+            continue
+        assert np.array_equal(single[f], got[f]), (world, f)
