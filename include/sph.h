@@ -252,6 +252,18 @@ const char *sph_strerror(int code);
  * would exceed it; the density calls on the same grid are then exact. */
 int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp, void *stream);
 
+/* Ghost exchange helper (x-slabs): copies the owned
+ * particles (xyzh_in/vm_in, n_own, device) whose x plane is the rank's
+ * first plane x_lo (list 0) or last plane x_hi - 1 (list 1), in input
+ * order, to sel_xyzh/sel_vm (float4 each): list k at [k * cap, k * cap +
+ * counts[k]).  counts: device int64[2].  Planes are found by the binning
+ * rule of sph_build_cells.  A list longer than cap sets SPH_ECAPACITY in the
+ * status word (the copy is truncated).  Workspace as for sph_build_cells
+ * with n_total >= n_own. */
+int sph_select_planes(const sph_grid *grid, int64_t n_own, const float *xyzh_in, const float *vm_in,
+                      float *sel_xyzh, float *sel_vm, int64_t cap, int64_t *counts, void *ws, size_t ws_bytes,
+                      void *stream);
+
 /* SPH_ABI_VERSION of the loaded library. */
 int sph_abi_version(void);
 

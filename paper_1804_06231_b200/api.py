@@ -228,6 +228,16 @@ def sph_drift(grid: SphGrid, cells: Cells, dt: float, max_disp: torch.Tensor | N
                                  _ptr(max_disp) if max_disp is not None else None, _stream(stream)), "sph_drift")
 
 
+def sph_select_planes(grid: SphGrid, xyzh: torch.Tensor, vm: torch.Tensor, n_own: int, sel_x: torch.Tensor,
+                      sel_v: torch.Tensor, counts: torch.Tensor, ws: torch.Tensor, stream=None) -> None:
+    """x-slab ghost exchange: the owned particles of planes x_lo (list 0) and x_hi - 1 (list 1)
+    in input order into sel_x/sel_v ((2, cap, 4) float32); counts: (2,) int64 device tensor."""
+    assert sel_x.shape[0] == 2 and sel_x.shape == sel_v.shape and counts.dtype == torch.int64
+    _check(_lib.load().sph_select_planes(ctypes.byref(grid), int(n_own), _ptr(xyzh), _ptr(vm), _ptr(sel_x),
+                                         _ptr(sel_v), sel_x.shape[1], _ptr(counts), _ptr(ws), ws.numel(),
+                                         _stream(stream)), "sph_select_planes")
+
+
 def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
     o = acc.struct()
     _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),

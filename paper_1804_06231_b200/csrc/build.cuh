@@ -154,6 +154,67 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_add(int *__restrict__ start, lo
         if (base + k < n) start[base + k] += add;
 }
 
+// ---- ghost exchange helper (sph_select_planes) ----------------------------
+// The owned particles of global plane x_lo (list 0) and x_hi - 1 (list 1), in input order.
+// k_sel_count: per block of SEL_B particles, how many fall in each list (blk[list * nblk + b]);
+// the three scan kernels turn that into offsets; k_sel_write recomputes the flags, ranks them
+// inside the block (warp ballots + a block scan) and copies the particles.
+constexpr int SEL_B = 1024;
+
+__device__ __forceinline__ int sel_list(const DevGrid &g, float x)
+{
+    int c = (int)floor((double)x * (double)g.nc[0] / g.box[0]);   // the binning rule of k_bin
+    c = c < 0 ? 0 : (c > g.nc[0] - 1 ? g.nc[0] - 1 : c);
+    return c == g.x_lo ? 0 : (c == g.x_hi - 1 ? 1 : -1);
+}
+
+__global__ void __launch_bounds__(SEL_B) k_sel_count(DevGrid g, long long n, const float4 *__restrict__ xyzh,
+                                                      int *__restrict__ blk, long long nblk)
+{
+    const long long p = blockIdx.x * (long long)SEL_B + threadIdx.x;
+    const int l = p < n ? sel_list(g, xyzh[p].x) : -1;
+    const int c0 = __syncthreads_count(l == 0), c1 = __syncthreads_count(l == 1);
+    if (threadIdx.x == 0) {
+        blk[blockIdx.x] = c0;
+        blk[nblk + blockIdx.x] = c1;
+    }
+}
+
+__global__ void __launch_bounds__(SEL_B) k_sel_write(DevGrid g, long long n, const float4 *__restrict__ xyzh,
+                                                      const float4 *__restrict__ vm, const int *__restrict__ off,
+                                                      long long nblk, float4 *sel_x, float4 *sel_v, long long cap,
+                                                      long long *counts, unsigned *status)
+{
+    __shared__ int wsum[2][SEL_B / 32];
+    const long long p = blockIdx.x * (long long)SEL_B + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int l = p < n ? sel_list(g, xyzh[p].x) : -1;
+    const unsigned b0 = __ballot_sync(0xffffffffu, l == 0), b1 = __ballot_sync(0xffffffffu, l == 1);
+    if (lane == 0) {
+        wsum[0][w] = __popc(b0);
+        wsum[1][w] = __popc(b1);
+    }
+    __syncthreads();
+    if (l >= 0) {
+        int before = 0;
+        for (int k = 0; k < w; ++k) before += wsum[l][k];
+        const unsigned mine = l == 0 ? b0 : b1;
+        const long long total0 = off[nblk];                            // particles of list 0
+        const long long base = l == 0 ? off[blockIdx.x] : (long long)off[nblk + blockIdx.x] - total0;
+        const long long r = base + before + __popc(mine & ((1u << lane) - 1u));
+        if (r < cap) {
+            sel_x[l * cap + r] = xyzh[p];
+            sel_v[l * cap + r] = vm[p];
+        } else {
+            set_status(status, ST_ECAPACITY);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        counts[0] = off[nblk];
+        counts[1] = (long long)off[2 * nblk] - off[nblk];
+    }
+}
+
 // 64-byte scatter record: the particle's 8 floats and its input index, written as two full
 // 32-byte sectors (two 256-bit stores) so a random slot costs no read-modify-write.
 struct alignas(64) ParticleRec {

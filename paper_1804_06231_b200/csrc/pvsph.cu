@@ -133,7 +133,8 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
     size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
-        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, row_home, total;
+        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, row_home, sel_blk,
+        sel_sum, total;
     long long tile_cap, huge_cap;
 };
 
@@ -188,6 +189,11 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 8, 256);
     w.row_home = o;                      // per local (x, y) row: any home particle (build -> k_v4_tiles)
     o = align_up(o + 4 * (size_t)g.nxl * g.ny, 256);
+    const long long nsel = 2 * ((n + SEL_B - 1) / SEL_B) + 1;
+    w.sel_blk = o;                       // sph_select_planes: per-block counts -> offsets
+    o = align_up(o + 4 * (size_t)nsel, 256);
+    w.sel_sum = o;
+    o = align_up(o + 4 * (size_t)((nsel + SCAN_TILE - 1) / SCAN_TILE + 1), 256);
     w.total = o;
     return w;
 }
@@ -430,6 +436,40 @@ int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp,
     if (cells->n <= 0) return SPH_OK;
     k_drift<<<grid_blocks(cells->n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
         reinterpret_cast<float4 *>(cells->xyzh), reinterpret_cast<const float4 *>(cells->vm), cells->n, dt, max_disp);
+    return check_launch();
+}
+
+int sph_select_planes(const sph_grid *grid, int64_t n_own, const float *xyzh_in, const float *vm_in,
+                      float *sel_xyzh, float *sel_vm, int64_t cap, int64_t *counts, void *ws, size_t ws_bytes,
+                      void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (n_own < 0 || cap < 0 || !counts || !ws || (n_own > 0 && (!xyzh_in || !vm_in))) return SPH_EINVAL;
+    if (cap > 0 && (!sel_xyzh || !sel_vm)) return SPH_EINVAL;
+    if (((uintptr_t)xyzh_in % 16) || ((uintptr_t)vm_in % 16) || ((uintptr_t)sel_xyzh % 16) || ((uintptr_t)sel_vm % 16))
+        return SPH_EINVAL;
+    Ws w = ws_layout(g, n_own);
+    if (ws_bytes < w.total) return SPH_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    if (n_own == 0) {
+        if ((e = cudaMemsetAsync(counts, 0, 16, s)) != cudaSuccess) return cuda_fail(e);
+        return SPH_OK;
+    }
+    const long long nblk = (n_own + SEL_B - 1) / SEL_B, nk = 2 * nblk;
+    int *blk = at<int>(ws, w.sel_blk), *sum = at<int>(ws, w.sel_sum);
+    unsigned *status = at<unsigned>(ws, w.status);
+    const float4 *x = reinterpret_cast<const float4 *>(xyzh_in), *v = reinterpret_cast<const float4 *>(vm_in);
+    k_sel_count<<<(int)nblk, SEL_B, 0, s>>>(g, n_own, x, blk, nblk);
+    const long long nt = (nk + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_tiles<<<(int)nt, SCAN_T, 0, s>>>(blk, nk, blk, sum, status, SEL_B);
+    k_scan_sums<<<1, SCAN_T, 0, s>>>(sum, nt, blk, nk);
+    k_scan_add<<<(int)nt, SCAN_T, 0, s>>>(blk, nk, sum);
+    k_sel_write<<<(int)nblk, SEL_B, 0, s>>>(g, n_own, x, v, blk, nblk, reinterpret_cast<float4 *>(sel_xyzh),
+                                             reinterpret_cast<float4 *>(sel_vm), cap,
+                                             reinterpret_cast<long long *>(counts), status);
     return check_launch();
 }
 

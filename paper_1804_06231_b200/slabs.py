@@ -1,11 +1,10 @@
 """x-slab domain decomposition over GPUs with a one-cell ghost layer.
 
-Rank r owns the cell planes [x_lo, x_hi) = [r nc/p, (r+1) nc/p) and the
-particles inside them, in global input order.  Every step:
+Rank r owns the cell planes [x_lo, x_hi) (equal or cost-balanced cuts) and
+the particles inside them, in global input order.  Every step:
 
-  1. bin the owned particles (sph_build_cells without ghosts); cells are
-     x-major, so the boundary planes x_lo and x_hi-1 are contiguous slices of
-     the cell-sorted arrays;
+  1. sph_select_planes copies the owned particles of the boundary planes x_lo
+     and x_hi-1, in input order (no binning pass);
   2. NCCL send/recv (torch.distributed P2P) of those planes to the left and
      right neighbours (periodic ring) -- counts first, then the particles --
      straight into the input buffer behind the owned particles;
@@ -13,9 +12,10 @@ particles inside them, in global input order.  Every step:
      sph_sort_cells, sph_density_all.
 
 The gather design needs no reverse exchange (ghosts are only j-sources).  With
-stable in-cell order (input order) and ghosts received in the sender's cell
-order, every particle sees the same neighbours in the same order as on one
-GPU, so the outputs are bitwise identical for any p (tests/test_gpu_slabs.py).
+stable in-cell order (home first, then input order) and ghosts received in the
+sender's input order (= the global order), every particle sees the same
+neighbours in the same order as on one GPU, so the outputs are bitwise
+identical for any p (tests/test_gpu_slabs.py).
 
 PyTorch is plumbing here: device buffers, the stream, and the process group.
 """
@@ -31,6 +31,7 @@ from . import api as pv
 
 BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_rec, k_stable_small/bitonic/big
 SORT_LAUNCHES = 6       # k_sort_small, k_sort_mid, k_sort_warp256, k_sort_big, k_sort_bitonic (medium, huge)
+SELECT_LAUNCHES = 5     # sph_select_planes: k_sel_count, 3 scan kernels, k_sel_write
 DENSITY_LAUNCHES = 8    # k_v4_tiles (count), 3 scan kernels, k_v4_tiles (write), k_density_v4, k_density_dense,
                         # k_unpermute
 
@@ -100,6 +101,7 @@ class Slab:
     n_global: int
     pset: object = None       # the full ParticleSet (single-GPU only)
     ghost_n: int = -1         # particles in the two ghost planes (known when cut from a full set)
+    edge_n: int = -1          # particles in the larger of its own first and last planes
 
     @staticmethod
     def single(p) -> "Slab":
@@ -117,8 +119,9 @@ class Slab:
         gid = np.nonzero((pl >= lo) & (pl < hi))[0]
         per_plane = np.bincount(pl, minlength=p.nc)
         ghost_n = int(per_plane[(lo - 1) % p.nc] + per_plane[hi % p.nc])
+        edge_n = int(max(per_plane[lo], per_plane[hi - 1]))
         return Slab(p.nc, p.box, p.gamma, rank, world, lo, hi, np.ascontiguousarray(p.xyzh[gid]),
-                    np.ascontiguousarray(p.vm[gid]), gid, p.n, ghost_n=ghost_n)
+                    np.ascontiguousarray(p.vm[gid]), gid, p.n, ghost_n=ghost_n, edge_n=edge_n)
 
     @staticmethod
     def from_config(cfg: str, rank: int, world: int, balance: bool = False) -> "Slab":
@@ -212,7 +215,12 @@ class SlabRunner:
         self.plane = self.grid.nc[1] * self.grid.nc[2]   # cells per x plane
         self.nxl = (slab.x_hi - slab.x_lo) + (2 if ghost else 0)
         self.launches_per_step = (BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES) * len(self.levels) + \
-            (BUILD_LAUNCHES if ghost else 0) + (len(self.levels) if split else 0)   # k_mark_needed per level
+            (SELECT_LAUNCHES if ghost else 0) + (len(self.levels) if split else 0)   # k_mark_needed per level
+        if ghost:                                # send buffers of the boundary planes (sph_select_planes)
+            scap = int(1.05 * slab.edge_n) + 4096 if slab.edge_n >= 0 else int(1.5 * per_plane) + 4096
+            self.sel_x = torch.empty((2, scap, 4), dtype=torch.float32, device=device)
+            self.sel_v = torch.empty((2, scap, 4), dtype=torch.float32, device=device)
+            self.sel_n = torch.zeros(2, dtype=torch.int64, device=device)
         self.device = device
         # finer level grids (one GPU): own cells and workspace each, same outputs
         self.extra = []
@@ -231,20 +239,17 @@ class SlabRunner:
             self.vin[:self.n_own].copy_(torch.from_numpy(self.slab.vm))
 
     # -- ghost exchange -----------------------------------------------------
-    def boundary_slices(self):
-        """Bin the owned particles and return the slot ranges of planes x_lo and x_hi-1."""
-        pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own, n_ghost=0)
-        P = self.plane
-        idx = torch.tensor([P, 2 * P, (self.nxl - 2) * P, (self.nxl - 1) * P], device=self.device)
-        lo_a, lo_b, hi_a, hi_b = self.cells.cell_start[idx].tolist()
-        return (lo_a, lo_b), (hi_a, hi_b)
+    def boundary_planes(self):
+        """The owned particles of planes x_lo and x_hi-1 in input order (sph_select_planes: no
+        binning pass), as ((xyzh, vm), (xyzh, vm)) views of the send buffers."""
+        pv.sph_select_planes(self.grid, self.xin, self.vin, self.n_own, self.sel_x, self.sel_v, self.sel_n, self.ws)
+        n_lo, n_hi = self.sel_n.tolist()
+        return (self.sel_x[0, :n_lo], self.sel_v[0, :n_lo]), (self.sel_x[1, :n_hi], self.sel_v[1, :n_hi])
 
     def exchange(self) -> None:
-        (lo_a, lo_b), (hi_a, hi_b) = self.boundary_slices()
-        xs, vs = self.cells.xyzh, self.cells.vm
+        send_lo, send_hi = self.boundary_planes()
         free = (self.xin[self.n_own:], self.vin[self.n_own:])
-        n_glo, n_ghi = exchange_planes(self.dist, self.rank, self.world, (xs[lo_a:lo_b], vs[lo_a:lo_b]),
-                                       (xs[hi_a:hi_b], vs[hi_a:hi_b]), free)
+        n_glo, n_ghi = exchange_planes(self.dist, self.rank, self.world, send_lo, send_hi, free)
         self.n_ghost = n_glo + n_ghi
 
     # -- one step -----------------------------------------------------------
@@ -361,11 +366,10 @@ class FakeRanks:
         self.n_global = p.n
 
     def step(self) -> None:
-        sl = [r.boundary_slices() for r in self.runners]
         planes = []
-        for r, ((lo_a, lo_b), (hi_a, hi_b)) in zip(self.runners, sl):
-            planes.append(((r.cells.xyzh[lo_a:lo_b].clone(), r.cells.vm[lo_a:lo_b].clone()),
-                           (r.cells.xyzh[hi_a:hi_b].clone(), r.cells.vm[hi_a:hi_b].clone())))
+        for r in self.runners:
+            (xl, vl), (xh, vh) = r.boundary_planes()
+            planes.append(((xl.clone(), vl.clone()), (xh.clone(), vh.clone())))
         W = self.world
         for k, r in enumerate(self.runners):
             gx_lo, gv_lo = planes[(k - 1) % W][1]      # left neighbour's plane x_hi-1

@@ -139,3 +139,27 @@ def test_levels_on_slabs_bitwise_equal_single(pv, world, balance):
         if f == "stats":
             continue
         assert np.array_equal(single[f], got[f]), (world, f)
+
+
+def test_select_planes_vs_numpy(pv):
+    """sph_select_planes: the owned particles of planes x_lo and x_hi-1, in input order, with
+    exact counts (the binning rule of sph_build_cells)."""
+    import torch
+    from paper_1804_06231_b200.slabs import Slab, planes_of
+    p = synth.make("c2")
+    s = Slab.from_set(p, 1, 3)
+    g = pv.make_grid(p.nc, 1.0, p.gamma, s.x_lo, s.x_hi, 1)
+    x, v = torch.from_numpy(s.xyzh).cuda(), torch.from_numpy(s.vm).cuda()
+    cap = s.n_own
+    sx = torch.empty((2, cap, 4), dtype=torch.float32, device="cuda")
+    sv = torch.empty_like(sx)
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+    ws = pv.alloc_workspace(g, s.n_own)
+    pv.sph_select_planes(g, x, v, s.n_own, sx, sv, cnt, ws)
+    pv.check_status(ws)
+    pl = planes_of(s.xyzh, p.nc)
+    for k, plane in enumerate((s.x_lo, s.x_hi - 1)):
+        idx = np.nonzero(pl == plane)[0]
+        assert int(cnt[k]) == idx.size > 0
+        assert np.array_equal(sx[k, :idx.size].cpu().numpy(), s.xyzh[idx])
+        assert np.array_equal(sv[k, :idx.size].cpu().numpy(), s.vm[idx])
