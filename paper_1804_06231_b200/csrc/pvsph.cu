@@ -133,8 +133,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Ws {
     size_t status, cell_of, rank, rec, orec, count, tile_sum, big_count, big_items, huge_count,
-        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, row_home, sel_blk,
-        sel_sum, total;
+        huge_items, mid_items, w256_items, rows, rows_sum, tiles, counter, gen, gtiles, gcount, row_home, total;
     long long tile_cap, huge_cap;
 };
 
@@ -189,11 +188,6 @@ Ws ws_layout(const DevGrid &g, long long n)
     o = align_up(o + 8, 256);
     w.row_home = o;                      // per local (x, y) row: any home particle (build -> k_v4_tiles)
     o = align_up(o + 4 * (size_t)g.nxl * g.ny, 256);
-    const long long nsel = 2 * ((n + SEL_B - 1) / SEL_B) + 1;
-    w.sel_blk = o;                       // sph_select_planes: per-block counts -> offsets
-    o = align_up(o + 4 * (size_t)nsel, 256);
-    w.sel_sum = o;
-    o = align_up(o + 4 * (size_t)((nsel + SCAN_TILE - 1) / SCAN_TILE + 1), 256);
     w.total = o;
     return w;
 }
@@ -450,16 +444,20 @@ int sph_select_planes(const sph_grid *grid, int64_t n_own, const float *xyzh_in,
     if (cap > 0 && (!sel_xyzh || !sel_vm)) return SPH_EINVAL;
     if (((uintptr_t)xyzh_in % 16) || ((uintptr_t)vm_in % 16) || ((uintptr_t)sel_xyzh % 16) || ((uintptr_t)sel_vm % 16))
         return SPH_EINVAL;
+    // scratch in the build's cell_of region: it starts at a fixed offset for any capacity and
+    // is written only inside sph_build_cells (the call counter and other state are untouched)
     Ws w = ws_layout(g, n_own);
-    if (ws_bytes < w.total) return SPH_EINVAL;
+    const long long nblk = (n_own + SEL_B - 1) / SEL_B, nk = 2 * nblk;
+    const size_t blk_off = w.cell_of, sum_off = align_up(blk_off + 4 * (size_t)(nk + 1), 16);
+    if (ws_bytes < w.total || sum_off + 4 * (size_t)((nk + SCAN_TILE - 1) / SCAN_TILE + 1) > w.rank)
+        return SPH_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e;
     if (n_own == 0) {
         if ((e = cudaMemsetAsync(counts, 0, 16, s)) != cudaSuccess) return cuda_fail(e);
         return SPH_OK;
     }
-    const long long nblk = (n_own + SEL_B - 1) / SEL_B, nk = 2 * nblk;
-    int *blk = at<int>(ws, w.sel_blk), *sum = at<int>(ws, w.sel_sum);
+    int *blk = at<int>(ws, blk_off), *sum = at<int>(ws, sum_off);
     unsigned *status = at<unsigned>(ws, w.status);
     const float4 *x = reinterpret_cast<const float4 *>(xyzh_in), *v = reinterpret_cast<const float4 *>(vm_in);
     k_sel_count<<<(int)nblk, SEL_B, 0, s>>>(g, n_own, x, blk, nblk);
