@@ -233,6 +233,9 @@ def test_pair_rejects_non_neighbours(pv):
     bad = torch.tensor([[0, 2 * 25 + 2 * 5 + 2]], dtype=torch.int32).cuda()   # offset (2,2,2)
     pv.sph_density_pair(dp.grid, dp.cells, bad, acc, dp.ws)
     assert pv.sph_status(dp.ws) == 1
+    pv.sph_status_reset(dp.ws)
+    pv.sph_density_pair_sym(dp.grid, dp.cells, bad, acc, dp.ws)           # the symmetric kernel too
+    assert pv.sph_status(dp.ws) == 1
 
 
 # ---------------------------------------------------------------------------

@@ -163,3 +163,19 @@ def test_select_planes_vs_numpy(pv):
         assert int(cnt[k]) == idx.size > 0
         assert np.array_equal(sx[k, :idx.size].cpu().numpy(), s.xyzh[idx])
         assert np.array_equal(sv[k, :idx.size].cpu().numpy(), s.vm[idx])
+
+
+def test_select_planes_capacity(pv):
+    """A boundary plane longer than the send buffer: SPH_ECAPACITY in the status word."""
+    import torch
+    from paper_1804_06231_b200.slabs import Slab
+    p = synth.make("c2")
+    s = Slab.from_set(p, 0, 2)
+    g = pv.make_grid(p.nc, 1.0, p.gamma, s.x_lo, s.x_hi, 1)
+    x, v = torch.from_numpy(s.xyzh).cuda(), torch.from_numpy(s.vm).cuda()
+    sx = torch.empty((2, 8, 4), dtype=torch.float32, device="cuda")
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+    ws = pv.alloc_workspace(g, s.n_own)
+    pv.sph_select_planes(g, x, v, s.n_own, sx, torch.empty_like(sx), cnt, ws)
+    assert pv.sph_status(ws) == 3
+    assert int(cnt[0]) > 8                       # the true count is still reported
