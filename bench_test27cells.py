@@ -16,8 +16,10 @@ the symmetric kernel `sph_density_pair_sym`, one evaluation per distance)
 in-range interactions and pseudo-Verlet candidates per pair, interactions/s; and the
 weighted total of one instance, 8 corner + 12 edge + 6 face pairs.  The paper's
 single-core AVX times are printed as context only (other hardware; Table 3).  The
-raw-interaction test of Table 2 (no neighbour search) has no counterpart here: the C ABI
-has no entry point that skips the distance test.
+raw-interaction test of Table 2 (one particle with 2560 others, full masks, no
+neighbour search) is `sph_calibrate` mode 2 (include/sph_calib.h): the same M4 interaction
+with FFMA2 on every (i, j), no distance test; its rate gives the time of one particle's 2560
+interactions on the whole GPU and the fraction of that rate the full pipeline reaches.
 
 usage: python bench_test27cells.py [--nc 24] [--reps 5] [--warmup 3]
 """
@@ -142,6 +144,20 @@ def main():
     # the whole-pass engine on the same set: self + 26 one-sided gathers of every cell
     out = pv.Out.alloc(p.n)
     ms_all = timed(lambda: pv.sph_density_all(dp.grid, dp.cells, out, dp.ws))
+    inter_all = sum(res[k]["interactions_per_cell"] if k == "self" else 0 for k in res) * ncell
+    inter_all += sum(res[k]["interactions_per_symmetric_pair"] * ncell * {"face": 3, "edge": 6, "corner": 4}[k]
+                     for k in ("face", "edge", "corner"))
+    # Table 2 analogue: full-mask interactions (sph_calibrate mode 2: 256 per thread per iteration)
+    import ctypes
+    from paper_1804_06231_b200 import _lib
+    L = _lib.load()
+    sm = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, threads, iters = sm * 8, 256, 40
+    buf = torch.zeros(1, device="cuda")
+    call = lambda: L.sph_calibrate(2, blocks, threads, iters, ctypes.c_void_p(buf.data_ptr()),   # noqa: E731
+                                   ctypes.c_void_p(s.cuda_stream))
+    ms_raw = timed(call)
+    raw_rate = 256 * iters * blocks * threads / (ms_raw * 1e-3)
     line = {"benchmark": "test27cells (batched, P:195)", "n_particles": p.n, "cells": ncell,
             "per_cell": args.per_cell, "gamma_h_over_cl": float(synth.GAMMA * p.xyzh[0, 3] * args.nc),
             "dtype": "f32", "data": "synthetic", "reps": args.reps, "warmup": args.warmup,
@@ -150,7 +166,12 @@ def main():
             "weighted_total_us_per_instance_sym_kernel": total_sym_us,
             "weighted_total_definition": "8 corner + 12 edge + 6 face symmetric pairs (P:250)",
             "paper_avx_weighted_total_us": 1e3 * PAPER_AVX_MS["total"],
-            "density_all_ms": ms_all, "density_all_us_per_cell": 1e3 * ms_all / ncell}
+            "density_all_ms": ms_all, "density_all_us_per_cell": 1e3 * ms_all / ncell,
+            "density_all_interactions_per_s": inter_all / (ms_all * 1e-3),
+            "raw_fullmask_interactions_per_s": raw_rate,
+            "raw_us_per_2560_interactions": 2560 / raw_rate * 1e6,
+            "paper_avx_raw_ms_per_2560": 0.0084,
+            "pipeline_fraction_of_raw": inter_all / (ms_all * 1e-3) / raw_rate}
     print(json.dumps(line))
 
 
