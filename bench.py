@@ -332,7 +332,7 @@ def run_ours(args):
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        e2e_ms, h2d, d2h = runner.e2e_time(steps=max(3, min(nst, 5)), warmup=1)
+        e2e_ms, h2d, d2h = runner.e2e_time(steps=max(3, nst), warmup=1)
         if dist:
             t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
