@@ -29,9 +29,11 @@
  * Conventions for every call:
  *   - All array pointers are DEVICE pointers unless stated otherwise; the
  *     caller allocates and owns all memory (inputs, sph_cells arrays,
- *     outputs, workspace).  The library allocates nothing and keeps no
- *     global mutable state; calls on different streams with disjoint
- *     outputs and workspaces may run concurrently.
+ *     outputs, workspace).  The library allocates nothing; its only global
+ *     state is one-time kernel attribute setup (first call) and the text of
+ *     the last CUDA error (sph_strerror).  Calls on different streams with
+ *     disjoint outputs and workspaces may run concurrently (after a first
+ *     call of each entry point from one thread).
  *   - The workspace (sph_workspace_bytes) is zero-filled by the caller once
  *     after allocation; afterwards the calls own its contents (it carries
  *     the status word and a sph_density_all call counter that tags output
