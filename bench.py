@@ -367,6 +367,8 @@ def run_ours(args):
                            "step": "ghost exchange + build_cells + sort_cells + density_all"},
                 "interactions_per_step": tot_inter, "candidates_per_step": tot_cand,
                 "hit_fraction": tot_inter / max(1, tot_cand),
+                "evaluations_per_s": tot_cand / (ms_step_max * 1e-3),              # SV §8(d)
+                "particles_per_s": part.n_global / (ms_step_max * 1e-3),
                 "stage_ms": {k: statistics.mean(v) for k, v in stage.items()},
                 "density_ms_max_over_ranks": dens_max,
                 "gpu_launches": runner.launches_per_step * nst,
