@@ -14,6 +14,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "packed.cuh"
 
 namespace pvsph {
 
@@ -54,7 +55,7 @@ __device__ __forceinline__ void m4(float x, float &w, float &dw)
 // One in-range neighbour j of i (raw sums; scaled in finalise).
 __device__ __forceinline__ void interact(const IPart &p, float dx, float dy, float dz, float r2, float4 vmj, Acc &a)
 {
-    float rinv = r2 > 0.0f ? rsqrtf(r2) : 0.0f;
+    float rinv = r2 > 0.0f ? rsqrt_nr(r2) : 0.0f;
     float r = r2 * rinv;
     float x = r * p.Hinv;
     float w, dw;

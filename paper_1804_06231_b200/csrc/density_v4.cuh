@@ -363,7 +363,7 @@ __device__ __forceinline__ void interact_pair(f2 Hinv2, f2 dx, f2 dy, f2 dz, f2 
     float r2a, r2b;
     upk(r2, r2a, r2b);
     // r^2 = 0 (coincident particles): rinv stays finite, x = 0 and w'(0) = 0 make every gradient term 0
-    f2 rinv = pk(rsqrt_fast(fmaxf(r2a, 1e-30f)), rsqrt_fast(fmaxf(r2b, 1e-30f)));
+    f2 rinv = rsqrt_nr2(pk(fmaxf(r2a, 1e-30f), fmaxf(r2b, 1e-30f)));
     f2 x = mul2(mul2(r2, rinv), Hinv2);
     f2 u = sub2(bc2(1.0f), x);
     f2 v = fma2(bc2(-2.0f), x, bc2(1.0f));

@@ -1,0 +1,731 @@
+// density_v5.cuh -- the production sph_density_all engine (round 2).
+//
+// Method (identical to every other engine): every home particle i gathers from its own
+// cell and the 26 neighbour cells; in a neighbour cell only the window of its list
+// sorted along the pair axis whose projected separation is below H_i + delta is tested
+// (Code 2; the per-particle bound of P:151-165); in-range pairs are interacted
+// and the sums are written once per particle.
+//
+// What changed against v4 (same tiles from k_v4_tiles, same staging by bulk copies, same
+// output records), all to cut issued instructions per candidate and per hit:
+//  * List entries are staged as BYTE offsets of the staged particle (P + e, V + e): no
+//    index scaling on the hot path.
+//  * Each direction is swept on its own: the lane's two windows of direction d (a prefix
+//    of the +d list, a suffix of the -d list) are one contiguous range L[wb, wb + tot) of
+//    the reversed layout, so a candidate costs no window select.
+//  * No per-candidate bounds test: the warp runs its longest window, and a lane whose
+//    window is shorter keeps reading ITS -d segment beyond the window.  Those entries have
+//    projected separation >= H_i + delta, hence r > H_i: the distance test rejects them
+//    (the paper's windows are themselves padded: "max_index_a[i] is padded to a
+//    multiple of the SIMD width").  Past the segment end the address is clamped (one
+//    VIADDMNMX) onto a sentinel slot that points at a staged particle at infinity.
+//  * Drains: two hits per lane with FFMA2/FMUL2/FADD2, w' and the h-derivative factor with
+//    the constants folded into the finalisation, rsqrt refined by one Newton step.
+//  * COUNT (statistics) counts exactly the window candidates (t < tot), i.e. Code 2.
+#pragma once
+
+#include "common.cuh"
+#include "density.cuh"
+#include "density_v4.cuh"
+#include "packed.cuh"
+
+namespace pvsph {
+
+constexpr int V5_WARPS = V4_WARPS;
+constexpr int V5_TP = V4_TP;
+constexpr int V5_Q = 24;                               // hit stack depth per lane, 2-byte entries
+constexpr int V5_MS = V4_MS;                           // staged particles (+1 sentinel)
+constexpr int V5_ML = V4_ML + 14 * V4_MAXH;            // list entries + sentinels: one per (home cell, direction) + one per home cell
+constexpr int V5_MLA = (V5_ML + 7) / 8 * 8;
+constexpr size_t V5_SMEM = (size_t)(V5_MS + 2) * 16 + (size_t)(V5_MS + 2) * 16 + (size_t)V4_MAXCELLS * 16 +
+                           (size_t)V5_MLA * 2 + (size_t)V4_HOFF * 4 + (size_t)V5_WARPS * V5_Q * 32 * 2 +
+                           (size_t)V4_MAXZ * 16;
+static_assert(V5_MS * 16 < 65536, "byte offsets of staged particles fit 16 bits");
+static_assert(((V5_MS + 1) * 16) % 16 == 0 && (V5_MLA * 2) % 16 == 0, "16-byte aligned shared arrays");
+static_assert(13 * V4_MAXH <= 2 * V5_TP, "two direction segments per thread");
+
+// Dynamic shared memory of k_density_v5 (byte offsets from its start):
+//   [0, V5_OFF_V)       P: float4 x, y, z, 0 per staged particle (low-face images pre-shifted
+//                       by -L); P[V5_MS] = the far sentinel
+//   [V5_OFF_V, ...)     V: float4 vx, vy, vz, m per staged particle
+//   tab, L, hoff, hit stacks, seq.
+// List entries and hit-stack entries are the 16-bit SHARED ADDRESSES of P entries (the
+// kernel checks that P lies below 64 KiB of the shared window), so a candidate is loaded with
+// one LDS.128 [e] and its (v, m) with LDS.128 [e + V5_OFF_V]: no base add on the hot path.
+constexpr unsigned V5_OFF_V = (V5_MS + 2) * 16;
+constexpr unsigned V5_OFF_TAB = V5_OFF_V + (V5_MS + 2) * 16;
+constexpr unsigned V5_OFF_L = V5_OFF_TAB + V4_MAXCELLS * 16;
+
+struct V5Stage {
+    const int4 *tab;          // {base, count, gstart, flags | home count << 8}
+    int nzs;
+    unsigned sb;              // shared address of P[0]
+    unsigned sl;              // shared address of L[0]
+    unsigned sent;            // shared address of the list sentinel P[V5_MS] (NaN)
+    unsigned pad;             // shared address of the drain padding P[V5_MS + 1] (far, finite, v = m = 0)
+};
+
+// Packed accumulators.  With q = min(x, u)(u + v) >= 0 the kernel slope is w' = -3 q and
+// 3w + x w' = 3 (w - x q); the factors -3 and 3 are applied in the finalisation.
+//   rho: m w, wc: w, srt: m (w - x q), st: (w - x q), Dq: m q/r (v_j - v_i).x_ij,
+//   P/N: m q/r times the two products of (v_j - v_i) x x_ij.
+struct Acc5 {
+    f2 rho, wc, srt, st, Dq, Px, Nx, Py, Ny, Pz, Nz;
+};
+
+// Two interactions of one lane (hits j0, j1 of particle i), all arithmetic packed.
+// M4 in branch-free form: w = u^3 - v^3/2, w' = -3 min(x, u)(u + v), u = max(0, 1 - x),
+// v = max(0, 1 - 2x): equal to the two-branch R1 spline on [0, 1) (min(x, u) = u - v there,
+// without cancellation) and exactly 0 (w, q and every term) for x >= 1, so a padding entry at
+// the far sentinel contributes nothing and no mask is needed.
+__device__ __forceinline__ void interact2(f2 nHinv, f2 dx, f2 dy, f2 dz, f2 m, f2 nvx, f2 nvy, f2 nvz, Acc5 &A)
+{
+    const f2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+    // r^2 = 0 (coincident particles, R7): rinv finite, x = 0 and min(x, u) = 0 zero every gradient term
+    const f2 rinv = rsqrt_nr2(pk(fmaxf(r2.x, 1e-30f), fmaxf(r2.y, 1e-30f)));
+    const f2 nx = mul2(mul2(r2, rinv), nHinv);                 // -x
+    f2 u = add2(nx, bc2(1.0f));
+    u = pk(fmaxf(u.x, 0.0f), fmaxf(u.y, 0.0f));
+    f2 v = fma2(nx, bc2(2.0f), bc2(1.0f));
+    v = pk(fmaxf(v.x, 0.0f), fmaxf(v.y, 0.0f));
+    const f2 mn = pk(fminf(-nx.x, u.x), fminf(-nx.y, u.y));
+    const f2 uu = mul2(u, u);
+    const f2 w = fma2(uu, u, mul2(mul2(v, v), mul2(v, bc2(-0.5f))));
+    const f2 q = mul2(mn, add2(u, v));
+    acc_fma2(A.rho, m, w);
+    acc_add2(A.wc, w);
+    const f2 t = fma2(nx, q, w);                               // w - x q
+    acc_fma2(A.srt, m, t);
+    acc_add2(A.st, t);
+    const f2 fac = mul2(mul2(m, q), rinv);
+    acc_fma2(A.Dq, fac, fma2(nvx, dx, fma2(nvy, dy, mul2(nvz, dz))));
+    const f2 fx = mul2(fac, nvx), fy = mul2(fac, nvy), fz = mul2(fac, nvz);
+    acc_fma2(A.Px, fz, dy);
+    acc_fma2(A.Nx, fy, dz);
+    acc_fma2(A.Py, fx, dz);
+    acc_fma2(A.Ny, fz, dx);
+    acc_fma2(A.Pz, fy, dx);
+    acc_fma2(A.Nz, fx, dy);
+}
+
+#ifdef V5_VOLATILE_BISECT
+#define V5_LDU16 lds_u16
+#define V5_LDF4 lds_f4
+#else
+#define V5_LDU16 ldsr_u16
+#define V5_LDF4 ldsr_f4
+#endif
+// Windows of directions D0, D1 (four bisections in lockstep): the number of leading entries
+// of each segment whose projected separation is below Hk.  Segment 2k (+d of direction k, read
+// backwards from L[mid - 1]) has sep = (x_j - h) . d, segment 2k+1 (-d, forwards from L[mid])
+// sep = (h - x_j) . d.  State per search: the shared address of the last entry known to be
+// inside (or of L[mid] / L[mid - 1] when none is).  Probes are clamped onto the sentinel that
+// bounds every segment (before the +d reversed list: the previous block's sentinel or the
+// home cell's leading one; after the -d list: its own), whose separation is never below Hk,
+// so no probe needs a validity test.  `top`: largest power of two <= the warp's longest
+// segment, so all lanes run the same steps (the exact per-particle bound).
+__device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], const unsigned lim[4], const float h[4][3],
+                                            const float ax[2][3], const float Hk[2], int len[4])
+{
+    unsigned a[4] = {amid[0], amid[0] - 2u, amid[1], amid[1] - 2u};   // + side: L[mid]; - side: L[mid - 1]
+    for (int st = top; st > 0; st >>= 1) {
+        const unsigned s2 = 2u * (unsigned)st;
+        unsigned pa[4];
+        pa[0] = max(a[0] - s2, lim[0]);
+        pa[1] = min(a[1] + s2, lim[1]);
+        pa[2] = max(a[2] - s2, lim[2]);
+        pa[3] = min(a[3] + s2, lim[3]);
+        unsigned e[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) e[k] = V5_LDU16(pa[k]);
+        float4 p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = V5_LDF4(e[k]);
+        // separations along the (unnormalised) direction; the - side measures h - x_j
+        float sp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float *A = ax[k >> 1];
+            const float dx = p[k].x - h[k][0], dy = p[k].y - h[k][1], dz = p[k].z - h[k][2];
+            const float sv = fmaf(A[0], dx, fmaf(A[1], dy, A[2] * dz));
+            sp[k] = (k & 1) ? -sv : sv;
+        }
+        if (sp[0] < Hk[0]) a[0] = pa[0];
+        if (sp[1] < Hk[0]) a[1] = pa[1];
+        if (sp[2] < Hk[1]) a[2] = pa[2];
+        if (sp[3] < Hk[1]) a[3] = pa[3];
+    }
+    len[0] = (int)(amid[0] - a[0]) >> 1;
+    len[1] = (int)(a[1] + 2u - amid[0]) >> 1;
+    len[2] = (int)(amid[1] - a[2]) >> 1;
+    len[3] = (int)(a[3] + 2u - amid[1]) >> 1;
+}
+
+#if defined(V5_OLD_BISECT) || defined(V5_CHECK_BISECT)
+__device__ unsigned long long g_v5dbg[16];
+template <int D0, int D1>
+__device__ __forceinline__ void v5_windows2_old(const V5Stage &S, int top, const int f[4], const int n[4],
+                                                const float h[4][3], const float Hk[2], int len[4])
+{
+    int lo[4] = {0, 0, 0, 0};
+    for (int st = top; st > 0; st >>= 1) {
+        unsigned e[4];
+        bool v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int kk = lo[k] + st;
+            v[k] = kk <= n[k];
+            e[k] = v[k] ? ldsr_u16(S.sl + 2u * (unsigned)((k & 1) ? f[k] + kk - 1 : f[k] - kk + 1)) : S.sent;
+        }
+        float4 p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) p[k] = ldsr_f4(e[k]);
+        const float s0 = v4_dot<D0>(p[0].x - h[0][0], p[0].y - h[0][1], p[0].z - h[0][2]);
+        const float s1 = v4_dot<D0>(h[1][0] - p[1].x, h[1][1] - p[1].y, h[1][2] - p[1].z);
+        const float s2 = v4_dot<D1>(p[2].x - h[2][0], p[2].y - h[2][1], p[2].z - h[2][2]);
+        const float s3 = v4_dot<D1>(h[3][0] - p[3].x, h[3][1] - p[3].y, h[3][2] - p[3].z);
+        if (v[0] && s0 < Hk[0]) lo[0] += st;
+        if (v[1] && s1 < Hk[0]) lo[1] += st;
+        if (v[2] && s2 < Hk[1]) lo[2] += st;
+        if (v[3] && s3 < Hk[1]) lo[3] += st;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) len[k] = lo[k];
+}
+#endif
+
+// One lane = one home particle of a staged tile (see density_v4.cuh for the tile geometry).
+// lpos: first list entry of its home cell's block, qh: its staged column, yoff: its row.
+template <bool COUNT, bool FRAMES>
+__device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c, OutRec *orec, const V5Stage &S,
+                                            unsigned qbase, bool active, int i, int yoff, int qh, int lpos,
+                                            unsigned cand[4], unsigned hits[4])
+{
+    const unsigned sQ = qbase + 2u * (threadIdx.x & 31);
+    float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
+    if (active) {
+        const float4 a = c.xyzh[i];
+        const float4 b = c.vm[i];
+        x = a.x; y = a.y; z = a.z;
+        vx = b.x; vy = b.y; vz = b.z; m = b.w;
+        const double H = (double)g.gamma * (double)a.w;   // exact product; H^2, 1/H rounded once
+        H2 = (float)(H * H);
+        Hinv = (float)(1.0 / H);
+        Hd = (float)H + g.delta;
+    }
+    const float xs = x - g.boxf[0], ys = y - g.boxf[1], zs = z - g.boxf[2];   // exact where used (x >= L/2)
+    const float Hd2 = Hd * 1.41421356237309505f, Hd3 = Hd * 1.73205080756887729f;   // (H + delta) sqrt(kind)
+    const f2 nHinv = bc2(-Hinv);
+    auto scell = [&](int ox, int oy, int oz) { return ((ox + 1) * 4 + oy + yoff + 1) * S.nzs + qh + oz; };
+    const int4 eh = S.tab[scell(0, 0, 0)];
+    const int kh = active ? i - eh.z : -1;                // in-cell index of i
+
+    Acc5 A;
+    A.rho = A.wc = A.srt = A.st = A.Dq = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
+    unsigned qp = sQ;                                     // stack top (next free slot)
+    int npop = 0;
+
+    auto home_of = [&](unsigned fl, float &hx, float &hy, float &hz) {
+        hx = (fl & 1u) ? xs : x;
+        hy = (fl & 2u) ? ys : y;
+        hz = (fl & 4u) ? zs : z;
+    };
+    // Stack entries: the staged particle's shared address (FRAMES: staged index | frame bits
+    // << 12).  A drain pops up to 2 NP entries per lane (fewer on lanes holding fewer; the
+    // missing ones are the far sentinel, whose terms are exactly 0) and evaluates them in NP
+    // independent packed pairs.
+    auto drain = [&](auto np_tag) {
+        constexpr int NP = decltype(np_tag)::value;
+        const unsigned n = (qp - sQ) >> 6;
+        const unsigned take = min(n, 2u * NP);
+        unsigned qv[2 * NP];
+#pragma unroll
+        for (int s2 = 0; s2 < 2 * NP; ++s2) qv[s2] = (unsigned)s2 < take ? lds_u16(qp - 64u * (s2 + 1)) : 0xffffffffu;
+        qp -= 64u * take;
+        npop += (int)take;
+#pragma unroll
+        for (int pr = 0; pr < NP; ++pr) {
+            unsigned e[2];
+            float hxv[2], hyv[2], hzv[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const unsigned qq = qv[2 * pr + k];
+                hxv[k] = x; hyv[k] = y; hzv[k] = z;
+                if (FRAMES) {
+                    e[k] = qq == 0xffffffffu ? S.pad : S.sb + ((qq & 0xfffu) << 4);
+                    if (qq != 0xffffffffu) home_of(qq >> 12, hxv[k], hyv[k], hzv[k]);
+                } else {
+                    e[k] = qq == 0xffffffffu ? S.pad : qq;
+                }
+            }
+            const float4 p0 = ldsr_f4(e[0]), p1 = ldsr_f4(e[1]);
+            const float4 v0 = ldsr_f4_at<V5_OFF_V>(e[0]), v1 = ldsr_f4_at<V5_OFF_V>(e[1]);
+            interact2(nHinv, pk(hxv[0] - p0.x, hxv[1] - p1.x), pk(hyv[0] - p0.y, hyv[1] - p1.y),
+                      pk(hzv[0] - p0.z, hzv[1] - p1.z), pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx),
+                      pk(v0.y - vy, v1.y - vy), pk(v0.z - vz, v1.z - vz), A);
+        }
+    };
+    // keep every stack at <= V5_Q - 9 entries (8 pushes follow before the next check); drain
+    // four per lane when most lanes hold four
+    auto drain_check = [&]() {
+        for (;;) {
+            const unsigned n = (qp - sQ) >> 6;
+            if (!(__popc(__ballot_sync(0xffffffffu, n >= 4)) >= 24 || __any_sync(0xffffffffu, n >= V5_Q - 8)))
+                break;
+            drain(std::integral_constant<int, 2>{});
+        }
+    };
+
+    // ---- the self cell: all j != i of the home cell (staged contiguously) ----
+    {
+        const int total = active ? eh.y : 0;
+        const int trip = __reduce_max_sync(0xffffffffu, total);
+        const unsigned pa = S.sb + 16u * (unsigned)eh.x;
+        for (int t = 0; t < trip; t += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int tt = t + u;
+                const bool ok = tt < total && tt != kh;
+                const unsigned e = ok ? pa + 16u * (unsigned)tt : S.sent;
+                const float4 p = ldsr_f4(e);
+                const float dx = x - p.x, dy = y - p.y, dz = z - p.z;
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (COUNT) cand[0] += ok ? 1u : 0u;
+                if (r2 < H2) {                             // the sentinel never passes
+                    sts_u16_push(qp, FRAMES ? (e - S.sb) >> 4 : e);
+                    qp += 64u;
+                    if (COUNT) ++hits[0];
+                }
+            }
+            drain_check();
+        }
+    }
+
+    // ---- 13 directions: windows two directions at a time, then one sweep per direction ----
+    int pos = lpos + 1;                                   // after the home cell's leading sentinel
+    for (int d0 = 0; d0 < 13; d0 += 2) {
+        const int nd = d0 + 1 < 13 ? 2 : 1;
+        int mid[2] = {0, 0}, sent[2] = {0, 0};
+        unsigned fl0v[2] = {0, 0}, fl1v[2] = {0, 0};
+        unsigned amid[2] = {S.sl, S.sl}, lim[4] = {S.sl, S.sl, S.sl, S.sl};
+        float hh[4][3];
+        float Hkv[2] = {-3e38f, -3e38f};
+        float axv[2][3] = {{0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f}};
+        int nmax = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int d = d0 + k;
+            hh[2 * k][0] = hh[2 * k + 1][0] = x;
+            hh[2 * k][1] = hh[2 * k + 1][1] = y;
+            hh[2 * k][2] = hh[2 * k + 1][2] = z;
+            if (k < nd) {
+                const int kind = v4_kind(d);
+                Hkv[k] = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
+                const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                axv[k][0] = (float)a0;
+                axv[k][1] = (float)a1;
+                axv[k][2] = (float)a2;
+                const int4 ep = S.tab[scell(a0, a1, a2)];
+                const int4 em = S.tab[scell(-a0, -a1, -a2)];
+                mid[k] = pos + ep.y;                      // boundary between the two reversed segments
+                sent[k] = mid[k] + em.y;                  // the sentinel slot after the -d segment
+                amid[k] = S.sl + 2u * (unsigned)mid[k];
+                lim[2 * k] = S.sl + 2u * (unsigned)(pos - 1);   // the sentinel before the +d segment
+                lim[2 * k + 1] = S.sl + 2u * (unsigned)sent[k];
+                pos = sent[k] + 1;
+                nmax = max(nmax, max(ep.y, em.y));
+                if (FRAMES) {
+                    fl0v[k] = (unsigned)ep.w & 7u;
+                    fl1v[k] = (unsigned)em.w & 7u;
+                    home_of(fl0v[k], hh[2 * k][0], hh[2 * k][1], hh[2 * k][2]);
+                    home_of(fl1v[k], hh[2 * k + 1][0], hh[2 * k + 1][1], hh[2 * k + 1][2]);
+                }
+            }
+        }
+        if (!active) Hkv[0] = Hkv[1] = -3e38f;           // inactive lanes (position 0): empty windows
+        nmax = __reduce_max_sync(0xffffffffu, nmax);
+        const int top = nmax > 0 ? 1 << (31 - __clz(nmax)) : 0;
+        int len[4] = {0, 0, 0, 0};
+#ifdef V5_OLD_BISECT
+        {
+            int f[4], nn[4];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                f[2 * k] = (int)((amid[k] - S.sl) >> 1) - 1;
+                f[2 * k + 1] = (int)((amid[k] - S.sl) >> 1);
+                nn[2 * k] = k < nd && active ? (int)((amid[k] - lim[2 * k]) >> 1) - 1 : 0;
+                nn[2 * k + 1] = k < nd && active ? (int)((lim[2 * k + 1] - amid[k]) >> 1) : 0;
+            }
+#define V5W2O(P) case P: v5_windows2_old<2 * P, (2 * P + 1 < 13 ? 2 * P + 1 : 0)>(S, top, f, nn, hh, Hkv, len); break;
+            switch (d0 >> 1) { V5W2O(0) V5W2O(1) V5W2O(2) V5W2O(3) V5W2O(4) V5W2O(5) V5W2O(6) }
+#undef V5W2O
+        }
+#else
+        v5_windows2(top, amid, lim, hh, axv, Hkv, len);
+#ifdef V5_CHECK_BISECT
+        {
+            int f[4], nn[4], lo2[4];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                f[2 * k] = (int)((amid[k] - S.sl) >> 1) - 1;
+                f[2 * k + 1] = (int)((amid[k] - S.sl) >> 1);
+                nn[2 * k] = k < nd && active ? (int)((amid[k] - lim[2 * k]) >> 1) - 1 : 0;
+                nn[2 * k + 1] = k < nd && active ? (int)((lim[2 * k + 1] - amid[k]) >> 1) : 0;
+            }
+#define V5W2O(P) case P: v5_windows2_old<2 * P, (2 * P + 1 < 13 ? 2 * P + 1 : 0)>(S, top, f, nn, hh, Hkv, lo2); break;
+            switch (d0 >> 1) { V5W2O(0) V5W2O(1) V5W2O(2) V5W2O(3) V5W2O(4) V5W2O(5) V5W2O(6) }
+#undef V5W2O
+            for (int k = 0; k < 4; ++k)
+                if (lo2[k] != len[k] && atomicAdd(&g_v5dbg[0], 1ull) == 0) {
+                    g_v5dbg[1] = d0; g_v5dbg[2] = k; g_v5dbg[3] = lo2[k]; g_v5dbg[4] = len[k];
+                    g_v5dbg[5] = nn[k]; g_v5dbg[6] = top; g_v5dbg[7] = amid[k >> 1]; g_v5dbg[8] = lim[k];
+                    g_v5dbg[9] = __float_as_uint(Hkv[k >> 1]);
+                }
+        }
+#endif
+#endif
+#pragma unroll 1
+        for (int k = 0; k < nd; ++k) {
+            const int kind = v4_kind(d0 + k);
+            // (selects, not indexing: the loop is not unrolled, to keep one copy of the drains)
+            const int len0 = k ? len[2] : len[0], tot = len0 + (k ? len[3] : len[1]);
+            const unsigned fl0k = k ? fl0v[1] : fl0v[0], fl1k = k ? fl1v[1] : fl1v[0];
+            const int trip = __reduce_max_sync(0xffffffffu, tot);
+            const unsigned lb = S.sl + 2u * (unsigned)((k ? mid[1] : mid[0]) - len0);
+            const unsigned ls = S.sl + 2u * (unsigned)(k ? sent[1] : sent[0]);
+            auto step = [&](int t, auto n_tag) {
+                constexpr int NU = decltype(n_tag)::value;
+                unsigned e[NU];
+#pragma unroll
+                for (int u = 0; u < NU; ++u) e[u] = ldsr_u16(min(lb + 2u * (unsigned)(t + u), ls));
+                float4 pp[NU];
+#pragma unroll
+                for (int u = 0; u < NU; ++u) pp[u] = ldsr_f4(e[u]);
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    const float4 p = pp[u];
+                    float hx = x, hy = y, hz = z;
+                    unsigned fl = 0;
+                    if (FRAMES) {
+                        fl = t + u < len0 ? fl0k : fl1k;
+                        home_of(fl, hx, hy, hz);
+                    }
+                    const float dx = hx - p.x, dy = hy - p.y, dz = hz - p.z;
+                    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                    if (COUNT) cand[kind] += t + u < tot ? 1u : 0u;
+                    if (r2 < H2) {                         // beyond the window: never (sep >= H + delta)
+                        sts_u16_push(qp, FRAMES ? ((e[u] - S.sb) >> 4) | (fl << 12) : e[u]);
+                        qp += 64u;
+                        if (COUNT) ++hits[kind];
+                    }
+                }
+            };
+            for (int t = 0; t < trip; t += 8) {
+                if (t + 4 < trip)
+                    step(t, std::integral_constant<int, 8>{});
+                else                                      // a tail of <= 4 candidates
+                    step(t, std::integral_constant<int, 4>{});
+                drain_check();
+            }
+        }
+    }
+    while (__any_sync(0xffffffffu, qp != sQ)) drain(std::integral_constant<int, 2>{});
+
+    if (active) {
+        // finalise: self term w(0) = 1/2, w(0) - 0 q = 1/2; K3 = 16/(pi H^3); rho_dh = -(K3 gamma/H) (3/2 m + 3 S_t);
+        // div = -(K3/H)(-3) D/rho with D = sum m q/r (v_j - v_i).x_ij ... see DESIGN.md §4.4
+        const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;
+        const float rho = K3 * fmaf(0.5f, m, sum2(A.rho));
+        const float wc = K3 * (0.5f + sum2(A.wc));
+        const float dh = -3.0f * K3 * g.gamma * Hinv;
+        const float rho_dh = dh * fmaf(0.5f, m, sum2(A.srt));
+        const float wc_dh = dh * (0.5f + sum2(A.st));
+        const float gf = -3.0f * K3 * Hinv / rho;
+        store_rec(orec, c.perm[i], rho, wc, rho_dh, wc_dh, gf * sum2(A.Dq), gf * (sum2(A.Px) - sum2(A.Nx)),
+                  gf * (sum2(A.Py) - sum2(A.Ny)), gf * (sum2(A.Pz) - sum2(A.Nz)), npop);
+    }
+}
+
+// Persistent CTAs over the k_v4_tiles list (same tiles and staging as v4; list block layout
+// per home cell: for d = 0..12 the +d list reversed, the -d list reversed, one sentinel).
+template <bool COUNT>
+__global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, OutRec *orec, sph_stats *st,
+                                                          const int4 *__restrict__ tiles,
+                                                          const int *__restrict__ ntiles_p, int *tile_counter,
+                                                          const unsigned *__restrict__ genp, unsigned *status)
+{
+    extern __shared__ __align__(16) unsigned char v5_smem[];
+    float4 *P = reinterpret_cast<float4 *>(v5_smem);
+    float4 *V = P + V5_MS + 2;
+    int4 *tab = reinterpret_cast<int4 *>(V + V5_MS + 2);
+    uint16_t *L = reinterpret_cast<uint16_t *>(tab + V4_MAXCELLS);
+    int *hoff = reinterpret_cast<int *>(L + V5_MLA);
+    uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_HOFF);
+    int4 *seq = reinterpret_cast<int4 *>(queue + V5_WARPS * V5_Q * 32);
+    __shared__ int4 s_next;
+    __shared__ int s_wsum[V5_WARPS];
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const unsigned mbar = smem_addr(&s_mbar);
+    unsigned mbar_phase = 0;
+
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const RowPairs rp = row_pairs(g);
+    const int ntiles = *ntiles_p;
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    const int4 kEnd = make_int4(-1, 0, 0, 0);
+    const unsigned sb = smem_addr(P);
+    // entries are 16-bit shared addresses of P: P must lie in the first 64 KiB of the window
+    // (it does: P starts the dynamic shared memory, after ~1 KiB of static shared memory)
+    if (sb + 16u * (V5_MS + 2) > 65536u) {
+        if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+        return;
+    }
+
+    int pf_start[2] = {0, 0}, pf_end[2] = {0, 0}, pf_nh[2] = {0, 0};
+    auto prefetch = [&](int4 td) {
+        if (td.x < 0) return;
+        const TileGeom t = tile_geom(g, rp, td);
+        if (!t.staged) return;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int s = 2 * threadIdx.x + k;
+            if (s < V4_ROWS * t.nzs) {
+                unsigned fl;
+                const long long cell = staged_cell(g, t, s, fl);
+                pf_start[k] = c.cell_start[cell];
+                pf_end[k] = c.cell_start[cell + 1];
+                pf_nh[k] = c.cell_nhome[cell];
+            }
+        }
+    };
+    if (threadIdx.x == 0) {
+        const int t0 = atomicAdd(tile_counter, 1);
+        s_next = t0 < ntiles ? tiles[t0] : kEnd;
+        s_gen = *genp;
+        // sentinels (never restaged).  P[V5_MS]: the list sentinel, NaN coordinates, so every
+        // comparison with it is false (window probes on either side, distance tests).
+        // P[V5_MS + 1]: the drain padding, far but finite (r^2 ~ 3e30) with (v, m) = 0, whose
+        // terms evaluate to exactly 0 (x >> 1, q = w = 0).
+        const float qnan = __int_as_float(0x7fc00000);
+        P[V5_MS] = make_float4(qnan, qnan, qnan, 0.0f);
+        V[V5_MS] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        P[V5_MS + 1] = make_float4(1e15f, 1e15f, 1e15f, 0.0f);
+        V[V5_MS + 1] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int4 td = s_next;
+    prefetch(td);
+
+    while (td.x >= 0) {
+        __syncthreads();                                  // s_next consumed, previous tile done
+        if (threadIdx.x == 0) {
+            const int t1 = atomicAdd(tile_counter, 1);
+            s_next = t1 < ntiles ? tiles[t1] : kEnd;
+        }
+        const TileGeom T = tile_geom(g, rp, td);
+        bool staged = T.staged;
+        if (staged) {
+            const int ncs = V4_ROWS * T.nzs;
+            int cnt2[2] = {0, 0};
+            int4 ent[2];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const int s = 2 * threadIdx.x + k;
+                ent[k] = make_int4(0, 0, 0, 0);
+                if (s < ncs) {
+                    unsigned fl;
+                    staged_cell(g, T, s, fl);
+                    cnt2[k] = pf_end[k] - pf_start[k];
+                    ent[k] = make_int4(0, cnt2[k], pf_start[k], (int)fl | (pf_nh[k] << 8));
+                }
+            }
+            if (2 * threadIdx.x < ncs) tab[2 * threadIdx.x] = ent[0];
+            if (2 * threadIdx.x + 1 < ncs) tab[2 * threadIdx.x + 1] = ent[1];
+            __syncthreads();
+            // direction blocks: (home cell h, direction d) -> n(+d) + n(-d) + 1 entries; two per thread
+            const int ndseg = 13 * T.nh;
+            int dsz[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int gs = 2 * threadIdx.x + j;
+                dsz[j] = 0;
+                if (gs < ndseg) {
+                    const int h = gs / 13, d = gs % 13;
+                    const int r = h / T.nzh, q = h % T.nzh + 1;
+                    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                    dsz[j] = tab[((a0 + 1) * 4 + a1 + r + 1) * T.nzs + q + a2].y +
+                             tab[((-a0 + 1) * 4 - a1 + r + 1) * T.nzs + q - a2].y + 1 + (d == 0 ? 1 : 0);
+                }
+            }
+            if (wl == V5_WARPS - 1) {
+                int4 sl = make_int4(0, 0, 0, 0);
+                int ns = 0;
+                if (lane < T.nzh) {
+                    const int4 ea = tab[5 * T.nzs + lane + 1];
+                    const int4 eb = tab[6 * T.nzs + lane + 1];
+                    sl = make_int4(ea.z, ea.w >> 8, eb.z, 0);
+                    ns = (ea.w >> 8) + (T.hasB ? (eb.w >> 8) : 0);
+                }
+                int xx = ns;
+#pragma unroll
+                for (int o2 = 1; o2 < 32; o2 <<= 1) {
+                    const int yv = __shfl_up_sync(0xffffffffu, xx, o2);
+                    if (lane >= o2) xx += yv;
+                }
+                sl.w = xx - ns;
+                if (lane < T.nzh) seq[lane] = sl;
+            }
+            int ptot;
+            const int pp = block_exscan((cnt2[0] + cnt2[1]) | ((dsz[0] + dsz[1]) << 16), s_wsum, ptot);
+            const int total = ptot & 0xffff, ltotal = ptot >> 16;
+            const int pre = pp & 0xffff;
+            int lpre = pp >> 16;
+            if (2 * threadIdx.x < ncs) tab[2 * threadIdx.x].x = pre;
+            if (2 * threadIdx.x + 1 < ncs) tab[2 * threadIdx.x + 1].x = pre + cnt2[0];
+            int *segoff = reinterpret_cast<int *>(queue);        // scratch: the hit stacks are idle now
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int gs = 2 * threadIdx.x + j;
+                if (gs < ndseg) {
+                    segoff[gs] = lpre;
+                    if (gs % 13 == 0) hoff[gs / 13] = lpre;
+                }
+                lpre += dsz[j];
+            }
+            if (total > V5_MS || ltotal > V5_ML || T.nh > V4_MAXH) staged = false;   // CTA-uniform
+            __syncthreads();
+            if (staged) {
+                if (wl == 0) {
+                    if (lane == 0) mbar_expect_tx(mbar, (unsigned)total * 32u);
+                    __syncwarp();
+                    const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
+                    for (int job = lane; job < V4_ROWS * 3; job += 32) {
+                        const int r = job / 3, piece = job % 3;
+                        const int q0 = piece == 0 ? 0 : (piece == 1 ? (wlo ? 1 : 0) : T.nzs - 1);
+                        const int q1 = piece == 0 ? (wlo ? 1 : 0) : (piece == 1 ? (whi ? T.nzs - 1 : T.nzs) : (whi ? T.nzs : T.nzs - 1));
+                        if (q1 <= q0) continue;
+                        const int4 ea = tab[r * T.nzs + q0];
+                        const int4 eb = tab[r * T.nzs + q1 - 1];
+                        const unsigned bytes = (unsigned)(eb.x + eb.y - ea.x) * 16u;
+                        if (bytes == 0) continue;
+                        bulk_g2s(smem_addr(P + ea.x), c.xyzh + ea.z, bytes, mbar);
+                        bulk_g2s(smem_addr(V + ea.x), c.vm + ea.z, bytes, mbar);
+                    }
+                }
+                // list segments (2 per direction block), entries turned into staged byte offsets
+                const int nseg = 2 * ndseg;
+                for (int gs2 = threadIdx.x; gs2 < nseg; gs2 += V5_TP) {
+                    const int gs = gs2 >> 1, neg = gs2 & 1;
+                    const int h = gs / 13, d = gs % 13, sg = neg ? -1 : 1;
+                    const int r = h / T.nzh, q = h % T.nzh + 1;
+                    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                    const int4 ep = tab[((a0 + 1) * 4 + a1 + r + 1) * T.nzs + q + a2];
+                    const int4 e = neg ? tab[((-a0 + 1) * 4 - a1 + r + 1) * T.nzs + q - a2] : ep;
+                    const int mid = segoff[gs] + (d == 0 ? 1 : 0) + ep.y;
+                    if (d == 0 && !neg) L[segoff[gs]] = (uint16_t)(sb + 16u * V5_MS);   // the home cell's leading sentinel
+                    // +d reversed ends at mid - 1 (entry 0 at mid - 1); -d reversed starts at mid
+                    // (its LAST list entry first); the sentinel after it
+                    const int dst0 = neg ? mid + e.y - 1 : mid - 1;        // slot of list entry 0
+                    if (neg) L[mid + e.y] = (uint16_t)(sb + 16u * V5_MS);
+                    const uint16_t *src = c.ord + (long long)d * c.cap + e.z;
+                    const int mis = (int)(((uintptr_t)src >> 1) & 7);
+                    const uint4 *wsrc = reinterpret_cast<const uint4 *>(src - mis);
+                    const int nw = (mis + e.y + 7) >> 3;
+                    for (int w0 = 0; w0 < nw; w0 += 4) {
+                        uint4 v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) v[u] = w0 + u < nw ? __ldg(wsrc + w0 + u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int k = 8 * (w0 + u) - mis;
+                            const unsigned wd[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                            for (int t = 0; t < 8; ++t) {
+                                const unsigned qv = (t & 1) ? wd[t >> 1] >> 16 : wd[t >> 1] & 0xffffu;
+                                if (k + t >= 0 && k + t < e.y) L[dst0 - k - t] = (uint16_t)(sb + 16u * (e.x + qv));
+                            }
+                        }
+                    }
+                }
+                mbar_wait(mbar, mbar_phase);
+                mbar_phase ^= 1u;
+                if (T.za == 0 || T.y0 == 0 || g.x_lo + T.xo == 0) {
+                    __syncthreads();
+                    for (int sc = wl; sc < V4_ROWS * T.nzs; sc += V5_WARPS) {
+                        const int4 e = tab[sc];
+                        if (!(e.w & 56)) continue;
+                        const float sx = (e.w & 8) ? g.boxf[0] : 0.0f;
+                        const float sy = (e.w & 16) ? g.boxf[1] : 0.0f;
+                        const float sz = (e.w & 32) ? g.boxf[2] : 0.0f;
+                        for (int k = lane; k < e.y; k += 32) {
+                            float4 qv = P[e.x + k];
+                            qv.x -= sx;
+                            qv.y -= sy;
+                            qv.z -= sz;
+                            P[e.x + k] = qv;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        __syncthreads();
+        const int4 td_next = s_next;
+        prefetch(td_next);
+
+        auto home_slot = [&](int h, int &slot, int &yo, int &tz) {
+            const int qq = T.first + h;
+            int lo = 0, hi = T.nzh - 1;
+            while (lo < hi) {
+                const int md = (lo + hi + 1) >> 1;
+                if (seq[md].w <= qq) lo = md; else hi = md - 1;
+            }
+            const int4 e = seq[lo];
+            const int loc = qq - e.w;
+            yo = loc < e.y ? 0 : 1;
+            slot = yo == 0 ? e.x + loc : e.z + (loc - e.y);
+            tz = lo;
+        };
+        if (staged) {
+            const int h = threadIdx.x;
+            const bool active = h < T.cnt;
+            int i = 0, yoff = 0, tz = 0, lpos = 0;
+            if (active) {
+                home_slot(h, i, yoff, tz);
+                lpos = hoff[yoff * T.nzh + tz];
+            } else {
+                i = seq[0].x;
+            }
+            const V5Stage S{tab, T.nzs, sb, smem_addr(L), sb + 16u * V5_MS, sb + 16u * (V5_MS + 1)};
+            const unsigned qb = smem_addr(queue + wl * V5_Q * 32);
+            if (wl * 32 < T.cnt) {
+                if (T.frames)
+                    v5_particle<COUNT, true>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
+                else
+                    v5_particle<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
+            }
+        } else if (T.cnt > 0) {
+            const long long rowA = ((long long)(T.xo + g.ghost_x) * g.ny + T.y0) * g.nz;
+            const int ntot = T.cnt > 0 ? T.cnt : -T.cnt;
+            for (int h = threadIdx.x; h < ntot; h += V5_TP) {
+                int qq = T.first + h, z = T.za, slot = 0;
+                for (;; ++z) {
+                    const long long ca = rowA + z;
+                    const int a0 = c.cell_start[ca], na = c.cell_nhome[ca];
+                    const int b0 = T.hasB ? c.cell_start[ca + g.nz] : 0;
+                    const int nb = T.hasB ? c.cell_nhome[ca + g.nz] : 0;
+                    if (qq < na) { slot = a0 + qq; break; }
+                    if (qq < na + nb) { slot = b0 + (qq - na); break; }
+                    qq -= na + nb;
+                }
+                v4_particle_global<COUNT>(g, c, orec, slot, cand, hits);
+            }
+        }
+        td = td_next;
+    }
+    flush_stats<COUNT>(st, cand, hits);
+}
+
+}  // namespace pvsph

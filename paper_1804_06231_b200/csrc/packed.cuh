@@ -30,6 +30,19 @@ __device__ __forceinline__ float rsqrt_fast(float x)
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// rsqrt refined by one Newton step, y (3/2 - x y^2 / 2): ~1 ulp instead of MUFU.RSQ's ~2
+// (R14: near the cut-off w' amplifies the rounding of x = r/H)
+__device__ __forceinline__ float rsqrt_nr(float x)
+{
+    const float y = rsqrt_fast(x);
+    return y * fmaf(-0.5f * x * y, y, 1.5f);
+}
+__device__ __forceinline__ f2 rsqrt_nr2(f2 x)
+{
+    const f2 y = make_float2(rsqrt_fast(x.x), rsqrt_fast(x.y));
+    const f2 t = __ffma2_rn(__fmul2_rn(x, make_float2(-0.5f, -0.5f)), __fmul2_rn(y, y), make_float2(1.5f, 1.5f));
+    return __fmul2_rn(y, t);
+}
 __device__ __forceinline__ float sum2(f2 v) { return v.x + v.y; }
 __device__ __forceinline__ f2 zero2() { return make_float2(0.0f, 0.0f); }
 
@@ -58,6 +71,14 @@ __device__ __forceinline__ float4 ldsr_f4(unsigned a)
 {
     float4 v;
     asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+// the same with a constant byte offset folded into the instruction ([reg + imm])
+template <unsigned OFF>
+__device__ __forceinline__ float4 ldsr_f4_at(unsigned a)
+{
+    float4 v;
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a), "n"(OFF));
     return v;
 }
 __device__ __forceinline__ unsigned ldsr_u16(unsigned a)
@@ -102,6 +123,12 @@ __device__ __forceinline__ void mbar_wait(unsigned a, unsigned parity)
 __device__ __forceinline__ void sts_u16(unsigned a, unsigned v)
 {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+// push onto a hit stack: volatile (ordered against the volatile pops), but no memory clobber,
+// so the read-only staged loads around it can still be scheduled freely
+__device__ __forceinline__ void sts_u16_push(unsigned a, unsigned v)
+{
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
 }
 __device__ __forceinline__ void sts_u32(unsigned a, unsigned v)
 {

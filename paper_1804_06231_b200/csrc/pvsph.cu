@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "../../include/sph_calib.h"
 #include "build.cuh"
@@ -12,6 +13,7 @@
 #include "common.cuh"
 #include "density.cuh"
 #include "density_v4.cuh"
+#include "density_v5.cuh"
 #include "density_pair.cuh"
 #include "density_dense.cuh"
 #include "sort.cuh"
@@ -26,6 +28,54 @@ int cuda_fail(cudaError_t e)
 {
     std::snprintf(g_cuda_msg, sizeof(g_cuda_msg), "CUDA error %d: %s", (int)e, cudaGetErrorString(e));
     return SPH_ECUDA;
+}
+
+// Per-device launch attributes (dynamic shared memory opt-ins, occupancy, SM count), set
+// once per device on first use: cudaFuncSetAttribute applies to the current device only.
+struct DevAttrs {
+    int sms = 0, v4_blocks_per_sm = 1, v5_blocks_per_sm = 1;
+};
+constexpr int kMaxDevices = 64;
+DevAttrs g_dev_attrs[kMaxDevices];
+std::once_flag g_dev_once[kMaxDevices];
+
+const DevAttrs &dev_attrs(int dev)
+{
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    std::call_once(g_dev_once[dev], [dev]() {
+        DevAttrs &a = g_dev_attrs[dev];
+        cudaDeviceGetAttribute(&a.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(k_density_v4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
+        cudaFuncSetAttribute(k_density_v4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
+        cudaFuncSetAttribute(k_density_v5<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V5_SMEM);
+        cudaFuncSetAttribute(k_density_v5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V5_SMEM);
+        cudaFuncSetAttribute(k_density_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
+        cudaFuncSetAttribute(k_density_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
+        cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
+        cudaFuncSetAttribute(k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_HUGE_MAX * 8);
+        cudaFuncSetAttribute(k_density_pair_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
+        cudaFuncSetAttribute(k_density_pair_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.v4_blocks_per_sm, k_density_v4<false>, V4_TP, V4_SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.v5_blocks_per_sm, k_density_v5<false>, V5_TP, V5_SMEM);
+        if (a.v4_blocks_per_sm < 1) a.v4_blocks_per_sm = 1;
+        if (a.v5_blocks_per_sm < 1) a.v5_blocks_per_sm = 1;
+        if (a.sms < 1) a.sms = 148;
+        cudaGetLastError();
+    });
+    return g_dev_attrs[dev];
+}
+
+// the attributes of the current device (set on first use)
+int ensure_attrs()
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e);
+    dev_attrs(dev);
+    return SPH_OK;
 }
 
 int check_launch()
@@ -279,11 +329,7 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
             g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, cells->cell_hmax,
             row_home, g.nz, big_items, big_count, bt_items, bt_count);
-        static bool bt_attr = false;
-        if (!bt_attr) {
-            cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
-            bt_attr = true;
-        }
+        if ((rc = ensure_attrs()) != SPH_OK) return rc;
         k_stable_bitonic<<<148, STABLE_BT_T, STABLE_BT_MAX * 8, s>>>(cells->cell_start, rec, xs, vs, cells->perm,
                                                                     bt_items, bt_count);
         k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, big_items,
@@ -331,12 +377,7 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     k_sort_mid<<<148 * 8, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, mid_items, huge_count + 2, need);
     k_sort_warp256<<<148 * 4, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, w256_items, huge_count + 3, need);
     k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count, need);
-    static bool huge_attr = false;
-    if (!huge_attr) {
-        cudaFuncSetAttribute(k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_HUGE_MAX * 8);
-        huge_attr = true;
-    }
+    if ((rc = ensure_attrs()) != SPH_OK) return rc;
     k_sort_bitonic<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, SORT_MED_MAX * 8, s>>>(
         g, c, cells->order, huge_items, huge_count, (int)w.huge_cap, need);
     k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, SORT_HUGE_MAX * 8, s>>>(
@@ -377,12 +418,7 @@ int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t
     cudaStream_t s = (cudaStream_t)stream;
     unsigned *status = at<unsigned>(ws, 0);
     const int2 *pr = reinterpret_cast<const int2 *>(pairs);
-    static bool pair_attr = false;
-    if (!pair_attr) {
-        cudaFuncSetAttribute(k_density_pair_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
-        cudaFuncSetAttribute(k_density_pair_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
-        pair_attr = true;
-    }
+    if ((rc = ensure_attrs()) != SPH_OK) return rc;
     const int blocks = grid_blocks(npairs, 1, 148 * 8);
     if (stats)
         k_density_pair_staged<true><<<blocks, PAIR_WARPS * 32, PAIR_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr,
@@ -405,12 +441,7 @@ int sph_density_pair_sym(const sph_grid *grid, const sph_cells *cells, const int
     cudaStream_t s = (cudaStream_t)stream;
     unsigned *status = at<unsigned>(ws, 0);
     const int2 *pr = reinterpret_cast<const int2 *>(pairs);
-    static bool sym_attr = false;
-    if (!sym_attr) {
-        cudaFuncSetAttribute(k_density_pair_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
-        cudaFuncSetAttribute(k_density_pair_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
-        sym_attr = true;
-    }
+    if ((rc = ensure_attrs()) != SPH_OK) return rc;
     const int blocks = grid_blocks(npairs, 1, 148 * 12);
     if (stats)
         k_density_pair_sym<true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dev_cells(cells), dev_out(acc), pr, npairs,
@@ -520,24 +551,25 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
                                                                       w.tile_cap, status, gen, gtiles, gcount,
                                                                       at<int>(ws, w.row_home));
     if ((e = cudaMemsetAsync(counter, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
-    static int blocks_per_sm = 0, sms = 0;
-    if (!blocks_per_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaFuncSetAttribute(k_density_v4<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
-        cudaFuncSetAttribute(k_density_v4<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V4_SMEM);
-        cudaFuncSetAttribute(k_density_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
-        cudaFuncSetAttribute(k_density_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_density_v4<false>, V4_TP, V4_SMEM);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
-    }
-    const int blocks = sms * blocks_per_sm;
+    const bool v4 = eng && eng[0] == 'v' && eng[1] == '4';   // round-1 engine (comparison only)
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return cuda_fail(e);
+    const DevAttrs &da = dev_attrs(dev);
+    const int blocks = da.sms * (v4 ? da.v4_blocks_per_sm : da.v5_blocks_per_sm);
     OutRec *orec = at<OutRec>(ws, w.orec);
-    if (stats)
-        k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter, gen);
-    else
-        k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter, gen);
+    if (v4) {
+        if (stats)
+            k_density_v4<true><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter, gen);
+        else
+            k_density_v4<false><<<blocks, V4_TP, V4_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter, gen);
+    } else {
+        if (stats)
+            k_density_v5<true><<<blocks, V5_TP, V5_SMEM, s>>>(g, dc, orec, stats, tiles, rows + nkeys, counter, gen, status);
+        else
+            k_density_v5<false><<<blocks, V5_TP, V5_SMEM, s>>>(g, dc, orec, nullptr, tiles, rows + nkeys, counter, gen,
+                                                              status);
+    }
+    const int sms = da.sms;
     // the slices k_v4_tiles could not stage (dense clustered cells): warp-level engine
     if (stats)
         k_density_dense<true><<<sms * 2, DENSE_WARPS * 32, DENSE_SMEM, s>>>(g, dc, orec, stats, tiles, gtiles, gcount,
@@ -576,6 +608,15 @@ int sph_debug_phase_cycles(unsigned long long *out8, int reset)
         unsigned long long z[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
     }
+    return SPH_OK;
+}
+#endif
+
+#ifdef V5_CHECK_BISECT
+int sph_debug_v5(unsigned long long *out16)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out16, g_v5dbg, 16 * sizeof(unsigned long long));
     return SPH_OK;
 }
 #endif

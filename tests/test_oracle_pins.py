@@ -177,6 +177,129 @@ def test_condition_scale_matches_radial_finite_difference(x):
     assert abs(sens - expect) <= 2e-3 * expect + 1e-12
 
 
+# --------------------------------------------------------------------------
+# Tolerance scales (readings R13, R14): A = sum_j |term_ij|, C = sum_j |term_ij| kappa_ij.
+# Each scale is pinned where a sum of |terms| has a closed form in terms of outputs that
+# are pinned themselves (or of W(0,h) = 0.41842911446446380/h^3), so multiplying any of
+# them by a constant (or dropping the self term) fails a test here.
+# --------------------------------------------------------------------------
+W0_COEF = 0.41842911446446380      # W(0,h) h^3 = 8/(pi gamma^3) (mpmath)
+
+
+def test_scale_rho_dh_lone_particle():
+    """Lone particle: the sums hold only the self term -3 m W(0,h)/h, so
+    A^rho_dh = 3 m W(0,h)/h and A^wcount_dh = 3 W(0,h)/h exactly; div/curl scales are 0."""
+    for h, m in ((0.1, 0.25), (0.0078125, 2.0 ** -20)):
+        xyzh = np.array([[0.3, 0.6, 0.9, h]], np.float32)
+        vm = np.array([[0.4, -1.0, 2.0, m]], np.float32)
+        a = _both(xyzh, vm)
+        h32, m32 = float(xyzh[0, 3]), float(vm[0, 3])
+        W0 = W0_COEF / h32 ** 3
+        assert abs(a["a_rho_dh"][0] / (3 * m32 * W0 / h32) - 1) < 1e-14
+        assert abs(a["a_wcount_dh"][0] / (3 * W0 / h32) - 1) < 1e-14
+        assert a["a_rho_dh"][0] == -a["rho_dh"][0] and a["a_wcount_dh"][0] == -a["wcount_dh"][0]
+        assert a["a_div"][0] == 0 and a["a_curl"][0] == 0 and a["c_div"][0] == 0 and a["c_curl"][0] == 0
+
+
+@pytest.mark.parametrize("x", [0.3, 0.45, 0.6, 0.85])
+def test_scale_rho_dh_pair_signs(x):
+    """Two particles: dW/dh of the pair term has the sign of -(3w + x w') = -(18x^3 - 15x^2 + 3/2)
+    for x < 1/2 and +3(1-x)^2(2x-1) for x > 1/2, the self term is -3 m_i W(0,h_i)/h_i < 0.
+    Same signs (x < 1/2): A = -rho_dh.  Opposite signs (x > 1/2): A = rho_dh + 6 m_i W(0,h_i)/h_i."""
+    h = 0.0625
+    H = GAMMA * h
+    u = np.array([1.0, 2.0, 2.0]) / 3.0
+    p0 = np.array([0.5, 0.5, 0.5])
+    xyzh = np.array([[*p0, h], [*(p0 + u * x * H), h]], np.float32)
+    vm = np.array([[0.0, 0.0, 0.0, 0.375], [0.0, 0.0, 0.0, 0.625]], np.float32)
+    a = _both(xyzh, vm)
+    h32, mi = float(xyzh[0, 3]), float(vm[0, 3])
+    self_rho = 3 * mi * W0_COEF / h32 ** 4
+    self_wc = 3 * W0_COEF / h32 ** 4
+    assert list(a["nngb"]) == [1, 1]
+    if x < 0.5:
+        assert abs(a["a_rho_dh"][0] + a["rho_dh"][0]) <= 1e-14 * a["a_rho_dh"][0]
+        assert abs(a["a_wcount_dh"][0] + a["wcount_dh"][0]) <= 1e-14 * a["a_wcount_dh"][0]
+    else:
+        assert abs(a["a_rho_dh"][0] - (a["rho_dh"][0] + 2 * self_rho)) <= 1e-13 * a["a_rho_dh"][0]
+        assert abs(a["a_wcount_dh"][0] - (a["wcount_dh"][0] + 2 * self_wc)) <= 1e-13 * a["a_wcount_dh"][0]
+        assert a["a_rho_dh"][0] > -a["rho_dh"][0]
+
+
+def test_scale_div_single_term_and_cancelling_pair():
+    """One neighbour: A^div = |div| (a single term).  Two mirror neighbours whose div terms
+    cancel exactly: div = 0 and rho A^div = 2 x (rho A^div of the single pair, same term)."""
+    h = 0.0625
+    H = GAMMA * h
+    d = np.array([1 / 64, 3 / 128, -1 / 32])      # dyadic (exact mirror images in fp32), |d| < H
+    p0 = np.array([0.5, 0.5, 0.5])
+    v0 = np.array([0.5, -0.25, 1.0])
+    vj = np.array([-1.0, 0.75, 0.125])
+    one = _both(np.array([[*p0, h], [*(p0 + d), h]], np.float32),
+                np.array([[*v0, 0.5], [*vj, 0.25]], np.float32))
+    assert one["div_v"][0] != 0
+    assert abs(one["a_div"][0] - abs(one["div_v"][0])) <= 1e-15 * abs(one["div_v"][0])
+    # k at -d with v_k = v_j: (v_i - v_k).(x_i - x_k) = -(v_i - v_j).(x_i - x_j)
+    two = _both(np.array([[*p0, h], [*(p0 + d), h], [*(p0 - d), h]], np.float32),
+                np.array([[*v0, 0.5], [*vj, 0.25], [*vj, 0.25]], np.float32))
+    assert abs(two["div_v"][0]) <= 1e-15 * two["a_div"][0]
+    lhs = two["a_div"][0] * two["rho"][0]
+    rhs = 2 * one["a_div"][0] * one["rho"][0]
+    assert abs(lhs - rhs) <= 1e-14 * rhs
+
+
+@pytest.mark.parametrize("perp", [True, False])
+def test_scale_curl_single_term(perp):
+    """One neighbour: A^curl = m_j |v_ij| |x_ij| |W'|/(r rho); the curl vector has norm
+    m_j |v_ij x x_ij| |W'|/(r rho), so A^curl sin(theta) = |curl| (theta = angle(v_ij, x_ij))."""
+    h = 0.0625
+    H = GAMMA * h
+    d = np.array([0.25, 0.5, 0.25]) * H
+    p0 = np.array([0.5, 0.5, 0.5])
+    vij = np.array([1.0, -1.0, 1.0]) if perp else np.array([1.0, 0.25, -0.5])   # (1,-1,1).(1,2,1) = 0
+    xyzh = np.array([[*p0, h], [*(p0 + d), h]], np.float32)
+    vm = np.array([[*vij, 0.5], [0.0, 0.0, 0.0, 0.25]], np.float32)
+    a = _both(xyzh, vm)
+    x = xyzh[:, :3].astype(np.float64)
+    xij = x[0] - x[1]
+    v = vm[0, :3].astype(np.float64)
+    sin = np.linalg.norm(np.cross(v, xij)) / (np.linalg.norm(v) * np.linalg.norm(xij))
+    cn = np.sqrt(a["curl_x"][0] ** 2 + a["curl_y"][0] ** 2 + a["curl_z"][0] ** 2)
+    assert cn > 0
+    assert abs(a["a_curl"][0] * sin - cn) <= 1e-13 * cn
+    if perp:
+        assert abs(sin - 1) < 1e-12
+
+
+@pytest.mark.parametrize("x", [0.2, 0.6, 0.9, 0.995])
+def test_condition_scale_curl_matches_radial_finite_difference(x):
+    """c_curl - a_curl = |d(rho curl)/d ln r| for one pair with v_ij perpendicular to x_ij
+    (reading R14; the curl analogue of the c_div pin): rho curl = m (v x u) r W'(r)/r
+    along a fixed unit direction u, whose log-derivative in r is x w''/w'."""
+    h = 0.0625
+    H = GAMMA * h
+    u = np.array([2.0, 1.0, 2.0]) / 3.0
+    p0 = np.array([0.5, 0.5, 0.5])
+    v = np.array([[1.0, 0.0, -1.0, 0.5], [0.0, 0.0, 0.0, 0.25]], np.float32)   # (1,0,-1).(2,1,2) = 0
+
+    def R(scale):
+        xyzh = np.array([[*p0, h], [*(p0 + u * x * H * scale), h]], np.float32)
+        a = oracle.bruteforce(xyzh, v)
+        d = xyzh[1, :3].astype(np.float64) - xyzh[0, :3].astype(np.float64)
+        c = np.array([a["curl_x"][0], a["curl_y"][0], a["curl_z"][0]]) * a["rho"][0]
+        return c, a, np.linalg.norm(d)
+
+    eps = 1e-4
+    c0, a0, _ = R(1.0)
+    c1, _, r1 = R(1.0 + eps)
+    c2, _, r2 = R(1.0 - eps)
+    sens = np.linalg.norm(c1 - c2) / np.log(r1 / r2)
+    expect = (a0["c_curl"][0] - a0["a_curl"][0]) * a0["rho"][0]
+    assert abs(sens - expect) <= 2e-3 * expect + 1e-12
+    # and A^curl itself: a single perpendicular term, A = |curl|
+    assert abs(a0["a_curl"][0] * a0["rho"][0] - np.linalg.norm(c0)) <= 1e-12 * np.linalg.norm(c0)
+
+
 def test_asymmetric_cutoffs():
     """H_j < r < H_i: i counts j, j does not count i (gather with h_i)."""
     xyzh = np.array([[0.5, 0.5, 0.5, 0.05], [0.58, 0.5, 0.5, 0.02]], np.float32)
