@@ -139,12 +139,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def _profile_traffic():
-    """dram bytes per density launch from the committed ncu capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "density_traffic.json")
+def _profile_ncu(config: str):
+    """The committed ncu capture of the density kernel at this config (profiles/r2/ncu_fp32.json,
+    written by scripts/ncu_fp32.sh + scripts/parse_fp32.py): the measured FP32 form, DRAM bytes,
+    warp efficiency and FMA-pipe activity of one launch.  None when absent."""
+    path = os.path.join(ROOT, "profiles", "r2", "ncu_fp32.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            return json.load(f).get(config)
     except (OSError, ValueError):
         return None
 
@@ -287,11 +289,14 @@ def run_ours(args):
     cand_sum, hit_sum = sum(counts["cand"]), sum(counts["hits"])
     assert hit_sum == nngb_sum, (hit_sum, nngb_sum)
     if dist:
-        t = torch.tensor([nngb_sum, cand_sum], dtype=torch.int64, device="cuda")
+        t = torch.tensor([nngb_sum, cand_sum, counts["band"]] + counts["cand"] + counts["hits"], dtype=torch.int64,
+                         device="cuda")
         dist.all_reduce(t)
-        tot_inter, tot_cand = int(t[0]), int(t[1])
+        tot_inter, tot_cand, tot_band = int(t[0]), int(t[1]), int(t[2])
+        tot_kind = ([int(v) for v in t[3:7]], [int(v) for v in t[7:11]])
     else:
-        tot_inter, tot_cand = nngb_sum, cand_sum
+        tot_inter, tot_cand, tot_band = nngb_sum, cand_sum, counts["band"]
+        tot_kind = (counts["cand"], counts["hits"])
 
     for _ in range(args.warmup):
         runner.step()
@@ -343,12 +348,23 @@ def run_ours(args):
     dens_ms_local = statistics.mean(stage["density"])
     flops = FLOP_CAND * cand_sum + FLOP_HIT * hit_sum          # this rank's density launch
     achieved = flops / (dens_ms_local * 1e-3) / 1e12
-    traffic = _profile_traffic()
-    roof = {"bound": "alu", "kernel": "k_density_v4 (sph_density_all incl. its tile list)", "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
+    prof = _profile_ncu(args.config)
+    roof = {"bound": "alu", "kernel": "k_density_v5 (sph_density_all incl. its tile list and transpose)",
+            "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
-            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (DESIGN.md §6.2)",
-            "traffic": (traffic or {}).get(args.config) if traffic else None,
+            "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (= ncu ffma peak_sustained x 2 x "
+                           "f_SM; DESIGN.md §6); MEASURED_PEAKS.json has no FP32 figure",
+            "useful_flops": "8 per pseudo-Verlet candidate + 48 per in-range interaction (SURVEY §8(d))",
+            "traffic": prof["dram_bytes"] if prof else None,
             "flops_per_launch": flops, "launch_ms": dens_ms_local}
+    if prof:       # the measured forms, from the committed ncu capture of the same kernel and config
+        roof.update({"measured_frac": prof["measured_frac"], "measured_tflops": prof["fp32_tflops_measured"],
+                     "hbm_frac": prof["hbm_frac_of_measured_6548"], "hbm_gbs": prof["hbm_gbs"],
+                     "warp_efficiency": prof["warp_efficiency"], "fma_pipe_active_pct": prof["fma_pipe_active_pct"],
+                     "issue_active_pct": prof["issue_active_pct"],
+                     "measured_source": "profiles/r2/ncu_fp32.json (ncu, one launch of %s at %s: F = 2 ffma + fadd + "
+                                        "fmul + 4 ffma2 + 2 fadd2 + 2 fmul2 over ncu's ffma peak)" %
+                                        (prof["kernel"], args.config)})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -367,6 +383,10 @@ def run_ours(args):
                            "step": "ghost exchange + build_cells + sort_cells + density_all"},
                 "interactions_per_step": tot_inter, "candidates_per_step": tot_cand,
                 "hit_fraction": tot_inter / max(1, tot_cand),
+                "per_orientation": {k: {"candidates": tot_kind[0][n], "interactions": tot_kind[1][n],
+                                        "hit_fraction": tot_kind[1][n] / max(1, tot_kind[0][n])}
+                                    for n, k in enumerate(("self", "face", "edge", "corner"))},
+                "band_pairs": tot_band,
                 "evaluations_per_s": tot_cand / (ms_step_max * 1e-3),              # SV §8(d)
                 "particles_per_s": part.n_global / (ms_step_max * 1e-3),
                 "stage_ms": {k: statistics.mean(v) for k, v in stage.items()},

@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 4
+#define SPH_ABI_VERSION 5
 
 #define SPH_OK 0
 #define SPH_EINVAL 1
@@ -159,10 +159,15 @@ typedef struct sph_out {
 
 /* Optional device-side counters (pass NULL to skip; counting costs time).
  * Index k: 0 self cell, 1 face, 2 edge, 3 corner neighbour cells.
- * cand = candidate distance evaluations, hits = in-range pairs. */
+ * cand = candidate distance evaluations (the pseudo-Verlet windows of Code 2,
+ * P:94-100), hits = in-range pairs, band = candidate pairs with
+ * |r^2 - H_i^2| < 1e-6 H_i^2 evaluated in fp32 (BASELINE north_star: pairs in
+ * that band are "counted and reported"; sph_density_all's engines count it,
+ * the accumulating API kernels leave it 0). */
 typedef struct sph_stats {
     unsigned long long cand[4];
     unsigned long long hits[4];
+    unsigned long long band;
 } sph_stats;
 
 /* Number of local cells of `grid` (< 0 on a bad grid). */

@@ -39,7 +39,7 @@ class SphOut(ctypes.Structure):
 
 
 class SphStats(ctypes.Structure):
-    _fields_ = [("cand", ctypes.c_uint64 * 4), ("hits", ctypes.c_uint64 * 4)]
+    _fields_ = [("cand", ctypes.c_uint64 * 4), ("hits", ctypes.c_uint64 * 4), ("band", ctypes.c_uint64)]
 
 
 _lib = None

@@ -160,14 +160,14 @@ class Out:
 
 class Stats:
     def __init__(self, device="cuda"):
-        self.buf = torch.zeros(8, dtype=torch.int64, device=device)
+        self.buf = torch.zeros(9, dtype=torch.int64, device=device)   # sph_stats: cand[4], hits[4], band
 
     def ptr(self):
         return _ptr(self.buf)
 
     def read(self) -> dict:
         v = self.buf.cpu().tolist()
-        return {"cand": v[:4], "hits": v[4:]}
+        return {"cand": v[:4], "hits": v[4:8], "band": v[8]}
 
 
 def alloc_workspace(grid: SphGrid, capacity: int, device="cuda") -> torch.Tensor:

@@ -268,7 +268,8 @@ __device__ __forceinline__ int kind_of(int ox, int oy, int oz)
 }
 
 template <bool COUNT>
-__device__ __forceinline__ void flush_stats(sph_stats *st, const unsigned cand[4], const unsigned hits[4])
+__device__ __forceinline__ void flush_stats(sph_stats *st, const unsigned cand[4], const unsigned hits[4],
+                                            unsigned band = 0)
 {
     if (!COUNT || !st) return;
 #pragma unroll
@@ -284,6 +285,10 @@ __device__ __forceinline__ void flush_stats(sph_stats *st, const unsigned cand[4
             atomicAdd(&st->hits[k], hv);
         }
     }
+    unsigned long long bv = band;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bv += __shfl_xor_sync(0xffffffffu, bv, o);
+    if ((threadIdx.x & 31) == 0 && bv) atomicAdd(&st->band, bv);
 }
 
 // ---- sph_density_all, reference engine: one warp per owned home cell -------

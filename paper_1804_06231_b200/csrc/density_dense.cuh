@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
     const unsigned sQ = smem_addr(V + DENSE_K) + 2u * lane;
     if (threadIdx.x == 0) s_gen = *genp;
     __syncthreads();                                      // the only barrier: s_gen published
-    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0}, band = 0;
     const RowPairs rp = row_pairs(g);
     const int ntiles = *gcount;
     const float bx = g.boxf[0], by = g.boxf[1], bz = g.boxf[2];
@@ -126,7 +126,10 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
                             const float4 p = ldsr_f4(sP + 16u * (unsigned)(ok ? k : 0));
                             const float dx = hx - p.x, dy = hy - p.y, dz = hz - p.z;
                             const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                            if (COUNT) cand[kind] += ok ? 1u : 0u;
+                            if (COUNT) {
+                                cand[kind] += ok ? 1u : 0u;
+                                band += ok && fabsf(r2 - H2) < 1e-6f * H2 ? 1u : 0u;
+                            }
                             if (ok && r2 < H2) {
                                 sts_u16(qp, (unsigned)k);
                                 qp += 64u;
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
             }
         }
     }
-    flush_stats<COUNT>(st, cand, hits);
+    flush_stats<COUNT>(st, cand, hits, band);
 }
 
 }  // namespace pvsph

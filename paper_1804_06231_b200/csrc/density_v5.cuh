@@ -33,7 +33,7 @@ namespace pvsph {
 
 constexpr int V5_WARPS = V4_WARPS;
 constexpr int V5_TP = V4_TP;
-constexpr int V5_Q = 24;                               // hit stack depth per lane, 2-byte entries
+constexpr int V5_Q = 32;                               // hit stack depth per lane, 2-byte entries
 constexpr int V5_MS = V4_MS;                           // staged particles (+1 sentinel)
 constexpr int V5_ML = V4_ML + 14 * V4_MAXH;            // list entries + sentinels: one per (home cell, direction) + one per home cell
 constexpr int V5_MLA = (V5_ML + 7) / 8 * 8;
@@ -161,7 +161,7 @@ __device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], con
     len[3] = (int)(a[3] + 2u - amid[1]) >> 1;
 }
 
-#if defined(V5_OLD_BISECT) || defined(V5_CHECK_BISECT)
+#if defined(V5_OLD_BISECT) || defined(V5_CHECK_BISECT) || defined(V5_STATS)
 __device__ unsigned long long g_v5dbg[16];
 template <int D0, int D1>
 __device__ __forceinline__ void v5_windows2_old(const V5Stage &S, int top, const int f[4], const int n[4],
@@ -199,7 +199,7 @@ __device__ __forceinline__ void v5_windows2_old(const V5Stage &S, int top, const
 template <bool COUNT, bool FRAMES>
 __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c, OutRec *orec, const V5Stage &S,
                                             unsigned qbase, bool active, int i, int yoff, int qh, int lpos,
-                                            unsigned cand[4], unsigned hits[4])
+                                            unsigned cand[4], unsigned hits[4], unsigned &band)
 {
     const unsigned sQ = qbase + 2u * (threadIdx.x & 31);
     float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
@@ -243,6 +243,12 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         for (int s2 = 0; s2 < 2 * NP; ++s2) qv[s2] = (unsigned)s2 < take ? lds_u16(qp - 64u * (s2 + 1)) : 0xffffffffu;
         qp -= 64u * take;
         npop += (int)take;
+#ifdef V5_STATS
+        {   // [10] drain lane-slots, [11] popped entries (real)
+            const unsigned tk = __reduce_add_sync(0xffffffffu, take);
+            if ((threadIdx.x & 31) == 0) { atomicAdd(&g_v5dbg[10], 64ull); atomicAdd(&g_v5dbg[11], (unsigned long long)tk); }
+        }
+#endif
 #pragma unroll
         for (int pr = 0; pr < NP; ++pr) {
             unsigned e[2];
@@ -290,7 +296,10 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                 const float4 p = ldsr_f4(e);
                 const float dx = x - p.x, dy = y - p.y, dz = z - p.z;
                 const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                if (COUNT) cand[0] += ok ? 1u : 0u;
+                if (COUNT) {
+                    cand[0] += ok ? 1u : 0u;
+                    band += ok && fabsf(r2 - H2) < 1e-6f * H2 ? 1u : 0u;
+                }
                 if (r2 < H2) {                             // the sentinel never passes
                     sts_u16_push(qp, FRAMES ? (e - S.sb) >> 4 : e);
                     qp += 64u;
@@ -412,7 +421,10 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                     }
                     const float dx = hx - p.x, dy = hy - p.y, dz = hz - p.z;
                     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-                    if (COUNT) cand[kind] += t + u < tot ? 1u : 0u;
+                    if (COUNT) {
+                        cand[kind] += t + u < tot ? 1u : 0u;
+                        band += t + u < tot && fabsf(r2 - H2) < 1e-6f * H2 ? 1u : 0u;
+                    }
                     if (r2 < H2) {                         // beyond the window: never (sep >= H + delta)
                         sts_u16_push(qp, FRAMES ? ((e[u] - S.sb) >> 4) | (fl << 12) : e[u]);
                         qp += 64u;
@@ -420,6 +432,15 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                     }
                 }
             };
+#ifdef V5_STATS
+            {   // [12] sweep lane-slots, [13] window candidates, [14] final-drain rounds
+                const unsigned tt = __reduce_add_sync(0xffffffffu, (unsigned)tot);
+                if ((threadIdx.x & 31) == 0) {
+                    atomicAdd(&g_v5dbg[12], 32ull * (unsigned long long)(((trip + 7) / 8) * 8 - ((trip % 8) && (trip % 8) <= 4 ? 4 : 0)));
+                    atomicAdd(&g_v5dbg[13], (unsigned long long)tt);
+                }
+            }
+#endif
             for (int t = 0; t < trip; t += 8) {
                 if (t + 4 < trip)
                     step(t, std::integral_constant<int, 8>{});
@@ -429,6 +450,13 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
             }
         }
     }
+#ifdef V5_STATS
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_v5dbg[9], 1ull);          // [9] warps
+    {
+        const unsigned left = __reduce_add_sync(0xffffffffu, (qp - sQ) >> 6);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_v5dbg[15], (unsigned long long)left);   // [15] hits left for the final drain
+    }
+#endif
     while (__any_sync(0xffffffffu, qp != sQ)) drain(std::integral_constant<int, 2>{});
 
     if (active) {
@@ -471,7 +499,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     const RowPairs rp = row_pairs(g);
     const int ntiles = *ntiles_p;
-    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0}, band = 0;
     const int4 kEnd = make_int4(-1, 0, 0, 0);
     const unsigned sb = smem_addr(P);
     // entries are 16-bit shared addresses of P: P must lie in the first 64 KiB of the window
@@ -702,9 +730,9 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
             const unsigned qb = smem_addr(queue + wl * V5_Q * 32);
             if (wl * 32 < T.cnt) {
                 if (T.frames)
-                    v5_particle<COUNT, true>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
+                    v5_particle<COUNT, true>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits, band);
                 else
-                    v5_particle<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits);
+                    v5_particle<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits, band);
             }
         } else if (T.cnt > 0) {
             const long long rowA = ((long long)(T.xo + g.ghost_x) * g.ny + T.y0) * g.nz;
@@ -725,7 +753,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
         }
         td = td_next;
     }
-    flush_stats<COUNT>(st, cand, hits);
+    flush_stats<COUNT>(st, cand, hits, band);
 }
 
 }  // namespace pvsph

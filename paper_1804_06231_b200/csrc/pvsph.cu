@@ -612,7 +612,7 @@ int sph_debug_phase_cycles(unsigned long long *out8, int reset)
 }
 #endif
 
-#ifdef V5_CHECK_BISECT
+#if defined(V5_CHECK_BISECT) || defined(V5_STATS)
 int sph_debug_v5(unsigned long long *out16)
 {
     cudaDeviceSynchronize();
