@@ -308,6 +308,10 @@ def level_grids(h, nc0: int, box=1.0, gamma=GAMMA, max_levels: int = 3):
     h = np.asarray(h, np.float32)
     ncs = [nc0 * 2 ** k for k in range(max_levels)]
     caps = [hcap(n) for n in ncs]
+    if h.size and float(h.max()) > caps[0]:
+        # such a particle would be home on no level (its outputs never written): the coarsest
+        # grid itself is too fine (sph_build_cells reports SPH_EH_RANGE for a single grid)
+        raise ValueError(f"h = {float(h.max())} exceeds the coarsest level's limit {caps[0]} (gamma h > box/nc0)")
     out = []
     for k, n in enumerate(ncs):
         lo = caps[k + 1] if k + 1 < len(ncs) else 0.0

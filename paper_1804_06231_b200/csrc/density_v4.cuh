@@ -123,6 +123,22 @@ __device__ unsigned long long g_phase_cycles[12];   // 0 stage, 1 search, 2 swee
 #endif
 
 // ---- tile list ------------------------------------------------------------------
+// row_home[(x, y) row] = 1 iff some cell of the row holds a home particle (cell_nhome > 0):
+// k_v4_tiles skips the other rows (fine level grids are mostly empty).  Computed by
+// sph_density_all itself from the cells, so it depends on no other call's workspace state.
+__global__ void k_row_home(long long nrows, int nz, const int *__restrict__ cell_nhome, int *__restrict__ row_home)
+{
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long row = warp; row < nrows; row += nwarps) {
+        int any = 0;
+        for (int z = lane; z < nz; z += 32) any |= cell_nhome[row * nz + z] > 0;
+        any = __any_sync(0xffffffffu, any);
+        if (lane == 0) row_home[row] = any;
+    }
+}
+
 struct RowPairs {
     int nxo, nyp, nby;
     long long nkeys;

@@ -538,6 +538,9 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
     const DevCells dc = dev_cells(cells);
     unsigned *gen = at<unsigned>(ws, w.gen);
     int *gtiles = at<int>(ws, w.gtiles), *gcount = at<int>(ws, w.gcount);
+    k_row_home<<<grid_blocks((long long)g.nxl * g.ny * 32, 256, 148 * 16), 256, 0, s>>>((long long)g.nxl * g.ny, g.nz,
+                                                                                      dc.cell_nhome,
+                                                                                      at<int>(ws, w.row_home));
     k_v4_tiles<false><<<grid_blocks(nkeys, 256, 148 * 8), 256, 0, s>>>(g, dc.cell_start, dc.cell_nhome, rows, tiles,
                                                                        w.tile_cap, status, gen, gtiles, gcount,
                                                                        at<int>(ws, w.row_home));

@@ -102,6 +102,7 @@ class Slab:
     pset: object = None       # the full ParticleSet (single-GPU only)
     ghost_n: int = -1         # particles in the two ghost planes (known when cut from a full set)
     edge_n: int = -1          # particles in the larger of its own first and last planes
+    block_max: int = -1       # the most particles of ANY rank's first or last plane (same on every rank)
 
     @staticmethod
     def single(p) -> "Slab":
@@ -120,8 +121,10 @@ class Slab:
         per_plane = np.bincount(pl, minlength=p.nc)
         ghost_n = int(per_plane[(lo - 1) % p.nc] + per_plane[hi % p.nc])
         edge_n = int(max(per_plane[lo], per_plane[hi - 1]))
+        all_b = bounds if bounds is not None else [slab_bounds(p.nc, world, r) for r in range(world)]
+        block_max = int(max(max(per_plane[a], per_plane[b - 1]) for a, b in all_b))
         return Slab(p.nc, p.box, p.gamma, rank, world, lo, hi, np.ascontiguousarray(p.xyzh[gid]),
-                    np.ascontiguousarray(p.vm[gid]), gid, p.n, ghost_n=ghost_n, edge_n=edge_n)
+                    np.ascontiguousarray(p.vm[gid]), gid, p.n, ghost_n=ghost_n, edge_n=edge_n, block_max=block_max)
 
     @staticmethod
     def from_config(cfg: str, rank: int, world: int, balance: bool = False) -> "Slab":
@@ -137,16 +140,17 @@ class Slab:
 
 
 def exchange_planes(dist, rank: int, world: int, send_lo, send_hi, recv) -> tuple[int, int]:
-    """Periodic-ring ghost exchange (NCCL P2P via torch.distributed, or gloo on CPU in tests).
+    """Periodic-ring ghost exchange of variable-size planes (counts first, then exact-size
+    receives; the counts cross to the host).  Kept for the gloo tests and small tools; the
+    runner uses exchange_fixed (no host synchronisation).
 
     send_lo = (xyzh, vm) of this rank's plane x_lo  -> goes to the left neighbour
     send_hi = (xyzh, vm) of this rank's plane x_hi-1 -> goes to the right neighbour
     recv    = (xyzh_buf, vm_buf): the left neighbour's plane x_hi-1 (our ghost plane
               x_lo-1) is written at [0, n_glo), the right neighbour's plane x_lo (our
               ghost plane x_hi) at [n_glo, n_glo + n_ghi).  Returns (n_glo, n_ghi).
-    Counts travel first so the receives have exact sizes.  With p = 2 both
-    neighbours are the same rank; NCCL matches same-peer messages in issue order,
-    so every rank issues sends [to right, to left] and receives [from left, from right]."""
+    With p = 2 both neighbours are the same rank; NCCL matches same-peer messages in issue
+    order, so every rank issues sends [to right, to left] and receives [from left, from right]."""
     left, right = (rank - 1) % world, (rank + 1) % world
     dev = send_lo[0].device
     cnt_send = torch.tensor([send_hi[0].shape[0], send_lo[0].shape[0]], dtype=torch.int64, device=dev)
@@ -175,6 +179,37 @@ def exchange_planes(dist, rank: int, world: int, send_lo, send_hi, recv) -> tupl
     return n_glo, n_ghi
 
 
+def exchange_fixed(dist, rank: int, world: int, send_x, send_v, send_n, recv_x, recv_v, recv_n):
+    """Fixed-capacity periodic-ring ghost exchange (no host synchronisation): every rank sends
+    its two whole send buffers and their device-side counts, and receives its two ghost blocks.
+
+    send_x, send_v: [2, cap, 4] -- block 0 = plane x_lo (to the left neighbour), block 1 =
+                    plane x_hi-1 (to the right neighbour); only the first send_n[k] rows are
+                    particles.  send_n: int64[2] on the device.
+    recv_x, recv_v: [2, cap, 4] -- block 0 from the left neighbour (our ghost plane x_lo-1),
+                    block 1 from the right (ghost plane x_hi); recv_n: int64[2] their counts.
+    cap must be the same on every rank (the message sizes must match).  Same-peer messages
+    match in issue order (p = 2): sends [to right, to left], receives [from left, from right].
+    Returns the torch.distributed work handles (wait() orders the current stream after them)."""
+    left, right = (rank - 1) % world, (rank + 1) % world
+    P = dist.P2POp
+    ops = [P(dist.isend, send_n[1:2], right), P(dist.isend, send_x[1], right), P(dist.isend, send_v[1], right),
+           P(dist.isend, send_n[0:1], left), P(dist.isend, send_x[0], left), P(dist.isend, send_v[0], left),
+           P(dist.irecv, recv_n[0:1], left), P(dist.irecv, recv_x[0], left), P(dist.irecv, recv_v[0], left),
+           P(dist.irecv, recv_n[1:2], right), P(dist.irecv, recv_x[1], right), P(dist.irecv, recv_v[1], right)]
+    return dist.batch_isend_irecv(ops)
+
+
+def mask_dead_ghosts(recv_x, recv_v, recv_n, dead_row_x, dead_row_v, ar):
+    """Rows beyond the received count of each ghost block become a 'dead' particle: inside the
+    box but in an OWNED plane of this rank, so sph_build_cells drops it as a ghost outside the
+    ghost planes (no slot, no error).  Device-side (torch.where), no host synchronisation."""
+    for k in range(2):
+        keep = (ar < recv_n[k])[:, None]
+        recv_x[k].copy_(torch.where(keep, recv_x[k], dead_row_x))
+        recv_v[k].copy_(torch.where(keep, recv_v[k], dead_row_v))
+
+
 class SlabRunner:
     """Device buffers and one density step of one rank."""
 
@@ -196,31 +231,44 @@ class SlabRunner:
         self.grid = pv.make_grid(slab.nc, slab.box, slab.gamma, slab.x_lo, slab.x_hi, int(ghost),
                                  self.levels[0][1:] if split else None)
         if ghost:
+            # ghost blocks of a FIXED capacity, equal on every rank (the P2P message sizes must
+            # match): the largest boundary plane of any rank + 5 % headroom for drift + 4096
             per_plane = self.n_own / max(1, slab.x_hi - slab.x_lo)
             if ghost_capacity is not None:
-                gcap = ghost_capacity
-            elif slab.ghost_n >= 0:              # exact (cut from the full set) + headroom for drift
-                gcap = int(1.05 * slab.ghost_n) + 4096
+                self.bcap = int(ghost_capacity)
+            elif slab.block_max >= 0:
+                self.bcap = int(1.05 * slab.block_max) + 4096
             else:
-                gcap = int(2 * 1.5 * per_plane + 4096)
+                self.bcap = int(1.5 * per_plane) + 4096
         else:
-            gcap = 0
-        self.cap = self.n_own + gcap
+            self.bcap = 0
+        self.cap = self.n_own + 2 * self.bcap
         self.xin = torch.zeros((max(self.cap, 1), 4), dtype=torch.float32, device=device)
         self.vin = torch.zeros((max(self.cap, 1), 4), dtype=torch.float32, device=device)
         self.cells = pv.Cells.alloc(self.grid, self.cap, device)
         self.ws = pv.alloc_workspace(self.grid, self.cells.capacity, device)
         self.out = pv.Out.alloc(self.n_own, device)
-        self.n_ghost = 0
+        self.n_ghost = 2 * self.bcap             # both ghost blocks always (rows past a block's count are dead)
         self.plane = self.grid.nc[1] * self.grid.nc[2]   # cells per x plane
         self.nxl = (slab.x_hi - slab.x_lo) + (2 if ghost else 0)
         self.launches_per_step = (BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES) * len(self.levels) + \
             (SELECT_LAUNCHES if ghost else 0) + (len(self.levels) if split else 0)   # k_mark_needed per level
-        if ghost:                                # send buffers of the boundary planes (sph_select_planes)
-            scap = int(1.05 * slab.edge_n) + 4096 if slab.edge_n >= 0 else int(1.5 * per_plane) + 4096
-            self.sel_x = torch.empty((2, scap, 4), dtype=torch.float32, device=device)
-            self.sel_v = torch.empty((2, scap, 4), dtype=torch.float32, device=device)
+        if ghost:
+            # send buffers of the boundary planes (sph_select_planes), the received counts, and
+            # the 'dead' row for unused ghost slots: inside the box in this rank's middle owned
+            # plane, which every level grid's build drops as a ghost outside its ghost planes
+            b = self.bcap
+            self.sel_x = torch.zeros((2, b, 4), dtype=torch.float32, device=device)
+            self.sel_v = torch.zeros((2, b, 4), dtype=torch.float32, device=device)
             self.sel_n = torch.zeros(2, dtype=torch.int64, device=device)
+            self.recv_n = torch.zeros(2, dtype=torch.int64, device=device)
+            self.ar = torch.arange(b, dtype=torch.int64, device=device)
+            cl = slab.box / slab.nc
+            xm = ((slab.x_lo + slab.x_hi) // 2 + 0.5) * cl
+            self.dead_x = torch.tensor([xm, 0.5 * slab.box, 0.5 * slab.box, 1e-6 * cl], dtype=torch.float32,
+                                       device=device)
+            self.dead_v = torch.tensor([0.0, 0.0, 0.0, 1.0], dtype=torch.float32, device=device)
+            self.comm = torch.cuda.Stream(device=device) if str(device).startswith("cuda") else None
         self.device = device
         # finer level grids (one GPU): own cells and workspace each, same outputs
         self.extra = []
@@ -239,18 +287,42 @@ class SlabRunner:
             self.vin[:self.n_own].copy_(torch.from_numpy(self.slab.vm))
 
     # -- ghost exchange -----------------------------------------------------
-    def boundary_planes(self):
-        """The owned particles of planes x_lo and x_hi-1 in input order (sph_select_planes: no
-        binning pass), as ((xyzh, vm), (xyzh, vm)) views of the send buffers."""
+    def ghost_blocks(self):
+        """Views of the two ghost blocks behind the owned particles: [2, bcap, 4]."""
+        a, b = self.n_own, self.n_own + 2 * self.bcap
+        return self.xin[a:b].view(2, self.bcap, 4), self.vin[a:b].view(2, self.bcap, 4)
+
+    def select(self) -> None:
+        """The owned particles of planes x_lo and x_hi-1 in input order into the send buffers
+        (sph_select_planes: no binning pass); the counts stay on the device."""
         pv.sph_select_planes(self.grid, self.xin, self.vin, self.n_own, self.sel_x, self.sel_v, self.sel_n, self.ws)
+
+    def boundary_planes(self):
+        """The selected planes as ((xyzh, vm), (xyzh, vm)) views (host sync for the counts:
+        tests and tools only; the step uses the fixed-capacity exchange)."""
+        self.select()
         n_lo, n_hi = self.sel_n.tolist()
         return (self.sel_x[0, :n_lo], self.sel_v[0, :n_lo]), (self.sel_x[1, :n_hi], self.sel_v[1, :n_hi])
 
     def exchange(self) -> None:
-        send_lo, send_hi = self.boundary_planes()
-        free = (self.xin[self.n_own:], self.vin[self.n_own:])
-        n_glo, n_ghi = exchange_planes(self.dist, self.rank, self.world, send_lo, send_hi, free)
-        self.n_ghost = n_glo + n_ghi
+        """Ghost exchange with no host synchronisation: select on the compute stream, the NCCL
+        P2P transfer of the fixed-capacity blocks and counts on the comm stream, then the compute
+        stream waits for it and marks the unused ghost rows dead."""
+        self.select()
+        rx, rv = self.ghost_blocks()
+        cs = torch.cuda.current_stream()
+        if self.comm is not None:
+            self.comm.wait_stream(cs)
+            with torch.cuda.stream(self.comm):
+                for w in exchange_fixed(self.dist, self.rank, self.world, self.sel_x, self.sel_v, self.sel_n,
+                                        rx, rv, self.recv_n):
+                    w.wait()
+            cs.wait_stream(self.comm)
+        else:
+            for w in exchange_fixed(self.dist, self.rank, self.world, self.sel_x, self.sel_v, self.sel_n,
+                                    rx, rv, self.recv_n):
+                w.wait()
+        mask_dead_ghosts(rx, rv, self.recv_n, self.dead_x, self.dead_v, self.ar)
 
     # -- one step -----------------------------------------------------------
     def step(self, stats=None, events=None) -> None:
@@ -281,6 +353,13 @@ class SlabRunner:
         rec(4)
 
     def check(self) -> None:
+        """Raise on any error of the last step (one host sync): the workspaces' status words and
+        a boundary plane larger than the fixed ghost block (sph_select_planes' overflow, whose
+        status bit the next build would clear)."""
+        if self.world > 1:
+            n = self.sel_n.tolist()
+            if max(n) > self.bcap:
+                raise RuntimeError(f"boundary plane of {max(n)} particles exceeds the ghost block capacity {self.bcap}")
         pv.check_status(self.ws)
         for _, _, ws in self.extra:
             pv.check_status(ws)
@@ -366,21 +445,23 @@ class FakeRanks:
         self.n_global = p.n
 
     def step(self) -> None:
-        planes = []
+        """The fixed-capacity exchange emulated with device copies: every runner's ghost block 0
+        receives its left neighbour's block 1 (plane x_hi-1) and block 1 its right neighbour's
+        block 0, counts included; then the same dead-row masking as the NCCL path."""
         for r in self.runners:
-            (xl, vl), (xh, vh) = r.boundary_planes()
-            planes.append(((xl.clone(), vl.clone()), (xh.clone(), vh.clone())))
+            r.select()
         W = self.world
         for k, r in enumerate(self.runners):
-            gx_lo, gv_lo = planes[(k - 1) % W][1]      # left neighbour's plane x_hi-1
-            gx_hi, gv_hi = planes[(k + 1) % W][0]      # right neighbour's plane x_lo
-            a, b = r.n_own, r.n_own + gx_lo.shape[0]
-            c = b + gx_hi.shape[0]
-            r.xin[a:b].copy_(gx_lo)
-            r.vin[a:b].copy_(gv_lo)
-            r.xin[b:c].copy_(gx_hi)
-            r.vin[b:c].copy_(gv_hi)
-            r.n_ghost = c - r.n_own
+            rx, rv = r.ghost_blocks()
+            left, right = self.runners[(k - 1) % W], self.runners[(k + 1) % W]
+            assert left.bcap == r.bcap == right.bcap
+            rx[0].copy_(left.sel_x[1])
+            rv[0].copy_(left.sel_v[1])
+            rx[1].copy_(right.sel_x[0])
+            rv[1].copy_(right.sel_v[0])
+            r.recv_n[0].copy_(left.sel_n[1])
+            r.recv_n[1].copy_(right.sel_n[0])
+            mask_dead_ghosts(rx, rv, r.recv_n, r.dead_x, r.dead_v, r.ar)
         for r in self.runners:
             r.compute()
         for r in self.runners:

@@ -126,3 +126,73 @@ def test_slab_ghost_counts_exact():
         lo, hi = b[r]
         assert s.ghost_n == int(((pl == (lo - 1) % 13) | (pl == hi % 13)).sum())
         assert s.n_own == int(((pl >= lo) & (pl < hi)).sum())
+
+
+def _worker_fixed(rank, world, port, sizes, cap, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1804_06231_b200.slabs import exchange_fixed, mask_dead_ghosts
+
+    def block(r, which):
+        x = torch.full((cap, 4), -5.0)
+        n = sizes[r][which]
+        x[:n, 0] = r
+        x[:n, 1] = which
+        x[:n, 2] = torch.arange(n, dtype=torch.float32)
+        return x
+
+    send_x = torch.stack([block(rank, 0), block(rank, 1)])
+    send_v = send_x + 1000.0
+    send_n = torch.tensor(sizes[rank], dtype=torch.int64)
+    recv_x = torch.zeros((2, cap, 4))
+    recv_v = torch.zeros((2, cap, 4))
+    recv_n = torch.zeros(2, dtype=torch.int64)
+    for w in exchange_fixed(dist, rank, world, send_x, send_v, send_n, recv_x, recv_v, recv_n):
+        w.wait()
+    dead_x = torch.tensor([7.0, 8.0, 9.0, 0.5])
+    dead_v = torch.tensor([0.0, 0.0, 0.0, 1.0])
+    mask_dead_ghosts(recv_x, recv_v, recv_n, dead_x, dead_v, torch.arange(cap))
+    left, right = (rank - 1) % world, (rank + 1) % world
+    ok = recv_n.tolist() == [sizes[left][1], sizes[right][0]]
+    for k, (src, which) in enumerate(((left, 1), (right, 0))):
+        n = sizes[src][which]
+        exp = block(src, which)
+        ok = ok and torch.equal(recv_x[k, :n], exp[:n]) and torch.equal(recv_v[k, :n], exp[:n] + 1000.0)
+        ok = ok and bool((recv_x[k, n:] == dead_x).all()) and bool((recv_v[k, n:] == dead_v).all())
+    q.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,sizes", [
+    (2, [(3, 5), (4, 2)]),
+    (2, [(0, 8), (8, 0)]),          # an empty and a full block
+    (3, [(1, 2), (3, 4), (5, 6)]),
+    (4, [(2, 0), (0, 3), (7, 1), (1, 1)]),
+])
+def test_fixed_capacity_exchange_gloo(world, sizes):
+    """The runner's exchange (no host sync): whole fixed-capacity blocks and device-side counts
+    over P2P, rows past each received count replaced by the dead row (dropped by the build)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_fixed, args=(r, world, port, sizes, 8, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
+
+
+def test_block_capacity_same_on_every_rank():
+    """The ghost blocks' capacity comes from the largest boundary plane of ANY rank, so every rank
+    sizes its P2P messages identically (equal and cost-balanced cuts)."""
+    from paper_1804_06231_b200.slabs import Slab, balanced_bounds, plane_costs, planes_of
+    p = synth.clustered_set("cl64k", seed=7, n=65536, nc=13, n_spheres=16)
+    pl = planes_of(p.xyzh, p.nc)
+    for bounds in (None, balanced_bounds(plane_costs(p.xyzh, p.nc), 3)):
+        slabs = [Slab.from_set(p, r, 3, bounds) for r in range(3)]
+        assert len({s.block_max for s in slabs}) == 1
+        assert all(s.block_max >= max((pl == s.x_lo).sum(), (pl == s.x_hi - 1).sum()) for s in slabs)
