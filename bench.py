@@ -48,6 +48,11 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--levels", type=int, default=0,
                     help="level passes (DESIGN.md §4.5); 0 = auto: 3 for the clustered c4, else 1")
+    ap.add_argument("--reuse", action="store_true",
+                    help="list-reuse time loop (P:102 max_dx; ReuseLoop): drift + density per step, cells and "
+                         "lists rebuilt only when the skin would be exceeded (1 GPU)")
+    ap.add_argument("--skin-frac", type=float, default=0.01, help="--reuse: skin / C_l")
+    ap.add_argument("--rebuild-every", type=int, default=4, help="--reuse: dt chosen so the skin lasts this many steps")
     ap.add_argument("--balance", type=int, default=-1,
                     help="N > 1: x-slab cuts by estimated work (1) or equal planes (0); -1 = auto: on for c4")
     return ap.parse_args()
@@ -400,8 +405,61 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_reuse(args):
+    """The list-reuse time loop on one GPU: K timed steps of drift + density
+    with the rebuilds (gather positions, build, sort) they trigger, inside the timed region."""
+    import numpy as np
+    import torch
+    import paper_1804_06231_b200 as pv
+    import synth
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    pv.load()
+    p = synth.make(args.config)
+    cl = p.box / p.nc
+    skin = args.skin_frac * cl
+    loop = pv.ReuseLoop(p.nc, p.n, skin, box=p.box)
+    x, v = torch.from_numpy(p.xyzh).cuda(), torch.from_numpy(p.vm).cuda()
+    loop.start(x, v)
+    dt = 0.999 * skin / args.rebuild_every / max(loop.vmax, 1e-30)
+    dt = min(dt, 0.999 * (skin - loop.step_bound(0.0)) / args.rebuild_every / max(loop.vmax, 1e-30))
+    st = pv.Stats()
+    loop.step(dt, stats=st)                             # counted step (outside the timed region)
+    loop.check()
+    counts = st.read()
+    for _ in range(args.warmup):
+        loop.step(dt)
+    torch.cuda.synchronize()
+    r0 = loop.rebuilds
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(args.steps):
+            loop.step(dt)
+        e1.record(s)
+        torch.cuda.synchronize()
+    loop.check()
+    ms = e0.elapsed_time(e1) / args.steps
+    inter = int(sum(counts["hits"]))
+    line = {"metric": METRIC, "value": inter / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "mode": "reuse",
+            "config": {"workload": f"{args.config} (BASELINE.json configs, DESIGN.md §3)", "n_particles": p.n,
+                       "cells": f"{p.nc}^3", "parallelism": "single", "skin_over_cl": args.skin_frac,
+                       "dt": dt, "step": "sph_drift + sph_density_all; rebuild (sph_gather_positions + "
+                                         "sph_build_cells + sph_sort_cells) when the skin would be exceeded",
+                       "l2": "inputs larger than L2; no flush"},
+            "rebuilds_in_timed_steps": loop.rebuilds - r0, "interactions_per_step": inter,
+            "candidates_per_step": int(sum(counts["cand"])), "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.reuse:
+        run_reuse(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

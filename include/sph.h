@@ -101,9 +101,11 @@ typedef struct sph_grid {
                         /*   largest displacement any particle may have had */
                         /*   since the cells and lists were built (moved by */
                         /*   sph_drift); 0 = none.  The build then requires */
-                        /*   gamma*h + 2*skin <= C_l for home particles and */
-                        /*   the density calls widen every window by 4*skin */
-                        /*   (DESIGN.md §4.6).                              */
+                        /*   gamma*h + 2*skin <= C_l for home particles.    */
+                        /*   sph_density_all widens the window in a neighbour */
+                        /*   cell c by 2*cells->cell_dx[c] (the per-cell    */
+                        /*   max_dx of P:102); the other density calls by   */
+                        /*   4*skin.                       */
 } sph_grid;
 
 /* Per-direction sorted lists ("index" of P:92).  For cell c and direction
@@ -134,6 +136,12 @@ typedef struct sph_grid {
  *                           boundary past its end (the density kernel reads
  *                           it in aligned 16-byte words; cudaMalloc
  *                           allocations satisfy this)
+ *   disp[capacity]          list reuse: per slot, an upper bound of
+ *                           |x - x_build| (0 after sph_build_cells,
+ *                           accumulated by sph_drift)
+ *   cell_dx[ncell]          per cell, the largest disp of its particles: the
+ *                           paper's max_dx (0 after a build); sph_density_all
+ *                           widens a window in neighbour cell c by 2*cell_dx[c]
  * n is written by sph_build_cells (stored particles).  16-byte alignment
  * is required for xyzh and vm. */
 typedef struct sph_cells {
@@ -147,6 +155,8 @@ typedef struct sph_cells {
     uint16_t *order;
     int32_t *slot_cell;
     int32_t *cell_nhome;
+    float *disp;
+    float *cell_dx;
 } sph_cells;
 
 /* Outputs, each an array of n_out elements indexed by INPUT index (only
@@ -252,12 +262,22 @@ const char *sph_strerror(int code);
 /* List reuse ("max_dx"): move every stored
  * particle of `cells` by its velocity, x <- fp32(x + fp32(v * dt)) per
  * component (two roundings), keeping cells, order and lists as they are.
- * Positions may leave [0, box) by up to the skin.  If max_disp (device
- * float, caller-initialised) is not NULL it receives the largest |v| dt
- * (atomic max).  The caller keeps the accumulated displacement below the
- * grid's skin and rebuilds (sph_build_cells + sph_sort_cells) before it
- * would exceed it; the density calls on the same grid are then exact. */
+ * Each slot's disp grows by the norm of its stored increment (rounded up),
+ * so disp bounds |x - x_build|; cell_dx[c] becomes the largest disp of cell
+ * c (the paper's max_dx).  Positions may leave [0, box) by up to the skin.
+ * If max_disp (device float, caller-initialised) is not NULL it receives
+ * the largest disp (atomic max).  The caller rebuilds (sph_gather_positions,
+ * sph_build_cells, sph_sort_cells) before it exceeds the grid's skin; the
+ * density calls on the same cells are then exact. */
 int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp, void *stream);
+
+/* The stored (possibly drifted) positions and h back in INPUT order,
+ * xyzh_out[4 * n_out] (device, 16-byte aligned), every coordinate wrapped
+ * into [0, box): the input of the next sph_build_cells when a reuse loop
+ * rebuilds.  Slots whose input index is >= n_out (ghosts)
+ * are skipped. */
+int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xyzh_out, int64_t n_out,
+                         void *stream);
 
 /* Ghost exchange helper (x-slabs): copies the owned
  * particles (xyzh_in/vm_in, n_own, device) whose x plane is the rank's

@@ -17,7 +17,8 @@ ERROR_NAMES = {0: "SPH_OK", 1: "SPH_EINVAL", 2: "SPH_EH_RANGE", 3: "SPH_ECAPACIT
 # Every function declared in include/sph.h (checked by tests/test_abi.py); sph_calibrate is
 # declared in include/sph_calib.h.
 EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cells", "sph_sort_cells",
-           "sph_density_self", "sph_density_pair", "sph_density_pair_sym", "sph_drift", "sph_select_planes", "sph_density_finalize", "sph_density_all", "sph_status",
+           "sph_density_self", "sph_density_pair", "sph_density_pair_sym", "sph_drift", "sph_gather_positions",
+           "sph_select_planes", "sph_density_finalize", "sph_density_all", "sph_status",
            "sph_status_reset", "sph_strerror")
 
 
@@ -30,7 +31,7 @@ class SphGrid(ctypes.Structure):
 class SphCells(ctypes.Structure):
     _fields_ = [("capacity", c_i64), ("n", c_i64), ("cell_start", c_vp), ("xyzh", c_vp), ("vm", c_vp),
                 ("perm", c_vp), ("cell_hmax", c_vp), ("order", c_vp), ("slot_cell", c_vp),
-                ("cell_nhome", c_vp)]
+                ("cell_nhome", c_vp), ("disp", c_vp), ("cell_dx", c_vp)]
 
 
 class SphOut(ctypes.Structure):
@@ -69,6 +70,7 @@ def load(path: str = LIB):
     L.sph_density_pair.argtypes = [G, C, c_vp, c_i64, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_pair_sym.argtypes = [G, C, c_vp, c_i64, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_drift.argtypes = [G, C, ctypes.c_float, c_vp, c_vp]
+    L.sph_gather_positions.argtypes = [G, C, c_vp, c_i64, c_vp]
     L.sph_select_planes.argtypes = [G, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_finalize.argtypes = [O, c_i64, c_vp]
     L.sph_density_all.argtypes = [G, C, O, S, c_vp, ctypes.c_size_t, c_vp]
@@ -79,7 +81,7 @@ def load(path: str = LIB):
     L.sph_strerror.argtypes = [ctypes.c_int]
     L.sph_strerror.restype = ctypes.c_char_p
     for f in ("sph_build_cells", "sph_sort_cells", "sph_density_self", "sph_density_pair", "sph_density_pair_sym",
-              "sph_drift", "sph_select_planes",
+              "sph_drift", "sph_gather_positions", "sph_select_planes",
               "sph_density_finalize",
               "sph_density_all", "sph_status", "sph_status_reset"):
         getattr(L, f).restype = ctypes.c_int

@@ -86,6 +86,8 @@ class Cells:
     order: torch.Tensor         # (13, capacity) int16 storage of the uint16 sorted lists (include/sph.h)
     slot_cell: torch.Tensor     # (capacity,) int32
     cell_nhome: torch.Tensor    # (ncell,) int32: home particles per cell
+    disp: torch.Tensor          # (capacity,) float32: displacement bound since the build (list reuse)
+    cell_dx: torch.Tensor       # (ncell,) float32: per-cell max_dx
     n: int = 0
 
     @staticmethod
@@ -99,7 +101,9 @@ class Cells:
                      torch.empty(nce, dtype=torch.float32, device=device),
                      torch.empty((_lib.SPH_NDIR, cap), dtype=torch.int16, device=device),
                      torch.empty(cap, dtype=torch.int32, device=device),
-                     torch.empty(nce, dtype=torch.int32, device=device))
+                     torch.empty(nce, dtype=torch.int32, device=device),
+                     torch.zeros(cap, dtype=torch.float32, device=device),
+                     torch.zeros(nce, dtype=torch.float32, device=device))
 
     def struct(self) -> SphCells:
         s = SphCells()
@@ -109,6 +113,7 @@ class Cells:
         s.perm, s.cell_hmax, s.order = self.perm.data_ptr(), self.cell_hmax.data_ptr(), self.order.data_ptr()
         s.slot_cell = self.slot_cell.data_ptr()
         s.cell_nhome = self.cell_nhome.data_ptr()
+        s.disp, s.cell_dx = self.disp.data_ptr(), self.cell_dx.data_ptr()
         return s
 
     def order_np(self):
@@ -221,11 +226,20 @@ def sph_density_pair_sym(grid: SphGrid, cells: Cells, pairs: torch.Tensor, acc: 
 
 
 def sph_drift(grid: SphGrid, cells: Cells, dt: float, max_disp: torch.Tensor | None = None, stream=None) -> None:
-    """List reuse: x <- x + v dt for the stored particles (include/sph.h); max_disp: a (1,)
-    float32 device tensor receiving the largest |v| dt (atomic max)."""
+    """List reuse: x <- x + v dt for the stored particles (include/sph.h), accumulating each
+    particle's displacement bound and the per-cell max_dx; max_disp: a (1,) float32
+    device tensor receiving the largest displacement bound since the build (atomic max)."""
     s = cells.struct()
     _check(_lib.load().sph_drift(ctypes.byref(grid), ctypes.byref(s), float(dt),
                                  _ptr(max_disp) if max_disp is not None else None, _stream(stream)), "sph_drift")
+
+
+def sph_gather_positions(grid: SphGrid, cells: Cells, xyzh_out: torch.Tensor, n_out: int, stream=None) -> None:
+    """The stored (drifted) positions back in input order, wrapped into the box (include/sph.h)."""
+    assert xyzh_out.is_contiguous() and xyzh_out.dtype == torch.float32
+    s = cells.struct()
+    _check(_lib.load().sph_gather_positions(ctypes.byref(grid), ctypes.byref(s), _ptr(xyzh_out), int(n_out),
+                                            _stream(stream)), "sph_gather_positions")
 
 
 def sph_select_planes(grid: SphGrid, xyzh: torch.Tensor, vm: torch.Tensor, n_own: int, sel_x: torch.Tensor,
@@ -289,6 +303,73 @@ class DensityPass:
 
     def check(self, stream=None) -> None:
         check_status(self.ws, stream)
+
+
+class ReuseLoop:
+    """Time loop with pseudo-Verlet list reuse ("max_dx").
+
+    Cells and sorted lists are built on a grid with a skin s.  Every step drifts the stored
+    particles (sph_drift: each particle's displacement bound and the per-cell max_dx grow) and
+    runs sph_density_all, whose window in a neighbour cell c is widened by 2 max_dx(c).  Before a
+    drift that could take any particle's accumulated displacement past s, the loop rebuilds:
+    the current positions are gathered back to input order and wrapped into the box
+    (sph_gather_positions), then sph_build_cells + sph_sort_cells.  The decision is made on the
+    host from a bound (largest |v| dt per step, measured once at start(), plus rounding), so a
+    step needs no host synchronisation."""
+
+    def __init__(self, nc, n: int, skin: float, box=1.0, gamma=GAMMA, device="cuda"):
+        self.dp = DensityPass(nc, n, box, gamma, device=device, skin=skin)
+        self.skin = float(skin)
+        self.n = int(n)
+        self.x = torch.empty((max(self.n, 1), 4), dtype=torch.float32, device=device)   # input order
+        self.v = None
+        self.vmax = 0.0
+        self.bound = 0.0                     # host bound of the displacement since the last build
+        self.rebuilds = 0
+        self.rebuild_steps = []
+        self.steps = 0
+        self.max_disp = torch.zeros(1, dtype=torch.float32, device=device)
+
+    def _build(self, stream=None):
+        sph_build_cells(self.dp.grid, self.x, self.v, self.dp.cells, self.dp.ws, stream=stream)
+        sph_sort_cells(self.dp.grid, self.dp.cells, self.dp.ws, stream=stream)
+        self.bound = 0.0
+        self.max_disp.zero_()
+
+    def start(self, xyzh: torch.Tensor, vm: torch.Tensor, stream=None) -> None:
+        """Initial state (input order, device) and the first build; one host sync for max |v|."""
+        self.x[:self.n].copy_(xyzh)
+        self.v = vm
+        self.vmax = float(torch.linalg.vector_norm(vm[:, :3].double(), dim=1).max().item()) if self.n else 0.0
+        self._build(stream)
+
+    def step_bound(self, dt: float) -> float:
+        """Upper bound of one drift's stored increment: |v| dt with both fp32 roundings (v dt,
+        then the position sum: <= 2^-24 |x| per component, |x| < box + skin)."""
+        box = max(self.dp.grid.box[0], self.dp.grid.box[1], self.dp.grid.box[2])
+        return self.vmax * abs(dt) * (1.0 + 2.0 ** -20) + 3.0 ** 0.5 * 2.0 ** -24 * (box + self.skin) * 1.01
+
+    def step(self, dt: float, stats: Stats | None = None, stream=None) -> Out:
+        inc = self.step_bound(dt)
+        if inc > self.skin:
+            raise ValueError(f"one drift ({inc}) exceeds the skin ({self.skin}): smaller dt or a larger skin")
+        if self.bound + inc > self.skin:     # this drift could leave the skin: rebuild from the current state
+            sph_gather_positions(self.dp.grid, self.dp.cells, self.x, self.n, stream=stream)
+            self._build(stream)
+            self.rebuilds += 1
+            self.rebuild_steps.append(self.steps)
+        sph_drift(self.dp.grid, self.dp.cells, dt, self.max_disp, stream=stream)
+        self.bound += inc
+        self.steps += 1
+        sph_density_all(self.dp.grid, self.dp.cells, self.dp.out, self.dp.ws, stats=stats, stream=stream)
+        return self.dp.out
+
+    def check(self, stream=None) -> None:
+        """Raise on errors; also verifies the device displacement against the host bound."""
+        self.dp.check(stream)
+        md = float(self.max_disp.item())
+        if md > self.skin:
+            raise RuntimeError(f"displacement {md} since the build exceeds the skin {self.skin}")
 
 
 def level_grids(h, nc0: int, box=1.0, gamma=GAMMA, max_levels: int = 3):

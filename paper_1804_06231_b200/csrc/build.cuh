@@ -247,8 +247,13 @@ __global__ void k_scatter_rec(DevGrid g, long long n_total, const int *__restric
 }
 
 // sph_drift: x <- fp32(x + fp32(v dt)) per component for every stored particle (list reuse,
-// DESIGN.md §4.6); the largest |v| dt to *max_disp (non-negative floats order like their bits).
+// P:102).  Per particle the exact stored increment x_new - x_old (fp32 subtraction
+// of nearby values: exact) is accumulated in disp[s] (its norm rounded up by 1e-6 relative, so
+// disp bounds |x - x_build| by the triangle inequality); per cell the paper's max_dx = the
+// largest disp of its particles (cell_dx, atomic max on the float bits: all values >= 0);
+// *max_disp (optional) = the largest of all.
 __global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm, long long n, float dt,
+                        float *__restrict__ disp, const int *__restrict__ slot_cell, float *__restrict__ cell_dx,
                         float *max_disp)
 {
     float mx = 0.0f;
@@ -256,12 +261,17 @@ __global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm
          s += (long long)gridDim.x * blockDim.x) {
         float4 p = xyzh[s];
         const float4 v = vm[s];
-        const float dx = __fmul_rn(v.x, dt), dy = __fmul_rn(v.y, dt), dz = __fmul_rn(v.z, dt);
-        p.x = __fadd_rn(p.x, dx);
-        p.y = __fadd_rn(p.y, dy);
-        p.z = __fadd_rn(p.z, dz);
+        const float nx = __fadd_rn(p.x, __fmul_rn(v.x, dt)), ny = __fadd_rn(p.y, __fmul_rn(v.y, dt)),
+                    nz = __fadd_rn(p.z, __fmul_rn(v.z, dt));
+        const float ax = nx - p.x, ay = ny - p.y, az = nz - p.z;   // the stored increment
+        p.x = nx;
+        p.y = ny;
+        p.z = nz;
         xyzh[s] = p;
-        mx = fmaxf(mx, sqrtf(fmaf(dx, dx, fmaf(dy, dy, dz * dz))));
+        const float d = disp[s] + sqrtf(fmaf(ax, ax, fmaf(ay, ay, az * az))) * 1.000001f;
+        disp[s] = d;
+        atomicMax(reinterpret_cast<int *>(cell_dx) + slot_cell[s], __float_as_int(d));
+        mx = fmaxf(mx, d);
     }
     if (max_disp) {
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
@@ -270,6 +280,31 @@ __global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int *>(max_disp), __float_as_int(mx));
+    }
+}
+
+// sph_gather_positions: the stored (drifted) positions back in input order, each coordinate
+// wrapped into [0, L) (x < 0 -> x + L, x >= L -> x - L; a sum that rounds to L becomes 0):
+// the input of the next sph_build_cells when a reuse loop rebuilds.
+__global__ void k_gather_positions(const float4 *__restrict__ xyzh, const int *__restrict__ perm, long long n,
+                                   long long n_out, float bx, float by, float bz, float4 *__restrict__ out)
+{
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n;
+         s += (long long)gridDim.x * blockDim.x) {
+        const int q = perm[s];
+        if (q < 0 || q >= n_out) continue;                 // ghosts / other ranks' particles
+        float4 p = xyzh[s];
+        const float b[3] = {bx, by, bz};
+        float c[3] = {p.x, p.y, p.z};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float v = c[k];
+            if (v < 0.0f) v += b[k];
+            else if (v >= b[k]) v -= b[k];
+            if (v >= b[k]) v = 0.0f;
+            c[k] = v;
+        }
+        out[q] = make_float4(c[0], c[1], c[2], p.w);
     }
 }
 

@@ -30,7 +30,8 @@ struct DevGrid {
     float boxf[3];
     float gamma;
     float h_home_min, h_home_max;   // level passes: home iff h_home_min < h <= h_home_max (max 0: all)
-    float delta;         // window margin SPH_DELTA_FRAC * min(cl) + 4 skin
+    float delta;         // window margin SPH_DELTA_FRAC * min(cl) + 4 skin (engines without per-cell max_dx)
+    float delta0;        // the fp32 part alone, SPH_DELTA_FRAC * min(cl): k_density_v5 adds 2 max_dx(cj)
     float skin;          // list reuse: largest displacement since the build (sph_grid.skin)
     float q[SPH_NDIR];   // Q_d = sum_a |d_a| C_a / |d|: projection of the cell offset on axis d
 };
@@ -45,6 +46,7 @@ struct DevCells {
     const uint16_t *ord;    // sorted lists (include/sph.h), [SPH_NDIR][cap]
     const int *slot_cell;
     const int *cell_nhome;
+    const float *cell_dx;   // per-cell max_dx since the build (sph_drift; workspace), or null
 };
 
 // Level passes: is a particle of smoothing length h a HOME particle of

@@ -33,13 +33,31 @@ namespace pvsph {
 
 constexpr int V5_WARPS = V4_WARPS;
 constexpr int V5_TP = V4_TP;
-constexpr int V5_Q = 32;                               // hit stack depth per lane, 2-byte entries
+#ifndef V5_STAGE_V
+#define V5_STAGE_V 1   // 0: (v, m) read from global memory (L1/L2) in the drains instead of staged
+#endif
+#ifndef V5_CTAS
+#define V5_CTAS 2
+#endif
+#ifndef V5_Q_DEPTH
+#define V5_Q_DEPTH 28
+#endif
+constexpr int V5_Q = V5_Q_DEPTH;                       // hit stack depth per lane, 2-byte entries
+#ifndef V5_NP
+#define V5_NP 2        // packed pairs per drain round (2 NP hits per lane)
+#endif
+#ifndef V5_TRIG
+#define V5_TRIG 24     // drain when this many lanes hold 2 NP hits
+#endif
+#ifndef V5_CHK
+#define V5_CHK 8       // candidates between drain checks (stacks kept below V5_Q - V5_CHK)
+#endif
 constexpr int V5_MS = V4_MS;                           // staged particles (+1 sentinel)
 constexpr int V5_ML = V4_ML + 14 * V4_MAXH;            // list entries + sentinels: one per (home cell, direction) + one per home cell
 constexpr int V5_MLA = (V5_ML + 7) / 8 * 8;
-constexpr size_t V5_SMEM = (size_t)(V5_MS + 2) * 16 + (size_t)(V5_MS + 2) * 16 + (size_t)V4_MAXCELLS * 16 +
+constexpr size_t V5_SMEM = (size_t)(V5_MS + 2) * 16 + (size_t)(V5_STAGE_V ? V5_MS + 2 : 0) * 16 + (size_t)V4_MAXCELLS * 16 +
                            (size_t)V5_MLA * 2 + (size_t)V4_HOFF * 4 + (size_t)V5_WARPS * V5_Q * 32 * 2 +
-                           (size_t)V4_MAXZ * 16;
+                           (size_t)V4_MAXZ * 16 + (size_t)V4_MAXCELLS * 4;
 static_assert(V5_MS * 16 < 65536, "byte offsets of staged particles fit 16 bits");
 static_assert(((V5_MS + 1) * 16) % 16 == 0 && (V5_MLA * 2) % 16 == 0, "16-byte aligned shared arrays");
 static_assert(13 * V4_MAXH <= 2 * V5_TP, "two direction segments per thread");
@@ -53,11 +71,12 @@ static_assert(13 * V4_MAXH <= 2 * V5_TP, "two direction segments per thread");
 // kernel checks that P lies below 64 KiB of the shared window), so a candidate is loaded with
 // one LDS.128 [e] and its (v, m) with LDS.128 [e + V5_OFF_V]: no base add on the hot path.
 constexpr unsigned V5_OFF_V = (V5_MS + 2) * 16;
-constexpr unsigned V5_OFF_TAB = V5_OFF_V + (V5_MS + 2) * 16;
+constexpr unsigned V5_OFF_TAB = V5_OFF_V + (V5_STAGE_V ? (V5_MS + 2) * 16 : 0);
 constexpr unsigned V5_OFF_L = V5_OFF_TAB + V4_MAXCELLS * 16;
 
 struct V5Stage {
     const int4 *tab;          // {base, count, gstart, flags | home count << 8}
+    const float *tdx;         // per staged cell: max_dx since the build (0 without reuse)
     int nzs;
     unsigned sb;              // shared address of P[0]
     unsigned sl;              // shared address of L[0]
@@ -125,7 +144,7 @@ __device__ __forceinline__ void interact2(f2 nHinv, f2 dx, f2 dy, f2 dz, f2 m, f
 // so no probe needs a validity test.  `top`: largest power of two <= the warp's longest
 // segment, so all lanes run the same steps (the exact per-particle bound).
 __device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], const unsigned lim[4], const float h[4][3],
-                                            const float ax[2][3], const float Hk[2], int len[4])
+                                            const float ax[2][3], const float Hk[4], int len[4])
 {
     unsigned a[4] = {amid[0], amid[0] - 2u, amid[1], amid[1] - 2u};   // + side: L[mid]; - side: L[mid - 1]
     for (int st = top; st > 0; st >>= 1) {
@@ -151,9 +170,9 @@ __device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], con
             sp[k] = (k & 1) ? -sv : sv;
         }
         if (sp[0] < Hk[0]) a[0] = pa[0];
-        if (sp[1] < Hk[0]) a[1] = pa[1];
-        if (sp[2] < Hk[1]) a[2] = pa[2];
-        if (sp[3] < Hk[1]) a[3] = pa[3];
+        if (sp[1] < Hk[1]) a[1] = pa[1];
+        if (sp[2] < Hk[2]) a[2] = pa[2];
+        if (sp[3] < Hk[3]) a[3] = pa[3];
     }
     len[0] = (int)(amid[0] - a[0]) >> 1;
     len[1] = (int)(a[1] + 2u - amid[0]) >> 1;
@@ -161,37 +180,8 @@ __device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], con
     len[3] = (int)(a[3] + 2u - amid[1]) >> 1;
 }
 
-#if defined(V5_OLD_BISECT) || defined(V5_CHECK_BISECT) || defined(V5_STATS)
-__device__ unsigned long long g_v5dbg[16];
-template <int D0, int D1>
-__device__ __forceinline__ void v5_windows2_old(const V5Stage &S, int top, const int f[4], const int n[4],
-                                                const float h[4][3], const float Hk[2], int len[4])
-{
-    int lo[4] = {0, 0, 0, 0};
-    for (int st = top; st > 0; st >>= 1) {
-        unsigned e[4];
-        bool v[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int kk = lo[k] + st;
-            v[k] = kk <= n[k];
-            e[k] = v[k] ? ldsr_u16(S.sl + 2u * (unsigned)((k & 1) ? f[k] + kk - 1 : f[k] - kk + 1)) : S.sent;
-        }
-        float4 p[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) p[k] = ldsr_f4(e[k]);
-        const float s0 = v4_dot<D0>(p[0].x - h[0][0], p[0].y - h[0][1], p[0].z - h[0][2]);
-        const float s1 = v4_dot<D0>(h[1][0] - p[1].x, h[1][1] - p[1].y, h[1][2] - p[1].z);
-        const float s2 = v4_dot<D1>(p[2].x - h[2][0], p[2].y - h[2][1], p[2].z - h[2][2]);
-        const float s3 = v4_dot<D1>(h[3][0] - p[3].x, h[3][1] - p[3].y, h[3][2] - p[3].z);
-        if (v[0] && s0 < Hk[0]) lo[0] += st;
-        if (v[1] && s1 < Hk[0]) lo[1] += st;
-        if (v[2] && s2 < Hk[1]) lo[2] += st;
-        if (v[3] && s3 < Hk[1]) lo[3] += st;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) len[k] = lo[k];
-}
+#ifdef V5_STATS
+__device__ unsigned long long g_v5dbg[16];   // profiling counters (scripts: exp builds only)
 #endif
 
 // One lane = one home particle of a staged tile (see density_v4.cuh for the tile geometry).
@@ -211,10 +201,9 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         const double H = (double)g.gamma * (double)a.w;   // exact product; H^2, 1/H rounded once
         H2 = (float)(H * H);
         Hinv = (float)(1.0 / H);
-        Hd = (float)H + g.delta;
+        Hd = (float)H + g.delta0;                          // + 2 max_dx of the neighbour cell, per segment
     }
     const float xs = x - g.boxf[0], ys = y - g.boxf[1], zs = z - g.boxf[2];   // exact where used (x >= L/2)
-    const float Hd2 = Hd * 1.41421356237309505f, Hd3 = Hd * 1.73205080756887729f;   // (H + delta) sqrt(kind)
     const f2 nHinv = bc2(-Hinv);
     auto scell = [&](int ox, int oy, int oz) { return ((ox + 1) * 4 + oy + yoff + 1) * S.nzs + qh + oz; };
     const int4 eh = S.tab[scell(0, 0, 0)];
@@ -265,7 +254,12 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                 }
             }
             const float4 p0 = ldsr_f4(e[0]), p1 = ldsr_f4(e[1]);
+#if V5_STAGE_V
             const float4 v0 = ldsr_f4_at<V5_OFF_V>(e[0]), v1 = ldsr_f4_at<V5_OFF_V>(e[1]);
+#else
+            // (v, m) from global memory: the staged position's w holds the particle's slot
+            const float4 v0 = __ldg(c.vm + __float_as_int(p0.w)), v1 = __ldg(c.vm + __float_as_int(p1.w));
+#endif
             interact2(nHinv, pk(hxv[0] - p0.x, hxv[1] - p1.x), pk(hyv[0] - p0.y, hyv[1] - p1.y),
                       pk(hzv[0] - p0.z, hzv[1] - p1.z), pk(v0.w, v1.w), pk(v0.x - vx, v1.x - vx),
                       pk(v0.y - vy, v1.y - vy), pk(v0.z - vz, v1.z - vz), A);
@@ -276,9 +270,10 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
     auto drain_check = [&]() {
         for (;;) {
             const unsigned n = (qp - sQ) >> 6;
-            if (!(__popc(__ballot_sync(0xffffffffu, n >= 4)) >= 24 || __any_sync(0xffffffffu, n >= V5_Q - 8)))
+            if (!(__popc(__ballot_sync(0xffffffffu, n >= 2 * V5_NP)) >= V5_TRIG ||
+                  __any_sync(0xffffffffu, n >= V5_Q - V5_CHK)))
                 break;
-            drain(std::integral_constant<int, 2>{});
+            drain(std::integral_constant<int, V5_NP>{});
         }
     };
 
@@ -318,7 +313,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         unsigned fl0v[2] = {0, 0}, fl1v[2] = {0, 0};
         unsigned amid[2] = {S.sl, S.sl}, lim[4] = {S.sl, S.sl, S.sl, S.sl};
         float hh[4][3];
-        float Hkv[2] = {-3e38f, -3e38f};
+        float Hkv[4] = {-3e38f, -3e38f, -3e38f, -3e38f};
         float axv[2][3] = {{0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f}};
         int nmax = 0;
 #pragma unroll
@@ -329,13 +324,18 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
             hh[2 * k][2] = hh[2 * k + 1][2] = z;
             if (k < nd) {
                 const int kind = v4_kind(d);
-                Hkv[k] = kind == 1 ? Hd : (kind == 2 ? Hd2 : Hd3);
+                const float sk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
                 const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
                 axv[k][0] = (float)a0;
                 axv[k][1] = (float)a1;
                 axv[k][2] = (float)a2;
-                const int4 ep = S.tab[scell(a0, a1, a2)];
-                const int4 em = S.tab[scell(-a0, -a1, -a2)];
+                const int cp = scell(a0, a1, a2), cm = scell(-a0, -a1, -a2);
+                const int4 ep = S.tab[cp];
+                const int4 em = S.tab[cm];
+                // window thresholds (H + delta + 2 max_dx(neighbour)) sqrt(kind): the stale list order
+                // of a drifted cell is off by at most 2 max_dx
+                Hkv[2 * k] = fmaf(2.0f, S.tdx[cp], Hd) * sk;
+                Hkv[2 * k + 1] = fmaf(2.0f, S.tdx[cm], Hd) * sk;
                 mid[k] = pos + ep.y;                      // boundary between the two reversed segments
                 sent[k] = mid[k] + em.y;                  // the sentinel slot after the -d segment
                 amid[k] = S.sl + 2u * (unsigned)mid[k];
@@ -351,48 +351,11 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                 }
             }
         }
-        if (!active) Hkv[0] = Hkv[1] = -3e38f;           // inactive lanes (position 0): empty windows
+        if (!active) Hkv[0] = Hkv[1] = Hkv[2] = Hkv[3] = -3e38f;   // inactive lanes (position 0): empty windows
         nmax = __reduce_max_sync(0xffffffffu, nmax);
         const int top = nmax > 0 ? 1 << (31 - __clz(nmax)) : 0;
         int len[4] = {0, 0, 0, 0};
-#ifdef V5_OLD_BISECT
-        {
-            int f[4], nn[4];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                f[2 * k] = (int)((amid[k] - S.sl) >> 1) - 1;
-                f[2 * k + 1] = (int)((amid[k] - S.sl) >> 1);
-                nn[2 * k] = k < nd && active ? (int)((amid[k] - lim[2 * k]) >> 1) - 1 : 0;
-                nn[2 * k + 1] = k < nd && active ? (int)((lim[2 * k + 1] - amid[k]) >> 1) : 0;
-            }
-#define V5W2O(P) case P: v5_windows2_old<2 * P, (2 * P + 1 < 13 ? 2 * P + 1 : 0)>(S, top, f, nn, hh, Hkv, len); break;
-            switch (d0 >> 1) { V5W2O(0) V5W2O(1) V5W2O(2) V5W2O(3) V5W2O(4) V5W2O(5) V5W2O(6) }
-#undef V5W2O
-        }
-#else
         v5_windows2(top, amid, lim, hh, axv, Hkv, len);
-#ifdef V5_CHECK_BISECT
-        {
-            int f[4], nn[4], lo2[4];
-#pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                f[2 * k] = (int)((amid[k] - S.sl) >> 1) - 1;
-                f[2 * k + 1] = (int)((amid[k] - S.sl) >> 1);
-                nn[2 * k] = k < nd && active ? (int)((amid[k] - lim[2 * k]) >> 1) - 1 : 0;
-                nn[2 * k + 1] = k < nd && active ? (int)((lim[2 * k + 1] - amid[k]) >> 1) : 0;
-            }
-#define V5W2O(P) case P: v5_windows2_old<2 * P, (2 * P + 1 < 13 ? 2 * P + 1 : 0)>(S, top, f, nn, hh, Hkv, lo2); break;
-            switch (d0 >> 1) { V5W2O(0) V5W2O(1) V5W2O(2) V5W2O(3) V5W2O(4) V5W2O(5) V5W2O(6) }
-#undef V5W2O
-            for (int k = 0; k < 4; ++k)
-                if (lo2[k] != len[k] && atomicAdd(&g_v5dbg[0], 1ull) == 0) {
-                    g_v5dbg[1] = d0; g_v5dbg[2] = k; g_v5dbg[3] = lo2[k]; g_v5dbg[4] = len[k];
-                    g_v5dbg[5] = nn[k]; g_v5dbg[6] = top; g_v5dbg[7] = amid[k >> 1]; g_v5dbg[8] = lim[k];
-                    g_v5dbg[9] = __float_as_uint(Hkv[k >> 1]);
-                }
-        }
-#endif
-#endif
 #pragma unroll 1
         for (int k = 0; k < nd; ++k) {
             const int kind = v4_kind(d0 + k);
@@ -441,11 +404,14 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                 }
             }
 #endif
-            for (int t = 0; t < trip; t += 8) {
-                if (t + 4 < trip)
-                    step(t, std::integral_constant<int, 8>{});
-                else                                      // a tail of <= 4 candidates
-                    step(t, std::integral_constant<int, 4>{});
+            for (int t0 = 0; t0 < trip; t0 += V5_CHK) {
+#pragma unroll 1
+                for (int t = t0; t < min(t0 + V5_CHK, trip); t += 8) {
+                    if (t + 4 < trip)
+                        step(t, std::integral_constant<int, 8>{});
+                    else                                  // a tail of <= 4 candidates
+                        step(t, std::integral_constant<int, 4>{});
+                }
                 drain_check();
             }
         }
@@ -457,7 +423,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         if ((threadIdx.x & 31) == 0) atomicAdd(&g_v5dbg[15], (unsigned long long)left);   // [15] hits left for the final drain
     }
 #endif
-    while (__any_sync(0xffffffffu, qp != sQ)) drain(std::integral_constant<int, 2>{});
+    while (__any_sync(0xffffffffu, qp != sQ)) drain(std::integral_constant<int, V5_NP>{});
 
     if (active) {
         // finalise: self term w(0) = 1/2, w(0) - 0 q = 1/2; K3 = 16/(pi H^3); rho_dh = -(K3 gamma/H) (3/2 m + 3 S_t);
@@ -477,7 +443,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
 // Persistent CTAs over the k_v4_tiles list (same tiles and staging as v4; list block layout
 // per home cell: for d = 0..12 the +d list reversed, the -d list reversed, one sentinel).
 template <bool COUNT>
-__global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, OutRec *orec, sph_stats *st,
+__global__ void __launch_bounds__(V5_TP, V5_CTAS) k_density_v5(DevGrid g, DevCells c, OutRec *orec, sph_stats *st,
                                                           const int4 *__restrict__ tiles,
                                                           const int *__restrict__ ntiles_p, int *tile_counter,
                                                           const unsigned *__restrict__ genp, unsigned *status)
@@ -485,11 +451,12 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
     extern __shared__ __align__(16) unsigned char v5_smem[];
     float4 *P = reinterpret_cast<float4 *>(v5_smem);
     float4 *V = P + V5_MS + 2;
-    int4 *tab = reinterpret_cast<int4 *>(V + V5_MS + 2);
+    int4 *tab = reinterpret_cast<int4 *>(V + (V5_STAGE_V ? V5_MS + 2 : 0));
     uint16_t *L = reinterpret_cast<uint16_t *>(tab + V4_MAXCELLS);
     int *hoff = reinterpret_cast<int *>(L + V5_MLA);
     uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_HOFF);
     int4 *seq = reinterpret_cast<int4 *>(queue + V5_WARPS * V5_Q * 32);
+    float *tdx = reinterpret_cast<float *>(seq + V4_MAXZ);
     __shared__ int4 s_next;
     __shared__ int s_wsum[V5_WARPS];
     __shared__ __align__(8) unsigned long long s_mbar;
@@ -510,6 +477,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
     }
 
     int pf_start[2] = {0, 0}, pf_end[2] = {0, 0}, pf_nh[2] = {0, 0};
+    float pf_dx[2] = {0.0f, 0.0f};
     auto prefetch = [&](int4 td) {
         if (td.x < 0) return;
         const TileGeom t = tile_geom(g, rp, td);
@@ -523,6 +491,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
                 pf_start[k] = c.cell_start[cell];
                 pf_end[k] = c.cell_start[cell + 1];
                 pf_nh[k] = c.cell_nhome[cell];
+                pf_dx[k] = c.cell_dx[cell];
             }
         }
     };
@@ -536,9 +505,9 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
         // terms evaluate to exactly 0 (x >> 1, q = w = 0).
         const float qnan = __int_as_float(0x7fc00000);
         P[V5_MS] = make_float4(qnan, qnan, qnan, 0.0f);
-        V[V5_MS] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (V5_STAGE_V) V[V5_MS] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         P[V5_MS + 1] = make_float4(1e15f, 1e15f, 1e15f, 0.0f);
-        V[V5_MS + 1] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (V5_STAGE_V) V[V5_MS + 1] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
         mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -569,8 +538,14 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
                     ent[k] = make_int4(0, cnt2[k], pf_start[k], (int)fl | (pf_nh[k] << 8));
                 }
             }
-            if (2 * threadIdx.x < ncs) tab[2 * threadIdx.x] = ent[0];
-            if (2 * threadIdx.x + 1 < ncs) tab[2 * threadIdx.x + 1] = ent[1];
+            if (2 * threadIdx.x < ncs) {
+                tab[2 * threadIdx.x] = ent[0];
+                tdx[2 * threadIdx.x] = pf_dx[0];
+            }
+            if (2 * threadIdx.x + 1 < ncs) {
+                tab[2 * threadIdx.x + 1] = ent[1];
+                tdx[2 * threadIdx.x + 1] = pf_dx[1];
+            }
             __syncthreads();
             // direction blocks: (home cell h, direction d) -> n(+d) + n(-d) + 1 entries; two per thread
             const int ndseg = 13 * T.nh;
@@ -626,7 +601,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
             __syncthreads();
             if (staged) {
                 if (wl == 0) {
-                    if (lane == 0) mbar_expect_tx(mbar, (unsigned)total * 32u);
+                    if (lane == 0) mbar_expect_tx(mbar, (unsigned)total * (V5_STAGE_V ? 32u : 16u));
                     __syncwarp();
                     const bool wlo = T.za == 0, whi = T.zb + 1 >= g.nz;
                     for (int job = lane; job < V4_ROWS * 3; job += 32) {
@@ -639,7 +614,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
                         const unsigned bytes = (unsigned)(eb.x + eb.y - ea.x) * 16u;
                         if (bytes == 0) continue;
                         bulk_g2s(smem_addr(P + ea.x), c.xyzh + ea.z, bytes, mbar);
-                        bulk_g2s(smem_addr(V + ea.x), c.vm + ea.z, bytes, mbar);
+                        if (V5_STAGE_V) bulk_g2s(smem_addr(V + ea.x), c.vm + ea.z, bytes, mbar);
                     }
                 }
                 // list segments (2 per direction block), entries turned into staged byte offsets
@@ -679,11 +654,13 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
                 }
                 mbar_wait(mbar, mbar_phase);
                 mbar_phase ^= 1u;
-                if (T.za == 0 || T.y0 == 0 || g.x_lo + T.xo == 0) {
+                if (!V5_STAGE_V || T.za == 0 || T.y0 == 0 || g.x_lo + T.xo == 0) {
+                    // staged cells of a -L periodic image (flags 3-5): x_j - L, exact (x_j >= L/2);
+                    // without staged (v, m): every staged position's w becomes its global slot
                     __syncthreads();
                     for (int sc = wl; sc < V4_ROWS * T.nzs; sc += V5_WARPS) {
                         const int4 e = tab[sc];
-                        if (!(e.w & 56)) continue;
+                        if (V5_STAGE_V && !(e.w & 56)) continue;
                         const float sx = (e.w & 8) ? g.boxf[0] : 0.0f;
                         const float sy = (e.w & 16) ? g.boxf[1] : 0.0f;
                         const float sz = (e.w & 32) ? g.boxf[2] : 0.0f;
@@ -692,6 +669,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
                             qv.x -= sx;
                             qv.y -= sy;
                             qv.z -= sz;
+                            if (!V5_STAGE_V) qv.w = __int_as_float(e.z + k);
                             P[e.x + k] = qv;
                         }
                     }
@@ -726,7 +704,7 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
             } else {
                 i = seq[0].x;
             }
-            const V5Stage S{tab, T.nzs, sb, smem_addr(L), sb + 16u * V5_MS, sb + 16u * (V5_MS + 1)};
+            const V5Stage S{tab, tdx, T.nzs, sb, smem_addr(L), sb + 16u * V5_MS, sb + 16u * (V5_MS + 1)};
             const unsigned qb = smem_addr(queue + wl * V5_Q * 32);
             if (wl * 32 < T.cnt) {
                 if (T.frames)
@@ -754,6 +732,35 @@ __global__ void __launch_bounds__(V5_TP, 2) k_density_v5(DevGrid g, DevCells c, 
         td = td_next;
     }
     flush_stats<COUNT>(st, cand, hits, band);
+}
+
+// sph_calibrate mode 3: the production interaction (interact2, two hits per lane with
+// FFMA2/FMUL2/FADD2, exactly as the v5 drains evaluate them) on full masks: every thread is one
+// i interacting with CALIB_NJ shared-memory neighbours per pass, no neighbour search (the
+// Table 2 analogue, for the engine the bench runs).
+__global__ void k_calib_interact2(float *out, int iters)
+{
+    constexpr int NJ = 256;
+    __shared__ float4 sx[NJ], sv[NJ];
+    for (int k = threadIdx.x; k < NJ; k += blockDim.x) {
+        const float t = (float)k / NJ;
+        sx[k] = make_float4(0.01f * t, 0.02f * (1.f - t), 0.005f * t, 0.f);
+        sv[k] = make_float4(t, -t, 0.5f * t, 1e-3f);
+    }
+    __syncthreads();
+    const float x = 0.0101f, y = 0.0102f, z = 0.0053f, vx = 0.3f, vy = -0.2f, vz = 0.1f;
+    const f2 nHinv = bc2(-1.0f / 0.05f);
+    Acc5 A;
+    A.rho = A.wc = A.srt = A.st = A.Dq = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
+    for (int i = 0; i < iters; ++i)
+        for (int k = 0; k < NJ; k += 2) {
+            const float4 p0 = sx[k], p1 = sx[k + 1], v0 = sv[k], v1 = sv[k + 1];
+            interact2(nHinv, pk(x - p0.x, x - p1.x), pk(y - p0.y, y - p1.y), pk(z - p0.z, z - p1.z), pk(v0.w, v1.w),
+                      pk(v0.x - vx, v1.x - vx), pk(v0.y - vy, v1.y - vy), pk(v0.z - vz, v1.z - vz), A);
+        }
+    const float s = sum2(A.rho) + sum2(A.wc) + sum2(A.srt) + sum2(A.st) + sum2(A.Dq) + sum2(A.Px) + sum2(A.Nx) +
+                    sum2(A.Py) + sum2(A.Ny) + sum2(A.Pz) + sum2(A.Nz);
+    if (s == 123.456f) out[0] = s;
 }
 
 }  // namespace pvsph

@@ -121,6 +121,7 @@ int make_grid(const sph_grid *gr, DevGrid &g)
     g.skin = gr->skin;
     // window margin: the fp32 margin of §4.2 plus 4 skin (stale sort order after drifts, §4.6)
     g.delta = (float)(SPH_DELTA_FRAC * clmin + 4.0 * (double)gr->skin);
+    g.delta0 = (float)(SPH_DELTA_FRAC * clmin);
     if (gr->skin > 0.0f && !(2.0 * (double)gr->skin < clmin)) return SPH_EINVAL;
     for (int d = 0; d < SPH_NDIR; ++d) {
         int nz = 0;
@@ -138,6 +139,7 @@ int make_grid(const sph_grid *gr, DevGrid &g)
 bool cells_ok(const sph_cells *c)
 {
     return c && c->cell_start && c->xyzh && c->vm && c->perm && c->cell_hmax && c->order && c->slot_cell && c->cell_nhome &&
+           c->disp && c->cell_dx &&
            c->capacity >= 0 &&
            c->capacity < (1LL << 31) && ((uintptr_t)c->xyzh % 16 == 0) && ((uintptr_t)c->vm % 16 == 0) &&
            ((uintptr_t)c->order % 2 == 0);
@@ -155,6 +157,7 @@ DevCells dev_cells(const sph_cells *c)
     d.ord = c->order;
     d.slot_cell = c->slot_cell;
     d.cell_nhome = c->cell_nhome;
+    d.cell_dx = c->cell_dx;
     return d;
 }
 
@@ -326,6 +329,9 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         int *row_home = at<int>(ws, w.row_home);
         if ((e = cudaMemsetAsync(bt_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
         if ((e = cudaMemsetAsync(row_home, 0, 4 * (size_t)g.nxl * g.ny, s)) != cudaSuccess) return cuda_fail(e);
+        // a fresh build: no displacement since it (list reuse, sph_drift)
+        if ((e = cudaMemsetAsync(cells->disp, 0, 4 * (size_t)n, s)) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaMemsetAsync(cells->cell_dx, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
             g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, cells->cell_hmax,
             row_home, g.nz, big_items, big_count, bt_items, bt_count);
@@ -338,6 +344,8 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     if (n == 0 && (e = cudaMemsetAsync(cells->cell_nhome, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
         return cuda_fail(e);
     if (n == 0 && (e = cudaMemsetAsync(cells->cell_hmax, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
+        return cuda_fail(e);
+    if (n == 0 && (e = cudaMemsetAsync(cells->cell_dx, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess)
         return cuda_fail(e);
     cells->n = n;
     return check_launch();
@@ -460,7 +468,21 @@ int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp,
     if (!cells_ok(cells) || !std::isfinite(dt)) return SPH_EINVAL;
     if (cells->n <= 0) return SPH_OK;
     k_drift<<<grid_blocks(cells->n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
-        reinterpret_cast<float4 *>(cells->xyzh), reinterpret_cast<const float4 *>(cells->vm), cells->n, dt, max_disp);
+        reinterpret_cast<float4 *>(cells->xyzh), reinterpret_cast<const float4 *>(cells->vm), cells->n, dt,
+        cells->disp, cells->slot_cell, cells->cell_dx, max_disp);
+    return check_launch();
+}
+
+int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xyzh_out, int64_t n_out, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || n_out < 0 || (n_out > 0 && !xyzh_out) || ((uintptr_t)xyzh_out % 16)) return SPH_EINVAL;
+    if (cells->n <= 0 || n_out == 0) return SPH_OK;
+    k_gather_positions<<<grid_blocks(cells->n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<const float4 *>(cells->xyzh), cells->perm, cells->n, n_out, g.boxf[0], g.boxf[1], g.boxf[2],
+        reinterpret_cast<float4 *>(xyzh_out));
     return check_launch();
 }
 
@@ -626,11 +648,12 @@ int sph_debug_v5(unsigned long long *out16)
 
 int sph_calibrate(int mode, int blocks, int threads, int iters, float *out, void *stream)
 {
-    if (mode < 0 || mode > 2 || blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out) return SPH_EINVAL;
+    if (mode < 0 || mode > 3 || blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !out) return SPH_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     if (mode == 0) k_calib_ffma<<<blocks, threads, 0, s>>>(out, iters);
     else if (mode == 1) k_calib_ffma2<<<blocks, threads, 0, s>>>(out, iters);
-    else k_calib_interact<<<blocks, threads, 0, s>>>(out, iters);
+    else if (mode == 2) k_calib_interact<<<blocks, threads, 0, s>>>(out, iters);
+    else k_calib_interact2<<<blocks, threads, 0, s>>>(out, iters);
     return check_launch();
 }
 

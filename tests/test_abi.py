@@ -95,6 +95,7 @@ def test_capacity_error_is_host_side(lib):
     c.capacity = 4
     fake = 256   # aligned non-null fake device addresses: never dereferenced on this path
     c.cell_start = c.xyzh = c.vm = c.perm = c.cell_hmax = c.order = c.slot_cell = c.cell_nhome = fake
+    c.disp = c.cell_dx = fake
     assert lib.sph_build_cells(ctypes.byref(g), 5, 0, ctypes.c_void_p(fake), ctypes.c_void_p(fake),
                                ctypes.byref(c), ctypes.c_void_p(fake), 1 << 30, None) == 3
     assert lib.sph_build_cells(ctypes.byref(g), 2, 1, ctypes.c_void_p(fake), ctypes.c_void_p(fake),
