@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--levels", type=int, default=0,
                     help="level passes (DESIGN.md §4.5); 0 = auto: 3 for the clustered c4, else 1")
+    ap.add_argument("--engine", default="gather", choices=["gather", "sym"],
+                    help="density pass: the gather engine (sph_density_all, default) or the coloured symmetric "
+                         "whole pass (sph_density_all_sym, SURVEY §8(f) #1)")
     ap.add_argument("--reuse", action="store_true",
                     help="list-reuse time loop (P:102 max_dx; ReuseLoop): drift + density per step, cells and "
                          "lists rebuilt only when the skin would be exceeded (1 GPU)")
@@ -281,7 +284,7 @@ def run_ours(args):
         part = slabs.Slab.from_set(p, rank, world, bounds)
         del p
     t_gen = time.perf_counter() - t_gen
-    runner = slabs.SlabRunner(part, dist=dist, levels=levels)
+    runner = slabs.SlabRunner(part, dist=dist, levels=levels, engine=args.engine)
     runner.upload()
     stream = torch.cuda.current_stream()
 
@@ -353,8 +356,9 @@ def run_ours(args):
     dens_ms_local = statistics.mean(stage["density"])
     flops = FLOP_CAND * cand_sum + FLOP_HIT * hit_sum          # this rank's density launch
     achieved = flops / (dens_ms_local * 1e-3) / 1e12
-    prof = _profile_ncu(args.config)
-    roof = {"bound": "alu", "kernel": "k_density_v5 (sph_density_all incl. its tile list and transpose)",
+    prof = _profile_ncu(args.config) if args.engine == "gather" else None
+    roof = {"bound": "alu", "kernel": "k_density_v5 (sph_density_all incl. its tile list and transpose)"
+            if args.engine == "gather" else "k_density_pair_sym colour phases (sph_density_all_sym)",
             "achieved": achieved, "peak": FP32_PEAK_TFLOPS,
             "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
             "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (= ncu ffma peak_sustained x 2 x "
@@ -385,7 +389,8 @@ def run_ours(args):
                            "slab_planes": [part.x_lo, part.x_hi] if world > 1 else None,
                            "level_grids": [lv[0] for lv in runner.levels],
                            "l2": "inputs (>= 4 GB at c5) larger than L2; no flush",
-                           "step": "ghost exchange + build_cells + sort_cells + density_all"},
+                           "step": "ghost exchange + build_cells + sort_cells + " +
+                                   ("density_all" if args.engine == "gather" else "density_all_sym (colour phases)")},
                 "interactions_per_step": tot_inter, "candidates_per_step": tot_cand,
                 "hit_fraction": tot_inter / max(1, tot_cand),
                 "per_orientation": {k: {"candidates": tot_kind[0][n], "interactions": tot_kind[1][n],

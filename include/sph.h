@@ -237,6 +237,21 @@ int sph_density_pair(const sph_grid *grid, const sph_cells *cells, const int32_t
 int sph_density_pair_sym(const sph_grid *grid, const sph_cells *cells, const int32_t *pairs, int64_t npairs,
                          sph_out *acc, sph_stats *stats, void *ws, size_t ws_bytes, void *stream);
 
+/* The symmetric sweep over the whole pass ("computing interactions
+ * symmetrically"): every unordered candidate pair is
+ * evaluated once and both particles accumulate, with the ownership made
+ * conflict-free by colouring instead of atomics: the self cells first, then
+ * for each of the 13 directions d and each cell colour (parity per axis, a
+ * third colour for the last cell of an odd periodic axis) one launch over
+ * the pairs (c, c + d) of that colour -- two cells of a colour are >= 2
+ * apart, so a launch writes disjoint particles (plain read-modify-writes,
+ * each j summing its hits in ascending i: deterministic; a j hit by more
+ * than 32 i of one pair falls back to an atomic add).  Outputs final (as
+ * sph_density_all), zeroed first.  Same cells/workspace contract as
+ * sph_density_all. */
+int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *out, sph_stats *stats, void *ws,
+                        size_t ws_bytes, void *stream);
+
 /* div_v /= rho and curl_v /= rho for the first n elements (after the self
  * and pair calls). */
 int sph_density_finalize(sph_out *acc, int64_t n, void *stream);

@@ -266,6 +266,15 @@ def sph_density_all(grid: SphGrid, cells: Cells, out: Out, ws: torch.Tensor, sta
            "sph_density_all")
 
 
+def sph_density_all_sym(grid: SphGrid, cells: Cells, out: Out, ws: torch.Tensor, stats: Stats | None = None,
+                        stream=None) -> None:
+    """The symmetric sweep over the whole pass, conflict-free by colour phases (include/sph.h)."""
+    s, o = cells.struct(), out.struct()
+    _check(_lib.load().sph_density_all_sym(ctypes.byref(grid), ctypes.byref(s), ctypes.byref(o),
+                                           stats.ptr() if stats else None, _ptr(ws), ws.numel(), _stream(stream)),
+           "sph_density_all_sym")
+
+
 def sph_status(ws: torch.Tensor, stream=None) -> int:
     return int(_lib.load().sph_status(_ptr(ws), _stream(stream)))
 

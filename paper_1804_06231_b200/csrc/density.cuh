@@ -355,6 +355,22 @@ __device__ __forceinline__ void atomic_out(const DevOut &o, int out, const Final
     atomicAdd(&o.nngb[out], nngb);
 }
 
+// The same without atomics, for passes whose launches write disjoint particles (the colour
+// phases of sph_density_all_sym): a read-modify-write in a fixed order, so deterministic.
+__device__ __forceinline__ void plain_out(const DevOut &o, int out, const Final &f, int nngb)
+{
+    if (out >= o.n_out) return;
+    o.rho[out] += f.rho;
+    o.wcount[out] += f.wc;
+    o.rho_dh[out] += f.rho_dh;
+    o.wcount_dh[out] += f.wc_dh;
+    o.div_v[out] += f.div;
+    o.curl_v[out] += f.cx;
+    o.curl_v[o.n_out + out] += f.cy;
+    o.curl_v[2 * o.n_out + out] += f.cz;
+    o.nngb[out] += nngb;
+}
+
 __device__ __forceinline__ bool owned_cell(const DevGrid &g, long long cell)
 {
     long long plane = (long long)g.ny * g.nz;
@@ -366,14 +382,19 @@ __device__ __forceinline__ bool owned_cell(const DevGrid &g, long long cell)
 constexpr int API_WARPS = 4;
 
 template <bool COUNT>
+// nlist < 0: |nlist| is the list's stride in ints and nlist_dev the device-side count (the
+// self pass of sph_density_all_sym reads the first int of its (c, c) records).
 __global__ void __launch_bounds__(API_WARPS * 32) k_density_self(DevGrid g, DevCells c, DevOut o, const int *list,
-                                                                  long long nlist, sph_stats *st, unsigned *status)
+                                                                  long long nlist, sph_stats *st, unsigned *status,
+                                                                  const int *nlist_dev = nullptr)
 {
     const int lane = threadIdx.x & 31;
     long long w = (long long)blockIdx.x * API_WARPS + (threadIdx.x >> 5);
     unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    const long long stride = nlist < 0 ? -nlist : 1;
+    if (nlist < 0) nlist = nlist_dev ? *nlist_dev : 0;
     if (w < nlist) {
-        long long cell = list[w];
+        long long cell = list[w * stride];
         if (!owned_cell(g, cell)) {
             if (lane == 0) set_status(status, ST_EINVAL);
         } else {

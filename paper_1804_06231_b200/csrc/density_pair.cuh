@@ -231,6 +231,7 @@ constexpr int SYM_JCAP = 32;             // bucket entries per j
 constexpr size_t SYM_SMEM = (size_t)SYM_MAXN * 16 * 4 + (size_t)SYM_MAXN * 4 * 2 + (size_t)SYM_MAXN * 2 +
                             (size_t)SYM_WARPS * SYM_Q * 32 * 2 + (size_t)SYM_MAXN * SYM_JCAP * 2;
 
+template <bool PLAIN>
 __device__ __forceinline__ void sym_flush(const DevGrid &g, const DevOut &o, int out, float Hinv, const Acc2 &B,
                                           int nn)
 {
@@ -244,13 +245,18 @@ __device__ __forceinline__ void sym_flush(const DevGrid &g, const DevOut &o, int
     f.cx = gf * (sum2(B.Px) - sum2(B.Nx));         // rho * curl v
     f.cy = gf * (sum2(B.Py) - sum2(B.Ny));
     f.cz = gf * (sum2(B.Pz) - sum2(B.Nz));
-    atomic_out(o, out, f, nn);
+    if (PLAIN) plain_out(o, out, f, nn);
+    else atomic_out(o, out, f, nn);
 }
 
-template <bool COUNT>
+// PLAIN (sph_density_all_sym's colour phases): no two pairs of a launch share a cell, so the
+// outputs take plain read-modify-writes, and each j sums its bucket in ascending i (the buckets
+// are sorted first): deterministic.  npairs_dev (optional): the device-side pair count.
+template <bool COUNT, bool PLAIN = false>
 __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, DevCells c, DevOut o,
                                                                      const int2 *pairs, long long npairs,
-                                                                     sph_stats *st, unsigned *status)
+                                                                     sph_stats *st, unsigned *status,
+                                                                     const int *npairs_dev = nullptr)
 {
     extern __shared__ __align__(16) unsigned char sym_smem[];
     float4 *Pi = reinterpret_cast<float4 *>(sym_smem);             // ci positions (home shift applied)
@@ -272,11 +278,15 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
     }
     __syncthreads();
     unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
+    if (npairs_dev) npairs = min(npairs, (long long)*npairs_dev);
+    if (npairs_dev) npairs = min(npairs, (long long)*npairs_dev);
 
     for (long long q = blockIdx.x; q < npairs; q += gridDim.x) {
         const int2 pr = pairs[q];
         const long long ci = pr.x, cj = pr.y;
-        if (!owned_cell(g, ci) || cj < 0 || cj >= g.ncell) {
+        // (PLAIN: ci may be a ghost cell whose +d neighbour is owned; only j accumulates then)
+        const bool i_owned = owned_cell(g, ci);
+        if ((!PLAIN && !i_owned) || ci < 0 || ci >= g.ncell || cj < 0 || cj >= g.ncell) {
             if (threadIdx.x == 0) set_status(status, ST_EINVAL);
             continue;
         }
@@ -302,13 +312,17 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
         const bool j_owned = owned_cell(g, cjc);
         if (ni > SYM_MAXN || nj > SYM_MAXN) {
             // dense cells: the two one-sided per-thread sweeps reading global memory
-            for (int i = si + threadIdx.x; i < si + ni; i += blockDim.x) {
+            for (int i = si + threadIdx.x; i_owned && i < si + ni; i += blockDim.x) {
                 IPart p = load_i(g, c, i, hc.corner);
                 Acc a;
                 acc_zero(a);
                 sweep_pair<COUNT>(g, c, p, cjc, ox, oy, oz, sh, a, cand[kind], hits[kind]);
-                if (a.nngb > 0) atomic_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
+                if (a.nngb > 0) {
+                    if (PLAIN) plain_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
+                    else atomic_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
+                }
             }
+            __syncthreads();              // (PLAIN) ci's outputs written before cj's sweep reads nothing of them
             if (j_owned) {
                 const HomeCell hj = home_cell(g, cjc);
                 int cic, sh2[3];
@@ -319,7 +333,10 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                     acc_zero(a);
                     unsigned dummy = 0;
                     sweep_pair<COUNT>(g, c, p, cic, -ox, -oy, -oz, sh2, a, dummy, hits[kind]);
-                    if (a.nngb > 0) atomic_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
+                    if (a.nngb > 0) {
+                        if (PLAIN) plain_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
+                        else atomic_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
+                    }
                 }
             }
             continue;
@@ -425,7 +442,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                     const bool hi = ok && r2 < H2, hj = ok && r2 < p.w;
                     if (COUNT) {
                         cand[kind] += ok ? 1u : 0u;
-                        hits[kind] += (hi ? 1u : 0u) + (hj ? 1u : 0u);
+                        hits[kind] += (hi && i_owned ? 1u : 0u) + (hj && j_owned ? 1u : 0u);
                     }
                     if (hi) {
                         sts_u16(qp, id);
@@ -443,7 +460,8 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                             interact_pair<true>(bc2(HinvJ[id]), pk(dx, 0.f), pk(dy, 0.f), pk(dz, 0.f), pk(m, 0.f),
                                                 pk(vj.x - vx, 0.f), pk(vj.y - vy, 0.f), pk(vj.z - vz, 0.f),
                                                 pk(1.0f, 0.0f), B);
-                            sym_flush(g, o, c.perm[sj + id], HinvJ[id], B, 1);
+                            // (a bucket overflow: several lanes may hit j at once -> atomic even in PLAIN)
+                            sym_flush<false>(g, o, c.perm[sj + id], HinvJ[id], B, 1);
                         }
                     }
                 }
@@ -456,7 +474,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                 }
             }
             while (__any_sync(0xffffffffu, qp != sQ)) drain(true);
-            if (active && nngb > 0) sym_flush(g, o, c.perm[si + e], Hinv, A, nngb);
+            if (active && nngb > 0 && i_owned) sym_flush<PLAIN>(g, o, c.perm[si + e], Hinv, A, nngb);
         }
         __syncthreads();                          // buckets complete
         // ---- phase 2: lane = j, its bucket of i ---------------------------------------------------
@@ -465,6 +483,18 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                 const int k = t0 + lane;
                 const bool active = k < nj;
                 const int nb = active ? min(JC[k], SYM_JCAP) : 0;
+                if (PLAIN && nb > 1) {        // ascending i: a fixed summation order (the bucket slots
+                    uint16_t *bk = JB + k * SYM_JCAP;   // came from shared-memory atomics in any order)
+                    for (int a1 = 1; a1 < nb; ++a1) {
+                        const uint16_t key = bk[a1];
+                        int b1 = a1 - 1;
+                        while (b1 >= 0 && bk[b1] > key) {
+                            bk[b1 + 1] = bk[b1];
+                            --b1;
+                        }
+                        bk[b1 + 1] = key;
+                    }
+                }
                 const float4 pj = active ? Pj[k] : make_float4(0.f, 0.f, 0.f, 0.f);
                 const float4 vj = active ? Vj[k] : make_float4(0.f, 0.f, 0.f, 0.f);
                 const float hinv = active ? HinvJ[k] : 0.0f;
@@ -483,12 +513,61 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                                         pk(vj.y - w0.y, vj.y - w1.y), pk(vj.z - w0.z, vj.z - w1.z),
                                         pk(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f), B);
                 }
-                if (nb > 0) sym_flush(g, o, c.perm[sj + k], hinv, B, nb);
+                if (nb > 0) sym_flush<PLAIN>(g, o, c.perm[sj + k], hinv, B, nb);
             }
         }
         __syncthreads();                          // shared memory reused by the next pair
     }
     flush_stats<COUNT>(st, cand, hits);
+}
+
+// ---- sph_density_all_sym: the symmetric sweep over the whole pass ----
+// Colour of a cell on one axis of n cells: parity, plus a third colour for the last cell of
+// an odd periodic axis; two cells of one colour are >= 2 apart (periodically), so for a fixed
+// direction d the pairs (c, c + d) of one colour share no cell: a launch per (d, colour)
+// writes disjoint particles without atomics.  The x axis of a slab (ghost planes) is not
+// periodic inside the rank: parity of the local plane.
+__host__ __device__ __forceinline__ int sym_axis_colours(int n, bool periodic)
+{
+    return periodic && (n & 1) ? 3 : 2;
+}
+
+__device__ __forceinline__ int sym_axis_colour(int x, int n, bool periodic)
+{
+    return periodic && (n & 1) && x == n - 1 ? 2 : (x & 1);
+}
+
+// Pairs (c, c + d) for the owned cells c of colour `col` (cells of either side empty are
+// skipped); also, with d < 0, the list of all owned non-empty cells (the self pass).
+__global__ void k_sym_phase_pairs(DevGrid g, const int *__restrict__ cell_start, int d, int col, int2 *pairs,
+                                  int *count)
+{
+    const long long plane = (long long)g.ny * g.nz;
+    const int cx = sym_axis_colours(g.nxl, !g.ghost_x), cy = sym_axis_colours(g.ny, true);
+    const int a0 = d >= 0 ? dir_component(d, 0) : 0, a1 = d >= 0 ? dir_component(d, 1) : 0,
+              a2 = d >= 0 ? dir_component(d, 2) : 0;
+    // d < 0: the owned cells; else every local cell (a low ghost cell pairs with its owned +d neighbour)
+    const long long ncells = d < 0 ? g.n_owned_cells : g.ncell;
+    for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < ncells;
+         w += (long long)gridDim.x * blockDim.x) {
+        const long long cell = d < 0 ? (w / plane + g.ghost_x) * plane + (w % plane) : w;
+        if (cell_start[cell + 1] == cell_start[cell]) continue;
+        if (d < 0) {
+            pairs[atomicAdd(count, 1)] = make_int2((int)cell, (int)cell);
+            continue;
+        }
+        const int ixl = (int)(cell / plane), iy = (int)((cell / g.nz) % g.ny), iz = (int)(cell % g.nz);
+        const int colour = (sym_axis_colour(ixl, g.nxl, !g.ghost_x) * cy + sym_axis_colour(iy, g.ny, true)) *
+                               sym_axis_colours(g.nz, true) + sym_axis_colour(iz, g.nz, true);
+        (void)cx;
+        if (colour != col) continue;
+        const HomeCell hc = home_cell(g, cell);
+        int cj, sh[3];
+        if (!neighbour(g, hc, a0, a1, a2, cj, sh)) continue;
+        if (cell_start[cj + 1] == cell_start[cj]) continue;
+        if (!owned_cell(g, cell) && !owned_cell(g, cj)) continue;   // ghost-ghost: nothing to write
+        pairs[atomicAdd(count, 1)] = make_int2((int)cell, cj);
+    }
 }
 
 }  // namespace pvsph

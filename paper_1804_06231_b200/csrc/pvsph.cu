@@ -58,6 +58,10 @@ const DevAttrs &dev_attrs(int dev)
         cudaFuncSetAttribute(k_density_pair_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
         cudaFuncSetAttribute(k_density_pair_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
         cudaFuncSetAttribute(k_density_pair_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SYM_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SYM_SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.v4_blocks_per_sm, k_density_v4<false>, V4_TP, V4_SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.v5_blocks_per_sm, k_density_v5<false>, V5_TP, V5_SMEM);
         if (a.v4_blocks_per_sm < 1) a.v4_blocks_per_sm = 1;
@@ -604,6 +608,65 @@ int sph_density_all(const sph_grid *grid, const sph_cells *cells, sph_out *out, 
                                                                           gcount, gcount + 1, gen);
     if (out->n_out > 0)
         k_unpermute<<<grid_blocks(out->n_out, 256, 148 * 16), 256, 0, s>>>(dev_out(out), orec, gen);
+    return check_launch();
+}
+
+int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *out, sph_stats *stats, void *ws,
+                        size_t ws_bytes, void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (!cells_ok(cells) || !out_ok(out) || !ws) return SPH_EINVAL;
+    Ws w = ws_layout(g, cells->capacity);
+    if (ws_bytes < w.total) return SPH_EINVAL;
+    if ((rc = ensure_attrs()) != SPH_OK) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    const DevOut o = dev_out(out);
+    const size_t nb = 4 * (size_t)out->n_out;
+    for (float *a : {out->rho, out->rho_dh, out->wcount, out->wcount_dh, out->div_v})
+        if (nb && (e = cudaMemsetAsync(a, 0, nb, s)) != cudaSuccess) return cuda_fail(e);
+    if (nb && (e = cudaMemsetAsync(out->curl_v, 0, 3 * nb, s)) != cudaSuccess) return cuda_fail(e);
+    if (nb && (e = cudaMemsetAsync(out->nngb, 0, nb, s)) != cudaSuccess) return cuda_fail(e);
+    const DevCells dc = dev_cells(cells);
+    unsigned *status = at<unsigned>(ws, w.status);
+    // scratch: the phase's pair list in the build's record region, its count in big_count
+    int2 *pairs = at<int2>(ws, w.rec);
+    int *count = at<int>(ws, w.big_count);
+    if (sizeof(ParticleRec) * (size_t)(cells->capacity > 0 ? cells->capacity : 1) < 8 * (size_t)g.ncell)
+        return SPH_EINVAL;
+    const int gen_blocks = grid_blocks(g.n_owned_cells, 256, 148 * 8);
+    const long long maxp = g.ncell;
+    // self cells (every ordered pair i != j and the self term): one warp per cell, exclusive
+    if ((e = cudaMemsetAsync(count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+    k_sym_phase_pairs<<<gen_blocks, 256, 0, s>>>(g, dc.cell_start, -1, 0, pairs, count);
+    // (the self kernel takes a cell list: the first int of each (c, c) record is the cell)
+    {
+        const int blocks = grid_blocks(g.n_owned_cells, API_WARPS, 1 << 30);
+        if (stats)
+            k_density_self<true><<<blocks, API_WARPS * 32, 0, s>>>(g, dc, o, reinterpret_cast<const int *>(pairs),
+                                                                   -2, stats, status, count);
+        else
+            k_density_self<false><<<blocks, API_WARPS * 32, 0, s>>>(g, dc, o, reinterpret_cast<const int *>(pairs),
+                                                                    -2, nullptr, status, count);
+    }
+    // the 13 directions x colours: symmetric pairs, no atomics
+    const int ncol = sym_axis_colours(g.nxl, !g.ghost_x) * sym_axis_colours(g.ny, true) * sym_axis_colours(g.nz, true);
+    for (int d = 0; d < SPH_NDIR; ++d)
+        for (int col = 0; col < ncol; ++col) {
+            if ((e = cudaMemsetAsync(count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+            k_sym_phase_pairs<<<gen_blocks, 256, 0, s>>>(g, dc.cell_start, d, col, pairs, count);
+            const int blocks = 148 * 3;
+            if (stats)
+                k_density_pair_sym<true, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dc, o, pairs, maxp, stats,
+                                                                                       status, count);
+            else
+                k_density_pair_sym<false, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dc, o, pairs, maxp, nullptr,
+                                                                                        status, count);
+        }
+    if (out->n_out > 0)
+        k_finalize<<<grid_blocks(out->n_out, 256, 148 * 32), 256, 0, s>>>(o, out->n_out);
     return check_launch();
 }
 

@@ -213,11 +213,15 @@ def mask_dead_ghosts(recv_x, recv_v, recv_n, dead_row_x, dead_row_v, ar):
 class SlabRunner:
     """Device buffers and one density step of one rank."""
 
-    def __init__(self, slab: Slab, dist=None, device="cuda", ghost_capacity: int | None = None, levels=None):
+    def __init__(self, slab: Slab, dist=None, device="cuda", ghost_capacity: int | None = None, levels=None,
+                 engine: str = "gather"):
         """levels: [(nc, h_min, h_max)] level passes; the first level's nc
         must be the slab's grid, the others multiples of it (on x-slabs each level owns the
         same x range)."""
         self.slab = slab
+        self.engine = engine                     # "gather" (sph_density_all) or "sym" (sph_density_all_sym)
+        if engine == "sym" and levels and len(levels) > 1:
+            raise ValueError("the symmetric whole pass runs on a single grid (no level passes)")
         self.dist = dist
         self.world = slab.world
         self.rank = slab.rank
@@ -347,7 +351,8 @@ class SlabRunner:
         for g, c, ws in self.extra:
             pv.sph_sort_cells(g, c, ws)
         rec(3)
-        pv.sph_density_all(self.grid, self.cells, self.out, self.ws, stats=stats)
+        dens = pv.sph_density_all_sym if self.engine == "sym" else pv.sph_density_all
+        dens(self.grid, self.cells, self.out, self.ws, stats=stats)
         for g, c, ws in self.extra:
             pv.sph_density_all(g, c, self.out, ws, stats=stats)
         rec(4)
