@@ -142,7 +142,10 @@ typedef struct sph_grid {
  *   cell_dx[ncell]          per cell, the largest disp of its particles: the
  *                           paper's max_dx (0 after a build); sph_density_all
  *                           widens a window in neighbour cell c by 2*cell_dx[c]
- * n is written by sph_build_cells (stored particles).  16-byte alignment
+ * n is written by sph_build_cells: the inputs it was given (owned + ghosts), an
+ * upper bound of the stored particles; the exact stored count is
+ * cell_start[ncell] (rejected inputs, e.g. ghosts outside the ghost planes,
+ * get no slot).  16-byte alignment
  * is required for xyzh and vm. */
 typedef struct sph_cells {
     int64_t capacity;

@@ -252,10 +252,13 @@ __global__ void k_scatter_rec(DevGrid g, long long n_total, const int *__restric
 // disp bounds |x - x_build| by the triangle inequality); per cell the paper's max_dx = the
 // largest disp of its particles (cell_dx, atomic max on the float bits: all values >= 0);
 // *max_disp (optional) = the largest of all.
-__global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm, long long n, float dt,
-                        float *__restrict__ disp, const int *__restrict__ slot_cell, float *__restrict__ cell_dx,
-                        float *max_disp)
+// n_stored: cell_start[ncell] (rejected inputs -- e.g. dead ghost rows -- have no slot, so the
+// stored count can be below the build's n).
+__global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm, const int *__restrict__ n_stored,
+                        float dt, float *__restrict__ disp, const int *__restrict__ slot_cell,
+                        float *__restrict__ cell_dx, float *max_disp)
 {
+    const long long n = *n_stored;
     float mx = 0.0f;
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n;
          s += (long long)gridDim.x * blockDim.x) {
@@ -286,9 +289,11 @@ __global__ void k_drift(float4 *__restrict__ xyzh, const float4 *__restrict__ vm
 // sph_gather_positions: the stored (drifted) positions back in input order, each coordinate
 // wrapped into [0, L) (x < 0 -> x + L, x >= L -> x - L; a sum that rounds to L becomes 0):
 // the input of the next sph_build_cells when a reuse loop rebuilds.
-__global__ void k_gather_positions(const float4 *__restrict__ xyzh, const int *__restrict__ perm, long long n,
-                                   long long n_out, float bx, float by, float bz, float4 *__restrict__ out)
+__global__ void k_gather_positions(const float4 *__restrict__ xyzh, const int *__restrict__ perm,
+                                   const int *__restrict__ n_stored, long long n_out, float bx, float by, float bz,
+                                   float4 *__restrict__ out)
 {
+    const long long n = *n_stored;       // cell_start[ncell]: slots past it were never written
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n;
          s += (long long)gridDim.x * blockDim.x) {
         const int q = perm[s];

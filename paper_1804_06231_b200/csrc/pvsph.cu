@@ -472,8 +472,8 @@ int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp,
     if (!cells_ok(cells) || !std::isfinite(dt)) return SPH_EINVAL;
     if (cells->n <= 0) return SPH_OK;
     k_drift<<<grid_blocks(cells->n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
-        reinterpret_cast<float4 *>(cells->xyzh), reinterpret_cast<const float4 *>(cells->vm), cells->n, dt,
-        cells->disp, cells->slot_cell, cells->cell_dx, max_disp);
+        reinterpret_cast<float4 *>(cells->xyzh), reinterpret_cast<const float4 *>(cells->vm),
+        cells->cell_start + g.ncell, dt, cells->disp, cells->slot_cell, cells->cell_dx, max_disp);
     return check_launch();
 }
 
@@ -485,8 +485,8 @@ int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xy
     if (!cells_ok(cells) || n_out < 0 || (n_out > 0 && !xyzh_out) || ((uintptr_t)xyzh_out % 16)) return SPH_EINVAL;
     if (cells->n <= 0 || n_out == 0) return SPH_OK;
     k_gather_positions<<<grid_blocks(cells->n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
-        reinterpret_cast<const float4 *>(cells->xyzh), cells->perm, cells->n, n_out, g.boxf[0], g.boxf[1], g.boxf[2],
-        reinterpret_cast<float4 *>(xyzh_out));
+        reinterpret_cast<const float4 *>(cells->xyzh), cells->perm, cells->cell_start + g.ncell, n_out, g.boxf[0],
+        g.boxf[1], g.boxf[2], reinterpret_cast<float4 *>(xyzh_out));
     return check_launch();
 }
 

@@ -481,3 +481,235 @@ class FakeRanks:
                     res[k] = np.zeros(self.n_global, v.dtype)
                 res[k][r.slab.gid] = v
         return res
+
+
+# ---------------------------------------------------------------------------
+# list reuse on x-slabs: drift, stale cells, rebuild with migration
+# ---------------------------------------------------------------------------
+def exchange_arrays(dist, rank: int, world: int, send_lo: list, send_hi: list, recv_lo: list, recv_hi: list,
+                    n_lo: int, n_hi: int, dev) -> tuple[int, int]:
+    """Variable-size periodic-ring exchange of several arrays per direction (migration at a
+    rebuild; host-synchronised counts).  send_lo goes to the left neighbour, send_hi to the
+    right; recv_lo[k][:n] receives from the left, recv_hi from the right.  Same-peer issue
+    order as exchange_planes.  Returns the received counts."""
+    left, right = (rank - 1) % world, (rank + 1) % world
+    cnt_send = torch.tensor([n_hi, n_lo], dtype=torch.int64, device=dev)
+    cnt_recv = torch.zeros(2, dtype=torch.int64, device=dev)
+    ops = [dist.P2POp(dist.isend, cnt_send[0:1], right), dist.P2POp(dist.isend, cnt_send[1:2], left),
+           dist.P2POp(dist.irecv, cnt_recv[0:1], left), dist.P2POp(dist.irecv, cnt_recv[1:2], right)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+    r_lo, r_hi = (int(v) for v in cnt_recv.tolist())
+    if r_lo > recv_lo[0].shape[0] or r_hi > recv_hi[0].shape[0]:
+        raise RuntimeError(f"migration capacity {recv_lo[0].shape[0]} < {max(r_lo, r_hi)}")
+    ops = []
+    if n_hi:
+        ops += [dist.P2POp(dist.isend, a[:n_hi], right) for a in send_hi]
+    if n_lo:
+        ops += [dist.P2POp(dist.isend, a[:n_lo], left) for a in send_lo]
+    if r_lo:
+        ops += [dist.P2POp(dist.irecv, a[:r_lo], left) for a in recv_lo]
+    if r_hi:
+        ops += [dist.P2POp(dist.irecv, a[:r_hi], right) for a in recv_hi]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return r_lo, r_hi
+
+
+def split_migrants(x: torch.Tensor, nc: int, box: float, x_lo: int, x_hi: int):
+    """Masks of the owned particles (wrapped positions) whose x plane -- the binning rule of
+    sph_build_cells -- is the left neighbour's last plane (x_lo - 1) or the right neighbour's
+    first (x_hi), and of those that stay.  A particle moves at most one plane between rebuilds
+    (displacement < skin < C_l / 2)."""
+    pl = torch.clamp(torch.floor(x[:, 0].double() * nc / box), 0, nc - 1).long()
+    lo = pl == (x_lo - 1) % nc
+    hi = (pl == x_hi % nc) & ~lo
+    return lo, hi, ~(lo | hi)
+
+
+class SlabReuse(SlabRunner):
+    """List reuse on x-slabs ("re-sort/re-bin (and migrate between slabs)
+    only past a threshold").  Each rank drifts all its stored particles -- owned ones and
+    the ghost copies, with identical fp32 increments -- and runs the density pass on the stale
+    cells; before a drift could take a displacement past the skin every rank rebuilds at the same
+    step (the bound uses the GLOBAL max |v|): positions gathered back to input order and wrapped
+    (sph_gather_positions), particles that crossed a slab face migrate to the neighbour, the
+    owned set is re-merged in global-id order (so in-cell orders, and the outputs, stay bitwise
+    those of one GPU), the ghost planes are exchanged again and the cells rebuilt.
+
+    transport: "dist" (torch.distributed P2P) or a FakeReuse coordinator (device copies)."""
+
+    def __init__(self, slab: Slab, skin: float, vmax_global: float, dist=None, device="cuda", headroom=0.15):
+        self.own_cap = int((1 + headroom) * slab.n_own) + 4096
+        n0 = slab.n_own
+        # SlabRunner sizes everything from n_own: build it for the headroom capacity, then shrink
+        slab_cap = Slab(slab.nc, slab.box, slab.gamma, slab.rank, slab.world, slab.x_lo, slab.x_hi,
+                        np.zeros((self.own_cap, 4), np.float32), np.zeros((self.own_cap, 4), np.float32),
+                        np.zeros(self.own_cap, np.int64), slab.n_global, None, slab.ghost_n, slab.edge_n,
+                        int(1.1 * slab.block_max) if slab.block_max >= 0 else -1)
+        super().__init__(slab_cap, dist=dist, device=device)
+        self.slab = slab
+        self.n_own = n0
+        self.skin = float(skin)
+        self.grid = pv.make_grid(slab.nc, slab.box, slab.gamma, slab.x_lo, slab.x_hi, int(self.world > 1), skin=skin)
+        self.vmax = float(vmax_global)
+        self.gid = torch.zeros(self.own_cap, dtype=torch.int64, device=device)
+        self.bound = 0.0
+        self.rebuilds = 0
+        mcap = int(0.1 * self.own_cap) + 4096
+        self.mig = [[torch.zeros((mcap, 4), dtype=torch.float32, device=device),
+                     torch.zeros((mcap, 4), dtype=torch.float32, device=device),
+                     torch.zeros(mcap, dtype=torch.int64, device=device)] for _ in range(4)]   # send lo/hi, recv lo/hi
+        self.out_view = None
+
+    def upload(self) -> None:
+        n = self.n_own
+        self.xin[:n].copy_(torch.from_numpy(self.slab.xyzh))
+        self.vin[:n].copy_(torch.from_numpy(self.slab.vm))
+        self.gid[:n].copy_(torch.from_numpy(np.asarray(self.slab.gid, np.int64)))
+        self.out = pv.Out.alloc(n, self.device)
+
+    def outputs(self) -> "pv.Out":
+        """The current owned particles' outputs (a view with n_out = n_own; curl rows keep the
+        allocation stride, so the density call gets the full-size struct)."""
+        return self.out
+
+    def _build(self):
+        pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own,
+                           n_ghost=self.n_ghost)
+        pv.sph_sort_cells(self.grid, self.cells, self.ws)
+        self.bound = 0.0
+
+    def step_bound(self, dt: float) -> float:
+        return self.vmax * abs(dt) * (1.0 + 2.0 ** -20) + 3.0 ** 0.5 * 2.0 ** -24 * (self.slab.box + self.skin) * 1.01
+
+    # -- rebuild pieces (the transport supplies the exchanges) --------------------------------
+    def gather_owned(self) -> None:
+        """Current positions of the owned particles back to their (input = gid) order, wrapped."""
+        pv.sph_gather_positions(self.grid, self.cells, self.xin, self.n_own)
+
+    def pack_migrants(self):
+        """Split the owned set: migrants to the left / right into the send buffers; returns
+        (n_lo, n_hi, keep_mask)."""
+        n = self.n_own
+        lo, hi, keep = split_migrants(self.xin[:n], self.slab.nc, self.slab.box, self.slab.x_lo, self.slab.x_hi)
+        out = []
+        for k, m in enumerate((lo, hi)):
+            idx = torch.nonzero(m).squeeze(1)
+            c = int(idx.numel())
+            if c > self.mig[k][0].shape[0]:
+                raise RuntimeError(f"migration buffer {self.mig[k][0].shape[0]} < {c}")
+            self.mig[k][0][:c].copy_(self.xin[:n][idx])
+            self.mig[k][1][:c].copy_(self.vin[:n][idx])
+            self.mig[k][2][:c].copy_(self.gid[:n][idx])
+            out.append(c)
+        return out[0], out[1], keep
+
+    def merge_owned(self, keep, r_lo: int, r_hi: int) -> None:
+        """The kept particles plus the received migrants, in ascending global id."""
+        n = self.n_own
+        kx, kv, kg = self.xin[:n][keep], self.vin[:n][keep], self.gid[:n][keep]
+        x = torch.cat([kx, self.mig[2][0][:r_lo], self.mig[3][0][:r_hi]])
+        v = torch.cat([kv, self.mig[2][1][:r_lo], self.mig[3][1][:r_hi]])
+        g = torch.cat([kg, self.mig[2][2][:r_lo], self.mig[3][2][:r_hi]])
+        order = torch.argsort(g)
+        m = int(g.numel())
+        if m > self.own_cap:
+            raise RuntimeError(f"owned capacity {self.own_cap} < {m}")
+        self.xin[:m].copy_(x[order])
+        self.vin[:m].copy_(v[order])
+        self.gid[:m].copy_(g[order])
+        self.n_own = m
+        self.out = pv.Out.alloc(m, self.device)      # outputs of the new owned set
+
+    def rebuild_local(self):
+        """After the (ghost) exchange: dead rows past the counts, then build and sort."""
+        self._build()
+        self.rebuilds += 1
+
+
+class ReuseTransport:
+    """Drives SlabReuse ranks through their exchanges: torch.distributed P2P for one rank per
+    process (`dist`), or all ranks in one process with device copies (fake ranks, tests)."""
+
+    def __init__(self, runners: list, dist=None):
+        self.r = runners
+        self.dist = dist
+
+    def _ghosts(self):
+        if self.dist is not None:
+            for rr in self.r:
+                rr.exchange()
+            return
+        W = len(self.r)
+        for rr in self.r:
+            rr.select()
+        for k, rr in enumerate(self.r):
+            rx, rv = rr.ghost_blocks()
+            left, right = self.r[(k - 1) % W], self.r[(k + 1) % W]
+            rx[0].copy_(left.sel_x[1])
+            rv[0].copy_(left.sel_v[1])
+            rx[1].copy_(right.sel_x[0])
+            rv[1].copy_(right.sel_v[0])
+            rr.recv_n[0].copy_(left.sel_n[1])
+            rr.recv_n[1].copy_(right.sel_n[0])
+            mask_dead_ghosts(rx, rv, rr.recv_n, rr.dead_x, rr.dead_v, rr.ar)
+
+    def _migrate(self):
+        packs = [rr.pack_migrants() for rr in self.r]
+        if self.dist is not None:
+            for rr, (n_lo, n_hi, keep) in zip(self.r, packs):
+                r_lo, r_hi = exchange_arrays(self.dist, rr.rank, rr.world, rr.mig[0], rr.mig[1], rr.mig[2],
+                                             rr.mig[3], n_lo, n_hi, rr.xin.device)
+                rr.merge_owned(keep, r_lo, r_hi)
+            return
+        W = len(self.r)
+        recv = []
+        for k, rr in enumerate(self.r):
+            left, right = self.r[(k - 1) % W], self.r[(k + 1) % W]
+            r_lo = packs[(k - 1) % W][1]            # the left neighbour's particles moving right
+            r_hi = packs[(k + 1) % W][0]            # the right neighbour's moving left
+            for a in range(3):
+                rr.mig[2][a][:r_lo].copy_(left.mig[1][a][:r_lo])
+                rr.mig[3][a][:r_hi].copy_(right.mig[0][a][:r_hi])
+            recv.append((r_lo, r_hi))
+        for rr, (n_lo, n_hi, keep), (r_lo, r_hi) in zip(self.r, packs, recv):
+            rr.merge_owned(keep, r_lo, r_hi)
+
+    def start(self):
+        for rr in self.r:
+            rr.upload()
+        self._ghosts()
+        for rr in self.r:
+            rr._build()
+
+    def step(self, dt: float, stats=None):
+        """One reuse step on every rank: rebuild (gather, migrate, ghosts, build, sort) first if
+        the displacement bound would pass the skin, then drift + density."""
+        rr0 = self.r[0]
+        inc = rr0.step_bound(dt)
+        if inc > rr0.skin:
+            raise ValueError("one drift exceeds the skin")
+        if rr0.bound + inc > rr0.skin:
+            for rr in self.r:
+                rr.gather_owned()
+            self._migrate()
+            self._ghosts()
+            for rr in self.r:
+                rr.rebuild_local()
+        for rr in self.r:
+            pv.sph_drift(rr.grid, rr.cells, dt)
+            rr.bound += inc
+            pv.sph_density_all(rr.grid, rr.cells, rr.out, rr.ws, stats=stats)
+
+    def gather(self, n_global: int) -> dict:
+        res = {}
+        for rr in self.r:
+            o = rr.out.to_numpy()
+            g = rr.gid[:rr.n_own].cpu().numpy()
+            for k, v in o.items():
+                if k not in res:
+                    res[k] = np.zeros(n_global, v.dtype)
+                res[k][g] = v
+        return res

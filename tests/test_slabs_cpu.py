@@ -196,3 +196,64 @@ def test_block_capacity_same_on_every_rank():
         slabs = [Slab.from_set(p, r, 3, bounds) for r in range(3)]
         assert len({s.block_max for s in slabs}) == 1
         assert all(s.block_max >= max((pl == s.x_lo).sum(), (pl == s.x_hi - 1).sum()) for s in slabs)
+
+
+def _worker_mig(rank, world, port, sizes, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1804_06231_b200.slabs import exchange_arrays
+    cap = 16
+
+    def arrs(r, which):
+        n = sizes[r][which]
+        x = torch.zeros((cap, 4))
+        x[:n, 0] = r
+        x[:n, 1] = which
+        x[:n, 2] = torch.arange(n, dtype=torch.float32)
+        g = torch.zeros(cap, dtype=torch.int64)
+        g[:n] = 1000 * r + 100 * which + torch.arange(n)
+        return [x, x + 7.0, g]
+
+    s_lo, s_hi = arrs(rank, 0), arrs(rank, 1)
+    r_lo = [torch.zeros((cap, 4)), torch.zeros((cap, 4)), torch.zeros(cap, dtype=torch.int64)]
+    r_hi = [torch.zeros((cap, 4)), torch.zeros((cap, 4)), torch.zeros(cap, dtype=torch.int64)]
+    n_rlo, n_rhi = exchange_arrays(dist, rank, world, s_lo, s_hi, r_lo, r_hi, sizes[rank][0], sizes[rank][1],
+                                   torch.device("cpu"))
+    left, right = (rank - 1) % world, (rank + 1) % world
+    ok = (n_rlo, n_rhi) == (sizes[left][1], sizes[right][0])
+    for got, (src, which), n in ((r_lo, (left, 1), n_rlo), (r_hi, (right, 0), n_rhi)):
+        exp = arrs(src, which)
+        ok = ok and all(torch.equal(a[:n], b[:n]) for a, b in zip(got, exp))
+    q.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,sizes", [(2, [(3, 5), (4, 0)]), (3, [(1, 2), (0, 4), (5, 6)])])
+def test_migration_exchange_gloo(world, sizes):
+    """Migration at a reuse rebuild (slabs.SlabReuse): variable-size exchange of positions,
+    (v, m) and global ids with both neighbours."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_mig, args=(r, world, port, sizes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
+
+
+def test_split_migrants_rule():
+    """A particle leaves its slab iff its x plane (the binning rule) is the neighbour's boundary
+    plane; periodic wrap for the first and last slabs."""
+    from paper_1804_06231_b200.slabs import split_migrants
+    nc = 10
+    x = torch.tensor([[0.05, 0, 0, 0], [0.15, 0, 0, 0], [0.35, 0, 0, 0], [0.45, 0, 0, 0], [0.95, 0, 0, 0]])
+    lo, hi, keep = split_migrants(x, nc, 1.0, 2, 4)        # slab planes [2, 4)
+    assert lo.tolist() == [False, True, False, False, False]
+    assert hi.tolist() == [False, False, False, True, False]
+    lo, hi, keep = split_migrants(x, nc, 1.0, 0, 4)        # first slab: the left neighbour owns plane 9
+    assert lo.tolist() == [False, False, False, False, True] and hi.tolist()[3]
