@@ -147,17 +147,21 @@ def main():
     inter_all = sum(res[k]["interactions_per_cell"] if k == "self" else 0 for k in res) * ncell
     inter_all += sum(res[k]["interactions_per_symmetric_pair"] * ncell * {"face": 3, "edge": 6, "corner": 4}[k]
                      for k in ("face", "edge", "corner"))
-    # Table 2 analogue: full-mask interactions (sph_calibrate mode 2: 256 per thread per iteration)
+    # Table 2 analogue: full-mask interactions (sph_calibrate mode 3: the production packed body
+    # interact2 of density_v5.cuh, 256 per thread per iteration; mode 2 = the scalar reference body)
     import ctypes
     from paper_1804_06231_b200 import _lib
     L = _lib.load()
     sm = torch.cuda.get_device_properties(0).multi_processor_count
     blocks, threads, iters = sm * 8, 256, 40
     buf = torch.zeros(1, device="cuda")
-    call = lambda: L.sph_calibrate(2, blocks, threads, iters, ctypes.c_void_p(buf.data_ptr()),   # noqa: E731
+    call = lambda: L.sph_calibrate(3, blocks, threads, iters, ctypes.c_void_p(buf.data_ptr()),   # noqa: E731
                                    ctypes.c_void_p(s.cuda_stream))
     ms_raw = timed(call)
     raw_rate = 256 * iters * blocks * threads / (ms_raw * 1e-3)
+    call2 = lambda: L.sph_calibrate(2, blocks, threads, iters, ctypes.c_void_p(buf.data_ptr()),   # noqa: E731
+                                    ctypes.c_void_p(s.cuda_stream))
+    raw_rate_scalar = 256 * iters * blocks * threads / (timed(call2) * 1e-3)
     line = {"benchmark": "test27cells (batched, P:195)", "n_particles": p.n, "cells": ncell,
             "per_cell": args.per_cell, "gamma_h_over_cl": float(synth.GAMMA * p.xyzh[0, 3] * args.nc),
             "dtype": "f32", "data": "synthetic", "reps": args.reps, "warmup": args.warmup,
@@ -169,6 +173,8 @@ def main():
             "density_all_ms": ms_all, "density_all_us_per_cell": 1e3 * ms_all / ncell,
             "density_all_interactions_per_s": inter_all / (ms_all * 1e-3),
             "raw_fullmask_interactions_per_s": raw_rate,
+            "raw_fullmask_body": "interact2 (density_v5.cuh, FFMA2 pairs: the production body)",
+            "raw_fullmask_interactions_per_s_scalar_body": raw_rate_scalar,
             "raw_us_per_2560_interactions": 2560 / raw_rate * 1e6,
             "paper_avx_raw_ms_per_2560": 0.0084,
             "pipeline_fraction_of_raw": inter_all / (ms_all * 1e-3) / raw_rate}

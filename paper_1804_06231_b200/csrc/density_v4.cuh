@@ -46,16 +46,23 @@
 
 namespace pvsph {
 
-constexpr int V4_WARPS = 8;
+// tile geometry (overridable at compile time for experiments: -DTILE_WARPS=4 ...)
+#ifndef TILE_WARPS
+#define TILE_WARPS 8
+#define TILE_MAXZ 21
+#define TILE_MS 2400
+#define TILE_ML 8192
+#endif
+constexpr int V4_WARPS = TILE_WARPS;
 constexpr int V4_CTAS = 2;               // resident CTAs per SM (launch bounds; smem below fits 2)
 constexpr int V4_TP = V4_WARPS * 32;     // home particles per tile: exactly V4_TP except where a limit cuts
 constexpr int V4_Q = 24;                 // hit stack depth per lane, 2-byte entries
 constexpr int V4_ROWS = 12;              // staged rows: ox in -1..1, oy in -1..2 (relative to the tile's first row)
-constexpr int V4_MAXZ = 21;              // staged cells per row (tiles span <= 19 slices)
+constexpr int V4_MAXZ = TILE_MAXZ;       // staged cells per row (tiles span <= 19 slices)
 constexpr int V4_MAXCELLS = V4_ROWS * V4_MAXZ;
 constexpr int V4_MAXH = 2 * (V4_MAXZ - 2);   // home cells per tile
-constexpr int V4_MS = 2400;              // staged particles (< 4096: 12-bit queue entries)
-constexpr int V4_ML = 8192;              // staged list entries (27 segments per home cell)
+constexpr int V4_MS = TILE_MS;           // staged particles (< 4096: 12-bit queue entries)
+constexpr int V4_ML = TILE_ML;           // staged list entries (27 segments per home cell)
 constexpr int V4_HOFF = (V4_MAXH + 4 + 3) / 4 * 4;      // ints, keeps the following arrays 16-byte aligned
 constexpr size_t V4_SMEM = (size_t)V4_MS * 32 + (size_t)V4_MAXCELLS * 16 + (size_t)V4_ML * 2 + (size_t)V4_HOFF * 4 +
                            (size_t)V4_WARPS * V4_Q * 32 * 2 + (size_t)V4_MAXZ * 16;

@@ -44,6 +44,9 @@ def main():
     t = timed(2, blocks, threads, it)
     res["fullmask_interactions_per_s"] = 256 * it * blocks * threads / t
     res["fullmask_tflops_48"] = res["fullmask_interactions_per_s"] * 48 / 1e12
+    t = timed(3, blocks, threads, it)                    # the production packed body (interact2)
+    res["fullmask_packed_interactions_per_s"] = 256 * it * blocks * threads / t
+    res["fullmask_packed_tflops_48"] = res["fullmask_packed_interactions_per_s"] * 48 / 1e12
     print(json.dumps(res))
 
 
