@@ -52,8 +52,8 @@ const DevAttrs &dev_attrs(int dev)
         cudaFuncSetAttribute(k_density_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
         cudaFuncSetAttribute(k_density_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
         cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
-        cudaFuncSetAttribute(k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_HUGE_MAX * 8);
+        cudaFuncSetAttribute(k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T));
         cudaFuncSetAttribute(k_density_pair_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
         cudaFuncSetAttribute(k_density_pair_staged<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
         cudaFuncSetAttribute(k_density_pair_sym<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
@@ -390,9 +390,9 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     k_sort_warp256<<<148 * 4, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, w256_items, huge_count + 3, need);
     k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count, need);
     if ((rc = ensure_attrs()) != SPH_OK) return rc;
-    k_sort_bitonic<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, SORT_MED_MAX * 8, s>>>(
+    k_sort_radix<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, radix_smem(SORT_MED_MAX, SORT_MED_T), s>>>(
         g, c, cells->order, huge_items, huge_count, (int)w.huge_cap, need);
-    k_sort_bitonic<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, SORT_HUGE_MAX * 8, s>>>(
+    k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T), s>>>(
         g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap, need);
     return check_launch();
 }

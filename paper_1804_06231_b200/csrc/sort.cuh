@@ -11,7 +11,7 @@
 // 32-bit composites (quantised fp32 key, in-cell index) ranked by counting.
 // Cells of up to SORT_MED = 128: k_sort_mid, one warp per cell, same composites.
 // Cells of up to SORT_W256 = 256: k_sort_warp256, a register bitonic sort per warp.
-// Medium/huge cells: bitonic sorts in shared memory (k_sort_bitonic).  Cells above
+// Medium/huge cells: stable LSD radix sorts in shared memory (k_sort_radix).  Cells above
 // SORT_HUGE_MAX are queued as (cell, chunk) items and ranked by k_sort_big, one
 // CTA per chunk of SORT_BIG_CHUNK elements, streaming the cell's 64-bit
 // composites (orderable fp32 key << 32 | input index) through shared memory.
@@ -25,10 +25,16 @@ namespace pvsph {
 constexpr int SORT_SMALL = 32;
 constexpr int SORT_MED = 128;           // cells above: bitonic sorts (k_sort_warp256, k_sort_bitonic)
 constexpr int SORT_W256 = 256;          //   up to here: one warp per cell, in registers (k_sort_warp256)
-constexpr int SORT_MED_MAX = 2048;      //   medium tier: 256 threads, 16 KB shared memory
-constexpr int SORT_MED_T = 256;
-constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 1024 threads, 128 KB; above it chunked ranking again
-constexpr int SORT_HUGE_T = 512;
+constexpr int SORT_MED_MAX = 2048;      //   medium tier (k_sort_radix): 128 threads, 33 KB shared memory
+#ifndef SORT_MED_THREADS
+#define SORT_MED_THREADS 128
+#endif
+constexpr int SORT_MED_T = SORT_MED_THREADS;
+constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 512 threads, 225 KB; above it chunked ranking again
+#ifndef SORT_HUGE_THREADS
+#define SORT_HUGE_THREADS 512
+#endif
+constexpr int SORT_HUGE_T = SORT_HUGE_THREADS;
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_BIG_CHUNK = 256;
 constexpr int SORT_BIG_TILE = 2048;
@@ -110,7 +116,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             continue;
         }
         if (n > SORT_MED && n <= SORT_HUGE_MAX) {
-            // medium cells from the front of the list, huge ones from the back (k_sort_bitonic)
+            // medium cells from the front of the list, huge ones from the back (k_sort_radix)
             if (lane == 0) {
                 if (n <= SORT_MED_MAX) huge_items[atomicAdd(&huge_count[0], 1)] = (int)cell;
                 else huge_items[huge_cap - 1 - atomicAdd(&huge_count[1], 1)] = (int)cell;
@@ -231,6 +237,148 @@ __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint1
             }
             bt_cta_merge<T>(hs, P, lane, w);
             for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
+            __syncthreads();
+        }
+    }
+}
+
+// One CTA per cell of SORT_W256 < n <= MAXN particles: for each direction a stable LSD radix
+// sort in shared memory.  The key is the fp64-projected fp32 key (pv_key) quantised to 24 bits
+// over the cell's key range [-sqrt(3) C_max, +sqrt(3) C_max] (quantum 2 sqrt(3) C_max / 2^24,
+// ~2e-7 C_l: the disorder the density sweeps tolerate, DESIGN.md §4.2 R5, as the 25-bit keys
+// of k_sort_small); equal keys keep the in-cell (input) order.  Three 8-bit passes.  Warp w
+// owns the contiguous segment [w S, (w+1) S) of the current buffer; the counters are per
+// (digit, warp), so one exclusive scan gives every warp its output offset per digit; the warp
+// walks its segment 32 elements at a time, ranking each lane among its digit peers
+// (__match_any_sync; RU batches in flight), so the scatter is stable.  The counters of the
+// next pass are filled during this pass's scatter (the destination's segment is known there)
+// and those of the first pass while the keys are computed: one sweep per pass.  Shared
+// memory: keys and indices double-buffered (12 B per element) plus 2 x 256 x NW counters.
+constexpr int radix_smem(int maxn, int t) { return maxn * 12 + 2 * 256 * (t / 32) * 4 + 64 * 4; }
+
+template <int T>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, int lane, int w)
+{
+    constexpr int NW = T / 32;
+    unsigned x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        unsigned s = lane < NW ? wsum[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < NW) wsum[32 + lane] = s - wsum[lane];      // exclusive warp offsets
+    }
+    __syncthreads();
+    return wsum[32 + w] + x - v;
+}
+
+template <int MAXN, int T, bool FROM_BACK>
+__global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_t *ord, const int *items,
+                                                 const int *count, int cap, const int *__restrict__ need)
+{
+    constexpr int NW = T / 32;
+    constexpr int NH = 256 * NW;                       // counters, [digit][warp]
+    constexpr int HPT = NH / T;                        // per thread in the scan
+    constexpr int RU = 4;                              // batches of 32 in flight per warp
+    static_assert(NH % T == 0, "radix: 256 x warps must be a multiple of the threads");
+    extern __shared__ unsigned rs[];
+    unsigned *keyA = rs, *keyB = rs + MAXN;
+    uint16_t *idxA = reinterpret_cast<uint16_t *>(rs + 2 * MAXN), *idxB = idxA + MAXN;
+    unsigned *histA = rs + 3 * MAXN, *histB = histA + NH;   // after the two u16 index arrays
+    unsigned *wsum = histB + NH;                       // [0, 32) warp totals, [32, 64) offsets
+    const int nitems = *count;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
+    const float scale = 16777216.0f / (2.0f * cmax);   // 2^24 over the key range
+    const float cmax_s = cmax * scale;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const long long cell = items[FROM_BACK ? cap - 1 - it : it];
+        const int s0 = c.cell_start[cell];
+        const int n = c.cell_start[cell + 1] - s0;
+        const int S = (n + NW - 1) / NW;
+        const float invS = 1.0f / (float)S;            // segment of slot e: floor((e + 0.5) / S), exact here
+        const int lo = min(n, w * S), hi = min(n, lo + S);
+        double corner[3];
+        cell_corner(g, cell, corner);
+        const int mask = need ? need[cell] : 0x1fff;
+        for (int d = 0; d < SPH_NDIR; ++d) {
+            if (!((mask >> d) & 1)) continue;          // CTA-uniform
+#pragma unroll
+            for (int q = 0; q < HPT; ++q) histA[threadIdx.x * HPT + q] = 0u;
+            __syncthreads();
+            for (int e = threadIdx.x; e < n; e += T) {
+                const float4 p = c.xyzh[s0 + e];
+                const float key = pv_key((double)p.x - corner[0], (double)p.y - corner[1],
+                                         (double)p.z - corner[2], d);
+                const unsigned k = (unsigned)min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 16777215);
+                keyA[e] = k;
+                idxA[e] = (uint16_t)e;
+                atomicAdd(&histA[(k & 255u) * NW + (int)(((float)e + 0.5f) * invS)], 1u);
+            }
+            unsigned *ks = keyA, *kd = keyB, *hc = histA, *hn = histB;
+            uint16_t *is = idxA, *id = idxB;
+#pragma unroll 1
+            for (int shift = 0; shift < 24; shift += 8) {
+                const bool more = shift < 16;
+                __syncthreads();                        // counters of this pass complete, last scatter done
+                unsigned loc[HPT], sum = 0u;
+#pragma unroll
+                for (int q = 0; q < HPT; ++q) { loc[q] = hc[threadIdx.x * HPT + q]; sum += loc[q]; }
+                unsigned run = block_excl_scan<T>(sum, wsum, lane, w);
+#pragma unroll
+                for (int q = 0; q < HPT; ++q) {
+                    hc[threadIdx.x * HPT + q] = run;
+                    run += loc[q];
+                    if (more) hn[threadIdx.x * HPT + q] = 0u;   // the last pass's offsets, free now
+                }
+                __syncthreads();
+                for (int b = lo; b < hi; b += 32 * RU) {
+                    unsigned k[RU], dg[RU], peers[RU];
+                    uint16_t ix[RU];
+#pragma unroll
+                    for (int u = 0; u < RU; ++u) {
+                        const int i = b + 32 * u + lane;
+                        k[u] = i < hi ? ks[i] : 0u;
+                        ix[u] = i < hi ? is[i] : (uint16_t)0;
+                        dg[u] = i < hi ? (k[u] >> shift) & 255u : 256u;   // 256: past the segment
+                    }
+#pragma unroll
+                    for (int u = 0; u < RU; ++u) peers[u] = __match_any_sync(0xffffffffu, dg[u]);
+#pragma unroll
+                    for (int u = 0; u < RU; ++u) {
+                        // batches in order: each reads its digit's running offset, scatters, and
+                        // the digit's lowest lane advances the offset before the next batch reads
+                        const unsigned r = __popc(peers[u] & lt_mask);
+                        const unsigned hx = min(dg[u], 255u) * NW + w;
+                        const unsigned base = hc[hx];
+                        if (dg[u] < 256u) {
+                            const unsigned pos = base + r;
+                            kd[pos] = k[u];
+                            id[pos] = ix[u];
+                            if (more)
+                                atomicAdd(&hn[((k[u] >> (shift + 8)) & 255u) * NW + (int)(((float)pos + 0.5f) * invS)], 1u);
+                        }
+                        __syncwarp();
+                        if (dg[u] < 256u && r == 0) hc[hx] = base + __popc(peers[u]);
+                        __syncwarp();
+                    }
+                }
+                unsigned *tk = ks; ks = kd; kd = tk;
+                uint16_t *ti = is; is = id; id = ti;
+                unsigned *th = hc; hc = hn; hn = th;
+            }
+            __syncthreads();
+            for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = is[k];
             __syncthreads();
         }
     }

@@ -313,19 +313,24 @@ def test_cell_occupancy_tile_boundaries(pv, occ):
     compare(run(pv, xyzh, vm, nc), oracle.bruteforce(xyzh, vm), None, f"occ{occ}")
 
 
-@pytest.mark.parametrize("occ", [33, 200, 1025, 2000, 16384, 16385])
-def test_sort_big_cells(pv, occ):
-    """Sorted lists of one dense cell on every sort path: chunked ranking (~35), shared-memory
-    bitonic sort (~1025 .. ~16384), chunked ranking again above it (16385 + background).  Each list is a
-    permutation of the cell, ascending in the oracle's fp64 projection (fp32 rounding allowed),
-    equal fp32 keys in input order."""
-    rng = np.random.default_rng(occ)
+@pytest.mark.parametrize("occ,qbits", [(33, 24), (200, 24), (300, 24), (1025, 24), (2000, 24), (2000, 5),
+                                       (5000, 24), (12000, 4), (16300, 24), (16385, 24)])
+def test_sort_big_cells(pv, occ, qbits):
+    """Sorted lists of one dense cell on every sort path: warp ranking (~35), warp bitonic
+    (~200), shared-memory radix sort (~300 .. ~16300), chunked ranking above it (16385 +
+    background).  Each list is a permutation of the cell, ascending in the oracle's fp64
+    projection (fp32 rounding allowed), equal fp32 keys in input order; qbits < 24 puts the
+    particles on a coarse lattice, so most keys are shared (the stability of the radix passes)."""
+    rng = np.random.default_rng(occ + qbits)
     nc = 3
     Cl = 1.0 / nc
     n_bg = 20
     xyzh = np.zeros((n_bg + occ, 4), np.float32)
     xyzh[:n_bg, :3] = rng.integers(0, 2 ** 24, size=(n_bg, 3)) / 2 ** 24
-    xyzh[n_bg:, :3] = np.floor((1 + rng.random((occ, 3))) * Cl * 2 ** 24) / 2 ** 24   # all in cell (1,1,1)
+    u = rng.random((occ, 3))
+    if qbits < 24:
+        u = (np.floor(u * 2 ** qbits) + 0.5) / 2 ** qbits
+    xyzh[n_bg:, :3] = np.floor((1 + u) * Cl * 2 ** 24) / 2 ** 24   # all in cell (1,1,1)
     xyzh[:, 3] = 0.5 * Cl / synth.GAMMA
     vm = np.zeros_like(xyzh)
     vm[:, 3] = 1.0 / (n_bg + occ)
