@@ -228,12 +228,42 @@ constexpr int SYM_WARPS = 4;
 constexpr int SYM_MAXN = 512;            // staged particles per cell (3 CTAs per SM)
 constexpr int SYM_Q = 16;
 constexpr int SYM_JCAP = 32;             // bucket entries per j
-constexpr size_t SYM_SMEM = (size_t)SYM_MAXN * 16 * 4 + (size_t)SYM_MAXN * 4 * 2 + (size_t)SYM_MAXN * 2 +
-                            (size_t)SYM_WARPS * SYM_Q * 32 * 2 + (size_t)SYM_MAXN * SYM_JCAP * 2;
+// shared memory of one team (TW warps working on one pair at a time, MAXN staged per cell)
+__host__ __device__ constexpr size_t sym_team_smem(int maxn, int tw)
+{
+    return (size_t)maxn * 16 * 4 + (size_t)maxn * 4 * 2 + (size_t)maxn * 2 + (size_t)tw * SYM_Q * 32 * 2 +
+           (size_t)maxn * SYM_JCAP * 2;
+}
+constexpr size_t SYM_SMEM = sym_team_smem(SYM_MAXN, SYM_WARPS);
+// sph_density_all_sym's colour phases: one warp per pair of cells of <= SYMW_MAXN particles
+// (16 pairs in flight per SM instead of three CTAs); larger pairs are deferred to the CTA form
+constexpr int SYMW_MAXN = 64;
+constexpr int SYMW_WARPS = 8;
+constexpr size_t SYMW_SMEM = sym_team_smem(SYMW_MAXN, 1) * SYMW_WARPS;
+static_assert(sym_team_smem(SYMW_MAXN, 1) % 16 == 0, "team slices must stay 16-byte aligned");
+
+// Per-slot accumulators of sph_density_all_sym (the ws output-record region, cell-sorted slot
+// order): a cell's particles are contiguous, so a pair's read-modify-writes are coalesced
+// 32-byte sectors instead of nine scattered words per particle; k_sym_merge adds them to the
+// outputs (input order) once at the end.
+struct alignas(32) SlotAcc {
+    float4 a, b;                 // rho, wcount, rho_dh, wcount_dh | rho div v, rho curl v
+    int nngb, pad[7];
+};
+
+__device__ __forceinline__ void slot_out(SlotAcc *acc, const Final &f, int nngb)
+{
+    float4 a = acc->a, b = acc->b;
+    a.x += f.rho; a.y += f.wc; a.z += f.rho_dh; a.w += f.wc_dh;
+    b.x += f.div; b.y += f.cx; b.z += f.cy; b.w += f.cz;
+    acc->a = a;
+    acc->b = b;
+    acc->nngb += nngb;
+}
 
 template <bool PLAIN>
-__device__ __forceinline__ void sym_flush(const DevGrid &g, const DevOut &o, int out, float Hinv, const Acc2 &B,
-                                          int nn)
+__device__ __forceinline__ void sym_flush(const DevGrid &g, const DevOut &o, SlotAcc *sacc, int slot, int out,
+                                          float Hinv, const Acc2 &B, int nn)
 {
     const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv, gf = K3 * Hinv;
     Final f;
@@ -245,49 +275,66 @@ __device__ __forceinline__ void sym_flush(const DevGrid &g, const DevOut &o, int
     f.cx = gf * (sum2(B.Px) - sum2(B.Nx));         // rho * curl v
     f.cy = gf * (sum2(B.Py) - sum2(B.Ny));
     f.cz = gf * (sum2(B.Pz) - sum2(B.Nz));
-    if (PLAIN) plain_out(o, out, f, nn);
+    if (PLAIN && sacc) slot_out(sacc + slot, f, nn);
+    else if (PLAIN) plain_out(o, out, f, nn);
     else atomic_out(o, out, f, nn);
 }
 
 // PLAIN (sph_density_all_sym's colour phases): no two pairs of a launch share a cell, so the
 // outputs take plain read-modify-writes, and each j sums its bucket in ascending i (the buckets
 // are sorted first): deterministic.  npairs_dev (optional): the device-side pair count.
-template <bool COUNT, bool PLAIN = false>
-__global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, DevCells c, DevOut o,
-                                                                     const int2 *pairs, long long npairs,
-                                                                     sph_stats *st, unsigned *status,
-                                                                     const int *npairs_dev = nullptr)
+// Teams: the CTA's NWARPS warps form NWARPS / TW teams of TW warps, each with its own shared-
+// memory slice and mbarrier, each working on its own pair (TW = 1: a warp per pair, warp
+// syncs only).  A pair with a cell above MAXN goes to big_pairs (when given: the caller runs
+// it through the CTA form afterwards), else to the per-thread global-memory sweeps.
+template <int TW, int NWARPS>
+__device__ __forceinline__ void team_sync(int team)
 {
+    if constexpr (TW == 1) __syncwarp();
+    else if constexpr (TW == NWARPS) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TW * 32) : "memory");
+}
+
+template <bool COUNT, bool PLAIN = false, int MAXN = SYM_MAXN, int TW = SYM_WARPS, int NWARPS = SYM_WARPS>
+__global__ void __launch_bounds__(NWARPS * 32) k_density_pair_sym(DevGrid g, DevCells c, DevOut o,
+                                                                  const int2 *pairs, long long npairs,
+                                                                  sph_stats *st, unsigned *status,
+                                                                  const int *npairs_dev = nullptr,
+                                                                  int2 *big_pairs = nullptr, int *big_count = nullptr,
+                                                                  SlotAcc *sacc = nullptr)
+{
+    constexpr int NTEAM = NWARPS / TW, TT = TW * 32;
+    static_assert(NWARPS % TW == 0, "teams must tile the CTA");
     extern __shared__ __align__(16) unsigned char sym_smem[];
-    float4 *Pi = reinterpret_cast<float4 *>(sym_smem);             // ci positions (home shift applied)
-    float4 *Vi = Pi + SYM_MAXN;                                      // ci (v, m)
-    float4 *Pj = Vi + SYM_MAXN;                                      // cj positions (pre-shifted), w = H_j^2
-    float4 *Vj = Pj + SYM_MAXN;                                      // cj (v, m)
-    float *HinvJ = reinterpret_cast<float *>(Vj + SYM_MAXN);         // 1 / H_j
-    int *JC = reinterpret_cast<int *>(HinvJ + SYM_MAXN);             // bucket fill of each j
-    uint16_t *Lj = reinterpret_cast<uint16_t *>(JC + SYM_MAXN);      // cj sorted along d
-    uint16_t *stacks = Lj + SYM_MAXN;
-    uint16_t *JB = stacks + SYM_WARPS * SYM_Q * 32;                  // [SYM_MAXN][SYM_JCAP] i of j's hits
-    __shared__ __align__(8) unsigned long long s_mbar;
-    const unsigned mbar = smem_addr(&s_mbar);
+    const int team = threadIdx.x / TT, tt = threadIdx.x % TT;
+    float4 *Pi = reinterpret_cast<float4 *>(sym_smem + sym_team_smem(MAXN, TW) * team);   // ci positions (home shift applied)
+    float4 *Vi = Pi + MAXN;                                          // ci (v, m)
+    float4 *Pj = Vi + MAXN;                                          // cj positions (pre-shifted), w = H_j^2
+    float4 *Vj = Pj + MAXN;                                          // cj (v, m)
+    float *HinvJ = reinterpret_cast<float *>(Vj + MAXN);             // 1 / H_j
+    int *JC = reinterpret_cast<int *>(HinvJ + MAXN);                 // bucket fill of each j
+    uint16_t *Lj = reinterpret_cast<uint16_t *>(JC + MAXN);          // cj sorted along d
+    uint16_t *stacks = Lj + MAXN;
+    uint16_t *JB = stacks + TW * SYM_Q * 32;                         // [MAXN][SYM_JCAP] i of j's hits
+    __shared__ __align__(8) unsigned long long s_mbar[NTEAM];
+    const unsigned mbar = smem_addr(&s_mbar[team]);
     unsigned phase = 0;
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
+    const int lane = threadIdx.x & 31, wl = tt >> 5;                 // wl: warp within the team
+    if (tt == 0) {
         mbar_init(mbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0};
     if (npairs_dev) npairs = min(npairs, (long long)*npairs_dev);
-    if (npairs_dev) npairs = min(npairs, (long long)*npairs_dev);
 
-    for (long long q = blockIdx.x; q < npairs; q += gridDim.x) {
+    for (long long q = (long long)blockIdx.x * NTEAM + team; q < npairs; q += (long long)gridDim.x * NTEAM) {
         const int2 pr = pairs[q];
         const long long ci = pr.x, cj = pr.y;
         // (PLAIN: ci may be a ghost cell whose +d neighbour is owned; only j accumulates then)
         const bool i_owned = owned_cell(g, ci);
         if ((!PLAIN && !i_owned) || ci < 0 || ci >= g.ncell || cj < 0 || cj >= g.ncell) {
-            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+            if (tt == 0) set_status(status, ST_EINVAL);
             continue;
         }
         const HomeCell hc = home_cell(g, ci);
@@ -298,7 +345,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
         oy = oy == g.ny - 1 ? -1 : (oy == 1 - g.ny ? 1 : oy);
         oz = oz == g.nz - 1 ? -1 : (oz == 1 - g.nz ? 1 : oz);
         if (ox < -1 || ox > 1 || oy < -1 || oy > 1 || oz < -1 || oz > 1 || !(ox | oy | oz)) {
-            if (threadIdx.x == 0) set_status(status, ST_EINVAL);
+            if (tt == 0) set_status(status, ST_EINVAL);
             continue;
         }
         int cjc, sh[3];
@@ -310,31 +357,37 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
         const int sj = c.cell_start[cjc], nj = c.cell_start[cjc + 1] - sj;
         if (ni == 0 || nj == 0) continue;
         const bool j_owned = owned_cell(g, cjc);
-        if (ni > SYM_MAXN || nj > SYM_MAXN) {
+        if (ni > MAXN || nj > MAXN) {
+            if (big_pairs) {                      // the CTA form takes it after this launch
+                if (tt == 0) big_pairs[atomicAdd(big_count, 1)] = pr;
+                continue;
+            }
             // dense cells: the two one-sided per-thread sweeps reading global memory
-            for (int i = si + threadIdx.x; i_owned && i < si + ni; i += blockDim.x) {
+            for (int i = si + tt; i_owned && i < si + ni; i += TT) {
                 IPart p = load_i(g, c, i, hc.corner);
                 Acc a;
                 acc_zero(a);
                 sweep_pair<COUNT>(g, c, p, cjc, ox, oy, oz, sh, a, cand[kind], hits[kind]);
                 if (a.nngb > 0) {
-                    if (PLAIN) plain_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
+                    if (PLAIN && sacc) slot_out(sacc + i, finalise(g, p, a, false), a.nngb);
+                    else if (PLAIN) plain_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
                     else atomic_out(o, c.perm[i], finalise(g, p, a, false), a.nngb);
                 }
             }
-            __syncthreads();              // (PLAIN) ci's outputs written before cj's sweep reads nothing of them
+            team_sync<TW, NWARPS>(team);              // (PLAIN) ci's outputs written before cj's sweep reads nothing of them
             if (j_owned) {
                 const HomeCell hj = home_cell(g, cjc);
                 int cic, sh2[3];
                 neighbour(g, hj, -ox, -oy, -oz, cic, sh2);
-                for (int j = sj + threadIdx.x; j < sj + nj; j += blockDim.x) {
+                for (int j = sj + tt; j < sj + nj; j += TT) {
                     IPart p = load_i(g, c, j, hj.corner);
                     Acc a;
                     acc_zero(a);
                     unsigned dummy = 0;
                     sweep_pair<COUNT>(g, c, p, cic, -ox, -oy, -oz, sh2, a, dummy, hits[kind]);
                     if (a.nngb > 0) {
-                        if (PLAIN) plain_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
+                        if (PLAIN && sacc) slot_out(sacc + j, finalise(g, p, a, false), a.nngb);
+                        else if (PLAIN) plain_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
                         else atomic_out(o, c.perm[j], finalise(g, p, a, false), a.nngb);
                     }
                 }
@@ -342,7 +395,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             continue;
         }
         // ---- staging: both cells (positions and v, m), cj's sorted list, empty buckets ----------
-        if (threadIdx.x == 0) {
+        if (tt == 0) {
             mbar_expect_tx(mbar, (unsigned)(2 * ni + 2 * nj) * 16u);
             bulk_g2s(smem_addr(Pi), c.xyzh + si, (unsigned)ni * 16u, mbar);
             bulk_g2s(smem_addr(Vi), c.vm + si, (unsigned)ni * 16u, mbar);
@@ -350,14 +403,14 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             bulk_g2s(smem_addr(Vj), c.vm + sj, (unsigned)nj * 16u, mbar);
         }
         const uint16_t *src = c.ord + (long long)d * c.cap + sj;
-        for (int k = threadIdx.x; k < nj; k += blockDim.x) {
+        for (int k = tt; k < nj; k += TT) {
             Lj[k] = src[k];
             JC[k] = 0;
         }
         mbar_wait(mbar, phase);
         phase ^= 1u;
         const float bx = g.boxf[0], by = g.boxf[1], bz = g.boxf[2];
-        for (int k = threadIdx.x; k < nj; k += blockDim.x) {
+        for (int k = tt; k < nj; k += TT) {
             float4 p = Pj[k];
             // cj beyond a low face: x_j - L, exact (x_j >= L/2); w <- H_j^2 as the gather rounds it
             p.x -= sh[0] < 0 ? bx : 0.0f;
@@ -368,7 +421,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             HinvJ[k] = (float)(1.0 / H);
             Pj[k] = p;
         }
-        for (int k = threadIdx.x; k < ni; k += blockDim.x) {
+        for (int k = tt; k < ni; k += TT) {
             // ci's home coordinate shifted by -L where cj lies beyond a high face (exact: x_i >= L/2)
             float4 p = Pi[k];
             p.x -= sh[0] > 0 ? bx : 0.0f;
@@ -377,14 +430,14 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
             Pi[k] = p;
         }
         const float Hjmax = (float)((double)g.gamma * (double)c.cell_hmax[cjc]);
-        __syncthreads();
+        team_sync<TW, NWARPS>(team);
 
         const unsigned sP = smem_addr(Pj), sV = smem_addr(Vj), sL = smem_addr(Lj);
         const unsigned sQ = smem_addr(stacks + wl * SYM_Q * 32) + 2u * lane;
         const float c0 = (float)dir_component(d, 0), c1 = (float)dir_component(d, 1), c2 = (float)dir_component(d, 2);
         const float rk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
         // ---- phase 1: lane = i ------------------------------------------------------------------
-        for (int t0 = wl * 32; t0 < ni; t0 += SYM_WARPS * 32) {
+        for (int t0 = wl * 32; t0 < ni; t0 += TT) {
             const int e = t0 + lane;
             const bool active = e < ni;
             float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, H2 = -1.f, Hinv = 0.f, Hk = 0.f, m = 0.f;
@@ -461,7 +514,7 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                                                 pk(vj.x - vx, 0.f), pk(vj.y - vy, 0.f), pk(vj.z - vz, 0.f),
                                                 pk(1.0f, 0.0f), B);
                             // (a bucket overflow: several lanes may hit j at once -> atomic even in PLAIN)
-                            sym_flush<false>(g, o, c.perm[sj + id], HinvJ[id], B, 1);
+                            sym_flush<false>(g, o, nullptr, 0, c.perm[sj + id], HinvJ[id], B, 1);
                         }
                     }
                 }
@@ -474,12 +527,12 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                 }
             }
             while (__any_sync(0xffffffffu, qp != sQ)) drain(true);
-            if (active && nngb > 0 && i_owned) sym_flush<PLAIN>(g, o, c.perm[si + e], Hinv, A, nngb);
+            if (active && nngb > 0 && i_owned) sym_flush<PLAIN>(g, o, sacc, si + e, c.perm[si + e], Hinv, A, nngb);
         }
-        __syncthreads();                          // buckets complete
+        team_sync<TW, NWARPS>(team);                          // buckets complete
         // ---- phase 2: lane = j, its bucket of i ---------------------------------------------------
         if (j_owned) {
-            for (int t0 = wl * 32; t0 < nj; t0 += SYM_WARPS * 32) {
+            for (int t0 = wl * 32; t0 < nj; t0 += TT) {
                 const int k = t0 + lane;
                 const bool active = k < nj;
                 const int nb = active ? min(JC[k], SYM_JCAP) : 0;
@@ -513,10 +566,10 @@ __global__ void __launch_bounds__(SYM_WARPS * 32) k_density_pair_sym(DevGrid g, 
                                         pk(vj.y - w0.y, vj.y - w1.y), pk(vj.z - w0.z, vj.z - w1.z),
                                         pk(a0 ? 1.0f : 0.0f, a1 ? 1.0f : 0.0f), B);
                 }
-                if (nb > 0) sym_flush<PLAIN>(g, o, c.perm[sj + k], hinv, B, nb);
+                if (nb > 0) sym_flush<PLAIN>(g, o, sacc, sj + k, c.perm[sj + k], hinv, B, nb);
             }
         }
-        __syncthreads();                          // shared memory reused by the next pair
+        team_sync<TW, NWARPS>(team);                          // shared memory reused by the next pair
     }
     flush_stats<COUNT>(st, cand, hits);
 }
@@ -537,15 +590,30 @@ __device__ __forceinline__ int sym_axis_colour(int x, int n, bool periodic)
     return periodic && (n & 1) && x == n - 1 ? 2 : (x & 1);
 }
 
-// Pairs (c, c + d) for the owned cells c of colour `col` (cells of either side empty are
-// skipped); also, with d < 0, the list of all owned non-empty cells (the self pass).
+// The colour axis of direction d: its first nonzero component.  Two pairs (c, c + d) and
+// (c', c' + d) of one direction share a cell only if c' = c +- d, i.e. their coordinates on
+// that axis are neighbours, which sym_axis_colour always tells apart: 2 (or 3) phases per
+// direction.
+__host__ __device__ __forceinline__ int sym_dir_axis(int d)
+{
+    return dir_component(d, 0) != 0 ? 0 : (dir_component(d, 1) != 0 ? 1 : 2);
+}
+
+__host__ __device__ __forceinline__ int sym_dir_colours(const DevGrid &g, int d)
+{
+    const int a = sym_dir_axis(d);
+    return a == 0 ? sym_axis_colours(g.nxl, !g.ghost_x) : sym_axis_colours(a == 1 ? g.ny : g.nz, true);
+}
+
+// Pairs (c, c + d) for the cells c of colour `col` along d's colour axis (cells of either side
+// empty are skipped); also, with d < 0, the list of all owned non-empty cells (the self pass).
 __global__ void k_sym_phase_pairs(DevGrid g, const int *__restrict__ cell_start, int d, int col, int2 *pairs,
                                   int *count)
 {
     const long long plane = (long long)g.ny * g.nz;
-    const int cx = sym_axis_colours(g.nxl, !g.ghost_x), cy = sym_axis_colours(g.ny, true);
     const int a0 = d >= 0 ? dir_component(d, 0) : 0, a1 = d >= 0 ? dir_component(d, 1) : 0,
               a2 = d >= 0 ? dir_component(d, 2) : 0;
+    const int axis = d >= 0 ? sym_dir_axis(d) : 0;
     // d < 0: the owned cells; else every local cell (a low ghost cell pairs with its owned +d neighbour)
     const long long ncells = d < 0 ? g.n_owned_cells : g.ncell;
     for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < ncells;
@@ -557,9 +625,8 @@ __global__ void k_sym_phase_pairs(DevGrid g, const int *__restrict__ cell_start,
             continue;
         }
         const int ixl = (int)(cell / plane), iy = (int)((cell / g.nz) % g.ny), iz = (int)(cell % g.nz);
-        const int colour = (sym_axis_colour(ixl, g.nxl, !g.ghost_x) * cy + sym_axis_colour(iy, g.ny, true)) *
-                               sym_axis_colours(g.nz, true) + sym_axis_colour(iz, g.nz, true);
-        (void)cx;
+        const int colour = axis == 0 ? sym_axis_colour(ixl, g.nxl, !g.ghost_x)
+                                     : (axis == 1 ? sym_axis_colour(iy, g.ny, true) : sym_axis_colour(iz, g.nz, true));
         if (colour != col) continue;
         const HomeCell hc = home_cell(g, cell);
         int cj, sh[3];
@@ -567,6 +634,31 @@ __global__ void k_sym_phase_pairs(DevGrid g, const int *__restrict__ cell_start,
         if (cell_start[cj + 1] == cell_start[cj]) continue;
         if (!owned_cell(g, cell) && !owned_cell(g, cj)) continue;   // ghost-ghost: nothing to write
         pairs[atomicAdd(count, 1)] = make_int2((int)cell, cj);
+    }
+}
+
+// sph_density_all_sym's last step: out[perm[s]] += slot accumulator s (the self pass wrote
+// out[] directly), then div v and curl v divided by rho (k_finalize's step) -- every owned
+// particle has exactly one slot.  Ghost slots (perm >= n_out) were never written.
+__global__ void k_sym_merge(DevOut o, const SlotAcc *__restrict__ acc, const int *__restrict__ perm,
+                            const int *__restrict__ n_stored)
+{
+    const long long n = *n_stored;
+    for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < n; s += (long long)gridDim.x * blockDim.x) {
+        const int p = perm[s];
+        if (p < 0 || p >= o.n_out) continue;
+        const float4 a = acc[s].a, b = acc[s].b;
+        const float rho = o.rho[p] + a.x;
+        const float rinv = rho != 0.0f ? 1.0f / rho : 0.0f;
+        o.rho[p] = rho;
+        o.wcount[p] += a.y;
+        o.rho_dh[p] += a.z;
+        o.wcount_dh[p] += a.w;
+        o.div_v[p] = (o.div_v[p] + b.x) * rinv;
+        o.curl_v[p] = (o.curl_v[p] + b.y) * rinv;
+        o.curl_v[o.n_out + p] = (o.curl_v[o.n_out + p] + b.z) * rinv;
+        o.curl_v[2 * o.n_out + p] = (o.curl_v[2 * o.n_out + p] + b.w) * rinv;
+        o.nngb[p] += acc[s].nngb;
     }
 }
 

@@ -60,6 +60,10 @@ const DevAttrs &dev_attrs(int dev)
         cudaFuncSetAttribute(k_density_pair_sym<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYM_SMEM);
         cudaFuncSetAttribute(k_density_pair_sym<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SYM_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<true, true, SYMW_MAXN, 1, SYMW_WARPS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYMW_SMEM);
+        cudaFuncSetAttribute(k_density_pair_sym<false, true, SYMW_MAXN, 1, SYMW_WARPS>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SYMW_SMEM);
         cudaFuncSetAttribute(k_density_pair_sym<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SYM_SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a.v4_blocks_per_sm, k_density_v4<false>, V4_TP, V4_SMEM);
@@ -652,21 +656,38 @@ int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *o
                                                                     -2, nullptr, status, count);
     }
     // the 13 directions x colours: symmetric pairs, no atomics
-    const int ncol = sym_axis_colours(g.nxl, !g.ghost_x) * sym_axis_colours(g.ny, true) * sym_axis_colours(g.nz, true);
+    // pairs with a cell above SYMW_MAXN: deferred to the CTA form (list after the phase's pairs,
+    // count in big_count + 1) when the scratch has room, else swept from global memory in place
+    const bool defer = sizeof(ParticleRec) * (size_t)cells->capacity >= 16 * (size_t)g.ncell;
+    int2 *big = defer ? pairs + g.ncell : nullptr;
+    int *big_n = defer ? count + 1 : nullptr;
+    // per-slot accumulators in the output-record region (SlotAcc = sizeof(OutRec) per slot)
+    static_assert(sizeof(SlotAcc) == sizeof(OutRec), "slot accumulators reuse the output-record region");
+    SlotAcc *sacc = at<SlotAcc>(ws, w.orec);
+    if ((e = cudaMemsetAsync(sacc, 0, sizeof(SlotAcc) * (size_t)(cells->capacity > 0 ? cells->capacity : 1), s)) !=
+        cudaSuccess)
+        return cuda_fail(e);
     for (int d = 0; d < SPH_NDIR; ++d)
-        for (int col = 0; col < ncol; ++col) {
-            if ((e = cudaMemsetAsync(count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+        for (int col = 0; col < sym_dir_colours(g, d); ++col) {
+            if ((e = cudaMemsetAsync(count, 0, 8, s)) != cudaSuccess) return cuda_fail(e);
             k_sym_phase_pairs<<<gen_blocks, 256, 0, s>>>(g, dc.cell_start, d, col, pairs, count);
+            const int wblocks = 148 * 2;
+            if (stats)
+                k_density_pair_sym<true, true, SYMW_MAXN, 1, SYMW_WARPS><<<wblocks, SYMW_WARPS * 32, SYMW_SMEM, s>>>(
+                    g, dc, o, pairs, maxp, stats, status, count, big, big_n, sacc);
+            else
+                k_density_pair_sym<false, true, SYMW_MAXN, 1, SYMW_WARPS><<<wblocks, SYMW_WARPS * 32, SYMW_SMEM, s>>>(
+                    g, dc, o, pairs, maxp, nullptr, status, count, big, big_n, sacc);
+            if (!defer) continue;
             const int blocks = 148 * 3;
             if (stats)
-                k_density_pair_sym<true, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dc, o, pairs, maxp, stats,
-                                                                                       status, count);
+                k_density_pair_sym<true, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(
+                    g, dc, o, big, maxp, stats, status, big_n, nullptr, nullptr, sacc);
             else
-                k_density_pair_sym<false, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(g, dc, o, pairs, maxp, nullptr,
-                                                                                        status, count);
+                k_density_pair_sym<false, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(
+                    g, dc, o, big, maxp, nullptr, status, big_n, nullptr, nullptr, sacc);
         }
-    if (out->n_out > 0)
-        k_finalize<<<grid_blocks(out->n_out, 256, 148 * 32), 256, 0, s>>>(o, out->n_out);
+    k_sym_merge<<<grid_blocks(cells->capacity, 256, 148 * 16), 256, 0, s>>>(o, sacc, dc.perm, dc.cell_start + g.ncell);
     return check_launch();
 }
 

@@ -30,10 +30,20 @@ import torch
 from . import api as pv
 
 BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_rec, k_stable_small/bitonic/big
-SORT_LAUNCHES = 6       # k_sort_small, k_sort_mid, k_sort_warp256, k_sort_big, k_sort_bitonic (medium, huge)
+SORT_LAUNCHES = 6       # k_sort_small, k_sort_mid, k_sort_warp256, k_sort_big, k_sort_radix (medium, huge)
 SELECT_LAUNCHES = 5     # sph_select_planes: k_sel_count, 3 scan kernels, k_sel_write
-DENSITY_LAUNCHES = 8    # k_v4_tiles (count), 3 scan kernels, k_v4_tiles (write), k_density_v4, k_density_dense,
-                        # k_unpermute
+DENSITY_LAUNCHES = 9    # k_row_home, k_v4_tiles (count), 3 scan kernels, k_v4_tiles (write), k_density_v5,
+                        # k_density_dense, k_unpermute
+
+
+def sym_launches(nxl: int, ny: int, nz: int, x_periodic: bool) -> int:
+    """Kernels of one sph_density_all_sym call: the self-pass list and k_density_self, per
+    colour phase the pair list, the warp-per-pair kernel and the CTA kernel of the deferred
+    large pairs, and k_sym_merge.  Direction 0 is coloured along z, 1..3 along y, 4..12 along
+    x (first nonzero component); an axis takes 3 colours when periodic and odd, else 2."""
+    col = lambda n, per: 3 if per and n % 2 else 2   # noqa: E731
+    phases = col(nz, True) + 3 * col(ny, True) + 9 * col(nxl, x_periodic)
+    return 2 + 3 * phases + 1
 
 
 def slab_bounds(nc: int, world: int, rank: int) -> tuple[int, int]:
@@ -255,7 +265,9 @@ class SlabRunner:
         self.n_ghost = 2 * self.bcap             # both ghost blocks always (rows past a block's count are dead)
         self.plane = self.grid.nc[1] * self.grid.nc[2]   # cells per x plane
         self.nxl = (slab.x_hi - slab.x_lo) + (2 if ghost else 0)
-        self.launches_per_step = (BUILD_LAUNCHES + SORT_LAUNCHES + DENSITY_LAUNCHES) * len(self.levels) + \
+        dens = DENSITY_LAUNCHES if engine != "sym" else \
+            sym_launches(slab.x_hi - slab.x_lo + (2 if ghost else 0), slab.nc, slab.nc, not ghost)
+        self.launches_per_step = (BUILD_LAUNCHES + SORT_LAUNCHES + dens) * len(self.levels) + \
             (SELECT_LAUNCHES if ghost else 0) + (len(self.levels) if split else 0)   # k_mark_needed per level
         if ghost:
             # send buffers of the boundary planes (sph_select_planes), the received counts, and
