@@ -358,7 +358,8 @@ class ReuseLoop:
         box = max(self.dp.grid.box[0], self.dp.grid.box[1], self.dp.grid.box[2])
         return self.vmax * abs(dt) * (1.0 + 2.0 ** -20) + 3.0 ** 0.5 * 2.0 ** -24 * (box + self.skin) * 1.01
 
-    def step(self, dt: float, stats: Stats | None = None, stream=None) -> Out:
+    def step(self, dt: float, stats: Stats | None = None, stream=None, events=None) -> Out:
+        """events (optional): two CUDA events recorded around sph_density_all (timing only)."""
         inc = self.step_bound(dt)
         if inc > self.skin:
             raise ValueError(f"one drift ({inc}) exceeds the skin ({self.skin}): smaller dt or a larger skin")
@@ -370,7 +371,11 @@ class ReuseLoop:
         sph_drift(self.dp.grid, self.dp.cells, dt, self.max_disp, stream=stream)
         self.bound += inc
         self.steps += 1
+        if events:
+            events[0].record(torch.cuda.current_stream() if stream is None else stream)
         sph_density_all(self.dp.grid, self.dp.cells, self.dp.out, self.dp.ws, stats=stats, stream=stream)
+        if events:
+            events[1].record(torch.cuda.current_stream() if stream is None else stream)
         return self.dp.out
 
     def check(self, stream=None) -> None:

@@ -16,8 +16,8 @@
 // 64 (stable read) + 40 (write) ~ 250 B (random-access granularity).
 #pragma once
 
-#include "bitonic.cuh"
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace pvsph {
 
@@ -317,8 +317,10 @@ constexpr int STABLE_SMALL = 128;
 constexpr int STABLE_WARPS = 8;
 constexpr int STABLE_BIG_CHUNK = 256;
 constexpr int STABLE_BIG_TILE = 4096;
-constexpr int STABLE_BT_MAX = 16384;     // cells of STABLE_SMALL < n <= this: k_stable_bitonic
+constexpr int STABLE_BT_MAX = 16384;     // cells of STABLE_SMALL < n <= this: k_stable_radix
 constexpr int STABLE_BT_T = 512;
+constexpr int STABLE_MED_MAX = 2048;     //   of which <= this: 128-thread CTAs
+constexpr int STABLE_MED_T = 128;
 
 // One warp per cell of <= STABLE_SMALL particles: rank each input index among the
 // cell's (all distinct) and move its record there.  Larger cells are queued as
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     float *__restrict__ cell_hmax,
                                                                     int *__restrict__ row_home, int nz,
                                                                     int2 *big_items, int *big_count, int *bt_items,
-                                                                    int *bt_count)
+                                                                    int *bt_count, int bt_cap)
 {
     __shared__ unsigned sh[STABLE_WARPS][STABLE_SMALL];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -378,8 +380,11 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             cell_hmax[cell] = hm;
             if (nh > 0) row_home[cell / nz] = 1;         // k_v4_tiles skips rows without home particles
         }
-        if (n > STABLE_SMALL && n <= STABLE_BT_MAX) {      // k_stable_bitonic
-            if (lane == 0) bt_items[atomicAdd(bt_count, 1)] = (int)cell;
+        if (n > STABLE_SMALL && n <= STABLE_BT_MAX) {      // k_stable_radix: medium from the front, huge from the back
+            if (lane == 0) {
+                if (n <= STABLE_MED_MAX) bt_items[atomicAdd(&bt_count[0], 1)] = (int)cell;
+                else bt_items[bt_cap - 1 - atomicAdd(&bt_count[1], 1)] = (int)cell;
+            }
             continue;
         }
         if (n > STABLE_SMALL) {
@@ -412,40 +417,112 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
     }
 }
 
-// One CTA per cell of STABLE_SMALL < n <= STABLE_BT_MAX particles: the records' keys (input
-// index | not-home bit << 31) with their in-cell position as 64-bit composites, bitonic-sorted
-// (bitonic.cuh: 256-element chunks in registers, distances >= 256 through shared memory), then
-// every record moved to its rank.  Keys are distinct, so the order is the stable one.
-__global__ void __launch_bounds__(STABLE_BT_T) k_stable_bitonic(const int *__restrict__ start,
-                                                                const ParticleRec *__restrict__ rec,
-                                                                float4 *__restrict__ xyzh, float4 *__restrict__ vm,
-                                                                int *__restrict__ perm, const int *__restrict__ items,
-                                                                const int *__restrict__ count)
+// One CTA per cell of STABLE_SMALL < n <= STABLE_BT_MAX particles: a stable LSD radix sort of
+// the records' keys (input index | not-home bit << 31, all distinct) in shared memory, then
+// every record moved to its rank: 8-bit digits, only the bytes in which the cell's keys differ (OR ^ AND over the cell; random input order: three of four), per
+// pass a count sweep, one exclusive scan over (digit, warp) and a stable MATCH-ranked
+// scatter of (key, in-cell position) -- the scheme of k_sort_radix (sort.cuh).
+// Two tiers as in sph_sort_cells: cells of <= STABLE_MED_MAX on 128-thread CTAs (33 KB, several
+// per SM; queued from the front of the item list), larger ones on 512 threads (212 KB; from
+// the back).
+constexpr int stable_radix_smem(int maxn, int t) { return maxn * 12 + 256 * (t / 32) * 4 + 64 * 4; }
+
+template <int MAXN, int T, bool FROM_BACK>
+__global__ void __launch_bounds__(T) k_stable_radix(const int *__restrict__ start,
+                                                   const ParticleRec *__restrict__ rec,
+                                                   float4 *__restrict__ xyzh, float4 *__restrict__ vm,
+                                                   int *__restrict__ perm, const int *__restrict__ items,
+                                                   const int *__restrict__ count, int cap)
 {
-    extern __shared__ unsigned long long hs[];            // STABLE_BT_MAX composites
-    constexpr int NW = STABLE_BT_T / 32;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int NW = T / 32, NH = 256 * NW, HPT = NH / T, RU = 4;
+    static_assert(NH % T == 0, "radix: 256 x warps must be a multiple of the threads");
+    extern __shared__ unsigned rs[];
+    unsigned *keyA = rs, *keyB = rs + MAXN;
+    uint16_t *idxA = reinterpret_cast<uint16_t *>(rs + 2 * MAXN), *idxB = idxA + MAXN;
+    unsigned *hist = rs + 3 * MAXN, *wsum = hist + NH;
+    __shared__ unsigned s_or, s_and;
     const int nitems = *count;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const long long cell = items[it];
+        const long long cell = items[FROM_BACK ? cap - 1 - it : it];
         const int s0 = start[cell], n = start[cell + 1] - s0;
-        int P = BT_CHUNK;
-        while (P < n) P <<= 1;
-        for (int ch = w; ch < P / BT_CHUNK; ch += NW) {
-            const int base = ch * BT_CHUNK;
-            unsigned long long v[BT_E];
-#pragma unroll
-            for (int q = 0; q < BT_E; ++q) {
-                const int e = base + lane * BT_E + q;
-                v[q] = e < n ? ((unsigned long long)(unsigned)rec[s0 + e].idx << 32) | (unsigned)e : ~0ull;
-            }
-            bt_sort_chunk(v, base, lane);
-#pragma unroll
-            for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
+        const int S = (n + NW - 1) / NW;
+        const int lo = min(n, w * S), hi = min(n, lo + S);
+        if (threadIdx.x == 0) { s_or = 0u; s_and = ~0u; }
+        __syncthreads();
+        unsigned o = 0u, a = ~0u;
+        for (int e = threadIdx.x; e < n; e += T) {
+            const unsigned k = (unsigned)rec[s0 + e].idx;
+            keyA[e] = k;
+            idxA[e] = (uint16_t)e;
+            o |= k;
+            a &= k;
         }
-        bt_cta_merge<STABLE_BT_T>(hs, P, lane, w);
-        for (int r = threadIdx.x; r < n; r += STABLE_BT_T)
-            stable_place(s0, (int)(hs[r] & 0xffffffffull), r, rec, xyzh, vm, perm);
+        o = __reduce_or_sync(0xffffffffu, o);
+        a = __reduce_and_sync(0xffffffffu, a);
+        if (lane == 0) { atomicOr(&s_or, o); atomicAnd(&s_and, a); }
+        __syncthreads();
+        const unsigned diff = s_or ^ s_and;
+        unsigned *ks = keyA, *kd = keyB;
+        uint16_t *is = idxA, *id = idxB;
+        for (int shift = 0; shift < 32; shift += 8) {
+            if (!((diff >> shift) & 255u)) continue;   // CTA-uniform: every key has this byte
+#pragma unroll
+            for (int q = 0; q < HPT; ++q) hist[threadIdx.x * HPT + q] = 0u;
+            __syncthreads();
+            for (int b = lo; b < hi; b += 32 * RU) {
+                unsigned dg[RU], peers[RU];
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const int i = b + 32 * u + lane;
+                    dg[u] = i < hi ? (ks[i] >> shift) & 255u : 256u;
+                }
+#pragma unroll
+                for (int u = 0; u < RU; ++u) peers[u] = __match_any_sync(0xffffffffu, dg[u]);
+#pragma unroll
+                for (int u = 0; u < RU; ++u)
+                    if (dg[u] < 256u && !(peers[u] & lt_mask)) atomicAdd(&hist[dg[u] * NW + w], __popc(peers[u]));
+            }
+            __syncthreads();
+            unsigned loc[HPT], sum = 0u;
+#pragma unroll
+            for (int q = 0; q < HPT; ++q) { loc[q] = hist[threadIdx.x * HPT + q]; sum += loc[q]; }
+            unsigned run = block_excl_scan<T>(sum, wsum, lane, w);
+#pragma unroll
+            for (int q = 0; q < HPT; ++q) { hist[threadIdx.x * HPT + q] = run; run += loc[q]; }
+            __syncthreads();
+            for (int b = lo; b < hi; b += 32 * RU) {
+                unsigned k[RU], dg[RU], peers[RU];
+                uint16_t ix[RU];
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const int i = b + 32 * u + lane;
+                    k[u] = i < hi ? ks[i] : 0u;
+                    ix[u] = i < hi ? is[i] : (uint16_t)0;
+                    dg[u] = i < hi ? (k[u] >> shift) & 255u : 256u;
+                }
+#pragma unroll
+                for (int u = 0; u < RU; ++u) peers[u] = __match_any_sync(0xffffffffu, dg[u]);
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const unsigned r = __popc(peers[u] & lt_mask);
+                    const unsigned hx = min(dg[u], 255u) * NW + w;
+                    const unsigned base = hist[hx];
+                    if (dg[u] < 256u) {
+                        kd[base + r] = k[u];
+                        id[base + r] = ix[u];
+                    }
+                    __syncwarp();
+                    if (dg[u] < 256u && r == 0) hist[hx] = base + __popc(peers[u]);
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            unsigned *tk = ks; ks = kd; kd = tk;
+            uint16_t *ti = is; is = id; id = ti;
+        }
+        for (int r = threadIdx.x; r < n; r += T) stable_place(s0, is[r], r, rec, xyzh, vm, perm);
         __syncthreads();
     }
 }

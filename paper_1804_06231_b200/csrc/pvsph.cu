@@ -51,7 +51,8 @@ const DevAttrs &dev_attrs(int dev)
         cudaFuncSetAttribute(k_density_v5<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)V5_SMEM);
         cudaFuncSetAttribute(k_density_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
         cudaFuncSetAttribute(k_density_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
-        cudaFuncSetAttribute(k_stable_bitonic, cudaFuncAttributeMaxDynamicSharedMemorySize, STABLE_BT_MAX * 8);
+        cudaFuncSetAttribute(k_stable_radix<STABLE_BT_MAX, STABLE_BT_T, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, stable_radix_smem(STABLE_BT_MAX, STABLE_BT_T));
         cudaFuncSetAttribute(k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T));
         cudaFuncSetAttribute(k_density_pair_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
@@ -335,17 +336,20 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         float4 *xs = reinterpret_cast<float4 *>(cells->xyzh), *vs = reinterpret_cast<float4 *>(cells->vm);
         int *bt_items = at<int>(ws, w.huge_items), *bt_count = at<int>(ws, w.huge_count);
         int *row_home = at<int>(ws, w.row_home);
-        if ((e = cudaMemsetAsync(bt_count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
+        if ((e = cudaMemsetAsync(bt_count, 0, 8, s)) != cudaSuccess) return cuda_fail(e);
         if ((e = cudaMemsetAsync(row_home, 0, 4 * (size_t)g.nxl * g.ny, s)) != cudaSuccess) return cuda_fail(e);
         // a fresh build: no displacement since it (list reuse, sph_drift)
         if ((e = cudaMemsetAsync(cells->disp, 0, 4 * (size_t)n, s)) != cudaSuccess) return cuda_fail(e);
         if ((e = cudaMemsetAsync(cells->cell_dx, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
         k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
             g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, cells->cell_hmax,
-            row_home, g.nz, big_items, big_count, bt_items, bt_count);
+            row_home, g.nz, big_items, big_count, bt_items, bt_count, (int)w.huge_cap);
         if ((rc = ensure_attrs()) != SPH_OK) return rc;
-        k_stable_bitonic<<<148, STABLE_BT_T, STABLE_BT_MAX * 8, s>>>(cells->cell_start, rec, xs, vs, cells->perm,
-                                                                    bt_items, bt_count);
+        k_stable_radix<STABLE_MED_MAX, STABLE_MED_T, false>
+            <<<148 * 8, STABLE_MED_T, stable_radix_smem(STABLE_MED_MAX, STABLE_MED_T), s>>>(
+                cells->cell_start, rec, xs, vs, cells->perm, bt_items, bt_count, (int)w.huge_cap);
+        k_stable_radix<STABLE_BT_MAX, STABLE_BT_T, true><<<148, STABLE_BT_T, stable_radix_smem(STABLE_BT_MAX, STABLE_BT_T), s>>>(
+            cells->cell_start, rec, xs, vs, cells->perm, bt_items, bt_count + 1, (int)w.huge_cap);
         k_stable_big<<<148 * 4, STABLE_BIG_CHUNK, 0, s>>>(cells->cell_start, rec, xs, vs, cells->perm, big_items,
                                                           big_count);
     }

@@ -17,13 +17,13 @@
 // composites (orderable fp32 key << 32 | input index) through shared memory.
 #pragma once
 
-#include "bitonic.cuh"
 #include "common.cuh"
+#include "radix.cuh"
 
 namespace pvsph {
 
 constexpr int SORT_SMALL = 32;
-constexpr int SORT_MED = 128;           // cells above: bitonic sorts (k_sort_warp256, k_sort_bitonic)
+constexpr int SORT_MED = 128;           // cells above: k_sort_warp256 (bitonic), k_sort_radix
 constexpr int SORT_W256 = 256;          //   up to here: one warp per cell, in registers (k_sort_warp256)
 constexpr int SORT_MED_MAX = 2048;      //   medium tier (k_sort_radix): 128 threads, 33 KB shared memory
 #ifndef SORT_MED_THREADS
@@ -189,59 +189,6 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
     }
 }
 
-// One CTA per cell of SORT_W256 < n <= MAXN particles (clustered data): for each direction the
-// 64-bit composites (orderable fp32 key << 32 | in-cell index; in-cell order is the input
-// order) are bitonic-sorted over P = next power of two >= n in shared memory, with every
-// exchange at distance j < 256 done in registers: a warp holds a 256-element chunk (8 per
-// lane; j < 8 inside the lane, 8 <= j < 256 by shuffles).  Each chunk is first sorted whole in
-// registers; then for every merge size k >= 512 the distances j >= 256 take one shared-memory
-// stage and a barrier each, the last eight distances one register pass.  FROM_BACK: the items
-// are stored from the back of the list (huge tier).
-template <int MAXN, int T, bool FROM_BACK>
-__global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint16_t *ord, const int *items,
-                                                   const int *count, int cap, const int *__restrict__ need)
-{
-    extern __shared__ unsigned long long hs[];           // MAXN composites
-    constexpr int NW = T / 32;
-    const int nitems = *count;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const long long cell = items[FROM_BACK ? cap - 1 - it : it];
-        const int s0 = c.cell_start[cell];
-        const int n = c.cell_start[cell + 1] - s0;
-        int P = BT_CHUNK;
-        while (P < n) P <<= 1;
-        double corner[3];
-        cell_corner(g, cell, corner);
-        const int mask = need ? need[cell] : 0x1fff;
-        for (int d = 0; d < SPH_NDIR; ++d) {
-            if (!((mask >> d) & 1)) continue;          // CTA-uniform
-            // chunks: composites straight into registers, sorted whole (k = 2 .. 256)
-            for (int ch = w; ch < P / BT_CHUNK; ch += NW) {
-                const int base = ch * BT_CHUNK;
-                unsigned long long v[BT_E];
-#pragma unroll
-                for (int q = 0; q < BT_E; ++q) {
-                    const int e = base + lane * BT_E + q;
-                    v[q] = ~0ull;
-                    if (e < n) {
-                        const float4 p = c.xyzh[s0 + e];
-                        const float key = pv_key((double)p.x - corner[0], (double)p.y - corner[1],
-                                                 (double)p.z - corner[2], d);
-                        v[q] = ((unsigned long long)float_order(key) << 32) | (unsigned)e;
-                    }
-                }
-                bt_sort_chunk(v, base, lane);
-#pragma unroll
-                for (int q = 0; q < BT_E; ++q) hs[base + lane * BT_E + q] = v[q];
-            }
-            bt_cta_merge<T>(hs, P, lane, w);
-            for (int k = threadIdx.x; k < n; k += T) ord[(long long)d * c.cap + s0 + k] = (uint16_t)(hs[k] & 0xffffffffull);
-            __syncthreads();
-        }
-    }
-}
-
 // One CTA per cell of SORT_W256 < n <= MAXN particles: for each direction a stable LSD radix
 // sort in shared memory.  The key is the fp64-projected fp32 key (pv_key) quantised to 24 bits
 // over the cell's key range [-sqrt(3) C_max, +sqrt(3) C_max] (quantum 2 sqrt(3) C_max / 2^24,
@@ -255,31 +202,6 @@ __global__ void __launch_bounds__(T) k_sort_bitonic(DevGrid g, DevCells c, uint1
 // and those of the first pass while the keys are computed: one sweep per pass.  Shared
 // memory: keys and indices double-buffered (12 B per element) plus 2 x 256 x NW counters.
 constexpr int radix_smem(int maxn, int t) { return maxn * 12 + 2 * 256 * (t / 32) * 4 + 64 * 4; }
-
-template <int T>
-__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, int lane, int w)
-{
-    constexpr int NW = T / 32;
-    unsigned x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        unsigned s = lane < NW ? wsum[lane] : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
-            if (lane >= o) s += y;
-        }
-        if (lane < NW) wsum[32 + lane] = s - wsum[lane];      // exclusive warp offsets
-    }
-    __syncthreads();
-    return wsum[32 + w] + x - v;
-}
 
 template <int MAXN, int T, bool FROM_BACK>
 __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_t *ord, const int *items,
@@ -384,8 +306,8 @@ __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_
     }
 }
 
-// Cells of SORT_MED < n <= SORT_W256 particles: one warp per cell, bitonic sort of the 64-bit
-// composites of k_sort_bitonic over P = 256 elements held in registers (lane l holds elements
+// Cells of SORT_MED < n <= SORT_W256 particles: one warp per cell, bitonic sort of 64-bit
+// composites (orderable fp32 key << 32 | in-cell index) over P = 256 elements held in registers (lane l holds elements
 // 8 l .. 8 l + 7): exchanges at distance j < 8 inside the lane, j >= 8 by warp shuffles; no
 // shared memory, no barrier, eight cells per CTA at a time.
 __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_warp256(DevGrid g, DevCells c, uint16_t *ord,

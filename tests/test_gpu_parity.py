@@ -347,6 +347,10 @@ def test_sort_big_cells(pv, occ, qbits):
     c = (1 * nc + 1) * nc + 1
     a, b = cs[c], cs[c + 1]
     assert b - a >= occ                              # plus the background particles that fall in it
+    # the build's stable pass (k_stable_small / k_stable_radix / k_stable_big): in-cell order =
+    # input order, every slot of every cell
+    for c0 in range(nc ** 3):
+        assert np.all(np.diff(perm[cs[c0]:cs[c0 + 1]]) > 0), c0
     for d in range(13):
         sl = a + order[d, a:b]
         assert np.array_equal(np.sort(sl), np.arange(a, b))
