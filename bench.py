@@ -404,6 +404,8 @@ def run_ours(args):
                 "evaluations_per_s": tot_cand / (ms_step_max * 1e-3),              # SV §8(d)
                 "particles_per_s": part.n_global / (ms_step_max * 1e-3),
                 "stage_ms": {k: statistics.mean(v) for k, v in stage.items()},
+                "stage_ms_stats": {k: {"median": statistics.median(v), "min": min(v), "max": max(v)}
+                                   for k, v in stage.items()},
                 "density_ms_max_over_ranks": dens_max,
                 "gpu_launches": runner.launches_per_step * nst,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),

@@ -44,6 +44,7 @@ for name in ("bench_c5", "bench_c3", "bench_c4", "bench_reuse_c5", "bench_sym_c3
         shutil.copy(src, os.path.join(out, name + ".json"))
         benches[name] = last_json(src)
 for name, dst in (("test27cells.json", "test27cells.json"), ("calib.json", "calib.json"),
+                  ("cpu_baselines.json", "cpu_baselines.json"),
                   ("launches_c5.csv", "launches_c5.csv"), ("launches_c4.csv", "launches_c4.csv")):
     if os.path.exists(g(name)):
         shutil.copy(g(name), os.path.join(out, dst))
@@ -184,6 +185,19 @@ cal = ""
 if os.path.exists(os.path.join(out, "calib.json")):
     cal = "```\n" + json.dumps(last_json(os.path.join(out, "calib.json")), indent=1) + "\n```\n"
 
+cpub = ""
+if os.path.exists(os.path.join(out, "cpu_baselines.json")):
+    cb = last_json(os.path.join(out, "cpu_baselines.json"))
+    cpub = [f"Host: {cb['cpu_model']}, {cb['host_threads']} hardware threads; {cb['protocol']}.", "",
+            "| config | variant | threads | sample | seconds median (min, max) | reps | interactions | interactions/s |",
+            "|---|---|---|---|---|---|---|---|"]
+    for r in cb["runs"]:
+        sc = r["seconds"]
+        cpub.append(f"| {r['config']} | {r['variant']} | {r['threads']} | {r['sample']} | {sc['median']:.4g} "
+                    f"({sc['min']:.4g}, {sc['max']:.4g}) | {r['reps']} | {r['interactions']:,} | "
+                    f"{r['interactions_per_s']:.3e} |")
+    cpub = "\n".join(cpub) + "\n"
+
 body = f"""# Round 2 profiles (B200, sm_100a, 1 GPU)
 
 Production engine: density v5 (`csrc/density_v5.cuh`, DESIGN.md §4.4), radix-sorted cluster
@@ -231,6 +245,9 @@ issue-bound.
 ## test27cells (SURVEY §8(f) #4, `bench_test27cells.py`)
 
 {t27}
+## CPU baselines (`scripts/cpu_baselines.py`: SURVEY §8(d) one-thread O2 for c1-c3, O1 brute force for c1/c2)
+
+{cpub}
 ## calibration (`scripts/calibrate.py`: FFMA / FFMA2 peaks and the production interaction rate)
 
 {cal}"""

@@ -1,12 +1,15 @@
-"""Per-phase warp-cycle breakdown of k_density_v4: build exp/so_phase.so with
-    nvcc ... -DPVSPH_PHASE_TIMING -o exp/so_phase.so paper_1804_06231_b200/csrc/pvsph.cu
-then run `python scripts/phase_timing.py c5` on a GPU (profiling helper, not product code)."""
+"""Per-phase warp-cycle breakdown of k_density_v4 (round 1): builds
+exp/so_phase.so (-DPVSPH_PHASE_TIMING) if it is missing or stale, then runs the v4 engine on one
+config: `PVSPH_ENGINE=v4 python scripts/phase_timing.py c5` on a GPU (profiling helper, not
+product code)."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import torch
 from paper_1804_06231_b200 import _lib
+from _variant import build_variant
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
-L = _lib.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "exp", os.environ.get("PHASE_SO", "so_phase.so")))
+L = _lib.load(build_variant("so_phase.so", ["PVSPH_PHASE_TIMING"]))
 import paper_1804_06231_b200 as pv
 import synth
 p = synth.make(cfg)

@@ -20,6 +20,7 @@ timeout 600 python bench.py --config c3 --engine sym --no-cpu --no-e2e > ${O}_be
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > ${O}_bench_ref_c5.json 2> ${O}_bench_ref_c5.err; echo "bench ref rc=$?"
 timeout 600 python bench_test27cells.py > ${O}_test27cells.json 2> ${O}_test27cells.err; echo "test27cells rc=$?"
 timeout 300 python scripts/calibrate.py > ${O}_calib.json 2> ${O}_calib.err; echo "calibrate rc=$?"
+timeout 900 python scripts/cpu_baselines.py > ${O}_cpu_baselines.json 2> ${O}_cpu_baselines.err; echo "cpu baselines rc=$?"
 # measured FP32 counters of the density kernel (c3, c4, c5)
 bash scripts/ncu_fp32.sh ${TAG} k_density_v5 c3 c4 c5
 # c5 launch list with DRAM bytes per launch (cold-cache, serialised)
