@@ -62,6 +62,10 @@ struct DevOut {
     int *nngb;
 };
 
+// The list along which k_density_dense orders a dense home cell's particles and sweeps the
+// cell itself (direction 0 = (0,0,1)); level passes sort it for every cell with home particles.
+constexpr int DENSE_SELF_DIR = 0;
+
 // The 13 canonical sort directions: first nonzero component > 0,
 // lexicographic order.  d = dir_index(canonical offset).
 __host__ __device__ __forceinline__ int dir_component(int d, int a)

@@ -4,14 +4,16 @@
 //
 //  * Work: the builder lists these tiles (each one slice: at most two home cells, <= V4_TP
 //    home particles); a warp claims a tile and takes its home cells in chunks of 32
-//    particles (lane = i).  No CTA barrier anywhere: warps run independently.
+//    particles (lane = i), in the order of the home cell's list along DENSE_SELF_DIR (z), so
+//    the 32 lanes are neighbours along z.  No CTA barrier anywhere: warps run independently.
 //  * Per neighbour cell (26, then the home cell itself) the warp stages the cell's sorted list
 //    from the end nearest to the home cell, DENSE_K entries at a time, as positions (low-face
 //    images pre-shifted by -L) and (v, m) in its own shared-memory slice.  Each lane's window
 //    (the exact per-particle bound) is found by bisection inside the chunk; a
 //    further chunk is staged only while some lane's window runs past the current one, so a
-//    huge neighbour cell costs only its near part.  The self cell is swept whole, chunk by
-//    chunk.
+//    huge neighbour cell costs only its near part.  The home cell itself is swept the same
+//    way along its z list, up and down from the warp's lowest position (R19): a
+//    cell of n particles with H << C_l costs ~n 2H/C_l candidates per particle, not n.
 //  * Hits go to the lane's LIFO stack and are drained two at a time with FFMA2 (as in
 //    k_density_v4); a chunk's hits are drained before the chunk is overwritten.  Sums stay
 //    in registers; one 64-byte record per particle at its input index (no atomics).
@@ -27,7 +29,9 @@ namespace pvsph {
 constexpr int DENSE_WARPS = 8;
 constexpr int DENSE_K = 256;             // staged entries per chunk (per warp)
 constexpr int DENSE_Q = 16;              // hit stack depth per lane
-constexpr size_t DENSE_WARP_SMEM = (size_t)DENSE_K * 32 + (size_t)DENSE_Q * 32 * 2;
+constexpr int DENSE_MAP = 256;           // home rank -> sorted position map of one tile part (>= V4_TP)
+constexpr size_t DENSE_WARP_SMEM = (size_t)DENSE_K * 32 + (size_t)DENSE_Q * 32 * 2 + (size_t)DENSE_MAP * 2;
+static_assert(DENSE_MAP >= V4_TP, "a tile part holds at most V4_TP home particles");
 constexpr size_t DENSE_SMEM = DENSE_WARP_SMEM * DENSE_WARPS;
 
 template <bool COUNT>
@@ -44,6 +48,7 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
     float4 *V = P + DENSE_K;
     const unsigned sP = smem_addr(P), sV = smem_addr(V);
     const unsigned sQ = smem_addr(V + DENSE_K) + 2u * lane;
+    uint16_t *pmap = reinterpret_cast<uint16_t *>(mine + (size_t)DENSE_K * 32 + (size_t)DENSE_Q * 32 * 2);
     if (threadIdx.x == 0) s_gen = *genp;
     __syncthreads();                                      // the only barrier: s_gen published
     unsigned cand[4] = {0, 0, 0, 0}, hits[4] = {0, 0, 0, 0}, band = 0;
@@ -66,11 +71,33 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
             const int lo = part == 0 ? max(q0, 0) : max(q0, na), hi = part == 0 ? min(q1, na) : min(q1, na + nb);
             if (lo >= hi) continue;
             const int cs = c.cell_start[hcell];
-            const int sbase = cs + (part == 0 ? lo : lo - na);
+            const int ncl = c.cell_start[hcell + 1] - cs;
+            const int nhome = part == 0 ? na : nb;
+            const int rlo = part == 0 ? lo : lo - na, rhi = part == 0 ? hi : hi - na;
             const HomeCell hc = home_cell(g, hcell);
-            for (int k0 = 0; k0 < hi - lo; k0 += 32) {
-                const bool active = k0 + lane < hi - lo;
-                const int i = sbase + k0 + (active ? lane : 0);
+            // The part's particles are the home particles of ranks [rlo, rhi) in the home cell's
+            // list along DENSE_SELF_DIR (home = in-cell index < nhome: home-first slots), so a
+            // warp's 32 lanes are neighbours along that axis and share their self-cell windows.
+            const uint16_t *Ls = c.ord + (long long)DENSE_SELF_DIR * c.cap + cs;
+            if (nhome == ncl) {
+                for (int r = lane; r < rhi - rlo; r += 32) pmap[r] = (uint16_t)(rlo + r);
+            } else {
+                int run = 0;                                  // home entries before position q0
+                for (int q0 = 0; q0 < ncl && run < rhi; q0 += 32) {
+                    const int q = q0 + lane;
+                    const bool home = q < ncl && (int)Ls[q] < nhome;
+                    const unsigned b = __ballot_sync(0xffffffffu, home);
+                    const int r = run + __popc(b & ((1u << lane) - 1u));
+                    if (home && r >= rlo && r < rhi) pmap[r - rlo] = (uint16_t)q;
+                    run += __popc(b);
+                }
+            }
+            __syncwarp();
+            for (int k0 = 0; k0 < rhi - rlo; k0 += 32) {
+                const bool active = k0 + lane < rhi - rlo;
+                const int pi = pmap[k0 + (active ? lane : 0)];       // this lane's sorted position
+                const int p0 = pmap[k0];                             // the warp's lowest
+                const int i = cs + Ls[pi];
                 float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f,
                       Hd = 0.f;
                 if (active) {
@@ -140,21 +167,52 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
                     }
                 };
 
-                // ---- the home cell: every j != i, chunk by chunk in slot order ------------------
-                {
-                    const int nh = c.cell_start[hcell + 1] - cs;
-                    hx = x; hy = y; hz = z;
-                    for (int j0 = 0; j0 < nh; j0 += DENSE_K) {
-                        const int kn = min(DENSE_K, nh - j0);
+                // One sorted sweep: staged chunks of the list L (entry q of the sweep = cell slot
+                // at(q)), positions pre-shifted by (px, py, pz); each lane's window is the leading
+                // entries with sep = (x_j - x_i) . a < H_i + delta (ascending along the sweep, up to
+                // the list order's disorder, which delta covers: R5), found by bisection inside
+                // the chunk; a further chunk is staged while some lane's window runs on.
+                auto windowed = [&](int nq, auto at, float ax, float ay, float az, float px, float py, float pz,
+                                    int kind, int skipq) {
+                    bool open = active;
+                    for (int j0 = 0; j0 < nq; j0 += DENSE_K) {
+                        if (!__any_sync(0xffffffffu, open)) break;
+                        const int kn = min(DENSE_K, nq - j0);
                         for (int e = lane; e < kn; e += 32) {
-                            P[e] = c.xyzh[cs + j0 + e];
-                            V[e] = c.vm[cs + j0 + e];
+                            const int jj = at(j0 + e);
+                            float4 p = c.xyzh[jj];
+                            p.x -= px; p.y -= py; p.z -= pz;
+                            P[e] = p;
+                            V[e] = c.vm[jj];
                         }
                         __syncwarp();
-                        sweep(0, active ? kn : 0, 0, i - cs - j0);
+                        int top = 1;
+                        while (2 * top <= kn) top <<= 1;
+                        int len = 0;
+                        for (int stp = top; stp > 0; stp >>= 1) {
+                            const int kk = len + stp;
+                            const bool v = open && kk <= kn;
+                            const float4 p = ldsr_f4(sP + 16u * (unsigned)(v ? kk - 1 : 0));
+                            const float sep = fmaf(ax, p.x - hx, fmaf(ay, p.y - hy, az * (p.z - hz)));
+                            if (v && sep < Hd) len = kk;
+                        }
+                        sweep(0, open ? len : 0, kind, skipq - j0);
                         drain_all();
+                        open = open && len == kn;
                         __syncwarp();
                     }
+                };
+
+                // ---- the home cell: along DENSE_SELF_DIR from the warp's lowest position p0, up
+                // (p0, p0 + 1, ...; i itself skipped) and down (p0 - 1, p0 - 2, ...) -------------
+                {
+                    float ax, ay, az;
+                    dir_unit(DENSE_SELF_DIR, ax, ay, az);
+                    hx = x; hy = y; hz = z;
+                    windowed(ncl - p0, [&](int q) { return cs + (int)Ls[p0 + q]; }, ax, ay, az, 0.f, 0.f, 0.f, 0,
+                             pi - p0);
+                    windowed(p0, [&](int q) { return cs + (int)Ls[p0 - 1 - q]; }, -ax, -ay, -az, 0.f, 0.f, 0.f, 0,
+                             -1 - (1 << 30));
                 }
                 // ---- the 26 neighbours: windows from the near end of the sorted lists ----------
                 for (int ox = -1; ox <= 1; ++ox)
@@ -177,35 +235,8 @@ __global__ void __launch_bounds__(DENSE_WARPS * 32, 2) k_density_dense(DevGrid g
                                         pz = sh[2] < 0 ? bz : 0.0f;
                             const int sj = c.cell_start[cj], nj = c.cell_start[cj + 1] - sj;
                             const uint16_t *L = c.ord + (long long)d * c.cap + sj;
-                            bool open = active;                    // this lane's window may go on
-                            for (int j0 = 0; j0 < nj; j0 += DENSE_K) {
-                                if (!__any_sync(0xffffffffu, open)) break;
-                                const int kn = min(DENSE_K, nj - j0);
-                                for (int e = lane; e < kn; e += 32) {
-                                    const int q = j0 + e;
-                                    const int jj = sj + L[sgn > 0 ? q : nj - 1 - q];
-                                    float4 p = c.xyzh[jj];
-                                    p.x -= px; p.y -= py; p.z -= pz;
-                                    P[e] = p;
-                                    V[e] = c.vm[jj];
-                                }
-                                __syncwarp();
-                                // window inside the chunk: leading entries with sep < H_i + delta
-                                int top = 1;
-                                while (2 * top <= kn) top <<= 1;
-                                int len = 0;
-                                for (int stp = top; stp > 0; stp >>= 1) {
-                                    const int kk = len + stp;
-                                    const bool v = open && kk <= kn;
-                                    const float4 p = ldsr_f4(sP + 16u * (unsigned)(v ? kk - 1 : 0));
-                                    const float sep = fmaf(ax, p.x - hx, fmaf(ay, p.y - hy, az * (p.z - hz)));
-                                    if (v && sep < Hd) len = kk;
-                                }
-                                sweep(0, open ? len : 0, kind, -1);
-                                drain_all();
-                                open = open && len == kn;
-                                __syncwarp();
-                            }
+                            windowed(nj, [&](int q) { return sj + (int)L[sgn > 0 ? q : nj - 1 - q]; }, ax, ay, az,
+                                     px, py, pz, kind, -1 - (1 << 30));
                         }
                 if (active) {
                     const float K3 = (16.0f / kPi) * Hinv * Hinv * Hinv;

@@ -59,7 +59,8 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
 }
 
 // Level passes: the list of cell j along direction d is read only when the
-// neighbour of j at offset +d or -d holds home particles of this grid; need[j] collects those
+// neighbour of j at offset +d or -d holds home particles of this grid, and a cell with home
+// particles reads its own list along DENSE_SELF_DIR (k_density_dense); need[j] collects those
 // directions as a 13-bit mask.
 __global__ void k_mark_needed(DevGrid g, const int *__restrict__ cell_nhome, int *__restrict__ need)
 {
@@ -67,6 +68,7 @@ __global__ void k_mark_needed(DevGrid g, const int *__restrict__ cell_nhome, int
     for (long long cell = blockIdx.x * (long long)blockDim.x + threadIdx.x; cell < g.ncell;
          cell += (long long)gridDim.x * blockDim.x) {
         if (cell_nhome[cell] == 0) continue;
+        atomicOr(&need[cell], 1 << DENSE_SELF_DIR);     // k_density_dense's self-cell sweep
         const int ixl = (int)(cell / plane), iy = (int)((cell / g.nz) % g.ny), iz = (int)(cell % g.nz);
         for (int ox = -1; ox <= 1; ++ox) {
             int jx = ixl + ox;
