@@ -46,6 +46,23 @@ __device__ __forceinline__ void count_lt(unsigned &r, unsigned a, unsigned b)
     asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(r) : "r"(a), "r"(b));
 }
 
+// The same for a, b < 2^31 as the sign bit of a - b (IMAD.IADD on the FMA pipe + LEA.HI):
+// mixing both forms spreads a rank loop over the FMA and ALU pipes (each takes one warp
+// instruction every two cycles), where compare + predicated add alone keep the ALU pipe full.
+__device__ __forceinline__ void count_lt_sign(unsigned &r, unsigned a, unsigned b)
+{
+    r += (a - b) >> 31;
+}
+
+#ifndef SORT_CNT_MODE
+#define SORT_CNT_MODE 1          // 0: compare + add only; 1: alternate with the sign form; 2: sign form only
+#endif
+__device__ __forceinline__ void count_lt_k(int k, unsigned &r, unsigned a, unsigned b)
+{
+    if (SORT_CNT_MODE == 2 || (SORT_CNT_MODE == 1 && (k & 1))) count_lt_sign(r, a, b);
+    else count_lt(r, a, b);
+}
+
 __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, double corner[3])
 {
     long long plane = (long long)g.ny * g.nz;
@@ -140,7 +157,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         double corner[3];
         cell_corner(g, cell, corner);
         // One particle per lane, all 13 directions ranked in one pass over the cell:
-        // composite = quantised key (25 bits) << 7 | in-cell index (the slot order is the
+        // composite = quantised key (25 bits) << 5 | in-cell index (the slot order is the
         // input order, so equal keys keep input order).  The fp32 key error (< 1e-6 C_l)
         // and the quantum 2 sqrt(3) C_l / 2^25 (~1e-7 C_l) are far below the window margin
         // delta = 2^-16 C_l; the density sweeps tolerate that much disorder.
@@ -162,7 +179,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             const float key = ((float)a0 * u0 + (float)a1 * u1 + (float)a2 * u2) * inv;
             // quantised key: floor((key + cmax) scale) as one FFMA and a rounding conversion
             const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
-            comp[d] = ((unsigned)qk << 7) | (unsigned)lane;
+            comp[d] = ((unsigned)qk << 5) | (unsigned)lane;     // < 2^30 (count_lt_sign)
             if (mine) S[lane * 16 + d] = comp[d];
         }
         __syncwarp();
@@ -174,13 +191,13 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             const uint4 c1 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 4]);
             const uint4 c2 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 8]);
             const unsigned c12 = S[m * 16 + 12];
-            count_lt(r[0], c0.x, comp[0]); count_lt(r[1], c0.y, comp[1]);
-            count_lt(r[2], c0.z, comp[2]); count_lt(r[3], c0.w, comp[3]);
-            count_lt(r[4], c1.x, comp[4]); count_lt(r[5], c1.y, comp[5]);
-            count_lt(r[6], c1.z, comp[6]); count_lt(r[7], c1.w, comp[7]);
-            count_lt(r[8], c2.x, comp[8]); count_lt(r[9], c2.y, comp[9]);
-            count_lt(r[10], c2.z, comp[10]); count_lt(r[11], c2.w, comp[11]);
-            count_lt(r[12], c12, comp[12]);
+            count_lt_k(0, r[0], c0.x, comp[0]); count_lt_k(1, r[1], c0.y, comp[1]);
+            count_lt_k(2, r[2], c0.z, comp[2]); count_lt_k(3, r[3], c0.w, comp[3]);
+            count_lt_k(4, r[4], c1.x, comp[4]); count_lt_k(5, r[5], c1.y, comp[5]);
+            count_lt_k(6, r[6], c1.z, comp[6]); count_lt_k(7, r[7], c1.w, comp[7]);
+            count_lt_k(8, r[8], c2.x, comp[8]); count_lt_k(9, r[9], c2.y, comp[9]);
+            count_lt_k(10, r[10], c2.z, comp[10]); count_lt_k(11, r[11], c2.w, comp[11]);
+            count_lt_k(12, r[12], c12, comp[12]);
         }
         if (mine) {
 #pragma unroll
@@ -379,8 +396,8 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_warp256(DevGrid g, Dev
 }
 
 // Cells of SORT_SMALL < n <= SORT_MED particles: one warp per cell, up to four particles per
-// lane, the 32-bit composites of k_sort_small (quantised key << 7 | in-cell index, n <= 128)
-// of one direction at a time in shared memory, ranked by counting.
+// lane, 31-bit composites (24-bit quantised key << 7 | in-cell index, n <= 128) of one
+// direction at a time in shared memory, ranked by counting.
 constexpr int SORT_MID_PER = SORT_MED / 32;
 
 __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCells c, uint16_t *ord,
@@ -393,7 +410,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
     unsigned *S = sh[w];
     const int nitems = *mid_count;
     const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
-    const float scale = 33554432.0f / (2.0f * cmax);
+    const float scale = 16777216.0f / (2.0f * cmax);   // 24-bit keys: composites < 2^31 (count_lt_sign)
     const float cmax_s = cmax * scale;
     for (int it = blockIdx.x * SORT_WARPS + w; it < nitems; it += gridDim.x * SORT_WARPS) {
         const long long cell = mid_items[it];
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
             for (int k = 0; k < SORT_MID_PER; ++k) {
                 const int e = lane + 32 * k;
                 const float key = ((float)a0 * u[k][0] + (float)a1 * u[k][1] + (float)a2 * u[k][2]) * inv;
-                const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
+                const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 16777215);
                 comp[k] = ((unsigned)qk << 7) | (unsigned)e;
                 if (e < n) S[e] = comp[k];
             }
@@ -432,7 +449,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
             for (int m = 0; m < n; ++m) {
                 const unsigned v = S[m];
 #pragma unroll
-                for (int k = 0; k < SORT_MID_PER; ++k) count_lt(r[k], v, comp[k]);
+                for (int k = 0; k < SORT_MID_PER; ++k) count_lt_k(k, r[k], v, comp[k]);
             }
 #pragma unroll
             for (int k = 0; k < SORT_MID_PER; ++k) {
