@@ -62,6 +62,13 @@ struct DevOut {
     int *nngb;
 };
 
+// The 13 directions as a constant table {a0, a1, a2, kind} (kind: 1 face, 2 edge, 3 corner),
+// the values of dir_component below; one LDC instead of the index arithmetic in loops that
+// run over d at run time (k_density_v5).
+__constant__ int4 c_dirs[13] = {{0, 0, 1, 1},  {0, 1, -1, 2}, {0, 1, 0, 1},  {0, 1, 1, 2},  {1, -1, -1, 3},
+                                {1, -1, 0, 2}, {1, -1, 1, 3}, {1, 0, -1, 2}, {1, 0, 0, 1},  {1, 0, 1, 2},
+                                {1, 1, -1, 3}, {1, 1, 0, 2},  {1, 1, 1, 3}};
+
 // The list along which k_density_dense orders a dense home cell's particles and sweeps the
 // cell itself (direction 0 = (0,0,1)); level passes sort it for every cell with home particles.
 constexpr int DENSE_SELF_DIR = 0;

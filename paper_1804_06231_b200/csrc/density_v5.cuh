@@ -323,9 +323,10 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
             hh[2 * k][1] = hh[2 * k + 1][1] = y;
             hh[2 * k][2] = hh[2 * k + 1][2] = z;
             if (k < nd) {
-                const int kind = v4_kind(d);
+                const int4 dv = c_dirs[d];
+                const int kind = dv.w;
                 const float sk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
-                const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                const int a0 = dv.x, a1 = dv.y, a2 = dv.z;
                 axv[k][0] = (float)a0;
                 axv[k][1] = (float)a1;
                 axv[k][2] = (float)a2;
@@ -358,7 +359,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         v5_windows2(top, amid, lim, hh, axv, Hkv, len);
 #pragma unroll 1
         for (int k = 0; k < nd; ++k) {
-            const int kind = v4_kind(d0 + k);
+            const int kind = c_dirs[d0 + k].w;
             // (selects, not indexing: the loop is not unrolled, to keep one copy of the drains)
             const int len0 = k ? len[2] : len[0], tot = len0 + (k ? len[3] : len[1]);
             const unsigned fl0k = k ? fl0v[1] : fl0v[0], fl1k = k ? fl1v[1] : fl1v[0];
@@ -557,7 +558,8 @@ __global__ void __launch_bounds__(V5_TP, V5_CTAS) k_density_v5(DevGrid g, DevCel
                 if (gs < ndseg) {
                     const int h = gs / 13, d = gs % 13;
                     const int r = h / T.nzh, q = h % T.nzh + 1;
-                    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                    const int4 dv = c_dirs[d];
+                    const int a0 = dv.x, a1 = dv.y, a2 = dv.z;
                     dsz[j] = tab[((a0 + 1) * 4 + a1 + r + 1) * T.nzs + q + a2].y +
                              tab[((-a0 + 1) * 4 - a1 + r + 1) * T.nzs + q - a2].y + 1 + (d == 0 ? 1 : 0);
                 }
@@ -623,7 +625,8 @@ __global__ void __launch_bounds__(V5_TP, V5_CTAS) k_density_v5(DevGrid g, DevCel
                     const int gs = gs2 >> 1, neg = gs2 & 1;
                     const int h = gs / 13, d = gs % 13, sg = neg ? -1 : 1;
                     const int r = h / T.nzh, q = h % T.nzh + 1;
-                    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+                    const int4 dv = c_dirs[d];
+                    const int a0 = dv.x, a1 = dv.y, a2 = dv.z;
                     const int4 ep = tab[((a0 + 1) * 4 + a1 + r + 1) * T.nzs + q + a2];
                     const int4 e = neg ? tab[((-a0 + 1) * 4 - a1 + r + 1) * T.nzs + q - a2] : ep;
                     const int mid = segoff[gs] + (d == 0 ? 1 : 0) + ep.y;
