@@ -267,12 +267,14 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
     };
     // keep every stack at <= V5_Q - 9 entries (8 pushes follow before the next check); drain
     // four per lane when most lanes hold four
+    // (one warp reduction: lanes holding >= 2 NP count 1, lanes near a full stack count 32, so
+    // the sum reaches V5_TRIG <= 32 iff V5_TRIG lanes hold 2 NP or some stack is nearly full)
+    static_assert(V5_TRIG <= 32 && V5_Q - V5_CHK >= 2 * V5_NP, "drain trigger encoding");
     auto drain_check = [&]() {
         for (;;) {
             const unsigned n = (qp - sQ) >> 6;
-            if (!(__popc(__ballot_sync(0xffffffffu, n >= 2 * V5_NP)) >= V5_TRIG ||
-                  __any_sync(0xffffffffu, n >= V5_Q - V5_CHK)))
-                break;
+            const unsigned vote = (n >= 2 * V5_NP ? 1u : 0u) + (n >= V5_Q - V5_CHK ? 32u : 0u);
+            if (__reduce_add_sync(0xffffffffu, vote) < (unsigned)V5_TRIG) break;
             drain(std::integral_constant<int, V5_NP>{});
         }
     };
