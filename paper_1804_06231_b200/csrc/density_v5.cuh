@@ -147,6 +147,10 @@ __device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], con
                                             const float ax[2][3], const float Hk[4], int len[4])
 {
     unsigned a[4] = {amid[0], amid[0] - 2u, amid[1], amid[1] - 2u};   // + side: L[mid]; - side: L[mid - 1]
+    // (x_j - h, y_j - h) as one FADD2 against the negated home pair: the same bits as two FADDs
+    f2 nh[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nh[k] = pk(-h[k][0], -h[k][1]);
     for (int st = top; st > 0; st >>= 1) {
         const unsigned s2 = 2u * (unsigned)st;
         unsigned pa[4];
@@ -165,8 +169,9 @@ __device__ __forceinline__ void v5_windows2(int top, const unsigned amid[2], con
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const float *A = ax[k >> 1];
-            const float dx = p[k].x - h[k][0], dy = p[k].y - h[k][1], dz = p[k].z - h[k][2];
-            const float sv = fmaf(A[0], dx, fmaf(A[1], dy, A[2] * dz));
+            const f2 dxy = add2(pk(p[k].x, p[k].y), nh[k]);
+            const float dz = p[k].z - h[k][2];
+            const float sv = fmaf(A[0], dxy.x, fmaf(A[1], dxy.y, A[2] * dz));
             sp[k] = (k & 1) ? -sv : sv;
         }
         if (sp[0] < Hk[0]) a[0] = pa[0];
@@ -204,6 +209,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         Hd = (float)H + g.delta0;                          // + 2 max_dx of the neighbour cell, per segment
     }
     const float xs = x - g.boxf[0], ys = y - g.boxf[1], zs = z - g.boxf[2];   // exact where used (x >= L/2)
+    const f2 nxy = pk(-x, -y);
     const f2 nHinv = bc2(-Hinv);
     auto scell = [&](int ox, int oy, int oz) { return ((ox + 1) * 4 + oy + yoff + 1) * S.nzs + qh + oz; };
     const int4 eh = S.tab[scell(0, 0, 0)];
@@ -291,8 +297,9 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                 const bool ok = tt < total && tt != kh;
                 const unsigned e = ok ? pa + 16u * (unsigned)tt : S.sent;
                 const float4 p = ldsr_f4(e);
-                const float dx = x - p.x, dy = y - p.y, dz = z - p.z;
-                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                const f2 dxy = add2(pk(p.x, p.y), nxy);          // (x_j - x_i, y_j - y_i): one FADD2
+                const float dz = z - p.z;
+                const float r2 = fmaf(dxy.x, dxy.x, fmaf(dxy.y, dxy.y, dz * dz));
                 if (COUNT) {
                     cand[0] += ok ? 1u : 0u;
                     band += ok && fabsf(r2 - H2) < 1e-6f * H2 ? 1u : 0u;
@@ -379,13 +386,17 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
 #pragma unroll
                 for (int u = 0; u < NU; ++u) {
                     const float4 p = pp[u];
-                    float hx = x, hy = y, hz = z;
                     unsigned fl = 0;
+                    float dx, dy, dz;
                     if (FRAMES) {
+                        float hx = x, hy = y, hz = z;
                         fl = t + u < len0 ? fl0k : fl1k;
                         home_of(fl, hx, hy, hz);
+                        dx = hx - p.x; dy = hy - p.y; dz = hz - p.z;
+                    } else {
+                        const f2 dxy = add2(pk(p.x, p.y), nxy);  // one FADD2; squares as before
+                        dx = dxy.x; dy = dxy.y; dz = z - p.z;
                     }
-                    const float dx = hx - p.x, dy = hy - p.y, dz = hz - p.z;
                     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
                     if (COUNT) {
                         cand[kind] += t + u < tot ? 1u : 0u;
