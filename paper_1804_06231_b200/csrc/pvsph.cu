@@ -53,6 +53,8 @@ const DevAttrs &dev_attrs(int dev)
         cudaFuncSetAttribute(k_density_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DENSE_SMEM);
         cudaFuncSetAttribute(k_stable_radix<STABLE_BT_MAX, STABLE_BT_T, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, stable_radix_smem(STABLE_BT_MAX, STABLE_BT_T));
+        cudaFuncSetAttribute(k_sort_radix<65535, SORT_GIANT_T, false, true, 2>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, radix_smem_global(SORT_GIANT_T));
         cudaFuncSetAttribute(k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T));
         cudaFuncSetAttribute(k_density_pair_staged<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PAIR_SMEM);
@@ -396,8 +398,11 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
         mid_items, huge_count + 2, w256_items, huge_count + 3, need);
     k_sort_mid<<<148 * 8, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, mid_items, huge_count + 2, need);
     k_sort_warp256<<<148 * 4, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, w256_items, huge_count + 3, need);
-    k_sort_big<<<148 * 4, SORT_BIG_CHUNK, 0, s>>>(g, c, cells->order, big_items, big_count, need);
     if ((rc = ensure_attrs()) != SPH_OK) return rc;
+    // cells above SORT_HUGE_MAX: key/index buffers in the build's record region (free after it)
+    k_sort_radix<65535, SORT_GIANT_T, false, true, 2><<<148, SORT_GIANT_T, radix_smem_global(SORT_GIANT_T), s>>>(
+        g, c, cells->order, reinterpret_cast<const int *>(big_items), big_count, 0, need,
+        at<unsigned>(ws, w.rec));
     k_sort_radix<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, radix_smem(SORT_MED_MAX, SORT_MED_T), s>>>(
         g, c, cells->order, huge_items, huge_count, (int)w.huge_cap, need);
     k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T), s>>>(

@@ -12,9 +12,7 @@
 // Cells of up to SORT_MED = 128: k_sort_mid, one warp per cell, same composites.
 // Cells of up to SORT_W256 = 256: k_sort_warp256, a register bitonic sort per warp.
 // Medium/huge cells: stable LSD radix sorts in shared memory (k_sort_radix).  Cells above
-// SORT_HUGE_MAX are queued as (cell, chunk) items and ranked by k_sort_big, one
-// CTA per chunk of SORT_BIG_CHUNK elements, streaming the cell's 64-bit
-// composites (orderable fp32 key << 32 | input index) through shared memory.
+// SORT_HUGE_MAX: the same radix sort with its key/index buffers in global scratch (L2).
 #pragma once
 
 #include "common.cuh"
@@ -36,8 +34,7 @@ constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 512 threads, 225 KB; abo
 #endif
 constexpr int SORT_HUGE_T = SORT_HUGE_THREADS;
 constexpr int SORT_WARPS = 8;
-constexpr int SORT_BIG_CHUNK = 256;
-constexpr int SORT_BIG_TILE = 2048;
+constexpr int SORT_GIANT_T = 1024;      // cells above SORT_HUGE_MAX (k_sort_radix<GLOBAL>)
 
 // r += (a < b) as a compare and a predicated add (the compiler's select form costs three
 // instructions per comparison in the rank loops below)
@@ -146,12 +143,8 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             if (lane == 0) mid_items[atomicAdd(mid_count, 1)] = (int)cell;
             continue;
         }
-        if (n > SORT_SMALL) {
-            if (lane == 0) {
-                int nch = (n + SORT_BIG_CHUNK - 1) / SORT_BIG_CHUNK;
-                int pos = atomicAdd(big_count, nch);
-                for (int k = 0; k < nch; ++k) big_items[pos + k] = make_int2((int)cell, k);
-            }
+        if (n > SORT_SMALL) {                              // above SORT_HUGE_MAX: k_sort_radix<GLOBAL>
+            if (lane == 0) big_items[atomicAdd(big_count, 1)] = make_int2((int)cell, 0);
             continue;
         }
         double corner[3];
@@ -222,9 +215,16 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
 // memory: keys and indices double-buffered (12 B per element) plus 2 x 256 x NW counters.
 constexpr int radix_smem(int maxn, int t) { return maxn * 12 + 2 * 256 * (t / 32) * 4 + 64 * 4; }
 
-template <int MAXN, int T, bool FROM_BACK>
+// GLOBAL (cells above SORT_HUGE_MAX): the key and index buffers live in global scratch -- 12 B
+// per particle at the cell's own slots of the build's record region, free once the build is
+// done, so no allocation and no overlap between cells; they stay in L2 for a cell of up to
+// 65535 -- and only the counters in shared memory.  Items: every ISTRIDE-th int.
+constexpr int radix_smem_global(int t) { return 2 * 256 * (t / 32) * 4 + 64 * 4; }
+
+template <int MAXN, int T, bool FROM_BACK, bool GLOBAL = false, int ISTRIDE = 1>
 __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_t *ord, const int *items,
-                                                 const int *count, int cap, const int *__restrict__ need)
+                                                 const int *count, int cap, const int *__restrict__ need,
+                                                 unsigned *gscratch = nullptr)
 {
     constexpr int NW = T / 32;
     constexpr int NH = 256 * NW;                       // counters, [digit][warp]
@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_
     extern __shared__ unsigned rs[];
     unsigned *keyA = rs, *keyB = rs + MAXN;
     uint16_t *idxA = reinterpret_cast<uint16_t *>(rs + 2 * MAXN), *idxB = idxA + MAXN;
-    unsigned *histA = rs + 3 * MAXN, *histB = histA + NH;   // after the two u16 index arrays
+    unsigned *histA = GLOBAL ? rs : rs + 3 * MAXN;     // after the two u16 index arrays
+    unsigned *histB = histA + NH;
     unsigned *wsum = histB + NH;                       // [0, 32) warp totals, [32, 64) offsets
     const int nitems = *count;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -243,9 +244,16 @@ __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_
     const float scale = 16777216.0f / (2.0f * cmax);   // 2^24 over the key range
     const float cmax_s = cmax * scale;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const long long cell = items[FROM_BACK ? cap - 1 - it : it];
+        const long long cell = items[(long long)ISTRIDE * (FROM_BACK ? cap - 1 - it : it)];
         const int s0 = c.cell_start[cell];
         const int n = c.cell_start[cell + 1] - s0;
+        if (GLOBAL) {
+            unsigned *base = gscratch + 3ll * s0;
+            keyA = base;
+            keyB = base + n;
+            idxA = reinterpret_cast<uint16_t *>(base + 2 * n);
+            idxB = idxA + n;
+        }
         const int S = (n + NW - 1) / NW;
         const float invS = 1.0f / (float)S;            // segment of slot e: floor((e + 0.5) / S), exact here
         const int lo = min(n, w * S), hi = min(n, lo + S);
@@ -458,56 +466,6 @@ __global__ void __launch_bounds__(SORT_WARPS * 32) k_sort_mid(DevGrid g, DevCell
             }
             __syncwarp();
         }
-    }
-}
-
-// One CTA per (cell, chunk) item; grid-strides over the queued items.
-__global__ void __launch_bounds__(SORT_BIG_CHUNK) k_sort_big(DevGrid g, DevCells c, uint16_t *ord,
-                                                              const int2 *big_items, const int *big_count,
-                                                              const int *__restrict__ need)
-{
-    __shared__ unsigned long long tile[SORT_BIG_TILE];
-    const int nitems = *big_count;
-    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        int2 item = big_items[it];
-        long long cell = item.x;
-        int s0 = c.cell_start[cell];
-        int n = c.cell_start[cell + 1] - s0;
-        double corner[3];
-        cell_corner(g, cell, corner);
-        int e = item.y * SORT_BIG_CHUNK + threadIdx.x;
-        bool mine = e < n;
-        double u0 = 0, u1 = 0, u2 = 0;
-        unsigned tie = 0;
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (mine) {
-            p = c.xyzh[s0 + e];
-            u0 = (double)p.x - corner[0];
-            u1 = (double)p.y - corner[1];
-            u2 = (double)p.z - corner[2];
-            tie = (unsigned)c.perm[s0 + e];
-        }
-        const int mask = need ? need[cell] : 0x1fff;
-        for (int d = 0; d < SPH_NDIR; ++d) {
-            if (!((mask >> d) & 1)) continue;          // CTA-uniform
-            float key = mine ? pv_key(u0, u1, u2, d) : 0.0f;
-            unsigned long long comp = ((unsigned long long)float_order(key) << 32) | tie;
-            int r = 0;
-            for (int t0 = 0; t0 < n; t0 += SORT_BIG_TILE) {
-                int tn = min(SORT_BIG_TILE, n - t0);
-                __syncthreads();
-                for (int m = threadIdx.x; m < tn; m += blockDim.x) {
-                    float4 p = c.xyzh[s0 + t0 + m];
-                    float km = pv_key((double)p.x - corner[0], (double)p.y - corner[1], (double)p.z - corner[2], d);
-                    tile[m] = ((unsigned long long)float_order(km) << 32) | (unsigned)c.perm[s0 + t0 + m];
-                }
-                __syncthreads();
-                if (mine)
-                    for (int m = 0; m < tn; ++m) r += tile[m] < comp;
-            }
-            if (mine) ord[(long long)d * c.cap + s0 + r] = (uint16_t)e;
-        }
-        __syncthreads();
     }
 }
 

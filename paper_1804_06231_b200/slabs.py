@@ -30,7 +30,7 @@ import torch
 from . import api as pv
 
 BUILD_LAUNCHES = 8      # k_bin, 3 scan kernels, k_scatter_rec, k_stable_small/bitonic/big
-SORT_LAUNCHES = 6       # k_sort_small, k_sort_mid, k_sort_warp256, k_sort_big, k_sort_radix (medium, huge)
+SORT_LAUNCHES = 6       # k_sort_small, k_sort_mid, k_sort_warp256, k_sort_radix (medium, huge, giant)
 SELECT_LAUNCHES = 5     # sph_select_planes: k_sel_count, 3 scan kernels, k_sel_write
 DENSITY_LAUNCHES = 9    # k_row_home, k_v4_tiles (count), 3 scan kernels, k_v4_tiles (write), k_density_v5,
                         # k_density_dense, k_unpermute
