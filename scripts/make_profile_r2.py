@@ -209,6 +209,12 @@ All numbers come from one `gpurun` call (`scripts/round2_measure.sh {tag}`), sum
 `ncu_density_c5_raw.csv` (every metric of one `--set full` capture of `k_density_v5<0>` at c5),
 `test27cells.json`, `calib.json`.
 
+Reproduce (one B200): `gpurun -- 'bash scripts/round2_measure.sh TAG'`, then here
+`python scripts/make_profile_r2.py TAG`.  The measurement script runs the GPU tests and smoke
+(unless `notests`), every bench line, test27cells, the calibration, the CPU baselines, the
+ncu counter captures (`scripts/ncu_fp32.sh`), the launch lists and one `--set full` capture;
+each ncu command only after the same command exited 0 without ncu.
+
 ## bench.py lines
 
 Roofline columns: `useful` = algorithmic flops (8 per candidate + 48 per interaction, SURVEY
