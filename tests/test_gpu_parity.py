@@ -315,11 +315,11 @@ def test_cell_occupancy_tile_boundaries(pv, occ):
 
 
 @pytest.mark.parametrize("occ,qbits", [(33, 24), (200, 24), (300, 24), (1025, 24), (2000, 24), (2000, 5),
-                                       (5000, 24), (12000, 4), (16300, 24), (16385, 24)])
+                                       (5000, 24), (12000, 4), (16300, 24), (16385, 24), (30000, 6)])
 def test_sort_big_cells(pv, occ, qbits):
     """Sorted lists of one dense cell on every sort path: warp ranking (~35), warp bitonic
-    (~200), shared-memory radix sort (~300 .. ~16300), chunked ranking above it (16385 +
-    background).  Each list is a permutation of the cell, ascending in the oracle's fp64
+    (~200), shared-memory radix sort (~300 .. ~16300), the radix sort with global scratch above
+    it (16385, 30000 + background).  Each list is a permutation of the cell, ascending in the oracle's fp64
     projection (fp32 rounding allowed), equal fp32 keys in input order; qbits < 24 puts the
     particles on a coarse lattice, so most keys are shared (the stability of the radix passes)."""
     rng = np.random.default_rng(occ + qbits)
