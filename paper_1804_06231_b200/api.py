@@ -340,7 +340,7 @@ class ReuseLoop:
         self.max_disp = torch.zeros(1, dtype=torch.float32, device=device)
 
     def _build(self, stream=None):
-        sph_build_cells(self.dp.grid, self.x, self.v, self.dp.cells, self.dp.ws, stream=stream)
+        sph_build_cells(self.dp.grid, self.x, self.v, self.dp.cells, self.dp.ws, n_own=self.n, stream=stream)
         sph_sort_cells(self.dp.grid, self.dp.cells, self.dp.ws, stream=stream)
         self.bound = 0.0
         self.max_disp.zero_()

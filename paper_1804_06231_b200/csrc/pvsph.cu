@@ -1,6 +1,7 @@
 // pvsph.cu -- C ABI of libpvsph.so (include/sph.h): argument checking,
 // workspace layout and kernel launches.  One translation unit (the kernels
 // live in the .cuh files) compiled for sm_100a only.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -647,10 +648,12 @@ int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *o
     // scratch: the phase's pair list in the build's record region, its count in big_count
     int2 *pairs = at<int2>(ws, w.rec);
     int *count = at<int>(ws, w.big_count);
-    if (sizeof(ParticleRec) * (size_t)(cells->capacity > 0 ? cells->capacity : 1) < 8 * (size_t)g.ncell)
-        return SPH_EINVAL;
+    // a phase lists at most one pair per non-empty cell, so at most min(ncell, capacity) pairs:
+    // two such lists (the phase's pairs, the deferred large ones) = 16 B per stored slot, inside
+    // the 64 B per slot of the record region
+    const long long maxp = std::min<long long>(g.ncell, cells->capacity > 0 ? cells->capacity : 1);
+    static_assert(sizeof(ParticleRec) >= 16, "two int2 pair lists per stored slot");
     const int gen_blocks = grid_blocks(g.n_owned_cells, 256, 148 * 8);
-    const long long maxp = g.ncell;
     // self cells (every ordered pair i != j and the self term): one warp per cell, exclusive
     if ((e = cudaMemsetAsync(count, 0, 4, s)) != cudaSuccess) return cuda_fail(e);
     k_sym_phase_pairs<<<gen_blocks, 256, 0, s>>>(g, dc.cell_start, -1, 0, pairs, count);
@@ -666,10 +669,9 @@ int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *o
     }
     // the 13 directions x colours: symmetric pairs, no atomics
     // pairs with a cell above SYMW_MAXN: deferred to the CTA form (list after the phase's pairs,
-    // count in big_count + 1) when the scratch has room, else swept from global memory in place
-    const bool defer = sizeof(ParticleRec) * (size_t)cells->capacity >= 16 * (size_t)g.ncell;
-    int2 *big = defer ? pairs + g.ncell : nullptr;
-    int *big_n = defer ? count + 1 : nullptr;
+    // count in big_count + 1)
+    int2 *big = pairs + maxp;
+    int *big_n = count + 1;
     // per-slot accumulators in the output-record region (SlotAcc = sizeof(OutRec) per slot)
     static_assert(sizeof(SlotAcc) == sizeof(OutRec), "slot accumulators reuse the output-record region");
     SlotAcc *sacc = at<SlotAcc>(ws, w.orec);
@@ -687,7 +689,6 @@ int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *o
             else
                 k_density_pair_sym<false, true, SYMW_MAXN, 1, SYMW_WARPS><<<wblocks, SYMW_WARPS * 32, SYMW_SMEM, s>>>(
                     g, dc, o, pairs, maxp, nullptr, status, count, big, big_n, sacc);
-            if (!defer) continue;
             const int blocks = 148 * 3;
             if (stats)
                 k_density_pair_sym<true, true><<<blocks, SYM_WARPS * 32, SYM_SMEM, s>>>(

@@ -271,6 +271,24 @@ def test_permutation_invariance(pv):
 # ---------------------------------------------------------------------------
 # edge cases
 # ---------------------------------------------------------------------------
+def test_zero_particles(pv):
+    """N = 0 through every call of the pass (build, sort, gather and symmetric density, reuse
+    drift): status OK, empty outputs, no launch error."""
+    x = torch.zeros((0, 4), dtype=torch.float32, device="cuda")
+    dp = pv.DensityPass(4, 0)
+    st = pv.Stats()
+    out = dp.run(x, x.clone(), stats=st)
+    dp.check()
+    assert out.to_numpy()["rho"].shape == (0,)
+    assert sum(st.read()["cand"]) == 0
+    pv.sph_density_all_sym(dp.grid, dp.cells, dp.out, dp.ws)
+    dp.check()
+    loop = pv.ReuseLoop(4, 0, 0.01 / 4)
+    loop.start(x.clone(), x.clone())
+    loop.step(0.0)
+    loop.check()
+
+
 def test_single_and_two_particles(pv):
     xyzh = np.array([[0.3, 0.6, 0.9, 0.1]], np.float32)
     vm = np.array([[0.4, -1.0, 2.0, 0.25]], np.float32)

@@ -77,3 +77,11 @@ def test_sym_all_on_slab_with_ghosts(pv):
     got = out.to_numpy()
     ref = oracle.celllist(p.xyzh, p.vm, p.nc, targets=r.slab.gid)
     compare(got, ref, None, "sym slab")
+
+
+def test_sym_all_sparse_grid(pv):
+    """Far more cells than particles (the phase pair lists are bounded by the stored particles,
+    not by the cells): 300 particles on a 12^3 grid == the oracle."""
+    p = synth.tiny_random_set(seed=41, n=300, nc=12, h_frac=0.9)
+    got, _ = _sym(pv, p)
+    compare(got, oracle.bruteforce(p.xyzh, p.vm), None, "sym sparse")
