@@ -289,6 +289,26 @@ def test_zero_particles(pv):
     loop.check()
 
 
+def test_empty_cell_and_pair_lists(pv):
+    """sph_density_self / sph_density_pair / sph_density_pair_sym with empty lists: no launch
+    error, the accumulators untouched."""
+    p = synth.make("c1")
+    x, v = torch.from_numpy(p.xyzh).cuda(), torch.from_numpy(p.vm).cuda()
+    dp = pv.DensityPass(p.nc, p.n)
+    pv.sph_build_cells(dp.grid, x, v, dp.cells, dp.ws)
+    pv.sph_sort_cells(dp.grid, dp.cells, dp.ws)
+    acc = pv.Out.alloc(p.n)
+    acc.zero_()
+    empty1 = torch.zeros(0, dtype=torch.int32, device="cuda")
+    empty2 = torch.zeros((0, 2), dtype=torch.int32, device="cuda")
+    pv.sph_density_self(dp.grid, dp.cells, empty1, acc, dp.ws)
+    pv.sph_density_pair(dp.grid, dp.cells, empty2, acc, dp.ws)
+    pv.sph_density_pair_sym(dp.grid, dp.cells, empty2, acc, dp.ws)
+    dp.check()
+    got = acc.to_numpy()
+    assert all(np.all(got[k] == 0) for k in got)
+
+
 def test_single_and_two_particles(pv):
     xyzh = np.array([[0.3, 0.6, 0.9, 0.1]], np.float32)
     vm = np.array([[0.4, -1.0, 2.0, 0.25]], np.float32)

@@ -42,7 +42,7 @@ def test_sym_all_vs_oracle(pv, cfg):
     assert sum(st["hits"]) == int(got["nngb"].astype(np.int64).sum())
 
 
-@pytest.mark.parametrize("nc", [5, 7, 8])
+@pytest.mark.parametrize("nc", [3, 4, 5, 7, 8])
 def test_sym_all_odd_and_even_grids(pv, nc):
     """Odd periodic axes need the third colour (cells nc-1 and 0 are neighbours)."""
     p = synth.tiny_random_set(seed=30 + nc, n=60 * nc ** 3, nc=nc, h_frac=0.8)
