@@ -46,11 +46,12 @@ constexpr int V5_Q = V5_Q_DEPTH;                       // hit stack depth per la
 #ifndef V5_NP
 #define V5_NP 2        // packed pairs per drain round (2 NP hits per lane)
 #endif
+constexpr int V5_GUARD = 2 * V5_NP;                    // of which padding guard slots (see v5_particle)
 #ifndef V5_TRIG
 #define V5_TRIG 24     // drain when this many lanes hold 2 NP hits
 #endif
 #ifndef V5_CHK
-#define V5_CHK 8       // candidates between drain checks (stacks kept below V5_Q - V5_CHK)
+#define V5_CHK 8       // candidates between drain checks (stacks kept below V5_Q - V5_GUARD - V5_CHK)
 #endif
 constexpr int V5_MS = V4_MS;                           // staged particles (+1 sentinel)
 constexpr int V5_ML = V4_ML + 14 * V4_MAXH;            // list entries + sentinels: one per (home cell, direction) + one per home cell
@@ -196,7 +197,11 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                                             unsigned qbase, bool active, int i, int yoff, int qh, int lpos,
                                             unsigned cand[4], unsigned hits[4], unsigned &band)
 {
-    const unsigned sQ = qbase + 2u * (threadIdx.x & 31);
+    // The lane's stack column: V5_GUARD guard slots holding the drain padding, then the entries
+    // (sQ = the first entry slot): a drain pops 2 NP entries unconditionally, and a lane holding
+    // fewer reads padding -- no per-entry test.
+    const unsigned sQg = qbase + 2u * (threadIdx.x & 31);
+    const unsigned sQ = sQg + 64u * V5_GUARD;
     float x = 0.f, y = 0.f, z = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, m = 0.f, H2 = -1.f, Hinv = 0.f, Hd = 0.f;
     if (active) {
         const float4 a = c.xyzh[i];
@@ -219,6 +224,11 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
     A.rho = A.wc = A.srt = A.st = A.Dq = A.Px = A.Nx = A.Py = A.Ny = A.Pz = A.Nz = zero2();
     unsigned qp = sQ;                                     // stack top (next free slot)
     int npop = 0;
+    {
+        const unsigned pad = FRAMES ? (S.pad - S.sb) >> 4 : S.pad;   // staged index V5_MS + 1, frame 0
+#pragma unroll
+        for (int k = 0; k < V5_GUARD; ++k) sts_u16_push(sQg + 64u * k, pad);
+    }
 
     auto home_of = [&](unsigned fl, float &hx, float &hy, float &hz) {
         hx = (fl & 1u) ? xs : x;
@@ -235,7 +245,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         const unsigned take = min(n, 2u * NP);
         unsigned qv[2 * NP];
 #pragma unroll
-        for (int s2 = 0; s2 < 2 * NP; ++s2) qv[s2] = (unsigned)s2 < take ? lds_u16(qp - 64u * (s2 + 1)) : 0xffffffffu;
+        for (int s2 = 0; s2 < 2 * NP; ++s2) qv[s2] = lds_u16(qp - 64u * (s2 + 1));   // below sQ: padding
         qp -= 64u * take;
         npop += (int)take;
 #ifdef V5_STATS
@@ -253,10 +263,10 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                 const unsigned qq = qv[2 * pr + k];
                 hxv[k] = x; hyv[k] = y; hzv[k] = z;
                 if (FRAMES) {
-                    e[k] = qq == 0xffffffffu ? S.pad : S.sb + ((qq & 0xfffu) << 4);
-                    if (qq != 0xffffffffu) home_of(qq >> 12, hxv[k], hyv[k], hzv[k]);
+                    e[k] = S.sb + ((qq & 0xfffu) << 4);
+                    home_of(qq >> 12, hxv[k], hyv[k], hzv[k]);
                 } else {
-                    e[k] = qq == 0xffffffffu ? S.pad : qq;
+                    e[k] = qq;
                 }
             }
             const float4 p0 = ldsr_f4(e[0]), p1 = ldsr_f4(e[1]);
@@ -271,15 +281,17 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                       pk(v0.y - vy, v1.y - vy), pk(v0.z - vz, v1.z - vz), A);
         }
     };
-    // keep every stack at <= V5_Q - 9 entries (8 pushes follow before the next check); drain
+    // keep every stack below V5_Q - V5_GUARD - V5_CHK entries (V5_CHK pushes follow before the next check); drain
     // four per lane when most lanes hold four
     // (one warp reduction: lanes holding >= 2 NP count 1, lanes near a full stack count 32, so
     // the sum reaches V5_TRIG <= 32 iff V5_TRIG lanes hold 2 NP or some stack is nearly full)
-    static_assert(V5_TRIG <= 32 && V5_Q - V5_CHK >= 2 * V5_NP, "drain trigger encoding");
+    static_assert(V5_TRIG <= 32 && V5_Q - V5_GUARD - V5_CHK >= 2 * V5_NP, "drain trigger encoding");
+    static_assert(V5_GUARD >= 2 * V5_NP, "a drain may read 2 NP slots below an empty stack");
+    static_assert(V5_MS + 1 < 4096, "the padding's staged index fits the 12-bit FRAMES field");
     auto drain_check = [&]() {
         for (;;) {
             const unsigned n = (qp - sQ) >> 6;
-            const unsigned vote = (n >= 2 * V5_NP ? 1u : 0u) + (n >= V5_Q - V5_CHK ? 32u : 0u);
+            const unsigned vote = (n >= 2 * V5_NP ? 1u : 0u) + (n >= V5_Q - V5_GUARD - V5_CHK ? 32u : 0u);
             if (__reduce_add_sync(0xffffffffu, vote) < (unsigned)V5_TRIG) break;
             drain(std::integral_constant<int, V5_NP>{});
         }
