@@ -59,6 +59,15 @@ for c in ("c3", "c4", "c5"):
         shutil.copy(p, os.path.join(out, f"{tag}_fp32_{c}.csv"))
 if fp32:
     json.dump(fp32, open(os.path.join(out, "ncu_fp32.json"), "w"), indent=1)
+symfp = None
+for tg in (tag, "r2s"):
+    sp = os.path.join(go, f"{tg}_sym_fp32_c3.csv")
+    if os.path.exists(sp):
+        symfp = parse_fp32.parse_multi(sp)
+        symfp["source"] = os.path.basename(sp)
+        shutil.copy(sp, os.path.join(out, os.path.basename(sp)))
+        json.dump(symfp, open(os.path.join(out, "ncu_sym_c3.json"), "w"), indent=1)
+        break
 
 rep = g("prof_c5.ncu-rep")
 summ = ""
@@ -126,19 +135,21 @@ for name, d in benches.items():
     e2e = ("%.3e (%.1f ms/step)" % (e["value"], e.get("ms_per_step", float("nan"))) if e.get("value")
            else "n/a (not measured on this line; see c3/c4/c5)")
     cfg = name.replace("bench_", "")
-    fp = fp32.get(cfg) if cfg in ("c3", "c4", "c5") else None
+    fp = fp32.get(cfg) if cfg in ("c3", "c4", "c5") else (symfp if cfg == "sym_c3" else None)
     why = ("n/a (39 colour-phase launches per pass: no single-launch counter form)" if "sym" in name else
            "n/a (see the c5 line: same kernel)" if "reuse" in name else "n/a (no ncu counters)")
     if r.get("measured_frac"):
         meas = "%.3f (%.2f TFLOP/s)" % (r["measured_frac"], r["measured_tflops"])
     elif fp:
-        meas = "%.3f (%.2f TFLOP/s; ncu_fp32.json)" % (fp["measured_frac"], fp["fp32_tflops_measured"])
+        meas = "%.3f (%.2f TFLOP/s; %s)" % (fp["measured_frac"], fp["fp32_tflops_measured"],
+                                            "ncu_sym_c3.json, 78 launches summed" if cfg == "sym_c3" else "ncu_fp32.json")
     else:
         meas = why
     hbmf = ("%.3f" % r["hbm_frac"] if r.get("hbm_frac") is not None else
             "%.3f" % (fp["hbm_gbs"] / HBM) if fp else why)
     weff = ("%.3f" % r["warp_efficiency"] if r.get("warp_efficiency") is not None else
-            "%.3f" % fp["warp_efficiency"] if fp else why)
+            "%.3f" % fp["warp_efficiency"] if fp and "warp_efficiency" in fp else
+            "n/a (not in the summed counter set)" if fp else why)
     if "build" in st:
         stages = f"{st['build']:.2f} / {st['sort']:.2f} / {st['density']:.2f}"
     elif "density" in st:

@@ -59,6 +59,38 @@ def parse(path):
     }
 
 
+def parse_multi(path):
+    """Sum of the FP32 counters, DRAM bytes and durations over EVERY launch in the log (the
+    symmetric pass: 2 kernels per colour phase); fractions of the summed time."""
+    rows = list(csv.reader(open(path)))
+    h = next(i for i, r in enumerate(rows) if "Metric Name" in r)
+    hdr = rows[h]
+    mi, vi, ii = hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
+    per = {}
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        try:
+            per.setdefault(r[ii], {})[r[mi]] = float(r[vi].replace(",", ""))
+        except ValueError:
+            pass
+    pre = "sm__sass_thread_inst_executed_op_"
+    F = t = dram = fs = 0.0
+    peak_rate = 0.0
+    for m in per.values():
+        g = lambda k: m.get(k, 0.0)   # noqa: E731
+        F += (2 * g(pre + "ffma_pred_on.sum") + g(pre + "fadd_pred_on.sum") + g(pre + "fmul_pred_on.sum") +
+              4 * g(pre + "ffma2_pred_on.sum") + 2 * g(pre + "fadd2_pred_on.sum") + 2 * g(pre + "fmul2_pred_on.sum"))
+        dt = g("gpu__time_duration.sum") * 1e-9
+        t += dt
+        dram += g("dram__bytes_read.sum") + g("dram__bytes_write.sum")
+        peak_rate += g(pre + "ffma_pred_on.sum.peak_sustained") * 2 * g("sm__cycles_elapsed.avg.per_second") * dt
+    peak = peak_rate / t if t else 0.0
+    return {"launches": len(per), "duration_ms": t * 1e3, "fp32_flops_executed": F,
+            "fp32_tflops_measured": F / t / 1e12 if t else None, "fp32_peak_tflops_ncu": peak / 1e12,
+            "measured_frac": F / t / peak if peak else None, "dram_bytes": dram, "hbm_gbs": dram / t / 1e9 if t else None}
+
+
 def main():
     out = sys.argv[1]
     res = {}

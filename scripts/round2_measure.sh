@@ -23,6 +23,8 @@ timeout 300 python scripts/calibrate.py > ${O}_calib.json 2> ${O}_calib.err; ech
 timeout 900 python scripts/cpu_baselines.py > ${O}_cpu_baselines.json 2> ${O}_cpu_baselines.err; echo "cpu baselines rc=$?"
 # measured FP32 counters of the density kernel (c3, c4, c5)
 bash scripts/ncu_fp32.sh ${TAG} k_density_v5 c3 c4 c5
+# the same counters summed over one symmetric whole pass at c3 (78 launches)
+bash scripts/ncu_sym.sh ${TAG}
 # c5 launch list with DRAM bytes per launch (cold-cache, serialised)
 timeout 300 python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > ${O}_launchplain.json 2>&1 &&
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
