@@ -244,14 +244,17 @@ int sph_density_pair_sym(const sph_grid *grid, const sph_cells *cells, const int
  * symmetrically"): every unordered candidate pair is
  * evaluated once and both particles accumulate, with the ownership made
  * conflict-free by colouring instead of atomics: the self cells first, then
- * for each of the 13 directions d and each cell colour (parity per axis, a
- * third colour for the last cell of an odd periodic axis) one launch over
- * the pairs (c, c + d) of that colour -- two cells of a colour are >= 2
- * apart, so a launch writes disjoint particles (plain read-modify-writes,
- * each j summing its hits in ascending i: deterministic; a j hit by more
+ * for each of the 13 directions d and each colour of d's first nonzero axis
+ * (parity, a third colour for the last cell of an odd periodic axis) one
+ * launch over the pairs (c, c + d) of that colour -- two pairs of one
+ * direction share a cell only if their cells are neighbours on that axis,
+ * so a launch writes disjoint particles (plain read-modify-writes into
+ * per-slot accumulators in the workspace, merged into the outputs at the
+ * end; each j sums its hits in ascending i: deterministic; a j hit by more
  * than 32 i of one pair falls back to an atomic add).  Outputs final (as
  * sph_density_all), zeroed first.  Same cells/workspace contract as
- * sph_density_all. */
+ * sph_density_all (the workspace's record regions hold the phase pair lists
+ * and the accumulators). */
 int sph_density_all_sym(const sph_grid *grid, const sph_cells *cells, sph_out *out, sph_stats *stats, void *ws,
                         size_t ws_bytes, void *stream);
 
