@@ -6,7 +6,8 @@ states x_k = x_0 + k v dt:
   * full: every step re-bins and re-sorts (sph_build_cells + sph_sort_cells + sph_density_all
     on a grid without skin);
   * reuse: cells and lists built once on a grid with skin s, then every step is
-    sph_drift + sph_density_all with windows widened by 4 s.
+    sph_drift + sph_density_all with each neighbour cell's window widened by 2 max_dx(c)
+    (its particles' largest displacement since the build, R17).
 dt is chosen so that the K drifts stay inside the skin (K |v|max dt <= s).  Both are timed
 with CUDA events over the K steps (after warm-up on separate buffers); the line reports the
 ms per step of each, the candidate increase caused by the wider windows, and the largest
