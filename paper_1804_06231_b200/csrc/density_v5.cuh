@@ -40,7 +40,7 @@ constexpr int V5_TP = V4_TP;
 #define V5_CTAS 2
 #endif
 #ifndef V5_Q_DEPTH
-#define V5_Q_DEPTH 28
+#define V5_Q_DEPTH 30     // (two CTAs per SM leave ~1 KB of shared memory at 30)
 #endif
 constexpr int V5_Q = V5_Q_DEPTH;                       // hit stack depth per lane, 2-byte entries
 #ifndef V5_NP
