@@ -257,3 +257,16 @@ def test_split_migrants_rule():
     assert hi.tolist() == [False, False, False, True, False]
     lo, hi, keep = split_migrants(x, nc, 1.0, 0, 4)        # first slab: the left neighbour owns plane 9
     assert lo.tolist() == [False, False, False, False, True] and hi.tolist()[3]
+
+
+def test_sym_launch_count_matches_the_colour_phases():
+    """slabs.sym_launches (the bench's gpu_launches for --engine sym) counts the kernels of one
+    sph_density_all_sym call: 2 (self list + self kernel) + 3 per colour phase + 1 merge, with
+    2 or 3 colours on each direction's first nonzero axis (13 directions: 1 along z, 3 along y,
+    9 along x) -- the same rule as k_sym_phase_pairs / sym_dir_colours in density_pair.cuh."""
+    from paper_1804_06231_b200 import slabs
+    col = lambda n, per: 3 if per and n % 2 else 2      # noqa: E731
+    for nx, ny, nz, per in [(47, 47, 47, True), (8, 8, 8, True), (7, 5, 6, True), (25, 184, 184, False)]:
+        phases = col(nz, True) + 3 * col(ny, True) + 9 * col(nx, per)
+        assert slabs.sym_launches(nx, ny, nz, per) == 3 + 3 * phases
+    assert slabs.sym_launches(47, 47, 47, True) == 3 + 3 * 39
