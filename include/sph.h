@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 5
+#define SPH_ABI_VERSION 6
 
 #define SPH_OK 0
 #define SPH_EINVAL 1
@@ -299,6 +299,16 @@ int sph_drift(const sph_grid *grid, sph_cells *cells, float dt, float *max_disp,
  * are skipped. */
 int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xyzh_out, int64_t n_out,
                          void *stream);
+
+/* Ghost exchange helper (x-slabs): after a fixed-capacity
+ * exchange, rows [counts[k], cap) of received block k (k = 0, 1; block k at
+ * xyzh/vm + 4 * k * cap floats, device, 16-byte aligned) become the "dead"
+ * particle (dead_xyzh, dead_vm: 4 floats each, host values passed by value
+ * as arrays): a position in the receiver's own middle plane, which every
+ * level grid's sph_build_cells drops as a ghost outside its ghost planes.
+ * counts: device int64[2], read on the device (no host synchronisation). */
+int sph_mask_ghost_rows(float *xyzh, float *vm, int64_t cap, const int64_t *counts, const float dead_xyzh[4],
+                        const float dead_vm[4], void *stream);
 
 /* Ghost exchange helper (x-slabs): copies the owned
  * particles (xyzh_in/vm_in, n_own, device) whose x plane is the rank's

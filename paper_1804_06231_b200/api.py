@@ -252,6 +252,19 @@ def sph_select_planes(grid: SphGrid, xyzh: torch.Tensor, vm: torch.Tensor, n_own
                                          _stream(stream)), "sph_select_planes")
 
 
+def sph_mask_ghost_rows(recv_x: torch.Tensor, recv_v: torch.Tensor, counts: torch.Tensor, dead_x, dead_v,
+                        stream=None) -> None:
+    """Rows past counts[k] of the received ghost blocks recv_x/recv_v ((2, cap, 4) float32,
+    device) become the dead particle (dead_x, dead_v: 4 host floats each); counts: (2,) int64
+    device tensor, read on the device."""
+    assert recv_x.shape[0] == 2 and recv_x.shape == recv_v.shape and counts.dtype == torch.int64
+    assert recv_x.is_contiguous() and recv_v.is_contiguous()
+    fx = (ctypes.c_float * 4)(*[float(a) for a in dead_x])
+    fv = (ctypes.c_float * 4)(*[float(a) for a in dead_v])
+    _check(_lib.load().sph_mask_ghost_rows(_ptr(recv_x), _ptr(recv_v), recv_x.shape[1], _ptr(counts), fx, fv,
+                                           _stream(stream)), "sph_mask_ghost_rows")
+
+
 def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
     o = acc.struct()
     _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),

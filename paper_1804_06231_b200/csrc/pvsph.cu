@@ -504,6 +504,34 @@ int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xy
     return check_launch();
 }
 
+__global__ void k_mask_ghost_rows(float4 *x, float4 *v, long long cap, const long long *__restrict__ counts,
+                                  float4 dx, float4 dv)
+{
+    const long long n0 = counts[0], n1 = counts[1];
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < 2 * cap;
+         r += (long long)gridDim.x * blockDim.x) {
+        const long long k = r >= cap, row = r - k * cap;
+        if (row >= (k ? n1 : n0)) {
+            x[r] = dx;
+            v[r] = dv;
+        }
+    }
+}
+
+int sph_mask_ghost_rows(float *xyzh, float *vm, int64_t cap, const int64_t *counts, const float dead_xyzh[4],
+                        const float dead_vm[4], void *stream)
+{
+    if (cap < 0 || !counts || !dead_xyzh || !dead_vm || (cap > 0 && (!xyzh || !vm))) return SPH_EINVAL;
+    if (((uintptr_t)xyzh % 16) || ((uintptr_t)vm % 16)) return SPH_EINVAL;
+    if (cap == 0) return SPH_OK;
+    const float4 dx = make_float4(dead_xyzh[0], dead_xyzh[1], dead_xyzh[2], dead_xyzh[3]);
+    const float4 dv = make_float4(dead_vm[0], dead_vm[1], dead_vm[2], dead_vm[3]);
+    k_mask_ghost_rows<<<grid_blocks(2 * cap, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<float4 *>(xyzh), reinterpret_cast<float4 *>(vm), cap,
+        reinterpret_cast<const long long *>(counts), dx, dv);
+    return check_launch();
+}
+
 int sph_select_planes(const sph_grid *grid, int64_t n_own, const float *xyzh_in, const float *vm_in,
                       float *sel_xyzh, float *sel_vm, int64_t cap, int64_t *counts, void *ws, size_t ws_bytes,
                       void *stream)

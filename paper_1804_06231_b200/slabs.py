@@ -210,10 +210,16 @@ def exchange_fixed(dist, rank: int, world: int, send_x, send_v, send_n, recv_x, 
     return dist.batch_isend_irecv(ops)
 
 
-def mask_dead_ghosts(recv_x, recv_v, recv_n, dead_row_x, dead_row_v, ar):
+def mask_dead_ghosts(recv_x, recv_v, recv_n, dead_row_x, dead_row_v, ar, dead_host=None):
     """Rows beyond the received count of each ghost block become a 'dead' particle: inside the
     box but in an OWNED plane of this rank, so sph_build_cells drops it as a ghost outside the
-    ghost planes (no slot, no error).  Device-side (torch.where), no host synchronisation."""
+    ghost planes (no slot, no error).  On the GPU: the library's sph_mask_ghost_rows (counts
+    read on the device, no host synchronisation; dead_host = the dead rows' host values).  The
+    torch.where form serves the CPU (gloo) tests of the exchange only."""
+    if recv_x.is_cuda:
+        dx, dv = dead_host if dead_host is not None else (dead_row_x.tolist(), dead_row_v.tolist())
+        pv.sph_mask_ghost_rows(recv_x, recv_v, recv_n, dx, dv)
+        return
     for k in range(2):
         keep = (ar < recv_n[k])[:, None]
         recv_x[k].copy_(torch.where(keep, recv_x[k], dead_row_x))
@@ -281,9 +287,9 @@ class SlabRunner:
             self.ar = torch.arange(b, dtype=torch.int64, device=device)
             cl = slab.box / slab.nc
             xm = ((slab.x_lo + slab.x_hi) // 2 + 0.5) * cl
-            self.dead_x = torch.tensor([xm, 0.5 * slab.box, 0.5 * slab.box, 1e-6 * cl], dtype=torch.float32,
-                                       device=device)
-            self.dead_v = torch.tensor([0.0, 0.0, 0.0, 1.0], dtype=torch.float32, device=device)
+            self.dead_host = ([xm, 0.5 * slab.box, 0.5 * slab.box, 1e-6 * cl], [0.0, 0.0, 0.0, 1.0])
+            self.dead_x = torch.tensor(self.dead_host[0], dtype=torch.float32, device=device)
+            self.dead_v = torch.tensor(self.dead_host[1], dtype=torch.float32, device=device)
             self.comm = torch.cuda.Stream(device=device) if str(device).startswith("cuda") else None
         self.device = device
         # finer level grids (one GPU): own cells and workspace each, same outputs
@@ -338,7 +344,7 @@ class SlabRunner:
             for w in exchange_fixed(self.dist, self.rank, self.world, self.sel_x, self.sel_v, self.sel_n,
                                     rx, rv, self.recv_n):
                 w.wait()
-        mask_dead_ghosts(rx, rv, self.recv_n, self.dead_x, self.dead_v, self.ar)
+        mask_dead_ghosts(rx, rv, self.recv_n, self.dead_x, self.dead_v, self.ar, self.dead_host)
 
     # -- one step -----------------------------------------------------------
     def step(self, stats=None, events=None) -> None:
@@ -478,7 +484,7 @@ class FakeRanks:
             rv[1].copy_(right.sel_v[0])
             r.recv_n[0].copy_(left.sel_n[1])
             r.recv_n[1].copy_(right.sel_n[0])
-            mask_dead_ghosts(rx, rv, r.recv_n, r.dead_x, r.dead_v, r.ar)
+            mask_dead_ghosts(rx, rv, r.recv_n, r.dead_x, r.dead_v, r.ar, r.dead_host)
         for r in self.runners:
             r.compute()
         for r in self.runners:
@@ -666,7 +672,7 @@ class ReuseTransport:
             rv[1].copy_(right.sel_v[0])
             rr.recv_n[0].copy_(left.sel_n[1])
             rr.recv_n[1].copy_(right.sel_n[0])
-            mask_dead_ghosts(rx, rv, rr.recv_n, rr.dead_x, rr.dead_v, rr.ar)
+            mask_dead_ghosts(rx, rv, rr.recv_n, rr.dead_x, rr.dead_v, rr.ar, rr.dead_host)
 
     def _migrate(self):
         packs = [rr.pack_migrants() for rr in self.r]

@@ -179,3 +179,25 @@ def test_select_planes_capacity(pv):
     pv.sph_select_planes(g, x, v, s.n_own, sx, torch.empty_like(sx), cnt, ws)
     assert pv.sph_status(ws) == 3
     assert int(cnt[0]) > 8                       # the true count is still reported
+
+
+def test_mask_ghost_rows(pv):
+    """sph_mask_ghost_rows: rows past each received count become the dead particle, the rest
+    is untouched; counts read on the device (here 3 of 8 and 8 of 8, then 0 of 8)."""
+    import torch
+    cap = 8
+    x = torch.rand((2, cap, 4), dtype=torch.float32, device="cuda")
+    v = torch.rand((2, cap, 4), dtype=torch.float32, device="cuda")
+    x0, v0 = x.clone(), v.clone()
+    dx, dv = [0.5, 0.25, 0.125, 1e-6], [0.0, 0.0, 0.0, 1.0]
+    for counts in ([3, 8], [0, 5]):
+        x.copy_(x0)
+        v.copy_(v0)
+        n = torch.tensor(counts, dtype=torch.int64, device="cuda")
+        pv.sph_mask_ghost_rows(x, v, n, dx, dv)
+        torch.cuda.synchronize()
+        for k in range(2):
+            c = counts[k]
+            assert torch.equal(x[k, :c], x0[k, :c]) and torch.equal(v[k, :c], v0[k, :c])
+            assert torch.all(x[k, c:] == torch.tensor(dx, device="cuda"))
+            assert torch.all(v[k, c:] == torch.tensor(dv, device="cuda"))
