@@ -310,6 +310,31 @@ int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xy
 int sph_mask_ghost_rows(float *xyzh, float *vm, int64_t cap, const int64_t *counts, const float dead_xyzh[4],
                         const float dead_vm[4], void *stream);
 
+/* Slab migration on a list-reuse rebuild: a stable three-way
+ * partition of the owned particles (xyzh/vm float4, gid int64; device, n;
+ * positions already wrapped into the box, in ascending gid) by x plane --
+ * list "lo": the left neighbour's last plane x_lo - 1 (mod nc), list "hi":
+ * the right neighbour's first plane x_hi (mod nc), list "keep": the rest --
+ * each in input order, into the caller's buffers (capacities cap_*).
+ * counts: device int64[3] (lo, hi, keep).  A list longer than its capacity
+ * sets SPH_ECAPACITY in the status word (the copy is truncated).  Planes by
+ * the binning rule of sph_build_cells.  Workspace as for sph_build_cells
+ * with n_total >= n. */
+int sph_partition_migrants(const sph_grid *grid, int64_t n, const float *xyzh, const float *vm, const int64_t *gid,
+                           float *lo_xyzh, float *lo_vm, int64_t *lo_gid, int64_t cap_lo, float *hi_xyzh,
+                           float *hi_vm, int64_t *hi_gid, int64_t cap_hi, float *keep_xyzh, float *keep_vm,
+                           int64_t *keep_gid, int64_t cap_keep, int64_t *counts, void *ws, size_t ws_bytes,
+                           void *stream);
+
+/* Merge of three particle lists (xyzh/vm float4, id int64; device), each
+ * ascending in id, ids distinct across the lists, into one ascending list
+ * out_* of na + nb + nc particles (must not alias the inputs).  The counts
+ * are host values. */
+int sph_merge_by_id(int64_t na, const float *a_xyzh, const float *a_vm, const int64_t *a_gid, int64_t nb,
+                    const float *b_xyzh, const float *b_vm, const int64_t *b_gid, int64_t nc, const float *c_xyzh,
+                    const float *c_vm, const int64_t *c_gid, float *out_xyzh, float *out_vm, int64_t *out_gid,
+                    void *stream);
+
 /* Ghost exchange helper (x-slabs): copies the owned
  * particles (xyzh_in/vm_in, n_own, device) whose x plane is the rank's
  * first plane x_lo (list 0) or last plane x_hi - 1 (list 1), in input

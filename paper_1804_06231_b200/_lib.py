@@ -18,7 +18,8 @@ ERROR_NAMES = {0: "SPH_OK", 1: "SPH_EINVAL", 2: "SPH_EH_RANGE", 3: "SPH_ECAPACIT
 # declared in include/sph_calib.h.
 EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cells", "sph_sort_cells",
            "sph_density_self", "sph_density_pair", "sph_density_pair_sym", "sph_drift", "sph_gather_positions",
-           "sph_select_planes", "sph_mask_ghost_rows", "sph_density_finalize", "sph_density_all", "sph_density_all_sym", "sph_status",
+           "sph_select_planes", "sph_mask_ghost_rows", "sph_partition_migrants", "sph_merge_by_id",
+           "sph_density_finalize", "sph_density_all", "sph_density_all_sym", "sph_status",
            "sph_status_reset", "sph_strerror")
 
 
@@ -74,6 +75,10 @@ def load(path: str = LIB):
     L.sph_select_planes.argtypes = [G, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
     L.sph_mask_ghost_rows.argtypes = [c_vp, c_vp, c_i64, c_vp, ctypes.POINTER(ctypes.c_float),
                                       ctypes.POINTER(ctypes.c_float), c_vp]
+    L.sph_partition_migrants.argtypes = [G, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
+                                         c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
+    L.sph_merge_by_id.argtypes = [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                  c_vp, c_vp, c_vp, c_vp]
     L.sph_density_finalize.argtypes = [O, c_i64, c_vp]
     L.sph_density_all.argtypes = [G, C, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_all_sym.argtypes = [G, C, O, S, c_vp, ctypes.c_size_t, c_vp]
@@ -85,6 +90,7 @@ def load(path: str = LIB):
     L.sph_strerror.restype = ctypes.c_char_p
     for f in ("sph_build_cells", "sph_sort_cells", "sph_density_self", "sph_density_pair", "sph_density_pair_sym",
               "sph_drift", "sph_gather_positions", "sph_select_planes", "sph_mask_ghost_rows",
+              "sph_partition_migrants", "sph_merge_by_id",
               "sph_density_finalize",
               "sph_density_all", "sph_density_all_sym", "sph_status", "sph_status_reset"):
         getattr(L, f).restype = ctypes.c_int

@@ -265,6 +265,32 @@ def sph_mask_ghost_rows(recv_x: torch.Tensor, recv_v: torch.Tensor, counts: torc
                                            _stream(stream)), "sph_mask_ghost_rows")
 
 
+def sph_partition_migrants(grid: SphGrid, n: int, xyzh: torch.Tensor, vm: torch.Tensor, gid: torch.Tensor,
+                           lo, hi, keep, counts: torch.Tensor, ws: torch.Tensor, stream=None) -> None:
+    """Stable three-way split of the n owned particles (wrapped positions, ascending gid) by x
+    plane: lo / hi / keep = [xyzh (cap, 4), vm (cap, 4), gid (cap,) int64] buffers; counts:
+    (3,) int64 device tensor."""
+    assert counts.dtype == torch.int64 and counts.numel() >= 3 and gid.dtype == torch.int64
+    args = []
+    for b in (lo, hi, keep):
+        assert b[2].dtype == torch.int64 and b[0].shape[0] == b[1].shape[0] == b[2].shape[0]
+        args += [_ptr(b[0]), _ptr(b[1]), _ptr(b[2]), int(b[0].shape[0])]
+    _check(_lib.load().sph_partition_migrants(ctypes.byref(grid), int(n), _ptr(xyzh), _ptr(vm), _ptr(gid), *args,
+                                              _ptr(counts), _ptr(ws), ws.numel(), _stream(stream)),
+           "sph_partition_migrants")
+
+
+def sph_merge_by_id(lists, out_x: torch.Tensor, out_v: torch.Tensor, out_g: torch.Tensor, stream=None) -> None:
+    """Merge of three (xyzh, vm, gid, n) lists, each ascending in gid, into out_* (n total)."""
+    assert len(lists) == 3
+    args = []
+    for x, v, g, n in lists:
+        assert g.dtype == torch.int64
+        args += [int(n), _ptr(x), _ptr(v), _ptr(g)]
+    _check(_lib.load().sph_merge_by_id(*args, _ptr(out_x), _ptr(out_v), _ptr(out_g), _stream(stream)),
+           "sph_merge_by_id")
+
+
 def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
     o = acc.struct()
     _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),

@@ -215,6 +215,112 @@ __global__ void __launch_bounds__(SEL_B) k_sel_write(DevGrid g, long long n, con
     }
 }
 
+// ---- slab migration on a reuse rebuild (sph_partition_migrants / sph_merge_by_id) --------
+// List 0: the owned particles whose (wrapped) x plane is the left neighbour's last plane
+// x_lo - 1, list 1: the right neighbour's first plane x_hi, list 2: the rest; each in input
+// order (a stable three-way partition, the scheme of k_sel_count / k_sel_write).
+__device__ __forceinline__ int mig_list(const DevGrid &g, float x)
+{
+    int c = (int)floor((double)x * (double)g.nc[0] / g.box[0]);   // the binning rule of k_bin
+    c = c < 0 ? 0 : (c > g.nc[0] - 1 ? g.nc[0] - 1 : c);
+    const int lo = (g.x_lo - 1 + g.nc[0]) % g.nc[0], hi = g.x_hi % g.nc[0];
+    return c == lo ? 0 : (c == hi ? 1 : 2);
+}
+
+__global__ void __launch_bounds__(SEL_B) k_mig_count(DevGrid g, long long n, const float4 *__restrict__ xyzh,
+                                                      int *__restrict__ blk, long long nblk)
+{
+    const long long p = blockIdx.x * (long long)SEL_B + threadIdx.x;
+    const int l = p < n ? mig_list(g, xyzh[p].x) : -1;
+    const int c0 = __syncthreads_count(l == 0), c1 = __syncthreads_count(l == 1), c2 = __syncthreads_count(l == 2);
+    if (threadIdx.x == 0) {
+        blk[blockIdx.x] = c0;
+        blk[nblk + blockIdx.x] = c1;
+        blk[2 * nblk + blockIdx.x] = c2;
+    }
+}
+
+struct MigOut {
+    float4 *x[3], *v[3];
+    long long *g[3];
+    long long cap[3];
+};
+
+__global__ void __launch_bounds__(SEL_B) k_mig_write(DevGrid g, long long n, const float4 *__restrict__ xyzh,
+                                                      const float4 *__restrict__ vm, const long long *__restrict__ gid,
+                                                      const int *__restrict__ off, long long nblk, MigOut o,
+                                                      long long *counts, unsigned *status)
+{
+    __shared__ int wsum[3][SEL_B / 32];
+    const long long p = blockIdx.x * (long long)SEL_B + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int l = p < n ? mig_list(g, xyzh[p].x) : -1;
+    unsigned b[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) b[k] = __ballot_sync(0xffffffffu, l == k);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) wsum[k][w] = __popc(b[k]);
+    }
+    __syncthreads();
+    if (l >= 0) {
+        int before = 0;
+        for (int k = 0; k < w; ++k) before += wsum[l][k];
+        const unsigned mine = l == 0 ? b[0] : (l == 1 ? b[1] : b[2]);
+        const long long base = (long long)off[l * nblk + blockIdx.x] - (l > 0 ? (long long)off[l * nblk] : 0ll);
+        const long long r = base + before + __popc(mine & ((1u << lane) - 1u));
+        if (r < o.cap[l]) {
+            o.x[l][r] = xyzh[p];
+            o.v[l][r] = vm[p];
+            o.g[l][r] = gid[p];
+        } else {
+            set_status(status, ST_ECAPACITY);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        counts[0] = off[nblk];
+        counts[1] = (long long)off[2 * nblk] - off[nblk];
+        counts[2] = (long long)off[3 * nblk] - off[2 * nblk];
+    }
+}
+
+// Merge of three lists, each ascending in id, ids distinct across them: element i of list L
+// goes to i + (elements of the other two lists with a smaller id), found by binary search.
+__device__ __forceinline__ long long lower_bound_id(const long long *a, long long n, long long key)
+{
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long m = (lo + hi) >> 1;
+        if (a[m] < key) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+struct MergeIn {
+    const float4 *x[3], *v[3];
+    const long long *g[3];
+    long long n[3];
+};
+
+__global__ void k_merge_by_id(MergeIn in, float4 *__restrict__ ox, float4 *__restrict__ ov, long long *__restrict__ og)
+{
+    const long long total = in.n[0] + in.n[1] + in.n[2];
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int l = t < in.n[0] ? 0 : (t < in.n[0] + in.n[1] ? 1 : 2);
+        const long long i = t - (l > 0 ? in.n[0] : 0) - (l > 1 ? in.n[1] : 0);
+        const long long key = in.g[l][i];
+        long long pos = i;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (k != l) pos += lower_bound_id(in.g[k], in.n[k], key);
+        ox[pos] = in.x[l][i];
+        ov[pos] = in.v[l][i];
+        og[pos] = key;
+    }
+}
+
 // 64-byte scatter record: the particle's 8 floats and its input index, written as two full
 // 32-byte sectors (two 256-bit stores) so a random slot costs no read-modify-write.
 struct alignas(64) ParticleRec {

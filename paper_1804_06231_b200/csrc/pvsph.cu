@@ -570,6 +570,84 @@ int sph_select_planes(const sph_grid *grid, int64_t n_own, const float *xyzh_in,
     return check_launch();
 }
 
+int sph_partition_migrants(const sph_grid *grid, int64_t n, const float *xyzh, const float *vm, const int64_t *gid,
+                           float *lo_xyzh, float *lo_vm, int64_t *lo_gid, int64_t cap_lo, float *hi_xyzh,
+                           float *hi_vm, int64_t *hi_gid, int64_t cap_hi, float *keep_xyzh, float *keep_vm,
+                           int64_t *keep_gid, int64_t cap_keep, int64_t *counts, void *ws, size_t ws_bytes,
+                           void *stream)
+{
+    DevGrid g;
+    int rc = make_grid(grid, g);
+    if (rc) return rc;
+    if (n < 0 || cap_lo < 0 || cap_hi < 0 || cap_keep < 0 || !counts || !ws) return SPH_EINVAL;
+    if (n > 0 && (!xyzh || !vm || !gid)) return SPH_EINVAL;
+    const float *outs[6] = {lo_xyzh, lo_vm, hi_xyzh, hi_vm, keep_xyzh, keep_vm};
+    const int64_t caps[3] = {cap_lo, cap_hi, cap_keep};
+    const int64_t *gids[3] = {lo_gid, hi_gid, keep_gid};
+    for (int k = 0; k < 3; ++k)
+        if (caps[k] > 0 && (!outs[2 * k] || !outs[2 * k + 1] || !gids[k])) return SPH_EINVAL;
+    const float *aligned[8] = {xyzh, vm, lo_xyzh, lo_vm, hi_xyzh, hi_vm, keep_xyzh, keep_vm};
+    for (const float *q : aligned)
+        if ((uintptr_t)q % 16) return SPH_EINVAL;
+    // scratch: the build's cell_of region, as sph_select_planes
+    Ws w = ws_layout(g, n);
+    const long long nblk = (n + SEL_B - 1) / SEL_B, nk = 3 * nblk;
+    const size_t blk_off = w.cell_of, sum_off = align_up(blk_off + 4 * (size_t)(nk + 1), 16);
+    if (ws_bytes < w.total || sum_off + 4 * (size_t)((nk + SCAN_TILE - 1) / SCAN_TILE + 1) > w.rank)
+        return SPH_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e;
+    if (n == 0) {
+        if ((e = cudaMemsetAsync(counts, 0, 24, s)) != cudaSuccess) return cuda_fail(e);
+        return SPH_OK;
+    }
+    int *blk = at<int>(ws, blk_off), *sum = at<int>(ws, sum_off);
+    unsigned *status = at<unsigned>(ws, w.status);
+    const float4 *x = reinterpret_cast<const float4 *>(xyzh), *v = reinterpret_cast<const float4 *>(vm);
+    MigOut o;
+    for (int k = 0; k < 3; ++k) {
+        o.x[k] = reinterpret_cast<float4 *>(const_cast<float *>(outs[2 * k]));
+        o.v[k] = reinterpret_cast<float4 *>(const_cast<float *>(outs[2 * k + 1]));
+        o.g[k] = reinterpret_cast<long long *>(const_cast<int64_t *>(gids[k]));
+        o.cap[k] = caps[k];
+    }
+    k_mig_count<<<(int)nblk, SEL_B, 0, s>>>(g, n, x, blk, nblk);
+    const long long nt = (nk + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_tiles<<<(int)nt, SCAN_T, 0, s>>>(blk, nk, blk, sum, status, SEL_B);
+    k_scan_sums<<<1, SCAN_T, 0, s>>>(sum, nt, blk, nk);
+    k_scan_add<<<(int)nt, SCAN_T, 0, s>>>(blk, nk, sum);
+    k_mig_write<<<(int)nblk, SEL_B, 0, s>>>(g, n, x, v, reinterpret_cast<const long long *>(gid), blk, nblk, o,
+                                             reinterpret_cast<long long *>(counts), status);
+    return check_launch();
+}
+
+int sph_merge_by_id(int64_t na, const float *a_xyzh, const float *a_vm, const int64_t *a_gid, int64_t nb,
+                    const float *b_xyzh, const float *b_vm, const int64_t *b_gid, int64_t nc, const float *c_xyzh,
+                    const float *c_vm, const int64_t *c_gid, float *out_xyzh, float *out_vm, int64_t *out_gid,
+                    void *stream)
+{
+    const int64_t ns[3] = {na, nb, nc};
+    const float *xs[3] = {a_xyzh, b_xyzh, c_xyzh}, *vs[3] = {a_vm, b_vm, c_vm};
+    const int64_t *gs[3] = {a_gid, b_gid, c_gid};
+    MergeIn in;
+    for (int k = 0; k < 3; ++k) {
+        if (ns[k] < 0 || (ns[k] > 0 && (!xs[k] || !vs[k] || !gs[k]))) return SPH_EINVAL;
+        if (((uintptr_t)xs[k] % 16) || ((uintptr_t)vs[k] % 16)) return SPH_EINVAL;
+        in.x[k] = reinterpret_cast<const float4 *>(xs[k]);
+        in.v[k] = reinterpret_cast<const float4 *>(vs[k]);
+        in.g[k] = reinterpret_cast<const long long *>(gs[k]);
+        in.n[k] = ns[k];
+    }
+    const long long total = na + nb + nc;
+    if (total == 0) return SPH_OK;
+    if (!out_xyzh || !out_vm || !out_gid || ((uintptr_t)out_xyzh % 16) || ((uintptr_t)out_vm % 16))
+        return SPH_EINVAL;
+    k_merge_by_id<<<grid_blocks(total, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+        in, reinterpret_cast<float4 *>(out_xyzh), reinterpret_cast<float4 *>(out_vm),
+        reinterpret_cast<long long *>(out_gid));
+    return check_launch();
+}
+
 int sph_density_finalize(sph_out *acc, int64_t n, void *stream)
 {
     if (!out_ok(acc) || n < 0 || n > acc->n_out) return SPH_EINVAL;

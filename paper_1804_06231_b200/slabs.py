@@ -539,7 +539,8 @@ def split_migrants(x: torch.Tensor, nc: int, box: float, x_lo: int, x_hi: int):
     """Masks of the owned particles (wrapped positions) whose x plane -- the binning rule of
     sph_build_cells -- is the left neighbour's last plane (x_lo - 1) or the right neighbour's
     first (x_hi), and of those that stay.  A particle moves at most one plane between rebuilds
-    (displacement < skin < C_l / 2)."""
+    (displacement < skin < C_l / 2).  The rule as host logic (CPU tests, and the reference the
+    GPU test holds sph_partition_migrants to); the product path calls the library."""
     pl = torch.clamp(torch.floor(x[:, 0].double() * nc / box), 0, nc - 1).long()
     lo = pl == (x_lo - 1) % nc
     hi = (pl == x_hi % nc) & ~lo
@@ -579,6 +580,10 @@ class SlabReuse(SlabRunner):
         self.mig = [[torch.zeros((mcap, 4), dtype=torch.float32, device=device),
                      torch.zeros((mcap, 4), dtype=torch.float32, device=device),
                      torch.zeros(mcap, dtype=torch.int64, device=device)] for _ in range(4)]   # send lo/hi, recv lo/hi
+        self.keep = [torch.zeros((self.own_cap, 4), dtype=torch.float32, device=device),
+                     torch.zeros((self.own_cap, 4), dtype=torch.float32, device=device),
+                     torch.zeros(self.own_cap, dtype=torch.int64, device=device)]             # the staying particles
+        self.mig_n = torch.zeros(3, dtype=torch.int64, device=device)
         self.out_view = None
 
     def upload(self) -> None:
@@ -608,36 +613,26 @@ class SlabReuse(SlabRunner):
         pv.sph_gather_positions(self.grid, self.cells, self.xin, self.n_own)
 
     def pack_migrants(self):
-        """Split the owned set: migrants to the left / right into the send buffers; returns
-        (n_lo, n_hi, keep_mask)."""
-        n = self.n_own
-        lo, hi, keep = split_migrants(self.xin[:n], self.slab.nc, self.slab.box, self.slab.x_lo, self.slab.x_hi)
-        out = []
-        for k, m in enumerate((lo, hi)):
-            idx = torch.nonzero(m).squeeze(1)
-            c = int(idx.numel())
-            if c > self.mig[k][0].shape[0]:
-                raise RuntimeError(f"migration buffer {self.mig[k][0].shape[0]} < {c}")
-            self.mig[k][0][:c].copy_(self.xin[:n][idx])
-            self.mig[k][1][:c].copy_(self.vin[:n][idx])
-            self.mig[k][2][:c].copy_(self.gid[:n][idx])
-            out.append(c)
-        return out[0], out[1], keep
+        """Split the owned set (sph_partition_migrants, stable): migrants to the left / right
+        into the send buffers, the rest into `keep`; returns (n_lo, n_hi, n_keep) -- one host
+        synchronisation per rebuild, for the message sizes."""
+        pv.sph_partition_migrants(self.grid, self.n_own, self.xin, self.vin, self.gid, self.mig[0], self.mig[1],
+                                  self.keep, self.mig_n, self.ws)
+        n_lo, n_hi, n_keep = (int(c) for c in self.mig_n.tolist())
+        if n_lo > self.mig[0][0].shape[0] or n_hi > self.mig[1][0].shape[0]:
+            raise RuntimeError(f"migration buffer {self.mig[0][0].shape[0]} < {max(n_lo, n_hi)}")
+        return n_lo, n_hi, n_keep
 
-    def merge_owned(self, keep, r_lo: int, r_hi: int) -> None:
-        """The kept particles plus the received migrants, in ascending global id."""
-        n = self.n_own
-        kx, kv, kg = self.xin[:n][keep], self.vin[:n][keep], self.gid[:n][keep]
-        x = torch.cat([kx, self.mig[2][0][:r_lo], self.mig[3][0][:r_hi]])
-        v = torch.cat([kv, self.mig[2][1][:r_lo], self.mig[3][1][:r_hi]])
-        g = torch.cat([kg, self.mig[2][2][:r_lo], self.mig[3][2][:r_hi]])
-        order = torch.argsort(g)
-        m = int(g.numel())
+    def merge_owned(self, n_keep: int, r_lo: int, r_hi: int) -> None:
+        """The kept particles plus the received migrants, in ascending global id
+        (sph_merge_by_id: all three lists are ascending already)."""
+        m = n_keep + r_lo + r_hi
         if m > self.own_cap:
             raise RuntimeError(f"owned capacity {self.own_cap} < {m}")
-        self.xin[:m].copy_(x[order])
-        self.vin[:m].copy_(v[order])
-        self.gid[:m].copy_(g[order])
+        pv.sph_merge_by_id([(self.keep[0], self.keep[1], self.keep[2], n_keep),
+                            (self.mig[2][0], self.mig[2][1], self.mig[2][2], r_lo),
+                            (self.mig[3][0], self.mig[3][1], self.mig[3][2], r_hi)],
+                           self.xin, self.vin, self.gid)
         self.n_own = m
         self.out = pv.Out.alloc(m, self.device)      # outputs of the new owned set
 

@@ -201,3 +201,44 @@ def test_mask_ghost_rows(pv):
             assert torch.equal(x[k, :c], x0[k, :c]) and torch.equal(v[k, :c], v0[k, :c])
             assert torch.all(x[k, c:] == torch.tensor(dx, device="cuda"))
             assert torch.all(v[k, c:] == torch.tensor(dv, device="cuda"))
+
+
+def test_partition_migrants_and_merge_by_id(pv):
+    """sph_partition_migrants == the split rule (stable, input order kept) on random wrapped
+    positions incl. the faces of the neighbour planes; sph_merge_by_id of the three lists (and
+    of received migrants with fresh ids) == the argsort-by-id merge; counts exact."""
+    import torch
+    from paper_1804_06231_b200.slabs import split_migrants
+    rng = np.random.default_rng(7)
+    nc, x_lo, x_hi, n = 10, 3, 6, 20000
+    x = np.zeros((n, 4), np.float32)
+    x[:, :3] = rng.random((n, 3))
+    x[:n // 10, 0] = (rng.integers(0, nc, n // 10) / nc).astype(np.float32)      # exactly on plane faces
+    x[:, 3] = 0.01
+    v = rng.standard_normal((n, 4)).astype(np.float32)
+    gid = np.sort(rng.choice(10 * n, n, replace=False)).astype(np.int64)
+    X, V, G = (torch.from_numpy(a).cuda() for a in (x, v, gid))
+    g = pv.make_grid(nc, 1.0, 1.825742, x_lo, x_hi, 1)
+    ws = pv.alloc_workspace(g, n)
+    bufs = [[torch.zeros((n, 4), dtype=torch.float32, device="cuda"), torch.zeros((n, 4), dtype=torch.float32,
+             device="cuda"), torch.zeros(n, dtype=torch.int64, device="cuda")] for _ in range(3)]
+    cnt = torch.zeros(3, dtype=torch.int64, device="cuda")
+    pv.sph_partition_migrants(g, n, X, V, G, bufs[0], bufs[1], bufs[2], cnt, ws)
+    assert pv.sph_status(ws) == 0
+    masks = split_migrants(X, nc, 1.0, x_lo, x_hi)
+    c = cnt.tolist()
+    for k, m in enumerate(masks):
+        idx = torch.nonzero(m).squeeze(1)
+        assert c[k] == idx.numel()
+        assert torch.equal(bufs[k][0][:c[k]], X[idx]) and torch.equal(bufs[k][1][:c[k]], V[idx])
+        assert torch.equal(bufs[k][2][:c[k]], G[idx])
+    # merge: keep + lo + hi back == the original set in gid order
+    ox, ov, og = torch.empty_like(X), torch.empty_like(V), torch.empty_like(G)
+    pv.sph_merge_by_id([(bufs[2][0], bufs[2][1], bufs[2][2], c[2]), (bufs[0][0], bufs[0][1], bufs[0][2], c[0]),
+                        (bufs[1][0], bufs[1][1], bufs[1][2], c[1])], ox, ov, og)
+    torch.cuda.synchronize()
+    assert torch.equal(og, G) and torch.equal(ox, X) and torch.equal(ov, V)
+    # an empty list and a partial capacity overflow
+    small = [[b[0][:5], b[1][:5], b[2][:5]] for b in bufs[:2]] + [bufs[2]]
+    pv.sph_partition_migrants(g, n, X, V, G, small[0], small[1], small[2], cnt, ws)
+    assert pv.sph_status(ws) == 3                  # SPH_ECAPACITY: a migrant list above 5
