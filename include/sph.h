@@ -310,6 +310,11 @@ int sph_gather_positions(const sph_grid *grid, const sph_cells *cells, float *xy
 int sph_mask_ghost_rows(float *xyzh, float *vm, int64_t cap, const int64_t *counts, const float dead_xyzh[4],
                         const float dead_vm[4], void *stream);
 
+/* max_i |v_i| (fp64 norms of the fp32 velocities vm[4 * i .. + 2], device,
+ * 16-byte aligned) into out (device double): the speed bound of a list-reuse
+ * loop's displacement check.  0 for n = 0. */
+int sph_max_speed(const float *vm, int64_t n, double *out, void *stream);
+
 /* Slab migration on a list-reuse rebuild: a stable three-way
  * partition of the owned particles (xyzh/vm float4, gid int64; device, n;
  * positions already wrapped into the box, in ascending gid) by x plane --

@@ -19,7 +19,7 @@ ERROR_NAMES = {0: "SPH_OK", 1: "SPH_EINVAL", 2: "SPH_EH_RANGE", 3: "SPH_ECAPACIT
 EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cells", "sph_sort_cells",
            "sph_density_self", "sph_density_pair", "sph_density_pair_sym", "sph_drift", "sph_gather_positions",
            "sph_select_planes", "sph_mask_ghost_rows", "sph_partition_migrants", "sph_merge_by_id",
-           "sph_density_finalize", "sph_density_all", "sph_density_all_sym", "sph_status",
+           "sph_max_speed", "sph_density_finalize", "sph_density_all", "sph_density_all_sym", "sph_status",
            "sph_status_reset", "sph_strerror")
 
 
@@ -79,6 +79,7 @@ def load(path: str = LIB):
                                          c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
     L.sph_merge_by_id.argtypes = [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                   c_vp, c_vp, c_vp, c_vp]
+    L.sph_max_speed.argtypes = [c_vp, c_i64, c_vp, c_vp]
     L.sph_density_finalize.argtypes = [O, c_i64, c_vp]
     L.sph_density_all.argtypes = [G, C, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_all_sym.argtypes = [G, C, O, S, c_vp, ctypes.c_size_t, c_vp]
@@ -90,7 +91,7 @@ def load(path: str = LIB):
     L.sph_strerror.restype = ctypes.c_char_p
     for f in ("sph_build_cells", "sph_sort_cells", "sph_density_self", "sph_density_pair", "sph_density_pair_sym",
               "sph_drift", "sph_gather_positions", "sph_select_planes", "sph_mask_ghost_rows",
-              "sph_partition_migrants", "sph_merge_by_id",
+              "sph_partition_migrants", "sph_merge_by_id", "sph_max_speed",
               "sph_density_finalize",
               "sph_density_all", "sph_density_all_sym", "sph_status", "sph_status_reset"):
         getattr(L, f).restype = ctypes.c_int

@@ -291,6 +291,14 @@ def sph_merge_by_id(lists, out_x: torch.Tensor, out_v: torch.Tensor, out_g: torc
            "sph_merge_by_id")
 
 
+def sph_max_speed(vm: torch.Tensor, n: int | None = None, stream=None) -> float:
+    """max |v| over the first n rows of vm ((N, 4) float32, device), fp64; one host sync."""
+    n = vm.shape[0] if n is None else int(n)
+    out = torch.zeros(1, dtype=torch.float64, device=vm.device)
+    _check(_lib.load().sph_max_speed(_ptr(vm), n, _ptr(out), _stream(stream)), "sph_max_speed")
+    return float(out.item())
+
+
 def sph_density_finalize(acc: Out, n: int | None = None, stream=None) -> None:
     o = acc.struct()
     _check(_lib.load().sph_density_finalize(ctypes.byref(o), acc.n_out if n is None else int(n), _stream(stream)),
@@ -388,7 +396,7 @@ class ReuseLoop:
         """Initial state (input order, device) and the first build; one host sync for max |v|."""
         self.x[:self.n].copy_(xyzh)
         self.v = vm
-        self.vmax = float(torch.linalg.vector_norm(vm[:, :3].double(), dim=1).max().item()) if self.n else 0.0
+        self.vmax = sph_max_speed(vm, self.n, stream) if self.n else 0.0
         self._build(stream)
 
     def step_bound(self, dt: float) -> float:

@@ -648,6 +648,31 @@ int sph_merge_by_id(int64_t na, const float *a_xyzh, const float *a_vm, const in
     return check_launch();
 }
 
+__global__ void k_max_speed(const float4 *__restrict__ vm, long long n, unsigned long long *out)
+{
+    double m = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float4 v = vm[i];
+        m = fmax(m, sqrt((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z));
+    }
+    // non-negative doubles order like their bit patterns
+    unsigned long long b = (unsigned long long)__double_as_longlong(m);
+    for (int o = 16; o > 0; o >>= 1) b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, b);
+}
+
+int sph_max_speed(const float *vm, int64_t n, double *out, void *stream)
+{
+    if (n < 0 || !out || (n > 0 && !vm) || ((uintptr_t)vm % 16)) return SPH_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(out, 0, 8, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (n == 0) return SPH_OK;
+    k_max_speed<<<grid_blocks(n, 256, 148 * 8), 256, 0, s>>>(reinterpret_cast<const float4 *>(vm), n,
+                                                             reinterpret_cast<unsigned long long *>(out));
+    return check_launch();
+}
+
 int sph_density_finalize(sph_out *acc, int64_t n, void *stream)
 {
     if (!out_ok(acc) || n < 0 || n > acc->n_out) return SPH_EINVAL;

@@ -220,3 +220,14 @@ def test_slab_reuse_with_migration_bitwise_equal_single(pv, world):
     for key in ref1:
         assert np.array_equal(got[key], ref1[key]), key
     compare(got, oracle.bruteforce(xh, p.vm), None, f"slab reuse p={world}")
+
+
+def test_max_speed(pv):
+    """sph_max_speed == max of the fp64 norms of the fp32 velocities (the reuse loop's speed
+    bound), 0 for no particles."""
+    rng = np.random.default_rng(3)
+    vm = rng.standard_normal((100003, 4)).astype(np.float32)
+    ref = float(np.max(np.sqrt((vm[:, :3].astype(np.float64) ** 2).sum(1))))
+    got = pv.sph_max_speed(torch.from_numpy(vm).cuda())
+    assert abs(got - ref) <= 1e-15 * ref
+    assert pv.sph_max_speed(torch.from_numpy(vm).cuda(), 0) == 0.0
