@@ -39,8 +39,15 @@ constexpr int V5_TP = V4_TP;
 #ifndef V5_CTAS
 #define V5_CTAS 2
 #endif
+#ifndef V5_CELLWIN
+#define V5_CELLWIN 1   // 1: cell-uniform windows from the tile setup (broadcast sweeps); 0: per-lane bisection
+#endif
 #ifndef V5_Q_DEPTH
+#if V5_CELLWIN
+#define V5_Q_DEPTH 26     // the window table takes the shared memory of 4 stack slots
+#else
 #define V5_Q_DEPTH 30     // (two CTAs per SM leave ~1 KB of shared memory at 30)
+#endif
 #endif
 constexpr int V5_Q = V5_Q_DEPTH;                       // hit stack depth per lane, 2-byte entries
 #ifndef V5_NP
@@ -58,7 +65,8 @@ constexpr int V5_ML = V4_ML + 14 * V4_MAXH;            // list entries + sentine
 constexpr int V5_MLA = (V5_ML + 7) / 8 * 8;
 constexpr size_t V5_SMEM = (size_t)(V5_MS + 2) * 16 + (size_t)(V5_STAGE_V ? V5_MS + 2 : 0) * 16 + (size_t)V4_MAXCELLS * 16 +
                            (size_t)V5_MLA * 2 + (size_t)V4_HOFF * 4 + (size_t)V5_WARPS * V5_Q * 32 * 2 +
-                           (size_t)V4_MAXZ * 16 + (size_t)V4_MAXCELLS * 4;
+                           (size_t)V4_MAXZ * 16 + (size_t)V4_MAXCELLS * 4 + (size_t)(V5_CELLWIN ? V4_MAXH * 13 * 4 : 0);
+static_assert(!V5_CELLWIN || V5_STAGE_V, "cell windows read h from the staged positions");
 static_assert(V5_MS * 16 < 65536, "byte offsets of staged particles fit 16 bits");
 static_assert(((V5_MS + 1) * 16) % 16 == 0 && (V5_MLA * 2) % 16 == 0, "16-byte aligned shared arrays");
 static_assert(13 * V4_MAXH <= 2 * V5_TP, "two direction segments per thread");
@@ -83,6 +91,7 @@ struct V5Stage {
     unsigned sl;              // shared address of L[0]
     unsigned sent;            // shared address of the list sentinel P[V5_MS] (NaN)
     unsigned pad;             // shared address of the drain padding P[V5_MS + 1] (far, finite, v = m = 0)
+    const unsigned *win;      // V5_CELLWIN: per (home cell, direction) the cell's windows W+ | W- << 16
 };
 
 // Packed accumulators.  With q = min(x, u)(u + v) >= 0 the kernel slope is w' = -3 q and
@@ -194,7 +203,7 @@ __device__ unsigned long long g_v5dbg[16];   // profiling counters (scripts: exp
 // lpos: first list entry of its home cell's block, qh: its staged column, yoff: its row.
 template <bool COUNT, bool FRAMES>
 __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c, OutRec *orec, const V5Stage &S,
-                                            unsigned qbase, bool active, int i, int yoff, int qh, int lpos,
+                                            unsigned qbase, bool active, int i, int yoff, int qh, int lpos, int hidx,
                                             unsigned cand[4], unsigned hits[4], unsigned &band)
 {
     // The lane's stack column: V5_GUARD guard slots holding the drain padding, then the entries
@@ -326,6 +335,95 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         }
     }
 
+#if V5_CELLWIN
+    // ---- 13 directions, cell-uniform windows (DESIGN.md §4.4 "v5, cell windows") ----
+    // The tile setup stored, per (home cell, direction), the union over the cell's home
+    // particles of their exact windows (W+ leading entries of the +d list, W- of the -d list,
+    // the paper's Code 2 bound with the cell's h_max: P:94-100).  Every lane of a home
+    // cell sweeps the same range L[mid - W+, mid + W-), so the lanes of one cell read the same
+    // list entry and the same staged particle (shared-memory broadcasts); an entry outside the
+    // lane's own window has projected separation >= H_i + delta, so r > H_i and the distance test
+    // rejects it (R16).  COUNT counts exactly the lane's own Code 2 window (sep < H_i + delta).
+    int pos = lpos + 1;                                   // after the home cell's leading sentinel
+#pragma unroll 1
+    for (int d = 0; d < 13; ++d) {
+        const int4 dv = c_dirs[d];
+        const int kind = dv.w;
+        const int cp = scell(dv.x, dv.y, dv.z), cm = scell(-dv.x, -dv.y, -dv.z);
+        const int4 ep = S.tab[cp];
+        const int4 em = S.tab[cm];
+        const int mid = pos + ep.y;                       // boundary between the two reversed segments
+        const int sent = mid + em.y;                      // the sentinel slot after the -d segment
+        pos = sent + 1;
+        const unsigned wv = active ? S.win[hidx * 13 + d] : 0u;
+        const int W0 = (int)(wv & 0xffffu), tot = W0 + (int)(wv >> 16);
+        const unsigned fl0k = FRAMES ? (unsigned)ep.w & 7u : 0u, fl1k = FRAMES ? (unsigned)em.w & 7u : 0u;
+        // COUNT only: the lane's exact window thresholds (as the per-lane bisection used them)
+        float cax[3] = {0.f, 0.f, 0.f}, chp[3] = {0.f, 0.f, 0.f}, chm[3] = {0.f, 0.f, 0.f}, cHp = -3e38f, cHm = -3e38f;
+        if (COUNT) {
+            const float sk = kind == 1 ? 1.0f : (kind == 2 ? 1.41421356237309505f : 1.73205080756887729f);
+            cax[0] = (float)dv.x; cax[1] = (float)dv.y; cax[2] = (float)dv.z;
+            home_of(fl0k, chp[0], chp[1], chp[2]);
+            home_of(fl1k, chm[0], chm[1], chm[2]);
+            if (active) {
+                cHp = fmaf(2.0f, S.tdx[cp], Hd) * sk;
+                cHm = fmaf(2.0f, S.tdx[cm], Hd) * sk;
+            }
+        }
+        const int trip = __reduce_max_sync(0xffffffffu, tot);
+        const unsigned lb = S.sl + 2u * (unsigned)(mid - W0);
+        const unsigned ls = S.sl + 2u * (unsigned)sent;
+        auto step = [&](int t, auto n_tag) {
+            constexpr int NU = decltype(n_tag)::value;
+            unsigned e[NU];
+#pragma unroll
+            for (int u = 0; u < NU; ++u) e[u] = ldsr_u16(min(lb + 2u * (unsigned)(t + u), ls));
+            float4 pp[NU];
+#pragma unroll
+            for (int u = 0; u < NU; ++u) pp[u] = ldsr_f4(e[u]);
+#pragma unroll
+            for (int u = 0; u < NU; ++u) {
+                const float4 p = pp[u];
+                unsigned fl = 0;
+                float dx, dy, dz;
+                if (FRAMES) {
+                    float hx = x, hy = y, hz = z;
+                    fl = t + u < W0 ? fl0k : fl1k;
+                    home_of(fl, hx, hy, hz);
+                    dx = hx - p.x; dy = hy - p.y; dz = hz - p.z;
+                } else {
+                    const f2 dxy = add2(pk(p.x, p.y), nxy);  // one FADD2; squares as before
+                    dx = dxy.x; dy = dxy.y; dz = z - p.z;
+                }
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                if (COUNT) {
+                    const bool plus = t + u < W0;
+                    const float *hh = plus ? chp : chm;
+                    const f2 dxy = add2(pk(p.x, p.y), pk(-hh[0], -hh[1]));
+                    const float sv = fmaf(cax[0], dxy.x, fmaf(cax[1], dxy.y, cax[2] * (p.z - hh[2])));
+                    const bool inw = t + u < tot && (plus ? sv < cHp : -sv < cHm);
+                    cand[kind] += inw ? 1u : 0u;
+                    band += inw && fabsf(r2 - H2) < 1e-6f * H2 ? 1u : 0u;
+                }
+                if (r2 < H2) {                             // outside the lane's window: never (sep >= H + delta)
+                    sts_u16_push(qp, FRAMES ? ((e[u] - S.sb) >> 4) | (fl << 12) : e[u]);
+                    qp += 64u;
+                    if (COUNT) ++hits[kind];
+                }
+            }
+        };
+        for (int t0 = 0; t0 < trip; t0 += V5_CHK) {
+#pragma unroll 1
+            for (int t = t0; t < min(t0 + V5_CHK, trip); t += 8) {
+                if (t + 4 < trip)
+                    step(t, std::integral_constant<int, 8>{});
+                else                                      // a tail of <= 4 candidates
+                    step(t, std::integral_constant<int, 4>{});
+            }
+            drain_check();
+        }
+    }
+#else
     // ---- 13 directions: windows two directions at a time, then one sweep per direction ----
     int pos = lpos + 1;                                   // after the home cell's leading sentinel
     for (int d0 = 0; d0 < 13; d0 += 2) {
@@ -442,6 +540,7 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
             }
         }
     }
+#endif
 #ifdef V5_STATS
     if ((threadIdx.x & 31) == 0) atomicAdd(&g_v5dbg[9], 1ull);          // [9] warps
     {
@@ -483,6 +582,7 @@ __global__ void __launch_bounds__(V5_TP, V5_CTAS) k_density_v5(DevGrid g, DevCel
     uint16_t *queue = reinterpret_cast<uint16_t *>(hoff + V4_HOFF);
     int4 *seq = reinterpret_cast<int4 *>(queue + V5_WARPS * V5_Q * 32);
     float *tdx = reinterpret_cast<float *>(seq + V4_MAXZ);
+    unsigned *win = reinterpret_cast<unsigned *>(tdx + V4_MAXCELLS);   // V5_CELLWIN only
     __shared__ int4 s_next;
     __shared__ int s_wsum[V5_WARPS];
     __shared__ __align__(8) unsigned long long s_mbar;
@@ -703,6 +803,64 @@ __global__ void __launch_bounds__(V5_TP, V5_CTAS) k_density_v5(DevGrid g, DevCel
                     }
                 }
                 __syncthreads();
+#if V5_CELLWIN
+                // Cell windows: per (home cell h, direction d) the union over h's home particles k
+                // of their exact windows, from a bound of the largest reach U+ = max_k (x_k.a + H_k
+                // + delta + 2 max_dx(c+d)) |a| (frames: the home side shifted as the lanes do), and
+                // U- the smallest; W+ = number of leading +d entries with x_j.a < U+, W- = leading
+                // -d entries with x_j.a > U-, by bisection on the staged (sorted) lists.  The bounds
+                // are widened by eps (fp32 rounding of the projections): a superset of every
+                // lane's window is all the sweep needs (R16).
+                {
+                    const float eps = 0x1p-18f * (fabsf(g.boxf[0]) + fabsf(g.boxf[1]) + fabsf(g.boxf[2]));
+                    const int njob = 13 * T.nh;
+                    const int *segoff = reinterpret_cast<const int *>(queue);
+                    for (int gs = threadIdx.x; gs < njob; gs += V5_TP) {
+                        const int h = gs / 13, d = gs % 13;
+                        const int r = h / T.nzh, q = h % T.nzh + 1;
+                        const int4 dv = c_dirs[d];
+                        const float a0 = (float)dv.x, a1 = (float)dv.y, a2 = (float)dv.z;
+                        const float sk = dv.w == 1 ? 1.0f : (dv.w == 2 ? 1.41421356237309505f : 1.73205080756887729f);
+                        const int4 eh = tab[(4 + r + 1) * T.nzs + q];
+                        const int cp = ((dv.x + 1) * 4 + dv.y + r + 1) * T.nzs + q + dv.z;
+                        const int cm = ((-dv.x + 1) * 4 - dv.y + r + 1) * T.nzs + q - dv.z;
+                        const int4 ep = tab[cp], em = tab[cm];
+                        const int nhome = eh.w >> 8;
+                        float up = -3e38f, um = 3e38f;
+                        for (int k = 0; k < nhome; ++k) {
+                            const float4 p4 = P[eh.x + k];
+                            const float sp = fmaf(a0, p4.x, fmaf(a1, p4.y, a2 * p4.z));
+                            const float hb = fmaf(g.gamma, p4.w, g.delta0) * 1.000001f * sk;   // >= the lane's (H + delta) |a|
+                            up = fmaxf(up, sp + hb);
+                            um = fminf(um, sp - hb);
+                        }
+                        auto fshift = [&](unsigned fl) {                 // (x - L f) . a = x . a - fshift
+                            return (fl & 1u ? g.boxf[0] * a0 : 0.0f) + (fl & 2u ? g.boxf[1] * a1 : 0.0f) +
+                                   (fl & 4u ? g.boxf[2] * a2 : 0.0f);
+                        };
+                        const unsigned flp = T.frames ? (unsigned)ep.w & 7u : 0u, flm = T.frames ? (unsigned)em.w & 7u : 0u;
+                        up = up - fshift(flp) + 2.0f * tdx[cp] * sk * 1.000001f + eps;
+                        um = um - fshift(flm) - 2.0f * tdx[cm] * sk * 1.000001f - eps;
+                        const int mid = segoff[gs] + (d == 0 ? 1 : 0) + ep.y;
+                        int w0 = 0, w1 = 0;
+                        if (nhome > 0) {
+                            const unsigned lbase = smem_addr(L);
+                            for (int st = ep.y > 0 ? 1 << (31 - __clz(ep.y)) : 0; st > 0; st >>= 1)
+                                if (w0 + st <= ep.y) {
+                                    const float4 pj = ldsr_f4(ldsr_u16(lbase + 2u * (unsigned)(mid - w0 - st)));
+                                    if (fmaf(a0, pj.x, fmaf(a1, pj.y, a2 * pj.z)) < up) w0 += st;
+                                }
+                            for (int st = em.y > 0 ? 1 << (31 - __clz(em.y)) : 0; st > 0; st >>= 1)
+                                if (w1 + st <= em.y) {
+                                    const float4 pj = ldsr_f4(ldsr_u16(lbase + 2u * (unsigned)(mid + w1 + st - 1)));
+                                    if (fmaf(a0, pj.x, fmaf(a1, pj.y, a2 * pj.z)) > um) w1 += st;
+                                }
+                        }
+                        win[gs] = (unsigned)w0 | ((unsigned)w1 << 16);
+                    }
+                }
+                __syncthreads();
+#endif
             }
         }
         __syncthreads();
@@ -732,13 +890,13 @@ __global__ void __launch_bounds__(V5_TP, V5_CTAS) k_density_v5(DevGrid g, DevCel
             } else {
                 i = seq[0].x;
             }
-            const V5Stage S{tab, tdx, T.nzs, sb, smem_addr(L), sb + 16u * V5_MS, sb + 16u * (V5_MS + 1)};
+            const V5Stage S{tab, tdx, T.nzs, sb, smem_addr(L), sb + 16u * V5_MS, sb + 16u * (V5_MS + 1), win};
             const unsigned qb = smem_addr(queue + wl * V5_Q * 32);
             if (wl * 32 < T.cnt) {
                 if (T.frames)
-                    v5_particle<COUNT, true>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits, band);
+                    v5_particle<COUNT, true>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, yoff * T.nzh + tz, cand, hits, band);
                 else
-                    v5_particle<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, cand, hits, band);
+                    v5_particle<COUNT, false>(g, c, orec, S, qb, active, i, yoff, tz + 1, lpos, yoff * T.nzh + tz, cand, hits, band);
             }
         } else if (T.cnt > 0) {
             const long long rowA = ((long long)(T.xo + g.ghost_x) * g.ny + T.y0) * g.nz;
