@@ -50,7 +50,7 @@ namespace pvsph {
 #ifndef TILE_WARPS
 #define TILE_WARPS 8
 #define TILE_MAXZ 21
-#define TILE_MS 2400
+#define TILE_MS 2336
 #define TILE_ML 8192
 #endif
 constexpr int V4_WARPS = TILE_WARPS;

@@ -44,7 +44,7 @@ constexpr int V5_TP = V4_TP;
 #endif
 #ifndef V5_Q_DEPTH
 #if V5_CELLWIN
-#define V5_Q_DEPTH 26     // the window table takes the shared memory of 4 stack slots
+#define V5_Q_DEPTH 30     // (with TILE_MS 2336 the window table fits beside 30 slots)
 #else
 #define V5_Q_DEPTH 30     // (two CTAs per SM leave ~1 KB of shared memory at 30)
 #endif
