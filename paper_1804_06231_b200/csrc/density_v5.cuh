@@ -42,6 +42,12 @@ constexpr int V5_TP = V4_TP;
 #ifndef V5_CELLWIN
 #define V5_CELLWIN 1   // 1: cell-uniform windows from the tile setup (broadcast sweeps); 0: per-lane bisection
 #endif
+#ifndef V5_TAIL2
+#define V5_TAIL2 1     // sweep tails of 1-2 candidates in a 2-wide step (c5 -0.5 ms)
+#endif
+#ifndef V5_SELFTAIL
+#define V5_SELFTAIL 1  // the self-cell sweep's tail in 4- or 2-wide steps (c5 -0.1 ms)
+#endif
 #ifndef V5_Q_DEPTH
 #if V5_CELLWIN
 #define V5_Q_DEPTH 30     // (with TILE_MS 2336 the window table fits beside 30 slots)
@@ -311,9 +317,10 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
         const int total = active ? eh.y : 0;
         const int trip = __reduce_max_sync(0xffffffffu, total);
         const unsigned pa = S.sb + 16u * (unsigned)eh.x;
-        for (int t = 0; t < trip; t += 8) {
+        auto sstep = [&](int t, auto n_tag) {
+            constexpr int NU = decltype(n_tag)::value;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < NU; ++u) {
                 const int tt = t + u;
                 const bool ok = tt < total && tt != kh;
                 const unsigned e = ok ? pa + 16u * (unsigned)tt : S.sent;
@@ -331,6 +338,18 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
                     if (COUNT) ++hits[0];
                 }
             }
+        };
+        for (int t = 0; t < trip; t += 8) {
+#if V5_SELFTAIL
+            if (t + 4 < trip)
+                sstep(t, std::integral_constant<int, 8>{});
+            else if (t + 2 < trip)
+                sstep(t, std::integral_constant<int, 4>{});
+            else
+                sstep(t, std::integral_constant<int, 2>{});
+#else
+            sstep(t, std::integral_constant<int, 8>{});
+#endif
             drain_check();
         }
     }
@@ -417,8 +436,15 @@ __device__ __forceinline__ void v5_particle(const DevGrid &g, const DevCells &c,
             for (int t = t0; t < min(t0 + V5_CHK, trip); t += 8) {
                 if (t + 4 < trip)
                     step(t, std::integral_constant<int, 8>{});
+#if V5_TAIL2
+                else if (t + 2 < trip)                    // a tail of 3 or 4 candidates
+                    step(t, std::integral_constant<int, 4>{});
+                else                                      // a tail of 1 or 2
+                    step(t, std::integral_constant<int, 2>{});
+#else
                 else                                      // a tail of <= 4 candidates
                     step(t, std::integral_constant<int, 4>{});
+#endif
             }
             drain_check();
         }
