@@ -112,6 +112,9 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
+    const float scale = 33554432.0f / (2.0f * cmax);         // 2^25 over the key range
+    const float cmax_s = cmax * scale;
     // 32 cells per warp step: lane l reads cell base + l, then the warp walks the non-empty
     // ones (sparse fine grids of level passes are mostly empty cells)
     for (long long base = cbeg + ((long long)blockIdx.x * SORT_WARPS + w) * 32; base < cend;
@@ -120,6 +123,14 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const int my_s0 = mycell < cend ? c.cell_start[mycell] : 0;
         int my_n = mycell < cend ? c.cell_start[mycell + 1] - my_s0 : 0;
         if (need && my_n > 0 && !need[mycell]) my_n = 0;     // lists never read on this level grid
+        // each lane the fp32 corner of ITS cell, once per 32 cells (the cell -> (x, y, z)
+        // divisions cost ~10 % of the warp's instructions when done per cell by every lane)
+        float my_corner[3] = {0.f, 0.f, 0.f};
+        if (my_n > 0 && my_n <= SORT_SMALL) {
+            double cd[3];
+            cell_corner(g, mycell, cd);
+            my_corner[0] = (float)cd[0]; my_corner[1] = (float)cd[1]; my_corner[2] = (float)cd[2];
+        }
         unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
       while (todo) {
         const int j = __ffs(todo) - 1;
@@ -147,8 +158,9 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             if (lane == 0) big_items[atomicAdd(big_count, 1)] = make_int2((int)cell, 0);
             continue;
         }
-        double corner[3];
-        cell_corner(g, cell, corner);
+        const float fc0 = __shfl_sync(0xffffffffu, my_corner[0], j);
+        const float fc1 = __shfl_sync(0xffffffffu, my_corner[1], j);
+        const float fc2 = __shfl_sync(0xffffffffu, my_corner[2], j);
         // One particle per lane, all 13 directions ranked in one pass over the cell:
         // composite = quantised key (25 bits) << 5 | in-cell index (the slot order is the
         // input order, so equal keys keep input order).  The fp32 key error (< 1e-6 C_l)
@@ -159,10 +171,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const float4 p = mine ? c.xyzh[s0 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
         // cell-local coordinates in fp32: x - fp32(corner) is exact (Sterbenz) unless both are
         // within a cell of 0, where the error is below ulp(C_l)
-        const float u0 = p.x - (float)corner[0], u1 = p.y - (float)corner[1], u2 = p.z - (float)corner[2];
-        const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
-        const float scale = 33554432.0f / (2.0f * cmax);     // 2^25 over the key range
-        const float cmax_s = cmax * scale;
+        const float u0 = p.x - fc0, u1 = p.y - fc1, u2 = p.z - fc2;
         unsigned comp[SPH_NDIR];
 #pragma unroll
         for (int d = 0; d < SPH_NDIR; ++d) {
