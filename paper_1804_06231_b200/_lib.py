@@ -52,10 +52,12 @@ class LibraryMissing(RuntimeError):
 
 
 def load(path: str = LIB):
-    """Load libpvsph.so.  Raises LibraryMissing (no fallback exists)."""
+    """Load libpvsph.so.  Raises LibraryMissing (no fallback exists).  PVSPH_LIB names another build
+    of the same library (A/B measurements of compile-time variants, scripts/)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("PVSPH_LIB", path)
     if not os.path.exists(path):
         raise LibraryMissing(f"{path} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
     L = ctypes.CDLL(path)
