@@ -393,7 +393,9 @@ def run_ours(args):
                            "slab_planes": [part.x_lo, part.x_hi] if world > 1 else None,
                            "level_grids": [lv[0] for lv in runner.levels],
                            "l2": "inputs (>= 4 GB at c5) larger than L2; no flush",
-                           "step": "ghost exchange + build_cells + sort_cells + " +
+                           "step": ("ghost exchange + build_sort_cells (fused; stage 'build' includes the small "
+                                    "cells' lists, 'sort' the larger cells' tiers) + " if len(runner.levels) == 1 else
+                                    "ghost exchange + build_cells + sort_cells + ") +
                                    ("density_all" if args.engine == "gather" else "density_all_sym (colour phases)")},
                 "interactions_per_step": tot_inter, "candidates_per_step": tot_cand,
                 "hit_fraction": tot_inter / max(1, tot_cand),

@@ -60,7 +60,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 6
+#define SPH_ABI_VERSION 7
 
 #define SPH_OK 0
 #define SPH_EINVAL 1
@@ -210,6 +210,16 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
  * particle are sorted: the others' lists are never read by sph_density_all. */
 int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end,
                    void *ws, size_t ws_bytes, void *stream);
+
+/* sph_build_cells followed by sph_sort_cells over all cells, with identical
+ * results (P:65, P:80 binning; P:92, P:102 the 13 sorted lists) and the same
+ * arguments, errors and workspace as sph_build_cells.  On a single grid
+ * (h_home_max <= 0) the lists of cells of up to 32 particles are computed
+ * inside the build's in-cell placement pass (the records are already in the
+ * warp), so the memory-bound placement and the issue-bound ranking overlap;
+ * level grids run the two calls unfused.  (ABI v7) */
+int sph_build_sort_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in,
+                         const float *vm_in, sph_cells *cells, void *ws, size_t ws_bytes, void *stream);
 
 /* (sph_density_self / sph_density_pair treat every particle of a listed cell
  * as home, whatever the grid's home range.)

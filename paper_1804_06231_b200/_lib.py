@@ -16,7 +16,7 @@ ERROR_NAMES = {0: "SPH_OK", 1: "SPH_EINVAL", 2: "SPH_EH_RANGE", 3: "SPH_ECAPACIT
 
 # Every function declared in include/sph.h (checked by tests/test_abi.py); sph_calibrate is
 # declared in include/sph_calib.h.
-EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cells", "sph_sort_cells",
+EXPORTS = ("sph_abi_version", "sph_ncell", "sph_workspace_bytes", "sph_build_cells", "sph_sort_cells", "sph_build_sort_cells",
            "sph_density_self", "sph_density_pair", "sph_density_pair_sym", "sph_drift", "sph_gather_positions",
            "sph_select_planes", "sph_mask_ghost_rows", "sph_partition_migrants", "sph_merge_by_id",
            "sph_max_speed", "sph_density_finalize", "sph_density_all", "sph_density_all_sym", "sph_status",
@@ -69,6 +69,7 @@ def load(path: str = LIB):
     L.sph_workspace_bytes.restype = ctypes.c_size_t
     L.sph_build_cells.argtypes = [G, c_i64, c_i64, c_vp, c_vp, C, c_vp, ctypes.c_size_t, c_vp]
     L.sph_sort_cells.argtypes = [G, C, c_i64, c_i64, c_vp, ctypes.c_size_t, c_vp]
+    L.sph_build_sort_cells.argtypes = [G, c_i64, c_i64, c_vp, c_vp, C, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_self.argtypes = [G, C, c_vp, c_i64, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_pair.argtypes = [G, C, c_vp, c_i64, O, S, c_vp, ctypes.c_size_t, c_vp]
     L.sph_density_pair_sym.argtypes = [G, C, c_vp, c_i64, O, S, c_vp, ctypes.c_size_t, c_vp]
@@ -91,7 +92,7 @@ def load(path: str = LIB):
     L.sph_calibrate.restype = ctypes.c_int
     L.sph_strerror.argtypes = [ctypes.c_int]
     L.sph_strerror.restype = ctypes.c_char_p
-    for f in ("sph_build_cells", "sph_sort_cells", "sph_density_self", "sph_density_pair", "sph_density_pair_sym",
+    for f in ("sph_build_cells", "sph_sort_cells", "sph_build_sort_cells", "sph_density_self", "sph_density_pair", "sph_density_pair_sym",
               "sph_drift", "sph_gather_positions", "sph_select_planes", "sph_mask_ghost_rows",
               "sph_partition_migrants", "sph_merge_by_id", "sph_max_speed",
               "sph_density_finalize",

@@ -191,6 +191,20 @@ def sph_build_cells(grid: SphGrid, xyzh_in: torch.Tensor, vm_in: torch.Tensor, c
     cells.n = int(s.n)
 
 
+def sph_build_sort_cells(grid: SphGrid, xyzh_in: torch.Tensor, vm_in: torch.Tensor, cells: Cells, ws: torch.Tensor,
+                         n_own: int | None = None, n_ghost: int = 0, stream=None) -> None:
+    """sph_build_cells + sph_sort_cells over all cells in one call (ABI v7; the small cells'
+    lists come out of the build's placement pass on a single grid)."""
+    n_total = xyzh_in.shape[0] if n_own is None else int(n_own) + int(n_ghost)
+    n_own = n_total - int(n_ghost) if n_own is None else int(n_own)
+    assert xyzh_in.is_contiguous() and vm_in.is_contiguous()
+    s = cells.struct()
+    _check(_lib.load().sph_build_sort_cells(ctypes.byref(grid), n_own, int(n_ghost), _ptr(xyzh_in), _ptr(vm_in),
+                                            ctypes.byref(s), _ptr(ws), ws.numel(), _stream(stream)),
+           "sph_build_sort_cells")
+    cells.n = int(s.n)
+
+
 def sph_sort_cells(grid: SphGrid, cells: Cells, ws: torch.Tensor, cell_begin: int = 0, cell_end: int = -1,
                    stream=None) -> None:
     s = cells.struct()
@@ -337,7 +351,7 @@ def check_status(ws: torch.Tensor, stream=None) -> None:
 # ---- convenience: one full density pass ---------------------------------------
 class DensityPass:
     """Owns the device buffers of one configuration and runs
-    build_cells -> sort_cells -> density_all (the hot path)."""
+    build_cells + sort_cells (one fused call) -> density_all (the hot path)."""
 
     def __init__(self, nc, n_own: int, box=1.0, gamma=GAMMA, capacity: int | None = None, device="cuda",
                  x_lo=0, x_hi=None, ghost_x=0, h_home=None, skin=0.0):
@@ -352,8 +366,8 @@ class DensityPass:
     def run(self, xyzh: torch.Tensor, vm: torch.Tensor, n_ghost: int = 0, stats: Stats | None = None,
             stream=None, out: Out | None = None) -> Out:
         out = self.out if out is None else out
-        sph_build_cells(self.grid, xyzh, vm, self.cells, self.ws, n_own=self.n_own, n_ghost=n_ghost, stream=stream)
-        sph_sort_cells(self.grid, self.cells, self.ws, stream=stream)
+        sph_build_sort_cells(self.grid, xyzh, vm, self.cells, self.ws, n_own=self.n_own, n_ghost=n_ghost,
+                             stream=stream)
         sph_density_all(self.grid, self.cells, out, self.ws, stats=stats, stream=stream)
         return out
 
@@ -387,8 +401,7 @@ class ReuseLoop:
         self.max_disp = torch.zeros(1, dtype=torch.float32, device=device)
 
     def _build(self, stream=None):
-        sph_build_cells(self.dp.grid, self.x, self.v, self.dp.cells, self.dp.ws, n_own=self.n, stream=stream)
-        sph_sort_cells(self.dp.grid, self.dp.cells, self.dp.ws, stream=stream)
+        sph_build_sort_cells(self.dp.grid, self.x, self.v, self.dp.cells, self.dp.ws, n_own=self.n, stream=stream)
         self.bound = 0.0
         self.max_disp.zero_()
 

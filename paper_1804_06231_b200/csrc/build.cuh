@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "radix.cuh"
+#include "sort_small.cuh"
 
 namespace pvsph {
 
@@ -442,6 +443,11 @@ __device__ __forceinline__ void stable_place(int s0, int e, int r, const Particl
     perm[s0 + r] = (int)(key & 0x7fffffffu);
 }
 
+// SORT (sph_build_sort_cells): a cell of <= SORT_SMALL particles also gets its 13 sorted lists
+// here, from the records the warp already holds (sort_small_lists, the small tier of
+// sph_sort_cells; identical lists): the memory-bound placement and the issue-bound ranking
+// overlap in one kernel, and the sort does not re-read the cell.
+template <bool SORT>
 __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long ncell, const int *__restrict__ start,
                                                                     const ParticleRec *__restrict__ rec,
                                                                     float4 *__restrict__ xyzh, float4 *__restrict__ vm,
@@ -450,11 +456,16 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                                                                     float *__restrict__ cell_hmax,
                                                                     int *__restrict__ row_home, int nz,
                                                                     int2 *big_items, int *big_count, int *bt_items,
-                                                                    int *bt_count, int bt_cap)
+                                                                    int *bt_count, int bt_cap, DevGrid g,
+                                                                    uint16_t *ord, long long cap)
 {
     __shared__ unsigned sh[STABLE_WARPS][STABLE_SMALL];
+    __shared__ unsigned ss[SORT ? STABLE_WARPS : 1][32 * 16];   // SORT: composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     constexpr int PER = STABLE_SMALL / 32;
+    const float cmax = 1.7320508075688772f * (float)fmax(g.cl[0], fmax(g.cl[1], g.cl[2]));
+    const float scale = 33554432.0f / (2.0f * cmax);         // as k_sort_small
+    const float cmax_s = cmax * scale;
     // 32 cells per warp step (empty cells cost one lane each: sparse fine grids)
     for (long long base = ((long long)blockIdx.x * STABLE_WARPS + w) * 32; base < ncell;
          base += (long long)gridDim.x * STABLE_WARPS * 32) {
@@ -464,6 +475,12 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
         if (mycell < ncell && my_n == 0) {
             cell_nhome[mycell] = 0;
             cell_hmax[mycell] = 0.0f;
+        }
+        float my_corner[3] = {0.f, 0.f, 0.f};              // SORT: the lane's own cell, once per 32 cells
+        if (SORT && my_n > 0 && my_n <= SORT_SMALL) {
+            double cd[3];
+            cell_corner(g, mycell, cd);
+            my_corner[0] = (float)cd[0]; my_corner[1] = (float)cd[1]; my_corner[2] = (float)cd[2];
         }
         unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
       while (todo) {
@@ -509,6 +526,7 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             if (e < n) sh[w][e] = v[k];
         }
         __syncwarp();
+        int r0 = 0;
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int e = lane + 32 * k;
@@ -516,9 +534,18 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
                 int r = 0;
                 for (int m = 0; m < n; ++m) r += sh[w][m] < v[k];
                 stable_place(s0, e, r, rec, xyzh, vm, perm);
+                if (k == 0) r0 = r;
             }
         }
         __syncwarp();
+        if (SORT && n <= SORT_SMALL) {
+            // lane e holds record e, placed at in-cell index r0
+            const float fc[3] = {__shfl_sync(0xffffffffu, my_corner[0], j), __shfl_sync(0xffffffffu, my_corner[1], j),
+                                 __shfl_sync(0xffffffffu, my_corner[2], j)};
+            const bool mine = lane < n;
+            const float4 p = mine ? rec[s0 + lane].xyzh : make_float4(0.f, 0.f, 0.f, 0.f);
+            sort_small_lists(ss[SORT ? w : 0], ord, cap, s0, n, mine, p, r0, fc, scale, cmax_s);
+        }
       }
     }
 }

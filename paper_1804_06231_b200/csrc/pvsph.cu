@@ -298,8 +298,13 @@ int sph_status_reset(void *ws, void *stream)
     return e == cudaSuccess ? SPH_OK : cuda_fail(e);
 }
 
-int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in, const float *vm_in,
-                    sph_cells *cells, void *ws, size_t ws_bytes, void *stream)
+}  // extern "C"
+
+namespace {
+
+// sph_build_cells; FUSE_SORT: the small cells' lists too (sph_build_sort_cells)
+int build_impl(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in, const float *vm_in,
+               sph_cells *cells, void *ws, size_t ws_bytes, void *stream, bool fuse_sort)
 {
     DevGrid g;
     int rc = make_grid(grid, g);
@@ -344,9 +349,16 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
         // a fresh build: no displacement since it (list reuse, sph_drift)
         if ((e = cudaMemsetAsync(cells->disp, 0, 4 * (size_t)n, s)) != cudaSuccess) return cuda_fail(e);
         if ((e = cudaMemsetAsync(cells->cell_dx, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
-        k_stable_small<<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
-            g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome, cells->cell_hmax,
-            row_home, g.nz, big_items, big_count, bt_items, bt_count, (int)w.huge_cap);
+        if (fuse_sort)
+            k_stable_small<true><<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
+                g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome,
+                cells->cell_hmax, row_home, g.nz, big_items, big_count, bt_items, bt_count, (int)w.huge_cap, g,
+                cells->order, cells->capacity);
+        else
+            k_stable_small<false><<<grid_blocks(g.ncell, STABLE_WARPS, 148 * 64), STABLE_WARPS * 32, 0, s>>>(
+                g.ncell, cells->cell_start, rec, xs, vs, cells->perm, cells->slot_cell, cells->cell_nhome,
+                cells->cell_hmax, row_home, g.nz, big_items, big_count, bt_items, bt_count, (int)w.huge_cap, g,
+                cells->order, cells->capacity);
         if ((rc = ensure_attrs()) != SPH_OK) return rc;
         k_stable_radix<STABLE_MED_MAX, STABLE_MED_T, false>
             <<<148 * 8, STABLE_MED_T, stable_radix_smem(STABLE_MED_MAX, STABLE_MED_T), s>>>(
@@ -366,8 +378,9 @@ int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const 
     return check_launch();
 }
 
-int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end, void *ws,
-                   size_t ws_bytes, void *stream)
+// sph_sort_cells; SMALL_DONE: cells of <= SORT_SMALL particles already have their lists
+int sort_impl(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end, void *ws,
+              size_t ws_bytes, void *stream, bool small_done)
 {
     DevGrid g;
     int rc = make_grid(grid, g);
@@ -396,7 +409,7 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     }
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
         g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap,
-        mid_items, huge_count + 2, w256_items, huge_count + 3, need);
+        mid_items, huge_count + 2, w256_items, huge_count + 3, need, small_done);
     k_sort_mid<<<148 * 8, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, mid_items, huge_count + 2, need);
     k_sort_warp256<<<148 * 4, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, w256_items, huge_count + 3, need);
     if ((rc = ensure_attrs()) != SPH_OK) return rc;
@@ -409,6 +422,32 @@ int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_be
     k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T), s>>>(
         g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap, need);
     return check_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
+int sph_build_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in, const float *vm_in,
+                    sph_cells *cells, void *ws, size_t ws_bytes, void *stream)
+{
+    return build_impl(grid, n_own, n_ghost, xyzh_in, vm_in, cells, ws, ws_bytes, stream, false);
+}
+
+int sph_sort_cells(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, int64_t cell_end, void *ws,
+                   size_t ws_bytes, void *stream)
+{
+    return sort_impl(grid, cells, cell_begin, cell_end, ws, ws_bytes, stream, false);
+}
+
+int sph_build_sort_cells(const sph_grid *grid, int64_t n_own, int64_t n_ghost, const float *xyzh_in,
+                         const float *vm_in, sph_cells *cells, void *ws, size_t ws_bytes, void *stream)
+{
+    // level grids sort only the cells next to home particles (known after the build): unfused
+    const bool fuse = grid && !(grid->h_home_max > 0.0f);
+    int rc = build_impl(grid, n_own, n_ghost, xyzh_in, vm_in, cells, ws, ws_bytes, stream, fuse);
+    if (rc) return rc;
+    return sort_impl(grid, cells, 0, -1, ws, ws_bytes, stream, fuse);
 }
 
 int sph_density_self(const sph_grid *grid, const sph_cells *cells, const int32_t *cell_list, int64_t ncells_list,

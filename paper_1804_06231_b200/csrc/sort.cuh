@@ -17,10 +17,10 @@
 
 #include "common.cuh"
 #include "radix.cuh"
+#include "sort_small.cuh"
 
 namespace pvsph {
 
-constexpr int SORT_SMALL = 32;
 constexpr int SORT_MED = 128;           // cells above: k_sort_warp256 (bitonic), k_sort_radix
 constexpr int SORT_W256 = 256;          //   up to here: one warp per cell, in registers (k_sort_warp256)
 constexpr int SORT_MED_MAX = 2048;      //   medium tier (k_sort_radix): 128 threads, 33 KB shared memory
@@ -35,42 +35,6 @@ constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 512 threads, 225 KB; abo
 constexpr int SORT_HUGE_T = SORT_HUGE_THREADS;
 constexpr int SORT_WARPS = 8;
 constexpr int SORT_GIANT_T = 1024;      // cells above SORT_HUGE_MAX (k_sort_radix<GLOBAL>)
-
-// r += (a < b) as a compare and a predicated add (the compiler's select form costs three
-// instructions per comparison in the rank loops below)
-__device__ __forceinline__ void count_lt(unsigned &r, unsigned a, unsigned b)
-{
-    asm("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}" : "+r"(r) : "r"(a), "r"(b));
-}
-
-// The same for a, b < 2^31 as the sign bit of a - b (IMAD.IADD on the FMA pipe + LEA.HI):
-// mixing both forms spreads a rank loop over the FMA and ALU pipes (each takes one warp
-// instruction every two cycles), where compare + predicated add alone keep the ALU pipe full.
-__device__ __forceinline__ void count_lt_sign(unsigned &r, unsigned a, unsigned b)
-{
-    r += (a - b) >> 31;
-}
-
-#ifndef SORT_CNT_MODE
-#define SORT_CNT_MODE 1          // 0: compare + add only; 1: alternate with the sign form; 2: sign form only
-#endif
-__device__ __forceinline__ void count_lt_k(int k, unsigned &r, unsigned a, unsigned b)
-{
-    if (SORT_CNT_MODE == 2 || (SORT_CNT_MODE == 1 && (k & 1))) count_lt_sign(r, a, b);
-    else count_lt(r, a, b);
-}
-
-__device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, double corner[3])
-{
-    long long plane = (long long)g.ny * g.nz;
-    int ixl = (int)(cell / plane);
-    int iy = (int)((cell / g.nz) % g.ny);
-    int iz = (int)(cell % g.nz);
-    int ixg = wrap_i(ixl - g.ghost_x + g.x_lo, g.nc[0]);
-    corner[0] = (double)ixg * g.cl[0];
-    corner[1] = (double)iy * g.cl[1];
-    corner[2] = (double)iz * g.cl[2];
-}
 
 // Level passes: the list of cell j along direction d is read only when the
 // neighbour of j at offset +d or -d holds home particles of this grid, and a cell with home
@@ -108,7 +72,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
                                                                     int *big_count, int *huge_items, int *huge_count,
                                                                     int huge_cap, int *mid_items, int *mid_count,
                                                                     int *w256_items, int *w256_count,
-                                                                    const int *__restrict__ need)
+                                                                    const int *__restrict__ need, bool small_done)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -123,6 +87,7 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         const int my_s0 = mycell < cend ? c.cell_start[mycell] : 0;
         int my_n = mycell < cend ? c.cell_start[mycell + 1] - my_s0 : 0;
         if (need && my_n > 0 && !need[mycell]) my_n = 0;     // lists never read on this level grid
+        if (small_done && my_n <= SORT_SMALL) my_n = 0;     // sph_build_sort_cells: written by the build
         // each lane the fp32 corner of ITS cell, once per 32 cells (the cell -> (x, y, z)
         // divisions cost ~10 % of the warp's instructions when done per cell by every lane)
         float my_corner[3] = {0.f, 0.f, 0.f};
@@ -158,53 +123,11 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             if (lane == 0) big_items[atomicAdd(big_count, 1)] = make_int2((int)cell, 0);
             continue;
         }
-        const float fc0 = __shfl_sync(0xffffffffu, my_corner[0], j);
-        const float fc1 = __shfl_sync(0xffffffffu, my_corner[1], j);
-        const float fc2 = __shfl_sync(0xffffffffu, my_corner[2], j);
-        // One particle per lane, all 13 directions ranked in one pass over the cell:
-        // composite = quantised key (25 bits) << 5 | in-cell index (the slot order is the
-        // input order, so equal keys keep input order).  The fp32 key error (< 1e-6 C_l)
-        // and the quantum 2 sqrt(3) C_l / 2^25 (~1e-7 C_l) are far below the window margin
-        // delta = 2^-16 C_l; the density sweeps tolerate that much disorder.
-        unsigned *S = sh[w];
+        const float fc[3] = {__shfl_sync(0xffffffffu, my_corner[0], j), __shfl_sync(0xffffffffu, my_corner[1], j),
+                             __shfl_sync(0xffffffffu, my_corner[2], j)};
         const bool mine = lane < n;
         const float4 p = mine ? c.xyzh[s0 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
-        // cell-local coordinates in fp32: x - fp32(corner) is exact (Sterbenz) unless both are
-        // within a cell of 0, where the error is below ulp(C_l)
-        const float u0 = p.x - fc0, u1 = p.y - fc1, u2 = p.z - fc2;
-        unsigned comp[SPH_NDIR];
-#pragma unroll
-        for (int d = 0; d < SPH_NDIR; ++d) {
-            const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
-            const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
-            const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
-            const float key = ((float)a0 * u0 + (float)a1 * u1 + (float)a2 * u2) * inv;
-            // quantised key: floor((key + cmax) scale) as one FFMA and a rounding conversion
-            const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
-            comp[d] = ((unsigned)qk << 5) | (unsigned)lane;     // < 2^30 (count_lt_sign)
-            if (mine) S[lane * 16 + d] = comp[d];
-        }
-        __syncwarp();
-        unsigned r[SPH_NDIR];
-#pragma unroll
-        for (int d = 0; d < SPH_NDIR; ++d) r[d] = 0;
-        for (int m = 0; m < n; ++m) {
-            const uint4 c0 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 0]);
-            const uint4 c1 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 4]);
-            const uint4 c2 = *reinterpret_cast<const uint4 *>(&S[m * 16 + 8]);
-            const unsigned c12 = S[m * 16 + 12];
-            count_lt_k(0, r[0], c0.x, comp[0]); count_lt_k(1, r[1], c0.y, comp[1]);
-            count_lt_k(2, r[2], c0.z, comp[2]); count_lt_k(3, r[3], c0.w, comp[3]);
-            count_lt_k(4, r[4], c1.x, comp[4]); count_lt_k(5, r[5], c1.y, comp[5]);
-            count_lt_k(6, r[6], c1.z, comp[6]); count_lt_k(7, r[7], c1.w, comp[7]);
-            count_lt_k(8, r[8], c2.x, comp[8]); count_lt_k(9, r[9], c2.y, comp[9]);
-            count_lt_k(10, r[10], c2.z, comp[10]); count_lt_k(11, r[11], c2.w, comp[11]);
-            count_lt_k(12, r[12], c12, comp[12]);
-        }
-        if (mine) {
-#pragma unroll
-            for (int d = 0; d < SPH_NDIR; ++d) ord[(long long)d * c.cap + s0 + r[d]] = (uint16_t)lane;
-        }
+        sort_small_lists(sh[w], ord, c.cap, s0, n, mine, p, lane, fc, scale, cmax_s);
         __syncwarp();
       }
     }

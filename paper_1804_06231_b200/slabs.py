@@ -360,6 +360,17 @@ class SlabRunner:
         """Build, sort and density of every level grid on the current inputs (owned particles
         and the n_ghost ghosts behind them)."""
         rec = rec or (lambda k: None)
+        if not self.extra:
+            # one grid: build and sort in one call (the small cells' lists come out of the build's
+            # placement pass); the "build" stage then holds both, "sort" only the larger cells' tiers
+            pv.sph_build_sort_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own,
+                                    n_ghost=self.n_ghost)
+            rec(2)
+            rec(3)
+            dens = pv.sph_density_all_sym if self.engine == "sym" else pv.sph_density_all
+            dens(self.grid, self.cells, self.out, self.ws, stats=stats)
+            rec(4)
+            return
         pv.sph_build_cells(self.grid, self.xin, self.vin, self.cells, self.ws, n_own=self.n_own,
                            n_ghost=self.n_ghost)
         for g, c, ws in self.extra:

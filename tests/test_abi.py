@@ -47,7 +47,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version_and_strerror(lib):
-    assert lib.sph_abi_version() == 6
+    assert lib.sph_abi_version() == 7
     for code in range(6):
         assert len(lib.sph_strerror(code)) > 0
 
