@@ -150,7 +150,9 @@ for name, d in benches.items():
     weff = ("%.3f" % r["warp_efficiency"] if r.get("warp_efficiency") is not None else
             "%.3f" % fp["warp_efficiency"] if fp and "warp_efficiency" in fp else
             "n/a (not in the summed counter set)" if fp else why)
-    if "build" in st:
+    if "build" in st and "fused" in str((d.get("config") or {}).get("step", "")):
+        stages = f"{st['build']:.2f} (build + sort, one fused call) / {st['density']:.2f}"
+    elif "build" in st:
         stages = f"{st['build']:.2f} / {st['sort']:.2f} / {st['density']:.2f}"
     elif "density" in st:
         stages = f"density {st['density']:.2f}, drift + rebuilds {st['drift_and_rebuilds']:.2f}"
