@@ -407,20 +407,23 @@ int sort_impl(const sph_grid *grid, const sph_cells *cells, int64_t cell_begin, 
         if ((e = cudaMemsetAsync(need, 0, 4 * (size_t)g.ncell, s)) != cudaSuccess) return cuda_fail(e);
         k_mark_needed<<<grid_blocks(g.ncell, 256, 148 * 32), 256, 0, s>>>(g, cells->cell_nhome, need);
     }
+    // huge cells' directions in groups over several CTAs (item = cell | group << 28)
+    const int huge_ngrp = g.ncell < (1ll << 28) ? SORT_DIR_GROUPS : 1;
+    static_assert(sizeof(ParticleRec) >= 12 * SORT_DIR_GROUPS, "giant-tier scratch stripes fit the record region");
     k_sort_small<<<grid_blocks(cell_end - cell_begin, SORT_WARPS, 148 * 64), SORT_WARPS * 32, 0, s>>>(
         g, c, cells->order, cell_begin, cell_end, big_items, big_count, huge_items, huge_count, (int)w.huge_cap,
-        mid_items, huge_count + 2, w256_items, huge_count + 3, need, small_done);
+        mid_items, huge_count + 2, w256_items, huge_count + 3, need, small_done, huge_ngrp);
     k_sort_mid<<<148 * 8, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, mid_items, huge_count + 2, need);
     k_sort_warp256<<<148 * 4, SORT_WARPS * 32, 0, s>>>(g, c, cells->order, w256_items, huge_count + 3, need);
     if ((rc = ensure_attrs()) != SPH_OK) return rc;
     // cells above SORT_HUGE_MAX: key/index buffers in the build's record region (free after it)
     k_sort_radix<65535, SORT_GIANT_T, false, true, 2><<<148, SORT_GIANT_T, radix_smem_global(SORT_GIANT_T), s>>>(
         g, c, cells->order, reinterpret_cast<const int *>(big_items), big_count, 0, need,
-        at<unsigned>(ws, w.rec));
+        at<unsigned>(ws, w.rec), SORT_DIR_GROUPS);
     k_sort_radix<SORT_MED_MAX, SORT_MED_T, false><<<148 * 8, SORT_MED_T, radix_smem(SORT_MED_MAX, SORT_MED_T), s>>>(
         g, c, cells->order, huge_items, huge_count, (int)w.huge_cap, need);
     k_sort_radix<SORT_HUGE_MAX, SORT_HUGE_T, true><<<148, SORT_HUGE_T, radix_smem(SORT_HUGE_MAX, SORT_HUGE_T), s>>>(
-        g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap, need);
+        g, c, cells->order, huge_items, huge_count + 1, (int)w.huge_cap, need, nullptr, huge_ngrp);
     return check_launch();
 }
 

@@ -34,7 +34,8 @@ constexpr int SORT_HUGE_MAX = 16384;    //   huge tier: 512 threads, 225 KB; abo
 #endif
 constexpr int SORT_HUGE_T = SORT_HUGE_THREADS;
 constexpr int SORT_WARPS = 8;
-constexpr int SORT_GIANT_T = 1024;      // cells above SORT_HUGE_MAX (k_sort_radix<GLOBAL>)
+constexpr int SORT_GIANT_T = 1024;
+constexpr int SORT_DIR_GROUPS = 5;     // direction groups of the huge and giant tiers (k_sort_radix)      // cells above SORT_HUGE_MAX (k_sort_radix<GLOBAL>)
 
 // Level passes: the list of cell j along direction d is read only when the
 // neighbour of j at offset +d or -d holds home particles of this grid, and a cell with home
@@ -72,7 +73,8 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
                                                                     int *big_count, int *huge_items, int *huge_count,
                                                                     int huge_cap, int *mid_items, int *mid_count,
                                                                     int *w256_items, int *w256_count,
-                                                                    const int *__restrict__ need, bool small_done)
+                                                                    const int *__restrict__ need, bool small_done,
+                                                                    int huge_ngrp)
 {
     __shared__ unsigned sh[SORT_WARPS][32 * 16];          // [lane][16] composites per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -110,8 +112,12 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
         if (n > SORT_MED && n <= SORT_HUGE_MAX) {
             // medium cells from the front of the list, huge ones from the back (k_sort_radix)
             if (lane == 0) {
-                if (n <= SORT_MED_MAX) huge_items[atomicAdd(&huge_count[0], 1)] = (int)cell;
-                else huge_items[huge_cap - 1 - atomicAdd(&huge_count[1], 1)] = (int)cell;
+                if (n <= SORT_MED_MAX) {
+                    huge_items[atomicAdd(&huge_count[0], 1)] = (int)cell;
+                } else {
+                    const int pos = atomicAdd(&huge_count[1], huge_ngrp);
+                    for (int gi = 0; gi < huge_ngrp; ++gi) huge_items[huge_cap - 1 - (pos + gi)] = (int)cell | (gi << 28);
+                }
             }
             continue;
         }
@@ -120,7 +126,10 @@ __global__ void __launch_bounds__(SORT_WARPS * 32, 4) k_sort_small(DevGrid g, De
             continue;
         }
         if (n > SORT_SMALL) {                              // above SORT_HUGE_MAX: k_sort_radix<GLOBAL>
-            if (lane == 0) big_items[atomicAdd(big_count, 1)] = make_int2((int)cell, 0);
+            if (lane == 0) {
+                const int pos = atomicAdd(big_count, SORT_DIR_GROUPS);
+                for (int gi = 0; gi < SORT_DIR_GROUPS; ++gi) big_items[pos + gi] = make_int2((int)cell, gi);
+            }
             continue;
         }
         const float fc[3] = {__shfl_sync(0xffffffffu, my_corner[0], j), __shfl_sync(0xffffffffu, my_corner[1], j),
@@ -153,10 +162,16 @@ constexpr int radix_smem(int maxn, int t) { return maxn * 12 + 2 * 256 * (t / 32
 // 65535 -- and only the counters in shared memory.  Items: every ISTRIDE-th int.
 constexpr int radix_smem_global(int t) { return 2 * 256 * (t / 32) * 4 + 64 * 4; }
 
+// Direction groups: a cell's 13 directions may be split into ngrp groups sorted by different
+// CTAs (the huge and giant tiers: a few big cells would otherwise leave most SMs idle while one
+// CTA walks all 13 directions).  Group gi holds directions [13 gi / ngrp, 13 (gi + 1) / ngrp).
+// Items: huge tier cell | gi << 28 (ngrp > 1 needs ncell < 2^28); giant tier (GLOBAL) int2
+// (cell, gi), whose scratch is the gi-th 12-byte-per-slot stripe of the record region (ngrp <= 5:
+// 5 x 12 B fit the 64-byte records).
 template <int MAXN, int T, bool FROM_BACK, bool GLOBAL = false, int ISTRIDE = 1>
 __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_t *ord, const int *items,
                                                  const int *count, int cap, const int *__restrict__ need,
-                                                 unsigned *gscratch = nullptr)
+                                                 unsigned *gscratch = nullptr, int ngrp = 1)
 {
     constexpr int NW = T / 32;
     constexpr int NH = 256 * NW;                       // counters, [digit][warp]
@@ -176,11 +191,15 @@ __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_
     const float scale = 16777216.0f / (2.0f * cmax);   // 2^24 over the key range
     const float cmax_s = cmax * scale;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-        const long long cell = items[(long long)ISTRIDE * (FROM_BACK ? cap - 1 - it : it)];
+        const long long ii = (long long)ISTRIDE * (FROM_BACK ? cap - 1 - it : it);
+        const int item = items[ii];
+        const long long cell = GLOBAL || ngrp == 1 ? item : (item & 0x0fffffff);
+        const int gi = GLOBAL ? items[ii + 1] : (ngrp == 1 ? 0 : (int)((unsigned)item >> 28));
+        const int d_lo = SPH_NDIR * gi / ngrp, d_hi = SPH_NDIR * (gi + 1) / ngrp;
         const int s0 = c.cell_start[cell];
         const int n = c.cell_start[cell + 1] - s0;
         if (GLOBAL) {
-            unsigned *base = gscratch + 3ll * s0;
+            unsigned *base = gscratch + 3ll * s0 + 3ll * gi * c.cap;
             keyA = base;
             keyB = base + n;
             idxA = reinterpret_cast<uint16_t *>(base + 2 * n);
@@ -192,7 +211,7 @@ __global__ void __launch_bounds__(T) k_sort_radix(DevGrid g, DevCells c, uint16_
         double corner[3];
         cell_corner(g, cell, corner);
         const int mask = need ? need[cell] : 0x1fff;
-        for (int d = 0; d < SPH_NDIR; ++d) {
+        for (int d = d_lo; d < d_hi; ++d) {
             if (!((mask >> d) & 1)) continue;          // CTA-uniform
 #pragma unroll
             for (int q = 0; q < HPT; ++q) histA[threadIdx.x * HPT + q] = 0u;
