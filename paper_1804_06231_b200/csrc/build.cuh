@@ -482,7 +482,32 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             cell_corner(g, mycell, cd);
             my_corner[0] = (float)cd[0]; my_corner[1] = (float)cd[1]; my_corner[2] = (float)cd[2];
         }
-        unsigned todo = __ballot_sync(0xffffffffu, my_n > 0);
+        bool tiny = false;
+        if (!SORT && my_n > 0 && my_n <= 2) {
+            // a cell of one or two particles (most non-empty cells of sparse level grids): the
+            // lane places it itself -- same order (key: home first, input order) and outputs
+            tiny = true;
+            const unsigned k0 = (unsigned)rec[my_s0].idx;
+            const unsigned k1 = my_n == 2 ? (unsigned)rec[my_s0 + 1].idx : 0xffffffffu;
+            const int first = my_n == 2 && k1 < k0 ? 1 : 0;
+            float hm = 0.0f;
+            int nh = 0;
+            for (int e = 0; e < my_n; ++e) {
+                const int src = my_s0 + (e == 0 ? first : 1 - first);
+                const float4 qx = rec[src].xyzh;
+                const unsigned key = (unsigned)rec[src].idx;
+                xyzh[my_s0 + e] = qx;
+                vm[my_s0 + e] = rec[src].vm;
+                perm[my_s0 + e] = (int)(key & 0x7fffffffu);
+                slot_cell[my_s0 + e] = (int)mycell;
+                nh += key < 0x80000000u ? 1 : 0;
+                hm = fmaxf(hm, qx.w);
+            }
+            cell_nhome[mycell] = nh;
+            cell_hmax[mycell] = hm;
+            if (nh > 0) row_home[mycell / nz] = 1;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, my_n > 0 && !tiny);
       while (todo) {
         const int j = __ffs(todo) - 1;
         todo &= todo - 1;

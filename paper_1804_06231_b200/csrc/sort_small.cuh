@@ -46,6 +46,20 @@ __device__ __forceinline__ void cell_corner(const DevGrid &g, long long cell, do
 }
 
 
+// The ranking composite of one particle along direction d: quantised key (25 bits) << 5 |
+// in-cell index; (u0, u1, u2) = position - fp32 cell corner.
+__device__ __forceinline__ unsigned small_composite(float u0, float u1, float u2, int d, int idx, float scale,
+                                                    float cmax_s)
+{
+    const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
+    const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
+    const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
+    const float key = ((float)a0 * u0 + (float)a1 * u1 + (float)a2 * u2) * inv;
+    // quantised key: floor((key + cmax) scale) as one FFMA and a rounding conversion
+    const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
+    return ((unsigned)qk << 5) | (unsigned)idx;     // < 2^30 (count_lt_sign)
+}
+
 // The 13 lists of one cell of n <= 32 particles, one particle per lane (sph_sort_cells' small
 // tier, also run inside the fused build, sph_build_sort_cells).  Lane l holds a particle p whose
 // in-cell index is idx (l itself in k_sort_small; the stable rank in the fused build); fc: the
@@ -64,13 +78,7 @@ __device__ __forceinline__ void sort_small_lists(unsigned *S, uint16_t *ord, lon
     unsigned comp[SPH_NDIR];
 #pragma unroll
     for (int d = 0; d < SPH_NDIR; ++d) {
-        const int a0 = dir_component(d, 0), a1 = dir_component(d, 1), a2 = dir_component(d, 2);
-        const int kd = (a0 != 0) + (a1 != 0) + (a2 != 0);
-        const float inv = kd == 1 ? 1.0f : (kd == 2 ? 0.70710678118654752f : 0.57735026918962576f);
-        const float key = ((float)a0 * u0 + (float)a1 * u1 + (float)a2 * u2) * inv;
-        // quantised key: floor((key + cmax) scale) as one FFMA and a rounding conversion
-        const int qk = min(max(__float2int_rd(fmaf(key, scale, cmax_s)), 0), 33554431);
-        comp[d] = ((unsigned)qk << 5) | (unsigned)idx;     // < 2^30 (count_lt_sign)
+        comp[d] = small_composite(u0, u1, u2, d, idx, scale, cmax_s);
         if (mine) S[lane * 16 + d] = comp[d];
     }
     __syncwarp();
