@@ -422,6 +422,7 @@ __global__ void k_gather_positions(const float4 *__restrict__ xyzh, const int *_
 
 constexpr int STABLE_SMALL = 128;
 constexpr int STABLE_WARPS = 8;
+constexpr int STABLE_LANE = 4;          // cells up to this size: one lane (k_stable_small)
 constexpr int STABLE_BIG_CHUNK = 256;
 constexpr int STABLE_BIG_TILE = 4096;
 constexpr int STABLE_BT_MAX = 16384;     // cells of STABLE_SMALL < n <= this: k_stable_radix
@@ -483,24 +484,27 @@ __global__ void __launch_bounds__(STABLE_WARPS * 32) k_stable_small(long long nc
             my_corner[0] = (float)cd[0]; my_corner[1] = (float)cd[1]; my_corner[2] = (float)cd[2];
         }
         bool tiny = false;
-        if (!SORT && my_n > 0 && my_n <= 2) {
-            // a cell of one or two particles (most non-empty cells of sparse level grids): the
-            // lane places it itself -- same order (key: home first, input order) and outputs
+        if (!SORT && my_n > 0 && my_n <= STABLE_LANE) {
+            // a cell of up to STABLE_LANE particles (most non-empty cells of sparse level grids):
+            // the lane places it itself -- same order (key: home first, input order) and outputs
             tiny = true;
-            const unsigned k0 = (unsigned)rec[my_s0].idx;
-            const unsigned k1 = my_n == 2 ? (unsigned)rec[my_s0 + 1].idx : 0xffffffffu;
-            const int first = my_n == 2 && k1 < k0 ? 1 : 0;
+            unsigned k[STABLE_LANE];
+#pragma unroll
+            for (int e = 0; e < STABLE_LANE; ++e) k[e] = e < my_n ? (unsigned)rec[my_s0 + e].idx : 0xffffffffu;
             float hm = 0.0f;
             int nh = 0;
-            for (int e = 0; e < my_n; ++e) {
-                const int src = my_s0 + (e == 0 ? first : 1 - first);
-                const float4 qx = rec[src].xyzh;
-                const unsigned key = (unsigned)rec[src].idx;
-                xyzh[my_s0 + e] = qx;
-                vm[my_s0 + e] = rec[src].vm;
-                perm[my_s0 + e] = (int)(key & 0x7fffffffu);
+#pragma unroll
+            for (int e = 0; e < STABLE_LANE; ++e) {
+                if (e >= my_n) break;
+                int r = 0;
+#pragma unroll
+                for (int m = 0; m < STABLE_LANE; ++m) r += k[m] < k[e] ? 1 : 0;   // keys distinct
+                const float4 qx = rec[my_s0 + e].xyzh;
+                xyzh[my_s0 + r] = qx;
+                vm[my_s0 + r] = rec[my_s0 + e].vm;
+                perm[my_s0 + r] = (int)(k[e] & 0x7fffffffu);
                 slot_cell[my_s0 + e] = (int)mycell;
-                nh += key < 0x80000000u ? 1 : 0;
+                nh += k[e] < 0x80000000u ? 1 : 0;
                 hm = fmaxf(hm, qx.w);
             }
             cell_nhome[mycell] = nh;
