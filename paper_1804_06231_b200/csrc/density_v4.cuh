@@ -151,22 +151,28 @@ struct RowPairs {
     long long nkeys;
 };
 
+#ifndef RP_BX
+#define RP_BX 4        // row-pair blocks: RP_BX x-planes by RP_BY row pairs
+#endif
+#ifndef RP_BY
+#define RP_BY 4
+#endif
 __host__ __device__ __forceinline__ RowPairs row_pairs(const DevGrid &g)
 {
     RowPairs r;
     r.nxo = g.x_hi - g.x_lo;
     r.nyp = (g.ny + 1) / 2;
-    r.nby = (r.nyp + 3) / 4;
-    r.nkeys = (long long)((r.nxo + 3) / 4) * r.nby * 16;
+    r.nby = (r.nyp + RP_BY - 1) / RP_BY;
+    r.nkeys = (long long)((r.nxo + RP_BX - 1) / RP_BX) * r.nby * (RP_BX * RP_BY);
     return r;
 }
 
 __host__ __device__ __forceinline__ void key_rowpair(const RowPairs &r, long long key, int &xo, int &yp)
 {
-    const long long blk = key / 16;
-    const int w = (int)(key % 16);
-    xo = (int)(blk / r.nby) * 4 + w / 4;
-    yp = (int)(blk % r.nby) * 4 + w % 4;
+    const long long blk = key / (RP_BX * RP_BY);
+    const int w = (int)(key % (RP_BX * RP_BY));
+    xo = (int)(blk / r.nby) * RP_BX + w / RP_BY;
+    yp = (int)(blk % r.nby) * RP_BY + w % RP_BY;
 }
 
 __host__ __device__ __forceinline__ long long v4_tile_capacity(const DevGrid &g, long long n)
