@@ -27,8 +27,14 @@
 namespace pvsph {
 
 constexpr int DENSE_WARPS = 8;
-constexpr int DENSE_K = 256;             // staged entries per chunk (per warp)
-constexpr int DENSE_Q = 16;              // hit stack depth per lane
+#ifndef DENSE_K_ENTRIES
+#define DENSE_K_ENTRIES 128   // A/B on c4: 64 / 96 / 128 / 160 / 256 / 512 -> density 23.9 / 24.1 / 23.8 / 24.1 / 24.2 / 30.5 ms
+#endif
+#ifndef DENSE_Q_DEPTH
+#define DENSE_Q_DEPTH 16
+#endif
+constexpr int DENSE_K = DENSE_K_ENTRIES; // staged entries per chunk (per warp)
+constexpr int DENSE_Q = DENSE_Q_DEPTH;   // hit stack depth per lane
 constexpr int DENSE_MAP = 256;           // home rank -> sorted position map of one tile part (>= V4_TP)
 constexpr size_t DENSE_WARP_SMEM = (size_t)DENSE_K * 32 + (size_t)DENSE_Q * 32 * 2 + (size_t)DENSE_MAP * 2;
 static_assert(DENSE_MAP >= V4_TP, "a tile part holds at most V4_TP home particles");
